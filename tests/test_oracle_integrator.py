@@ -1,0 +1,164 @@
+"""Pins for the whole oracle integrator and the dense diagnostic (no GPU).
+
+The closed form must equal exp(lambda Phi D Phi^T) F exactly (up to
+rounding) -- it is an identity of the low-rank matrix,
+not an approximation -- so it is checked against a dense matrix exponential
+computed by a different algorithm (symmetric eigendecomposition / scipy
+expm), plus closed forms, invariants and limits.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg
+
+from oracle import dense, rfd
+
+C_R = rfd.l1_ball_mass()
+
+
+def _lowrank_dense(plan):
+    """W~ = Phi D Phi^T as an explicit N x N matrix (tiny N only)."""
+    P = rfd.features(plan.X, plan.omega)
+    d = np.concatenate([plan.nu, plan.nu])
+    return P @ (d[:, None] * P.T)
+
+
+def _cloud(n, seed=0):
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal((n, 3))
+    return (g / np.linalg.norm(g, axis=1, keepdims=True)).astype(np.float32), rng
+
+
+@pytest.mark.parametrize("n,m,eps,lam", [(300, 8, 0.3, -0.7), (1000, 16, 0.15, -0.5),
+                                         (600, 64, 0.2, -1.5), (400, 32, 0.25, 0.4)])
+def test_identity_against_dense_expm(n, m, eps, lam):
+    X, rng = _cloud(n, seed=n)
+    F = rng.standard_normal((n, 3))
+    plan = rfd.Plan(X, eps, lam, m, seed=7, c_r=C_R)
+    out = plan.apply(F)["out"]
+    ref = dense.symmetric_expm_apply(_lowrank_dense(plan), lam, F)
+    assert np.abs(out - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+def test_identity_against_scipy_expm_small():
+    X, rng = _cloud(120, seed=3)
+    F = rng.standard_normal((120, 2))
+    plan = rfd.Plan(X, 0.3, -0.8, 12, seed=2, c_r=C_R)
+    ref = scipy.linalg.expm(-0.8 * _lowrank_dense(plan)) @ F
+    out = plan.apply(F)["out"]
+    assert np.abs(out - ref).max() <= 1e-11 * np.abs(ref).max()
+
+
+def test_single_point_closed_form():
+    X = np.array([[0.3, -0.2, 0.9]], np.float32)
+    F = np.array([[1.5, -2.0, 0.25]])
+    plan = rfd.Plan(X, 0.1, -0.6, 16, seed=0, c_r=C_R)
+    out = plan.apply(F)["out"]
+    np.testing.assert_allclose(out, math.exp(-0.6 * plan.nu.sum()) * F, rtol=1e-13)
+
+
+def test_two_coincident_points_closed_form():
+    X = np.array([[0.1, 0.2, 0.3], [0.1, 0.2, 0.3]], np.float32)
+    F = np.array([[1.0, 2.0], [-3.0, 0.5]])
+    lam = -0.4
+    plan = rfd.Plan(X, 0.15, lam, 16, seed=1, c_r=C_R)
+    s = plan.nu.sum()
+    ref = F + 0.5 * math.expm1(2 * lam * s) * np.ones((2, 2)) @ F
+    np.testing.assert_allclose(plan.apply(F)["out"], ref, rtol=1e-13, atol=1e-14)
+
+
+def test_first_order_in_lambda():
+    X, rng = _cloud(200, seed=5)
+    F = rng.standard_normal((200, 3))
+    lam = 1e-6
+    plan = rfd.Plan(X, 0.2, lam, 16, seed=4, c_r=C_R)
+    first = _lowrank_dense(plan) @ F
+    got = (plan.apply(F)["out"] - F) / lam
+    assert np.abs(got - first).max() <= 1e-4 * np.abs(first).max()
+
+
+def test_lambda_zero_identity():
+    X, rng = _cloud(50, seed=6)
+    F = rng.standard_normal((50, 3))
+    plan = rfd.Plan(X, 0.2, 0.0, 8, seed=4, c_r=C_R)
+    np.testing.assert_array_equal(plan.apply(F)["out"], F)
+
+
+def test_semigroup_symmetry_linearity_permutation():
+    X, rng = _cloud(300, seed=8)
+    F = rng.standard_normal((300, 2))
+    lam = -0.7
+    full = rfd.Plan(X, 0.3, lam, 8, seed=3, c_r=C_R)
+    half = rfd.Plan(X, 0.3, lam / 2, 8, seed=3, c_r=C_R)
+    a = full.apply(F)["out"]
+    b = half.apply(half.apply(F)["out"])["out"]
+    assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
+    u = rng.standard_normal(300)
+    v = rng.standard_normal(300)
+    Ku = full.apply(u)["out"][:, 0]
+    Kv = full.apply(v)["out"][:, 0]
+    assert abs(u @ Kv - Ku @ v) <= 1e-12 * abs(u @ Kv)
+    G2 = rng.standard_normal((300, 2))
+    np.testing.assert_allclose(full.apply(2 * F - G2)["out"], 2 * a - full.apply(G2)["out"],
+                               atol=1e-11)
+    perm = rng.permutation(300)
+    pplan = rfd.Plan(X[perm], 0.3, lam, 8, seed=3, c_r=C_R)
+    np.testing.assert_allclose(pplan.apply(F[perm])["out"], a[perm], atol=1e-11)
+
+
+def test_rows_subset_matches_full():
+    X, rng = _cloud(500, seed=9)
+    F = rng.standard_normal((500, 4))
+    plan = rfd.Plan(X, 0.2, -1.0, 16, seed=5, c_r=C_R)
+    full = plan.apply(F)["out"]
+    rows = np.array([0, 17, 499, 250])
+    np.testing.assert_allclose(plan.apply(F, rows=rows)["out"], full[rows], rtol=1e-14, atol=1e-14)
+
+
+def _median_mse(m, norm, seeds=20):
+    X, _ = _cloud(400, seed=11)
+    eps = 0.15
+    truth = dense.epsilon_graph(X, eps, norm)
+    P_cache = []
+    mses = []
+    for s in range(seeds):
+        om, _ = rfd.frequencies(1000 + s, m)
+        nu = rfd.importance_weights(om, eps, C_R)
+        P = rfd.features(X, om)
+        W = P @ (np.concatenate([nu, nu])[:, None] * P.T)
+        mses.append(np.mean((W - truth) ** 2))
+    del P_cache
+    return float(np.median(mses))
+
+
+def test_adjacency_error_falls_with_m_and_is_cube_graph():
+    # Approximation quality vs the exact graph: parity unpinned; trend only
+    # (Lemma 2.7's 1/m variance term; A2, A9).
+    inf16, inf256 = _median_mse(16, "inf"), _median_mse(256, "inf")
+    assert inf256 < 0.5 * inf16
+    assert inf16 < _median_mse(16, 1)
+
+
+def test_dense_spec_examples():
+    # SPEC.md:199-201.
+    X = np.eye(3)
+    np.testing.assert_allclose(dense.symmetric_expm_apply(np.eye(3), 1.0, X), math.e * X, rtol=1e-14)
+    np.testing.assert_allclose(
+        dense.symmetric_expm_apply(np.diag([0.0, math.log(2.0)]), 1.0, np.ones(2))[:, 0],
+        [1.0, 2.0], rtol=1e-14)
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((30, 30))
+    W = A + A.T
+    np.testing.assert_allclose(dense.symmetric_expm_apply(W, 0.1, np.eye(30)),
+                               scipy.linalg.expm(0.1 * W), rtol=1e-10, atol=1e-12)
+
+
+def test_dense_graph_two_points():
+    X = np.array([[0.0, 0.0, 0.0], [0.1, 0.1, 0.0]])
+    # L-inf distance 0.1 <= 0.15 but L1 distance 0.2 > 0.15.
+    assert dense.epsilon_graph(X, 0.15, "inf")[0, 1] == 1.0
+    assert dense.epsilon_graph(X, 0.15, 1)[0, 1] == 0.0
+    np.testing.assert_allclose(dense.exact_diffusion(X, np.eye(2), 0.15, 1.0, 1), np.eye(2) * math.e,
+                               rtol=1e-14)
