@@ -1,0 +1,398 @@
+"""Benchmark of the RFD hot path on B200 (contract: see DESIGN.md Sec. 8).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl rfd|reference]
+
+One STEP = one pass of the whole hot path over
+the BASELINE.json scoring config (cfg 5: N = 4,194,304 points in the unit
+cube, m = 256, d = 16, eps = 0.01, lambda = -0.3): rfd_plan_create
+(frequencies, Gram, core) + rfd_integrate (pass 1, Y, pass 2), inputs
+resident in HBM.  value = N * d * steps * ranks / max-over-ranks time
+(points x dims / s).  Multi-GPU: each rank integrates its own independent
+cloud (weak scaling, no data-path collective).
+
+Extra keys: ``integrate`` (inference only, plan reused: the paper's
+"inference"), ``roofline`` for the dominant kernel (timed with
+CUDA events on its launch stream inside the timed region), ``kernels`` (every
+kernel's share), ``e2e`` (host buffers through the C ABI), ``cpu_baseline``
+(the fp64 oracle on a bounded sample, rank 0, N = 1 only), ``clocks`` (NVML
+samples during the timed region), ``gpu_launches``.
+"""
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import make_config  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# B200 unit counts (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz; CUDA
+# throughput table for cc 10.0: 128 FP32 FMA and 16 MUFU results / clk / SM).
+SMS, FMA_PER_CLK, MUFU_PER_CLK = 148, 128, 16
+METRIC = "GFI points x dims / s (RFD plan + integrate, cfg5 N=4M m=256 d=16)"
+UNIT = "points*dims/s"
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "src": "fallback (B200_PROFILING.md)"}
+    if os.path.exists(PEAKS_PATH):
+        with open(PEAKS_PATH) as f:
+            j = json.load(f)
+        p.update({k: j[k] for k in ("hbm_gbs", "sm_max_mhz") if k in j})
+        p["src"] = "measured (MEASURED_PEAKS.json)"
+    return p
+
+
+# ------------------------------------------------------------------ work model
+def kernel_work(name, N, m, d):
+    """Algorithmic work of one launch: (FMA, MUFU, bytes)."""
+    r = 2 * m
+    if name == "rfd_gram_partial":      # G = Phi^T Phi, upper triangle + features
+        return N * r * (r + 1) / 2 + 3.0 * N * m, 2.0 * N * m, 16.0 * N
+    if name == "rfd_pass1":             # S = Phi^T F
+        return 2.0 * N * m * min(d, 16) + 3.0 * N * m, 2.0 * N * m, N * (16 + 4 * min(d, 16))
+    if name == "rfd_pass2":             # out = F + Phi Y
+        return 2.0 * N * m * min(d, 16) + 3.0 * N * m, 2.0 * N * m, N * (16 + 8 * min(d, 16))
+    return None
+
+
+def roofline_of(name, N, m, d, ms_per_launch, pk):
+    w = kernel_work(name, N, m, d)
+    if w is None or ms_per_launch <= 0:
+        return None
+    fma, mufu, byts = w
+    clk = pk["sm_max_mhz"] * 1e6
+    fma_peak = SMS * FMA_PER_CLK * clk
+    mufu_peak = SMS * MUFU_PER_CLK * clk
+    t = ms_per_launch * 1e-3
+    t_fma, t_mufu, t_hbm = fma / fma_peak, mufu / mufu_peak, byts / (pk["hbm_gbs"] * 1e9)
+    bound = max((t_fma, "alu"), (t_mufu, "sfu"), (t_hbm, "hbm"))
+    if bound[1] == "hbm":
+        return {"bound": "hbm", "achieved": byts / t / 1e9, "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": t_hbm / t, "traffic": None}
+    if bound[1] == "alu":
+        return {"bound": "alu", "achieved": 2 * fma / t / 1e12, "peak": 2 * fma_peak / 1e12,
+                "unit": "TFLOP/s", "frac": t_fma / t, "traffic": None,
+                "peak_note": "fp32 FMA pipe: 148 SM x 128 FMA/clk x %.0f MHz (derived)" % pk["sm_max_mhz"]}
+    return {"bound": "sfu", "achieved": mufu / t / 1e12, "peak": mufu_peak / 1e12,
+            "unit": "Tops/s", "frac": t_mufu / t, "traffic": None}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML samples of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, device_index):
+        self.ok = False
+        self.samples = []
+        self.reasons = set()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = self._handle(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # no NVML: report it, keep timing on the device
+            self.err = str(e)
+
+    def _handle(self, idx):
+        import torch
+        pynvml = self.nv
+        try:
+            bus = torch.cuda.get_device_properties(idx).pci_bus_id
+            return pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode() if isinstance(bus, str) else bus)
+        except Exception:
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[idx]) if vis else idx
+            return pynvml.nvmlDeviceGetHandleByIndex(phys)
+
+    def _loop(self):
+        while not self.stop:
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        self.stop = False
+        if self.ok:
+            self.t = threading.Thread(target=self._loop, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self.stop = True
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": self.err}
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ arms
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "rfd" else "gloo"
+        if args.impl == "rfd":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+        pg = dist
+    elif args.impl == "rfd":
+        torch.cuda.set_device(0)
+    return rank, world, local, pg
+
+
+def max_over_ranks(val, pg):
+    if pg is None:
+        return val
+    import torch
+    t = torch.tensor([val], dtype=torch.float64, device="cuda" if pg.get_backend() == "nccl" else "cpu")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+def run_rfd(args, rank, world, local, pg):
+    import torch
+    from paper_2302_00942_b200 import rfd
+
+    p, x, F = make_config(5)
+    if rank > 0:  # each rank: its own independent cloud (weak scaling)
+        rng = np.random.default_rng(4 + 1000 * rank)
+        x = rng.random(x.shape, dtype=np.float32)
+        F = rng.standard_normal(F.shape, dtype=np.float32)
+    N, m, d = p["n"], p["m"], p["d"]
+    seed = p["seed"] + 1000 * rank
+    stream = torch.cuda.current_stream()
+    xd = torch.from_numpy(x).cuda()
+    Fd = torch.from_numpy(F).cuda()
+    outd = torch.empty_like(Fd)
+    pk = peaks()
+
+    def step():
+        plan = rfd.Plan(xd, p["eps"], p["lam"], m, seed)
+        plan.integrate(Fd, out=outd)
+        plan.close()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K full steps
+    sampler = ClockSampler(torch.cuda.current_device())
+    rfd.profile_enable(True)
+    rfd.profile_read()
+    l0 = rfd.launch_count()
+    barrier(pg)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(pg)
+    launches = rfd.launch_count() - l0
+    prof = rfd.profile_read()
+    rfd.profile_enable(False)
+    ms = ev0.elapsed_time(ev1)
+    ms_max = max_over_ranks(ms, pg)
+    ms_step = ms_max / args.steps
+
+    # ---- inference only (plan reused), same protocol
+    plan = rfd.Plan(xd, p["eps"], p["lam"], m, seed)
+    for _ in range(args.warmup):
+        plan.integrate(Fd, out=outd)
+    torch.cuda.synchronize()
+    barrier(pg)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        plan.integrate(Fd, out=outd)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ims = max_over_ranks(ev0.elapsed_time(ev1), pg) / args.steps
+    rfd.profile_enable(True)
+    rfd.profile_read()
+    for _ in range(args.steps):
+        plan.integrate(Fd, out=outd)
+    iprof = rfd.profile_read()
+    rfd.profile_enable(False)
+    plan.close()
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(x).pin_memory()
+        Fh = torch.from_numpy(F).pin_memory()
+        oh = torch.empty_like(Fh).pin_memory()
+
+        def e2e_step():
+            pl = rfd.Plan(xh, p["eps"], p["lam"], m, seed)  # H2D of the points inside
+            pl.integrate_host(Fh, oh)                        # H2D F, integrate, D2H out
+            pl.close()
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier(pg)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ems = max_over_ranks(ev0.elapsed_time(ev1), pg) / args.steps
+        e2e = {"value": N * d * world / (ems * 1e-3), "unit": UNIT,
+               "ms_per_step": ems, "h2d_bytes_per_step": int(xh.numel() * 4 + Fh.numel() * 4),
+               "d2h_bytes_per_step": int(oh.numel() * 4)}
+
+    # ---- kernels, dominant kernel roofline
+    total = sum(v[1] for v in prof.values()) or 1.0
+    kernels = {}
+    for name, (cnt, tms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        per = tms / cnt
+        kernels[name] = {"launches": cnt, "ms_per_launch": per, "share": tms / total}
+        rl = roofline_of(name, N, m, d, per, pk)
+        if rl:
+            kernels[name]["roofline_frac"] = rl["frac"]
+            kernels[name]["bound"] = rl["bound"]
+    dom = max(prof.items(), key=lambda kv: kv[1][1])[0]
+    roof = roofline_of(dom, N, m, d, prof[dom][1] / prof[dom][0], pk) or {}
+    roof = dict(roof, kernel=dom, peak_src=pk["src"])
+
+    ikern = {}
+    itotal = sum(v[1] for v in iprof.values()) or 1.0
+    for name, (cnt, tms) in iprof.items():
+        rl = roofline_of(name, N, m, d, tms / cnt, pk)
+        ikern[name] = {"ms_per_launch": tms / cnt, "share": tms / itotal,
+                       "roofline_frac": rl["frac"] if rl else None}
+    # integrate roofline (north star: slower of HBM bytes and FMA+SFU work)
+    fma_i = N * (4.0 * m * d + 6.0 * m)
+    mufu_i = 4.0 * N * m
+    byts_i = N * (24.0 + 12.0 * d)
+    clk = pk["sm_max_mhz"] * 1e6
+    t_roof = max(fma_i / (SMS * FMA_PER_CLK * clk), mufu_i / (SMS * MUFU_PER_CLK * clk),
+                 byts_i / (pk["hbm_gbs"] * 1e9))
+    integ = {"value": N * d * world / (ims * 1e-3), "unit": UNIT, "ms_per_call": ims,
+             "roofline_ms": t_roof * 1e3, "roofline_frac": t_roof / (ims * 1e-3),
+             "roofline_bound": "fp32 FMA pipe (4md+6m FMA/pt at 148x128/clk, %.0f MHz)" % pk["sm_max_mhz"],
+             "hbm_gbs_achieved": byts_i / (ims * 1e-3) / 1e9, "kernels": ikern}
+    return dict(N=N, m=m, d=d, ms_step=ms_step, launches=launches, roofline=roof,
+                kernels=kernels, integrate=integ, e2e=e2e, clocks=sampler.summary(), params=p)
+
+
+def oracle_sample(n_sample, steps=1):
+    """The oracle as it stands on a bounded sample of cfg 5 (first n_sample
+    points of the same generator recipe): plan + apply, all rows."""
+    from oracle import rfd as orf
+    p, x, F = make_config(5, n=n_sample)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        pl = orf.Plan(x, p["eps"], p["lam"], p["m"], p["seed"])
+        pl.apply(F)
+    dt = (time.perf_counter() - t0) / steps
+    return p, n_sample * p["d"] / dt, dt
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["rfd", "reference"], default="rfd")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 20)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank, world, local, pg = dist_setup(args)
+    p = make_config.__globals__["CONFIGS"][5]
+    cfg_desc = {"workload": "cfg5_cube: N=4194304 uniform unit-cube points, m=256, d=16, "
+                            "eps=0.01, lambda=-0.3 (BASELINE.json configs[4])",
+                "N": p["n"], "m": p["m"], "d": p["d"], "eps": p["eps"], "lambda": p["lam"],
+                "step": "rfd_plan_create + rfd_integrate",
+                "l2": "inputs larger than L2 (F + out = 537 MB, points 67 MB per step)"}
+
+    if args.impl == "reference":
+        # The oracle (fp64 numpy) as it stands, on host cores; rank 0 only.
+        if rank != 0:
+            return
+        ns = 65536
+        for _ in range(args.warmup):
+            oracle_sample(ns)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            oracle_sample(ns)
+        dt = (time.perf_counter() - t0) / args.steps
+        val = ns * p["d"] / dt
+        line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "impl": "reference",
+                "config": dict(cfg_desc, sample="first 65536 points of the cfg5 recipe per step"),
+                "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+                                 "sample": "cfg5 recipe, N=65536 points, m=256, d=16, plan+apply"},
+                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    res = run_rfd(args, rank, world, local, pg)
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        _, cval, cdt = oracle_sample(args.cpu_sample)
+        cpu = {"value": cval, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+               "sample": "cfg5 recipe, first %d points, m=256, d=16, plan+apply (%.1f s)"
+                         % (args.cpu_sample, cdt)}
+    value = res["N"] * res["d"] * world / (res["ms_step"] * 1e-3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic", "config": dict(cfg_desc, parallelism="dp%d (independent clouds)" % world),
+            "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
+            "gpu_launches": res["launches"], "clocks": res["clocks"],
+            "integrate": res["integrate"], "kernels": res["kernels"]}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

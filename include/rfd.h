@@ -1,0 +1,169 @@
+/*
+ * rfd.h -- C ABI of the B200-native RFDiffusion (RFD) graph-field integrator.
+ *
+ * What it computes (arXiv 2302.00942, Sec. 2.4 "RFDiffusion",
+ * lines 283-366, Eq. 13 at PAPER.md:351-358):
+ *
+ *     out = exp(lambda * W~) F,     W~ = Phi D Phi^T  (N x N, never formed)
+ *
+ * for a point cloud x_1..x_N in R^3 and a field F (N x d), where
+ *   omega_k ~ N(0, I_3) truncated to ||omega||_1 <= R = 10
+ *   nu_k    = tau(omega_k) / (m p(omega_k)),  D = diag(nu, nu)
+ *   tau(w)  = prod_c sin(2 pi eps w_c) / (pi w_c)                 (2pi-corrected)
+ *   phi(x)  = [cos 2 pi omega_k.x ; sin 2 pi omega_k.x]_{k<m}
+ * evaluated in closed form, inverse-free (reading A5):
+ *   out = F + Phi . C^ . (Phi^T F),  C^ = lambda D phi1(lambda G D),  G = Phi^T Phi.
+ *
+ * Plan creation is the paper's "pre-processing" (linear in N, cubic in m,
+ * PAPER.md:359); rfd_integrate is its "inference" (linear in N, quadratic
+ * in m).  The random stream is part of the contract (A14):
+ * frequency k, attempt a uses Philox4x32-10 with counter (k, a, 0x52464421, 0)
+ * and key (seed & 0xffffffff, seed >> 32); uniforms (w + 0.5) 2^-32;
+ * Box-Muller z0 = sqrt(-2 ln u0) cos 2pi u1, z1 = sqrt(-2 ln u0) sin 2pi u1,
+ * z2 = sqrt(-2 ln u2) cos 2pi u3; accept iff |z0|+|z1|+|z2| <= R; omega = fp32(z).
+ *
+ * Conventions for every entry point:
+ *   - Arrays are row-major fp32 unless stated; "device" pointers are CUDA
+ *     device (or managed) memory of the current device, 16-byte aligned.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is
+ *     enqueued on it; calls on one plan must be ordered on one stream.
+ *   - No exception crosses the ABI.  A non-OK status leaves a message for
+ *     rfd_last_error() (thread-local) and leaves any existing plan unchanged.
+ *   - There is no CPU fallback: every arithmetic step runs in the library's
+ *     CUDA kernels (sm_100a).  Without a usable GPU the calls return
+ *     RFD_ECUDA.
+ */
+#ifndef RFD_H_
+#define RFD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rfd_plan rfd_plan;          /* opaque; owns all derived state   */
+typedef struct CUstream_st* rfd_stream;    /* == cudaStream_t                   */
+
+typedef enum {
+  RFD_OK = 0,
+  RFD_EINVAL = 1,  /* bad argument: n<1, m<1 or m>RFD_MAX_M, d<1, batch<1,
+                      eps not finite or <= 0, lambda not finite, NULL or
+                      misaligned pointer                                       */
+  RFD_ECUDA = 2,   /* CUDA runtime error (no device, launch failure, ...)      */
+  RFD_ENOMEM = 3,  /* device allocation failed                                 */
+  RFD_ERANGE = 4   /* exp(lambda W~) overflows (e.g. lambda > 0 with large
+                      ||lambda G D||, or negative nu with lambda < 0), or the
+                      frequency sampler exhausted its 64 attempts              */
+} rfd_status;
+
+#define RFD_MAX_M 512          /* frequencies; r = 2m feature columns <= 1024 */
+#define RFD_TRUNCATION_R 10.0  /* L1 radius of the frequency proposal (A6)   */
+
+/*
+ * rfd_plan_create -- pre-processing for one point cloud.
+ *   points  N x 3 fp32, HOST or DEVICE memory (detected); copied into the
+ *           plan's own layout, so the caller may free it when this returns.
+ *   n       number of points N >= 1.
+ *   eps     epsilon-graph radius (> 0).  Enters only nu (tau).
+ *   lambda  diffusion multiplier (any finite real; exp(lambda W~)).
+ *   m       number of random frequencies, 1 <= m <= RFD_MAX_M (r = 2m).
+ *   seed    Philox key (see the stream layout above).
+ *   plan_out receives the new plan on RFD_OK (NULL otherwise).
+ * Steps: frequencies + nu (a1-a2), Gram G = Phi^T Phi (a4), core C^ (a5).
+ * Blocks the host until the plan is ready (it reads back the core's scaling
+ * exponent and an overflow flag).  Errors: EINVAL, ENOMEM, ECUDA, ERANGE.
+ */
+rfd_status rfd_plan_create(const float* points, int64_t n, double eps,
+                           double lambda, int32_t m, uint64_t seed,
+                           rfd_stream stream, rfd_plan** plan_out);
+
+/*
+ * rfd_plan_create_batched -- `batch` independent clouds of n points each,
+ * points laid out batch x n x 3.  The clouds share omega and nu (one seed)
+ * and each gets its own G_b and C^_b.  This is the repeated-application
+ * pattern of the paper's Alg. 1 over many clouds.
+ */
+rfd_status rfd_plan_create_batched(const float* points, int32_t batch,
+                                   int64_t n, double eps, double lambda,
+                                   int32_t m, uint64_t seed, rfd_stream stream,
+                                   rfd_plan** plan_out);
+
+/*
+ * rfd_integrate -- inference, Eq. 13 in bracket order:
+ *   S = Phi^T F (a6), Y = C^ S (a7), out = F + Phi Y (a8).
+ *   F    DEVICE, (batch x) N x d fp32.   out  DEVICE, same shape; may alias F.
+ *   d    field channels >= 1.
+ * Fully asynchronous on `stream`; CUDA-graph capturable once the plan's
+ * workspace has been sized for this d (any earlier call with d' >= d).
+ * Errors: EINVAL (NULL/misaligned pointers, d < 1), ENOMEM (workspace
+ * growth), ECUDA.
+ */
+rfd_status rfd_integrate(rfd_plan* plan, const float* F, int32_t d, float* out,
+                         rfd_stream stream);
+
+/*
+ * rfd_integrate_host -- the same with HOST buffers: copies F host->device,
+ * integrates, copies out device->host, all enqueued on `stream`.  With
+ * pinned host memory the call is asynchronous (synchronize `stream` before
+ * reading out); with pageable memory the copies block the host.
+ */
+rfd_status rfd_integrate_host(rfd_plan* plan, const float* F_host, int32_t d,
+                              float* out_host, rfd_stream stream);
+
+/* rfd_destroy -- frees the plan and its device memory.  NULL-safe. */
+void rfd_destroy(rfd_plan* plan);
+
+/* rfd_last_error -- message for the last non-OK status of this thread. */
+const char* rfd_last_error(void);
+
+/* Plan geometry. */
+typedef struct {
+  int64_t n;        /* points per cloud                       */
+  int32_t batch;    /* clouds                                 */
+  int32_t m;        /* frequencies                            */
+  int32_t r;        /* feature columns, 2m                    */
+  int32_t scaling;  /* squarings s used by the core           */
+  int32_t symmetric;/* 1: core via D^1/2 G D^1/2 (all nu > 0) */
+  double eps, lambda;
+  uint64_t seed;
+} rfd_plan_info_t;
+rfd_status rfd_plan_info(const rfd_plan* plan, rfd_plan_info_t* info);
+
+/*
+ * rfd_plan_export -- copy plan state to HOST memory (tests / introspection).
+ * Feature index order is the paper's: columns 0..m-1 cosines, m..2m-1 sines.
+ *   RFD_OMEGA  m x 3 fp32          RFD_NU    m fp64
+ *   RFD_GRAM   batch x r x r fp64  RFD_CORE  batch x r x r fp64
+ *   RFD_S      batch x r x d fp64  RFD_Y     batch x r x d fp32
+ *              (S, Y: from the last rfd_integrate on this plan)
+ * `bytes` must equal the field's size.  Synchronizes the device.
+ */
+typedef enum {
+  RFD_OMEGA = 0, RFD_NU = 1, RFD_GRAM = 2, RFD_CORE = 3, RFD_S = 4, RFD_Y = 5
+} rfd_field;
+rfd_status rfd_plan_export(const rfd_plan* plan, rfd_field which,
+                           void* host_dst, size_t bytes);
+
+/*
+ * Instrumentation (bench / tests).
+ *   rfd_launch_count  kernels this library has launched in this process.
+ *   rfd_profile_enable(1) brackets every subsequent launch with CUDA events
+ *     on its stream; rfd_profile_read synchronizes, then returns up to `cap`
+ *     per-kernel aggregates (name, launches, total ms) since the last
+ *     enable / read, and resets them.  Returns the number of entries.
+ */
+uint64_t rfd_launch_count(void);
+rfd_status rfd_profile_enable(int on);
+typedef struct {
+  char name[48];
+  int64_t launches;
+  double total_ms;
+} rfd_profile_entry;
+int32_t rfd_profile_read(rfd_profile_entry* entries, int32_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RFD_H_ */

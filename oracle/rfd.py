@@ -46,12 +46,15 @@ Pins (tests/test_oracle_rfd.py, tests/test_oracle_integrator.py):
     (the paper prints no values for synthetic inputs); trend test only.
 """
 
+import concurrent.futures
 import math
+import os
 
 import numpy as np
 import scipy.integrate
 import scipy.linalg
 import scipy.special
+import threadpoolctl
 
 from . import philox
 
@@ -195,15 +198,34 @@ def estimator(z, omega, eps, c_r):
 # --------------------------------------------------------------------------
 # a4, a6  sums over points
 # --------------------------------------------------------------------------
+def _chunk_sum(fn, n, chunk, init):
+    """sum_{chunks in point order} fn(start, stop).  Chunk terms may be
+    evaluated by a thread pool (numpy releases the GIL); they are added in
+    chunk order, so the result does not depend on the thread count."""
+    starts = list(range(0, n, chunk))
+    workers = min(len(starts), os.cpu_count() or 1, 8)
+    total = init
+    if workers <= 1:
+        for s in starts:
+            total = total + fn(s, min(s + chunk, n))
+        return total
+    # One BLAS thread per worker: the pool already occupies the cores.
+    with threadpoolctl.threadpool_limits(1), \
+            concurrent.futures.ThreadPoolExecutor(max_workers=workers) as ex:
+        for term in ex.map(lambda s: fn(s, min(s + chunk, n)), starts):
+            total = total + term
+    return total
+
+
 def gram(X, omega, chunk=CHUNK):
     """G = Phi^T Phi (2m x 2m): B^T A of PAPER.md:337, 355 without D."""
     X = np.asarray(X)
     r = 2 * np.asarray(omega).shape[0]
-    G = np.zeros((r, r))
-    for s in range(0, X.shape[0], chunk):
-        P = features(X[s:s + chunk], omega)
-        G += P.T @ P
-    return G
+
+    def term(s, e):
+        P = features(X[s:e], omega)
+        return P.T @ P
+    return _chunk_sum(term, X.shape[0], chunk, np.zeros((r, r)))
 
 
 def project(X, omega, F, chunk=CHUNK):
@@ -211,10 +233,10 @@ def project(X, omega, F, chunk=CHUNK):
     X = np.asarray(X)
     F = np.asarray(F, np.float64).reshape(X.shape[0], -1)
     r = 2 * np.asarray(omega).shape[0]
-    S = np.zeros((r, F.shape[1]))
-    for s in range(0, X.shape[0], chunk):
-        S += features(X[s:s + chunk], omega).T @ F[s:s + chunk]
-    return S
+
+    def term(s, e):
+        return features(X[s:e], omega).T @ F[s:e]
+    return _chunk_sum(term, X.shape[0], chunk, np.zeros((r, F.shape[1])))
 
 
 # --------------------------------------------------------------------------

@@ -1,0 +1,494 @@
+// Host side of the C ABI (include/rfd.h): argument validation, the plan
+// object (device buffers it owns), launch sequencing, status codes, launch
+// counting and event-based per-kernel timing.  No arithmetic of the method
+// runs here: every step of the path is one of the kernels in k_*.cu.  The
+// one host-computed quantity is the constant C_R = P(||Z||_1 <= R) of the
+// truncated proposal (A7), fixed by R alone.
+#include <math.h>
+#include <string.h>
+
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rfd.h"
+#include "rfd_internal.h"
+
+// ------------------------------------------------------------------ errors
+namespace {
+thread_local std::string g_last_error;
+
+rfd_status fail(rfd_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+rfd_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(e == cudaErrorMemoryAllocation ? RFD_ENOMEM : RFD_ECUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define RFD_CUDA(call)                                     \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);    \
+  } while (0)
+
+// ------------------------------------------------------------------ launches
+std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_profiling{0};
+std::mutex g_prof_mu;
+struct Pending {
+  const char* name;
+  cudaEvent_t a, b;
+};
+std::vector<Pending> g_pending;
+std::vector<cudaEvent_t> g_free_events;
+std::map<std::string, std::pair<int64_t, double>> g_prof;
+thread_local cudaEvent_t t_open_event = nullptr;
+
+cudaEvent_t take_event() {
+  if (!g_free_events.empty()) {
+    cudaEvent_t e = g_free_events.back();
+    g_free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+namespace rfd {
+void launch_begin(const char*, cudaStream_t s) {
+  if (g_profiling.load(std::memory_order_relaxed)) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    t_open_event = take_event();
+    cudaEventRecord(t_open_event, s);
+  }
+}
+void launch_end(const char* name, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (t_open_event) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t b = take_event();
+    cudaEventRecord(b, s);
+    g_pending.push_back(Pending{name, t_open_event, b});
+    t_open_event = nullptr;
+  }
+}
+}  // namespace rfd
+
+// ------------------------------------------------------------------ plan
+struct rfd_plan {
+  int device = 0;
+  int sms = 148;
+  int64_t n = 0;
+  int batch = 1;
+  int m = 0;
+  int r = 0;
+  double eps = 0, lambda = 0;
+  uint64_t seed = 0;
+  int scaling = 0;
+  int symmetric = 1;
+  rfd::PassGeom pg{};
+  // owned device state
+  float4* pts = nullptr;      // batch*n
+  float4* omega4 = nullptr;   // m
+  double* nu = nullptr;       // m
+  double* G = nullptr;        // batch*r*r (interleaved)
+  double* C = nullptr;        // batch*r*r (interleaved)
+  int* flags = nullptr;       // [0] nu/sampler flags, [2] s_max, [3] overflow
+  // integrate workspace (grows with d)
+  int ws_d = 0;
+  float* s_partial = nullptr; // batch*chunks*r*16
+  double* S = nullptr;        // batch*r*d
+  float* Y = nullptr;         // batch*r*d
+  int last_d = 0;
+  // host-buffer staging
+  float* stage = nullptr;
+  size_t stage_elems = 0;
+};
+
+namespace {
+
+double l1_ball_mass(double R) {
+  // C_R = int_0^R int_0^{R-a} h(a) h(b) erf((R-a-b)/sqrt2) db da with the
+  // half-normal density h(t) = 2 exp(-t^2/2)/sqrt(2 pi); composite 16-point
+  // Gauss-Legendre in both variables.
+  static const double xg[8] = {0.0950125098376374, 0.2816035507792589, 0.4580167776572274,
+                               0.6178762444026438, 0.7554044083550030, 0.8656312023878318,
+                               0.9445750230732326, 0.9894009349916499};
+  static const double wg[8] = {0.1894506104550685, 0.1826034150449236, 0.1691565193950025,
+                               0.1495959888165767, 0.1246289712555339, 0.0951585116824928,
+                               0.0622535239386479, 0.0271524594117541};
+  const int panels = 96;
+  auto h = [](double t) { return 2.0 * exp(-0.5 * t * t) / sqrt(2.0 * M_PI); };
+  auto inner = [&](double a) {
+    const double L = R - a;
+    double acc = 0.0;
+    for (int p = 0; p < panels; ++p) {
+      const double lo = L * p / panels, hi = L * (p + 1) / panels;
+      const double mid = 0.5 * (lo + hi), half = 0.5 * (hi - lo);
+      for (int q = 0; q < 8; ++q)
+        for (int sgn = -1; sgn <= 1; sgn += 2) {
+          const double b = mid + sgn * half * xg[q];
+          acc += half * wg[q] * h(b) * erf((R - a - b) / sqrt(2.0));
+        }
+    }
+    return acc;
+  };
+  double acc = 0.0;
+  for (int p = 0; p < panels; ++p) {
+    const double lo = R * p / panels, hi = R * (p + 1) / panels;
+    const double mid = 0.5 * (lo + hi), half = 0.5 * (hi - lo);
+    for (int q = 0; q < 8; ++q)
+      for (int sgn = -1; sgn <= 1; sgn += 2) {
+        const double a = mid + sgn * half * xg[q];
+        acc += half * wg[q] * h(a) * inner(a);
+      }
+  }
+  return acc;
+}
+
+double cached_c_r() {
+  static double c = -1.0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (c < 0) c = l1_ball_mass(RFD_TRUNCATION_R);
+  return c;
+}
+
+bool is_device_pointer(const void* p) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+void free_plan(rfd_plan* p) {
+  if (!p) return;
+  cudaFree(p->pts);
+  cudaFree(p->omega4);
+  cudaFree(p->nu);
+  cudaFree(p->G);
+  cudaFree(p->C);
+  cudaFree(p->flags);
+  cudaFree(p->s_partial);
+  cudaFree(p->S);
+  cudaFree(p->Y);
+  cudaFree(p->stage);
+  delete p;
+}
+
+template <typename T>
+cudaError_t dalloc(T** ptr, size_t count) {
+  return cudaMalloc(reinterpret_cast<void**>(ptr), count * sizeof(T) + 16);
+}
+
+struct TempBuffers {
+  std::vector<void*> bufs;
+  ~TempBuffers() {
+    for (void* b : bufs) cudaFree(b);
+  }
+  template <typename T>
+  cudaError_t alloc(T** ptr, size_t count) {
+    cudaError_t e = dalloc(ptr, count);
+    if (e == cudaSuccess) bufs.push_back(*ptr);
+    return e;
+  }
+};
+
+rfd_status create_impl(const float* points, int batch, int64_t n, double eps, double lambda,
+                       int m, uint64_t seed, cudaStream_t st, rfd_plan** plan_out) {
+  if (!plan_out) return fail(RFD_EINVAL, "plan_out is NULL");
+  *plan_out = nullptr;
+  if (!points) return fail(RFD_EINVAL, "points is NULL");
+  if (n < 1) return fail(RFD_EINVAL, "n must be >= 1");
+  if (batch < 1) return fail(RFD_EINVAL, "batch must be >= 1");
+  if (m < 1 || m > RFD_MAX_M) return fail(RFD_EINVAL, "m must be in [1, RFD_MAX_M]");
+  if (!(eps > 0.0) || !isfinite(eps)) return fail(RFD_EINVAL, "eps must be finite and > 0");
+  if (!isfinite(lambda)) return fail(RFD_EINVAL, "lambda must be finite");
+  if (reinterpret_cast<uintptr_t>(points) % 4 != 0)
+    return fail(RFD_EINVAL, "points must be 4-byte aligned");
+
+  int dev = 0;
+  RFD_CUDA(cudaGetDevice(&dev));
+  rfd_plan* p = new rfd_plan();
+  struct Guard {
+    rfd_plan* p;
+    bool keep = false;
+    ~Guard() {
+      if (!keep) free_plan(p);
+    }
+  } guard{p};
+  p->device = dev;
+  RFD_CUDA(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, dev));
+  p->n = n;
+  p->batch = batch;
+  p->m = m;
+  p->r = 2 * m;
+  p->eps = eps;
+  p->lambda = lambda;
+  p->seed = seed;
+  const int64_t total = n * batch;
+  const size_t rr = size_t(p->r) * p->r;
+
+  RFD_CUDA(dalloc(&p->pts, size_t(total)));
+  RFD_CUDA(dalloc(&p->omega4, size_t(m)));
+  RFD_CUDA(dalloc(&p->nu, size_t(m)));
+  RFD_CUDA(dalloc(&p->G, rr * batch));
+  RFD_CUDA(dalloc(&p->C, rr * batch));
+  RFD_CUDA(dalloc(&p->flags, size_t(4)));
+  RFD_CUDA(cudaMemsetAsync(p->flags, 0, 4 * sizeof(int), st));
+
+  TempBuffers tmp;
+  const float* dev_xyz = points;
+  if (!is_device_pointer(points)) {
+    float* staged = nullptr;
+    RFD_CUDA(tmp.alloc(&staged, size_t(total) * 3));
+    RFD_CUDA(cudaMemcpyAsync(staged, points, size_t(total) * 3 * sizeof(float),
+                             cudaMemcpyHostToDevice, st));
+    dev_xyz = staged;
+  }
+  rfd::launch_pack_points(dev_xyz, p->pts, total, st);
+  rfd::launch_freq(p->omega4, p->nu, p->flags, m, seed, eps, RFD_TRUNCATION_R, cached_c_r(), st);
+
+  // a4: Gram.
+  const rfd::GramGeom gg = rfd::gram_geometry(m, n, batch, p->sms);
+  float* gpart = nullptr;
+  RFD_CUDA(tmp.alloc(&gpart, rfd::gram_partial_elems(gg, batch)));
+  rfd::launch_gram(p->pts, p->omega4, m, n, batch, gg, gpart, p->G, st);
+
+  // a5: core, scaling exponent first.
+  double *Z = nullptr, *P0 = nullptr, *P1 = nullptr, *E0 = nullptr, *E1 = nullptr;
+  RFD_CUDA(tmp.alloc(&Z, rr * batch));
+  RFD_CUDA(tmp.alloc(&P0, rr * batch));
+  RFD_CUDA(tmp.alloc(&P1, rr * batch));
+  RFD_CUDA(tmp.alloc(&E0, rr * batch));
+  RFD_CUDA(tmp.alloc(&E1, rr * batch));
+  rfd::launch_core_prep(p->G, p->nu, p->flags, lambda, m, batch, Z, p->flags + 2, st);
+  RFD_CUDA(cudaGetLastError());
+  int hflags[4] = {0, 0, 0, 0};
+  RFD_CUDA(cudaMemcpyAsync(hflags, p->flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
+  RFD_CUDA(cudaStreamSynchronize(st));
+  if (hflags[0] & 2)
+    return fail(RFD_ERANGE, "frequency sampler exhausted its attempts (R too small?)");
+  if (hflags[2] > 200) return fail(RFD_ERANGE, "core: ||lambda G D|| is not finite or too large");
+  p->symmetric = (hflags[0] & 1) ? 0 : 1;
+  p->scaling = hflags[2];
+  rfd::launch_core_eval(Z, p->nu, p->flags, lambda, m, batch, p->scaling, P0, P1, E0, E1, p->C,
+                        p->flags + 3, st);
+  RFD_CUDA(cudaGetLastError());
+  RFD_CUDA(cudaMemcpyAsync(hflags, p->flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
+  RFD_CUDA(cudaStreamSynchronize(st));
+  if (hflags[3])
+    return fail(RFD_ERANGE, "core: exp(lambda W~) overflows (lambda > 0 or negative nu)");
+
+  p->pg = rfd::pass_geometry(m, n, batch, p->sms);
+  guard.keep = true;
+  *plan_out = p;
+  return RFD_OK;
+}
+
+rfd_status ensure_workspace(rfd_plan* p, int d) {
+  if (p->ws_d >= d) return RFD_OK;
+  cudaFree(p->s_partial);
+  cudaFree(p->S);
+  cudaFree(p->Y);
+  p->s_partial = nullptr;
+  p->S = nullptr;
+  p->Y = nullptr;
+  p->ws_d = 0;
+  const size_t part = size_t(p->batch) * p->pg.chunks * p->r * 16;
+  RFD_CUDA(dalloc(&p->s_partial, part));
+  RFD_CUDA(dalloc(&p->S, size_t(p->batch) * p->r * d));
+  RFD_CUDA(dalloc(&p->Y, size_t(p->batch) * p->r * d));
+  p->ws_d = d;
+  return RFD_OK;
+}
+
+rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaStream_t st) {
+  if (!p) return fail(RFD_EINVAL, "plan is NULL");
+  if (!F || !out) return fail(RFD_EINVAL, "F/out is NULL");
+  if (d < 1) return fail(RFD_EINVAL, "d must be >= 1");
+  if (reinterpret_cast<uintptr_t>(F) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0)
+    return fail(RFD_EINVAL, "F/out must be 16-byte aligned");
+  rfd_status rs = ensure_workspace(p, d);
+  if (rs != RFD_OK) return rs;
+  for (int c0 = 0; c0 < d; c0 += 16) {
+    const int dc = (d - c0 < 16) ? d - c0 : 16;
+    rfd::launch_pass1(p->pts, p->omega4, p->m, p->n, p->batch, p->pg, F, d, c0, dc, p->s_partial,
+                      st);
+    rfd::launch_reduce_S(p->s_partial, p->m, p->batch, p->pg.chunks, d, c0, dc, p->S, st);
+  }
+  rfd::launch_core_apply(p->C, p->S, p->m, p->batch, d, p->Y, st);
+  for (int c0 = 0; c0 < d; c0 += 16) {
+    const int dc = (d - c0 < 16) ? d - c0 : 16;
+    rfd::launch_pass2(p->pts, p->omega4, p->m, p->n, p->batch, p->pg, p->Y, F, out, d, c0, dc,
+                      st);
+  }
+  RFD_CUDA(cudaGetLastError());
+  p->last_d = d;
+  return RFD_OK;
+}
+
+// interleaved feature index (2k + t) for the paper's blocked index (t m + k)
+inline int interleaved(int a, int m) { return a < m ? 2 * a : 2 * (a - m) + 1; }
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+rfd_status rfd_plan_create(const float* points, int64_t n, double eps, double lambda, int32_t m,
+                           uint64_t seed, rfd_stream stream, rfd_plan** plan_out) {
+  return create_impl(points, 1, n, eps, lambda, m, seed, reinterpret_cast<cudaStream_t>(stream),
+                     plan_out);
+}
+
+rfd_status rfd_plan_create_batched(const float* points, int32_t batch, int64_t n, double eps,
+                                   double lambda, int32_t m, uint64_t seed, rfd_stream stream,
+                                   rfd_plan** plan_out) {
+  return create_impl(points, batch, n, eps, lambda, m, seed,
+                     reinterpret_cast<cudaStream_t>(stream), plan_out);
+}
+
+rfd_status rfd_integrate(rfd_plan* plan, const float* F, int32_t d, float* out,
+                         rfd_stream stream) {
+  return integrate_impl(plan, F, d, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+rfd_status rfd_integrate_host(rfd_plan* plan, const float* F_host, int32_t d, float* out_host,
+                              rfd_stream stream) {
+  if (!plan) return fail(RFD_EINVAL, "plan is NULL");
+  if (!F_host || !out_host) return fail(RFD_EINVAL, "F/out is NULL");
+  if (d < 1) return fail(RFD_EINVAL, "d must be >= 1");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t elems = size_t(plan->batch) * plan->n * d;
+  if (plan->stage_elems < elems) {
+    cudaFree(plan->stage);
+    plan->stage = nullptr;
+    plan->stage_elems = 0;
+    RFD_CUDA(dalloc(&plan->stage, elems));
+    plan->stage_elems = elems;
+  }
+  RFD_CUDA(cudaMemcpyAsync(plan->stage, F_host, elems * sizeof(float), cudaMemcpyHostToDevice, st));
+  rfd_status rs = integrate_impl(plan, plan->stage, d, plan->stage, st);
+  if (rs != RFD_OK) return rs;
+  RFD_CUDA(cudaMemcpyAsync(out_host, plan->stage, elems * sizeof(float), cudaMemcpyDeviceToHost, st));
+  return RFD_OK;
+}
+
+void rfd_destroy(rfd_plan* plan) { free_plan(plan); }
+
+const char* rfd_last_error(void) { return g_last_error.c_str(); }
+
+rfd_status rfd_plan_info(const rfd_plan* p, rfd_plan_info_t* info) {
+  if (!p || !info) return fail(RFD_EINVAL, "NULL argument");
+  info->n = p->n;
+  info->batch = p->batch;
+  info->m = p->m;
+  info->r = p->r;
+  info->scaling = p->scaling;
+  info->symmetric = p->symmetric;
+  info->eps = p->eps;
+  info->lambda = p->lambda;
+  info->seed = p->seed;
+  return RFD_OK;
+}
+
+rfd_status rfd_plan_export(const rfd_plan* p, rfd_field which, void* host_dst, size_t bytes) {
+  if (!p || !host_dst) return fail(RFD_EINVAL, "NULL argument");
+  const int m = p->m, r = p->r, B = p->batch, d = p->last_d;
+  RFD_CUDA(cudaDeviceSynchronize());
+  switch (which) {
+    case RFD_OMEGA: {
+      if (bytes != size_t(m) * 3 * sizeof(float)) return fail(RFD_EINVAL, "size mismatch");
+      std::vector<float4> w(m);
+      RFD_CUDA(cudaMemcpy(w.data(), p->omega4, m * sizeof(float4), cudaMemcpyDeviceToHost));
+      float* o = static_cast<float*>(host_dst);
+      for (int k = 0; k < m; ++k) {
+        o[3 * k] = w[k].x;
+        o[3 * k + 1] = w[k].y;
+        o[3 * k + 2] = w[k].z;
+      }
+      return RFD_OK;
+    }
+    case RFD_NU:
+      if (bytes != size_t(m) * sizeof(double)) return fail(RFD_EINVAL, "size mismatch");
+      RFD_CUDA(cudaMemcpy(host_dst, p->nu, bytes, cudaMemcpyDeviceToHost));
+      return RFD_OK;
+    case RFD_GRAM:
+    case RFD_CORE: {
+      const size_t cnt = size_t(B) * r * r;
+      if (bytes != cnt * sizeof(double)) return fail(RFD_EINVAL, "size mismatch");
+      std::vector<double> tmp(cnt);
+      RFD_CUDA(cudaMemcpy(tmp.data(), which == RFD_GRAM ? p->G : p->C, bytes,
+                          cudaMemcpyDeviceToHost));
+      double* o = static_cast<double*>(host_dst);
+      for (int b = 0; b < B; ++b)
+        for (int a = 0; a < r; ++a)
+          for (int c = 0; c < r; ++c)
+            o[(size_t(b) * r + a) * r + c] =
+                tmp[(size_t(b) * r + interleaved(a, m)) * r + interleaved(c, m)];
+      return RFD_OK;
+    }
+    case RFD_S:
+    case RFD_Y: {
+      if (d < 1) return fail(RFD_EINVAL, "no integrate has run on this plan");
+      const size_t cnt = size_t(B) * r * d;
+      const size_t es = which == RFD_S ? sizeof(double) : sizeof(float);
+      if (bytes != cnt * es) return fail(RFD_EINVAL, "size mismatch");
+      std::vector<unsigned char> tmp(cnt * es);
+      RFD_CUDA(cudaMemcpy(tmp.data(), which == RFD_S ? static_cast<void*>(p->S) : p->Y, bytes,
+                          cudaMemcpyDeviceToHost));
+      unsigned char* o = static_cast<unsigned char*>(host_dst);
+      for (int b = 0; b < B; ++b)
+        for (int a = 0; a < r; ++a)
+          memcpy(o + ((size_t(b) * r + a) * d) * es,
+                 tmp.data() + ((size_t(b) * r + interleaved(a, m)) * d) * es, d * es);
+      return RFD_OK;
+    }
+  }
+  return fail(RFD_EINVAL, "unknown field");
+}
+
+uint64_t rfd_launch_count(void) { return g_launches.load(); }
+
+rfd_status rfd_profile_enable(int on) {
+  g_profiling.store(on ? 1 : 0);
+  return RFD_OK;
+}
+
+int32_t rfd_profile_read(rfd_profile_entry* entries, int32_t cap) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (const Pending& pe : g_pending) {
+    float ms = 0.0f;
+    cudaEventSynchronize(pe.b);
+    cudaEventElapsedTime(&ms, pe.a, pe.b);
+    auto& agg = g_prof[pe.name];
+    agg.first += 1;
+    agg.second += ms;
+    g_free_events.push_back(pe.a);
+    g_free_events.push_back(pe.b);
+  }
+  g_pending.clear();
+  int32_t i = 0;
+  for (const auto& kv : g_prof) {
+    if (i >= cap || !entries) break;
+    strncpy(entries[i].name, kv.first.c_str(), sizeof(entries[i].name) - 1);
+    entries[i].name[sizeof(entries[i].name) - 1] = '\0';
+    entries[i].launches = kv.second.first;
+    entries[i].total_ms = kv.second.second;
+    ++i;
+  }
+  g_prof.clear();
+  return i;
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// Internal declarations shared by the host plan object and the kernels.
+//
+// Internal feature layout ("interleaved"): feature 2k is cos(2 pi omega_k.x),
+// feature 2k+1 is sin(2 pi omega_k.x).  G, C^, S and Y are stored in this
+// order on the device; rfd_plan_export permutes to the paper's
+// [cos block; sin block] order.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rfd {
+
+constexpr uint32_t kFreqTag = 0x52464421u;  // counter word 2 (A14)
+constexpr int kMaxAttempts = 64;
+
+// ---------------------------------------------------------------- launching
+// Every kernel launch goes through launch_begin/launch_end so that the
+// library can count launches and (optionally) time them with events.
+void launch_begin(const char* name, cudaStream_t s);
+void launch_end(const char* name, cudaStream_t s);
+
+struct LaunchScope {
+  const char* name;
+  cudaStream_t s;
+  LaunchScope(const char* n, cudaStream_t st) : name(n), s(st) { launch_begin(n, st); }
+  ~LaunchScope() { launch_end(name, s); }
+};
+
+// ---------------------------------------------------------------- K0 freq
+// omega4[k] = (wx, wy, wz, 0) fp32, nu[k] fp64; flags[0] |= 1 if some nu <= 0,
+// flags[0] |= 2 if the sampler ran out of attempts.
+void launch_freq(float4* omega4, double* nu, int* flags, int m, uint64_t seed,
+                 double eps, double R, double c_r, cudaStream_t s);
+
+// ---------------------------------------------------------------- pack
+void launch_pack_points(const float* xyz, float4* pts, int64_t total, cudaStream_t s);
+
+// ---------------------------------------------------------------- Gram
+struct GramGeom {
+  int r;          // 2m
+  int tile;       // 64 or 128
+  int tiles1d;    // ceil(r / tile)
+  int ntiles;     // upper-triangle tiles
+  int chunks;     // point chunks per cloud
+  int64_t chunk;  // points per chunk (multiple of 16)
+};
+GramGeom gram_geometry(int m, int64_t n, int batch, int sms);
+size_t gram_partial_elems(const GramGeom& g, int batch);
+void launch_gram(const float4* pts, const float4* omega4, int m, int64_t n,
+                 int batch, const GramGeom& g, float* partial, double* G,
+                 cudaStream_t s);
+
+// ---------------------------------------------------------------- core
+// Z_b = lambda D^1/2 G D^1/2 (symmetric route) or lambda G D; writes the
+// 1-norm based scaling exponent to *smax (atomicMax over the batch).
+void launch_core_prep(const double* G, const double* nu, const int* flags,
+                      double lambda, int m, int batch, double* Z, int* smax,
+                      cudaStream_t s);
+// Taylor (degree kTaylor) of phi1 and exp at Z / 2^s, then s doublings,
+// then C^ = lambda D^1/2 P D^1/2 (or lambda D P); flags[1] = 1 on overflow.
+void launch_core_eval(const double* Z, const double* nu, const int* flags,
+                      double lambda, int m, int batch, int s_scale,
+                      double* P0, double* P1, double* E0, double* E1,
+                      double* C, int* oflag, cudaStream_t s);
+
+// ---------------------------------------------------------------- passes
+struct PassGeom {
+  int fblocks;    // ceil(m / 32)
+  int chunks;     // pass-1 point chunks per cloud
+  int64_t chunk;  // points per pass-1 chunk
+  int p2_blocks;  // pass-2 persistent grid size
+};
+PassGeom pass_geometry(int m, int64_t n, int batch, int sms);
+// Partial S for columns [c0, c0 + dc) of F (row stride d):
+// partial[b][chunk][2m][dc] fp32 (interleaved features).
+void launch_pass1(const float4* pts, const float4* omega4, int m, int64_t n,
+                  int batch, const PassGeom& g, const float* F, int d, int c0,
+                  int dc, float* partial, cudaStream_t s);
+// S[b][2m][d] fp64 += fixed-order sum of the chunk partials of columns
+// [c0, c0+dc); then (after all chunks) Y = C^ S in fp32.
+void launch_reduce_S(const float* partial, int m, int batch, int chunks,
+                     int d, int c0, int dc, double* S, cudaStream_t s);
+void launch_core_apply(const double* C, const double* S, int m, int batch,
+                       int d, float* Y, cudaStream_t s);
+void launch_pass2(const float4* pts, const float4* omega4, int m, int64_t n,
+                  int batch, const PassGeom& g, const float* Y, const float* F,
+                  float* out, int d, int c0, int dc, cudaStream_t s);
+
+}  // namespace rfd

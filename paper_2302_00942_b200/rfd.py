@@ -1,0 +1,239 @@
+"""Thin ctypes binding of the C ABI in ``include/rfd.h`` (argument marshalling only).
+
+Every step of the method runs in the CUDA kernels of ``lib/librfd.so``; this
+module only turns torch tensors / numpy arrays into pointers, streams and
+sizes, and status codes into exceptions.  There is no fallback: if the
+library is missing, importing the binding's entry points raises.
+
+Names follow the ABI: ``Plan`` wraps ``rfd_plan_create`` /
+``rfd_plan_create_batched`` / ``rfd_destroy``; ``Plan.integrate`` wraps
+``rfd_integrate``; ``Plan.integrate_host`` wraps ``rfd_integrate_host``.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "librfd.so")
+
+RFD_OK, RFD_EINVAL, RFD_ECUDA, RFD_ENOMEM, RFD_ERANGE = range(5)
+RFD_MAX_M = 512
+FIELDS = {"omega": 0, "nu": 1, "gram": 2, "core": 3, "S": 4, "Y": 5}
+
+# Every symbol include/rfd.h declares (checked by tests/test_abi.py).
+EXPORTED = ("rfd_plan_create", "rfd_plan_create_batched", "rfd_integrate",
+            "rfd_integrate_host", "rfd_destroy", "rfd_last_error", "rfd_plan_info",
+            "rfd_plan_export", "rfd_launch_count", "rfd_profile_enable",
+            "rfd_profile_read")
+
+
+class RFDError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("rfd status %d: %s" % (status, msg))
+        self.status = status
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("batch", ctypes.c_int32), ("m", ctypes.c_int32),
+                ("r", ctypes.c_int32), ("scaling", ctypes.c_int32),
+                ("symmetric", ctypes.c_int32), ("eps", ctypes.c_double),
+                ("lam", ctypes.c_double), ("seed", ctypes.c_uint64)]
+
+
+class ProfileEntry(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 48), ("launches", ctypes.c_int64),
+                ("total_ms", ctypes.c_double)]
+
+
+_lib = None
+
+
+def load_library(path=LIB_PATH):
+    """Load librfd.so (raises if it has not been built: no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError("librfd.so not built at %s; run `python -m "
+                           "paper_2302_00942_b200.build` (there is no CPU fallback)" % path)
+    lib = ctypes.CDLL(path)
+    vp, i64, i32, dbl, u64 = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                              ctypes.c_double, ctypes.c_uint64)
+    pp = ctypes.POINTER(ctypes.c_void_p)
+    lib.rfd_plan_create.argtypes = [vp, i64, dbl, dbl, i32, u64, vp, pp]
+    lib.rfd_plan_create_batched.argtypes = [vp, i32, i64, dbl, dbl, i32, u64, vp, pp]
+    lib.rfd_integrate.argtypes = [vp, vp, i32, vp, vp]
+    lib.rfd_integrate_host.argtypes = [vp, vp, i32, vp, vp]
+    lib.rfd_destroy.argtypes = [vp]
+    lib.rfd_destroy.restype = None
+    lib.rfd_last_error.restype = ctypes.c_char_p
+    lib.rfd_plan_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
+    lib.rfd_plan_export.argtypes = [vp, ctypes.c_int, vp, ctypes.c_size_t]
+    lib.rfd_launch_count.restype = ctypes.c_uint64
+    lib.rfd_profile_enable.argtypes = [ctypes.c_int]
+    lib.rfd_profile_read.argtypes = [ctypes.POINTER(ProfileEntry), i32]
+    lib.rfd_profile_read.restype = i32
+    for name in ("rfd_plan_create", "rfd_plan_create_batched", "rfd_integrate",
+                 "rfd_integrate_host", "rfd_plan_info", "rfd_plan_export",
+                 "rfd_profile_enable"):
+        getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(status):
+    if status != RFD_OK:
+        raise RFDError(status, load_library().rfd_last_error().decode())
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(a):
+    """Data pointer of a contiguous torch tensor or numpy array."""
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return ctypes.c_void_p(a.ctypes.data)
+    if not a.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return ctypes.c_void_p(a.data_ptr())
+
+
+def _check_f32(a, name):
+    dt = a.dtype
+    ok = (dt == np.float32) if isinstance(a, np.ndarray) else (str(dt) == "torch.float32")
+    if not ok:
+        raise TypeError("%s must be float32" % name)
+
+
+class Plan:
+    """An RFD plan: omega, nu, G and the core C^ for one cloud or a batch.
+
+    ``points``: (N, 3) or, batched, (B, N, 3) float32 -- a CUDA tensor or a
+    host tensor / numpy array (the library copies it).
+    """
+
+    def __init__(self, points, eps, lam, m, seed, stream=None):
+        lib = load_library()
+        _check_f32(points, "points")
+        shape = tuple(points.shape)
+        self._keep = points
+        handle = ctypes.c_void_p()
+        s = _stream_handle(stream)
+        if len(shape) == 2 and shape[1] == 3:
+            self.batch, self.n = 1, shape[0]
+            st = lib.rfd_plan_create(_ptr(points), self.n, float(eps), float(lam), int(m),
+                                     int(seed), s, ctypes.byref(handle))
+        elif len(shape) == 3 and shape[2] == 3:
+            self.batch, self.n = shape[0], shape[1]
+            st = lib.rfd_plan_create_batched(_ptr(points), self.batch, self.n, float(eps),
+                                             float(lam), int(m), int(seed), s,
+                                             ctypes.byref(handle))
+        else:
+            raise ValueError("points must be (N, 3) or (B, N, 3)")
+        _check(st)
+        self._h = handle
+        self.m, self.r = int(m), 2 * int(m)
+        self.eps, self.lam, self.seed = float(eps), float(lam), int(seed)
+        self._keep = None
+
+    # -- lifecycle ---------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load_library().rfd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- inference -----------------------------------------------------------
+    def _field_dims(self, F):
+        shape = tuple(F.shape)
+        lead = (self.batch, self.n) if self.batch > 1 else (self.n,)
+        if shape[:len(lead)] != lead or len(shape) > len(lead) + 1:
+            raise ValueError("F must have shape %s or %s + (d,)" % (lead, lead))
+        return 1 if len(shape) == len(lead) else shape[-1]
+
+    def integrate(self, F, out=None, stream=None):
+        """out = exp(lambda W~) F for a CUDA float32 tensor F ((B,) N[, d]).
+
+        ``out`` may be F itself (in place).  Asynchronous on ``stream``.
+        """
+        import torch
+        _check_f32(F, "F")
+        if not F.is_cuda:
+            raise ValueError("F must be a CUDA tensor (use integrate_host for host buffers)")
+        d = self._field_dims(F)
+        if out is None:
+            out = torch.empty_like(F)
+        elif out.shape != F.shape or not out.is_cuda:
+            raise ValueError("out must be a CUDA tensor shaped like F")
+        _check(load_library().rfd_integrate(self._h, _ptr(F), d, _ptr(out),
+                                            _stream_handle(stream)))
+        return out
+
+    def integrate_host(self, F_host, out_host, stream=None):
+        """Same with HOST buffers (pinned for asynchrony): H2D, integrate, D2H."""
+        _check_f32(F_host, "F")
+        _check_f32(out_host, "out")
+        d = self._field_dims(F_host)
+        _check(load_library().rfd_integrate_host(self._h, _ptr(F_host), d, _ptr(out_host),
+                                                 _stream_handle(stream)))
+        return out_host
+
+    # -- introspection -------------------------------------------------------
+    def info(self):
+        inf = PlanInfo()
+        _check(load_library().rfd_plan_info(self._h, ctypes.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in PlanInfo._fields_}
+
+    def export(self, field, d=None):
+        """Copy plan state to host numpy (paper's [cos; sin] feature order)."""
+        B, m, r = self.batch, self.m, self.r
+        if field == "omega":
+            arr = np.empty((m, 3), np.float32)
+        elif field == "nu":
+            arr = np.empty((m,), np.float64)
+        elif field in ("gram", "core"):
+            arr = np.empty((B, r, r), np.float64)
+        elif field in ("S", "Y"):
+            if d is None:
+                raise ValueError("pass d (the d of the last integrate)")
+            arr = np.empty((B, r, d), np.float64 if field == "S" else np.float32)
+        else:
+            raise ValueError("unknown field %r" % field)
+        _check(load_library().rfd_plan_export(self._h, FIELDS[field], _ptr(arr), arr.nbytes))
+        if field in ("gram", "core", "S", "Y") and B == 1:
+            arr = arr[0]
+        return arr
+
+
+def launch_count():
+    return int(load_library().rfd_launch_count())
+
+
+def profile_enable(on=True):
+    _check(load_library().rfd_profile_enable(1 if on else 0))
+
+
+def profile_read(cap=64):
+    """{kernel name: (launches, total_ms)} since the last enable/read (synchronizes)."""
+    arr = (ProfileEntry * cap)()
+    k = load_library().rfd_profile_read(arr, cap)
+    return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms)) for i in range(k)}

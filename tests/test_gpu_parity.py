@@ -1,0 +1,242 @@
+"""CUDA path vs the fp64 oracle, through the C ABI (needs a B200).
+
+Tolerance (BASELINE.json north star; A13): normwise
+    max_{i,c} |out_gpu - out_ref| / max_{i,c} |out_ref| <= 1e-4,
+and the same gate on the correction Delta = out - F, which is only 0.5-1.2 %
+of max|out| on the random-field configs and would otherwise be invisible.
+Intermediates (G, C^, S, Y) are compared normwise against their own max-abs.
+omega is compared bit for bit (the stream is part of the contract, A14).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import rfd as orf  # noqa: E402
+from paper_2302_00942_b200 import rfd  # noqa: E402
+from workloads import make_config  # noqa: E402
+
+TOL = 1e-4
+
+
+def relerr(got, ref):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.abs(got - ref).max() / np.abs(ref).max())
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rfd.load_library()
+
+
+def _run_single(x, F, p):
+    xd = torch.from_numpy(x).cuda()
+    Fd = torch.from_numpy(np.ascontiguousarray(F)).cuda()
+    plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
+    out = plan.integrate(Fd).cpu().numpy()
+    return plan, out
+
+
+def _check_against_oracle(plan, out, x, F, p, rows=None, d=None):
+    ref = orf.Plan(x, p["eps"], p["lam"], p["m"], p["seed"])
+    omega = plan.export("omega")
+    np.testing.assert_array_equal(omega, ref.omega)
+    np.testing.assert_allclose(plan.export("nu"), ref.nu, rtol=1e-12)
+    errs = {"G": relerr(plan.export("gram"), ref.G), "C": relerr(plan.export("core"), ref.C)}
+    res = ref.apply(F, rows=rows)
+    d = F.reshape(F.shape[0], -1).shape[1]
+    errs["S"] = relerr(plan.export("S", d=d), res["S"])
+    errs["Y"] = relerr(plan.export("Y", d=d), res["Y"])
+    F2 = F.reshape(F.shape[0], -1).astype(np.float64)
+    o2 = out.reshape(out.shape[0], -1)
+    if rows is not None:
+        F2, o2 = F2[rows], o2[rows]
+    errs["out"] = relerr(o2, res["out"])
+    errs["delta"] = relerr(o2 - F2, res["out"] - F2)
+    print(p["name"], {k: "%.2e" % v for k, v in errs.items()})
+    for k, v in errs.items():
+        assert v <= TOL, (k, v)
+    return errs
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_config_parity(cfg):
+    p, x, F = make_config(cfg)
+    plan, out = _run_single(x, F, p)
+    _check_against_oracle(plan, out, x, F, p)
+
+
+@pytest.mark.slow
+def test_config5_full_size_parity():
+    # Full N = 4M, m = 256, d = 16, in the launch configuration bench.py times;
+    # out compared on 4096 sampled rows (every row still enters G and S).
+    p, x, F = make_config(5)
+    plan, out = _run_single(x, F, p)
+    rows = np.arange(0, x.shape[0], 1024)
+    rows = np.concatenate([rows, [x.shape[0] - 1]])
+    _check_against_oracle(plan, out, x, F, p, rows=rows)
+
+
+def test_config3_batched_fifty_applications():
+    p, x, V = make_config(3)
+    B, n, A = p["clouds"], p["n"], p["applications"]
+    xd = torch.from_numpy(x).cuda()
+    plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
+    Vd = torch.from_numpy(V).cuda()  # (A, B, n, 1)
+    outs = torch.empty_like(Vd)
+    for t in range(A):
+        plan.integrate(Vd[t], out=outs[t])
+    outs = outs.cpu().numpy()
+    G = plan.export("gram")
+    C = plan.export("core")
+    worst = {"out": 0.0, "delta": 0.0, "G": 0.0, "C": 0.0}
+    for b in range(B):
+        ref = orf.Plan(x[b], p["eps"], p["lam"], p["m"], p["seed"])
+        # The integrator is linear in F: the 50 applications of cloud b are the
+        # 50 columns of one oracle apply.
+        Fb = V[:, b, :, 0].T.astype(np.float64)
+        res = ref.apply(Fb)
+        ob = outs[:, b, :, 0].T
+        for t in range(A):
+            worst["out"] = max(worst["out"], relerr(ob[:, t], res["out"][:, t]))
+            worst["delta"] = max(worst["delta"], relerr(ob[:, t] - Fb[:, t], res["out"][:, t] - Fb[:, t]))
+        worst["G"] = max(worst["G"], relerr(G[b], ref.G))
+        worst["C"] = max(worst["C"], relerr(C[b], ref.C))
+    print("cfg3", {k: "%.2e" % v for k, v in worst.items()})
+    for k, v in worst.items():
+        assert v <= TOL, (k, v)
+
+
+def test_omega_bitwise_all_seeds():
+    for cfg in (1, 2, 3, 4, 5):
+        p, x, _ = make_config(cfg) if cfg != 5 else make_config(5, n=1024)
+        xs = x.reshape(-1, 3)[:64].copy()
+        plan = rfd.Plan(torch.from_numpy(xs).cuda(), p["eps"], p["lam"], p["m"], p["seed"])
+        om, _ = orf.frequencies(p["seed"], p["m"])
+        np.testing.assert_array_equal(plan.export("omega"), om)
+        assert plan.info()["symmetric"] == 1
+
+
+# ---------------------------------------------------------------- edge cases
+def _sphere(n, seed):
+    g = np.random.default_rng(seed).standard_normal((n, 3))
+    return (g / np.linalg.norm(g, axis=1, keepdims=True)).astype(np.float32)
+
+
+@pytest.mark.parametrize("n,m,d", [(1, 16, 3), (2, 8, 1), (37, 1, 2), (1000, 40, 5),
+                                   (4099, 33, 20), (3001, 512, 4), (70001, 96, 37),
+                                   (12345, 128, 16)])
+def test_ragged_shapes_parity(n, m, d):
+    x = _sphere(n, n + m)
+    F = np.random.default_rng(d).standard_normal((n, d)).astype(np.float32)
+    p = dict(name="ragged n=%d m=%d d=%d" % (n, m, d), eps=0.2, lam=-0.8, m=m, seed=11)
+    plan, out = _run_single(x, F, p)
+    _check_against_oracle(plan, out, x, F, p)
+
+
+def test_single_point_closed_form():
+    x = np.array([[0.3, -0.2, 0.9]], np.float32)
+    F = np.array([[1.5, -2.0, 0.25, 4.0]], np.float32)
+    plan, out = _run_single(x, F, dict(eps=0.1, lam=-0.6, m=16, seed=0))
+    s = plan.export("nu").sum()
+    np.testing.assert_allclose(out, math.exp(-0.6 * s) * F, rtol=2e-6)
+
+
+def test_two_coincident_points_closed_form():
+    x = np.array([[0.1, 0.2, 0.3], [0.1, 0.2, 0.3]], np.float32)
+    F = np.array([[1.0, 2.0], [-3.0, 0.5]], np.float32)
+    plan, out = _run_single(x, F, dict(eps=0.15, lam=-0.4, m=16, seed=1))
+    s = plan.export("nu").sum()
+    ref = F + 0.5 * math.expm1(2 * -0.4 * s) * np.ones((2, 2)) @ F
+    np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-6)
+
+
+def test_lambda_zero_is_exact_identity():
+    x = _sphere(5000, 3)
+    F = np.random.default_rng(0).standard_normal((5000, 3)).astype(np.float32)
+    _, out = _run_single(x, F, dict(eps=0.1, lam=0.0, m=64, seed=2))
+    np.testing.assert_array_equal(out, F)
+
+
+def test_properties_determinism_inplace_linearity_symmetry_semigroup():
+    p, x, F = make_config(2)
+    xd = torch.from_numpy(x).cuda()
+    Fd = torch.from_numpy(F).cuda()
+    plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
+    a = plan.integrate(Fd)
+    b = plan.integrate(Fd)
+    assert torch.equal(a, b)  # bitwise deterministic
+    plan2 = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
+    assert torch.equal(plan2.integrate(Fd), a)
+    Fi = Fd.clone()
+    plan.integrate(Fi, out=Fi)  # in place
+    assert torch.equal(Fi, a)
+    G2 = torch.randn_like(Fd)
+    lin = plan.integrate(2 * Fd - G2)
+    assert relerr((lin).cpu().numpy(), (2 * a - plan.integrate(G2)).cpu().numpy()) < 1e-5
+    u = torch.randn(x.shape[0], 1, device="cuda")
+    v = torch.randn(x.shape[0], 1, device="cuda")
+    Ku, Kv = plan.integrate(u), plan.integrate(v)
+    lhs, rhs = float((u * Kv).double().sum()), float((Ku * v).double().sum())
+    assert abs(lhs - rhs) <= 1e-5 * abs(lhs)
+    half = rfd.Plan(xd, p["eps"], p["lam"] / 2, p["m"], p["seed"])
+    two = half.integrate(half.integrate(Fd))
+    assert relerr(two.cpu().numpy(), a.cpu().numpy()) < 1e-4
+
+
+def test_host_buffers_match_device():
+    p, x, F = make_config(4)
+    plan = rfd.Plan(x, p["eps"], p["lam"], p["m"], p["seed"])  # host points
+    Fh = torch.from_numpy(F).pin_memory()
+    oh = torch.empty_like(Fh).pin_memory()
+    plan.integrate_host(Fh, oh)
+    torch.cuda.synchronize()
+    od = plan.integrate(Fh.cuda()).cpu()
+    assert torch.equal(oh, od)
+
+
+def test_overflow_reports_erange():
+    p, x, F = make_config(2)
+    with pytest.raises(rfd.RFDError) as ei:
+        rfd.Plan(torch.from_numpy(x).cuda(), p["eps"], 200.0, p["m"], p["seed"])
+    assert ei.value.status == rfd.RFD_ERANGE
+
+
+def test_cuda_graph_capture_of_reuse_loop():
+    p, x, V = make_config(3)
+    xd = torch.from_numpy(x).cuda()
+    plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
+    Vd = torch.from_numpy(V[:10]).cuda()
+    eager = torch.stack([plan.integrate(Vd[t]) for t in range(10)])
+    outs = torch.empty_like(Vd)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        plan.integrate(Vd[0], out=outs[0])  # workspace sized before capture
+        with torch.cuda.graph(g, stream=s):
+            for t in range(10):
+                plan.integrate(Vd[t], out=outs[t], stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(outs, eager)
+
+
+def test_launch_counter_and_profiler():
+    p, x, F = make_config(1)
+    c0 = rfd.launch_count()
+    plan = rfd.Plan(torch.from_numpy(x).cuda(), p["eps"], p["lam"], p["m"], p["seed"])
+    rfd.profile_enable(True)
+    plan.integrate(torch.from_numpy(F).cuda())
+    prof = rfd.profile_read()
+    rfd.profile_enable(False)
+    assert rfd.launch_count() > c0
+    assert {"rfd_pass1", "rfd_pass2", "rfd_reduce_S", "rfd_core_apply"} <= set(prof)
+    assert all(v[1] > 0 for v in prof.values())
