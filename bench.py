@@ -108,15 +108,14 @@ class ClockSampler:
             self.err = str(e)
 
     def _handle(self, idx):
-        import torch
-        pynvml = self.nv
-        try:
-            bus = torch.cuda.get_device_properties(idx).pci_bus_id
-            return pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode() if isinstance(bus, str) else bus)
-        except Exception:
-            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            phys = int(vis.split(",")[idx]) if vis else idx
-            return pynvml.nvmlDeviceGetHandleByIndex(phys)
+        # NVML indexes physical GPUs; map through CUDA_VISIBLE_DEVICES.
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        toks = [t.strip() for t in vis.split(",") if t.strip()]
+        if toks and idx < len(toks) and toks[idx].isdigit():
+            return self.nv.nvmlDeviceGetHandleByIndex(int(toks[idx]))
+        if toks and idx < len(toks) and toks[idx].startswith("GPU-"):
+            return self.nv.nvmlDeviceGetHandleByUUID(toks[idx])
+        return self.nv.nvmlDeviceGetHandleByIndex(idx)
 
     def _loop(self):
         while not self.stop:

@@ -134,10 +134,34 @@ def _sphere(n, seed):
                                    (4099, 33, 20), (3001, 512, 4), (70001, 96, 37),
                                    (12345, 128, 16)])
 def test_ragged_shapes_parity(n, m, d):
+    # eps = 0.05 keeps every sinc factor in its first lobe (all nu > 0:
+    # symmetric core route).
     x = _sphere(n, n + m)
     F = np.random.default_rng(d).standard_normal((n, d)).astype(np.float32)
-    p = dict(name="ragged n=%d m=%d d=%d" % (n, m, d), eps=0.2, lam=-0.8, m=m, seed=11)
+    p = dict(name="ragged n=%d m=%d d=%d" % (n, m, d), eps=0.05, lam=-0.8, m=m, seed=11)
     plan, out = _run_single(x, F, p)
+    assert plan.info()["symmetric"] == 1
+    _check_against_oracle(plan, out, x, F, p)
+
+
+@pytest.mark.parametrize("n,m,seed,lam", [(1000, 40, 11, -0.8), (3001, 96, 14, -0.3),
+                                          (2000, 128, 13, 0.05)])
+def test_negative_nu_nonsymmetric_route(n, m, seed, lam):
+    # eps = 0.2 puts some frequencies in a negative sinc lobe (nu < 0): the core
+    # runs on lambda G D directly.  Where the oracle's exact result overflows
+    # fp32 the library must refuse the plan with RFD_ERANGE instead.
+    x = _sphere(n, seed)
+    F = np.random.default_rng(seed).standard_normal((n, 3)).astype(np.float32)
+    p = dict(name="nonsym n=%d m=%d" % (n, m), eps=0.2, lam=lam, m=m, seed=seed)
+    ref = orf.Plan(x, p["eps"], p["lam"], p["m"], p["seed"])
+    assert (ref.nu < 0).any()
+    if not np.isfinite(ref.C).all() or np.abs(ref.C).max() > 1e30:
+        with pytest.raises(rfd.RFDError) as ei:
+            _run_single(x, F, p)
+        assert ei.value.status == rfd.RFD_ERANGE
+        return
+    plan, out = _run_single(x, F, p)
+    assert plan.info()["symmetric"] == 0
     _check_against_oracle(plan, out, x, F, p)
 
 
