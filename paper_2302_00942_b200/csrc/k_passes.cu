@@ -246,9 +246,13 @@ void pass2_t(int blocks, cudaStream_t s, const float4* pts, const float4* omega4
                          160 * 1024);
     configured = true;
   }
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass2_kernel<DC, PPT>, 256, smem);
-  if (occ < 1) occ = 1;
+  static size_t occ_smem = ~size_t(0);
+  static int occ = 1;
+  if (occ_smem != smem) {  // occupancy depends only on the shared-memory size
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass2_kernel<DC, PPT>, 256, smem);
+    if (occ < 1) occ = 1;
+    occ_smem = smem;
+  }
   constexpr int TP = 256 * PPT;
   const int64_t ntiles = ((n + TP - 1) / TP) * batch;
   int64_t grid = int64_t(blocks) * occ;

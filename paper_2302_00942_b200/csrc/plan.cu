@@ -5,6 +5,7 @@
 // one host-computed quantity is the constant C_R = P(||Z||_1 <= R) of the
 // truncated proposal (A7), fixed by R alone.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -110,6 +111,7 @@ struct rfd_plan {
   // host-buffer staging
   float* stage = nullptr;
   size_t stage_elems = 0;
+  cudaStream_t stream = nullptr;  // stream of the last call (frees are ordered on it)
 };
 
 namespace {
@@ -170,34 +172,73 @@ bool is_device_pointer(const void* p) {
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
-void free_plan(rfd_plan* p) {
-  if (!p) return;
-  cudaFree(p->pts);
-  cudaFree(p->omega4);
-  cudaFree(p->nu);
-  cudaFree(p->G);
-  cudaFree(p->C);
-  cudaFree(p->flags);
-  cudaFree(p->s_partial);
-  cudaFree(p->S);
-  cudaFree(p->Y);
-  cudaFree(p->stage);
-  delete p;
+// Stream-ordered allocations from a library-owned pool that keeps its
+// memory (release threshold = max): plan creation and workspace growth then
+// cost no cudaMalloc/cudaFree round trips after the first use.
+cudaMemPool_t library_pool(int dev) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  uint64_t thr = ~uint64_t(0);
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  pools[dev] = pool;
+  return pool;
 }
 
 template <typename T>
-cudaError_t dalloc(T** ptr, size_t count) {
-  return cudaMalloc(reinterpret_cast<void**>(ptr), count * sizeof(T) + 16);
+cudaError_t dalloc(T** ptr, size_t count, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool = library_pool(dev);
+  const size_t bytes = count * sizeof(T) + 16;
+  if (!pool) return cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, s);
+  return cudaMallocFromPoolAsync(reinterpret_cast<void**>(ptr), bytes, pool, s);
+}
+
+template <typename T>
+void dfree(T*& ptr, cudaStream_t s) {
+  if (ptr) cudaFreeAsync(ptr, s);
+  ptr = nullptr;
+}
+
+void free_plan(rfd_plan* p) {
+  if (!p) return;
+  cudaStream_t s = p->stream;
+  cudaStreamSynchronize(s);
+  dfree(p->pts, s);
+  dfree(p->omega4, s);
+  dfree(p->nu, s);
+  dfree(p->G, s);
+  dfree(p->C, s);
+  dfree(p->flags, s);
+  dfree(p->s_partial, s);
+  dfree(p->S, s);
+  dfree(p->Y, s);
+  dfree(p->stage, s);
+  delete p;
 }
 
 struct TempBuffers {
+  cudaStream_t s;
   std::vector<void*> bufs;
+  explicit TempBuffers(cudaStream_t st) : s(st) {}
   ~TempBuffers() {
-    for (void* b : bufs) cudaFree(b);
+    for (void* b : bufs) cudaFreeAsync(b, s);
   }
   template <typename T>
   cudaError_t alloc(T** ptr, size_t count) {
-    cudaError_t e = dalloc(ptr, count);
+    cudaError_t e = dalloc(ptr, count, s);
     if (e == cudaSuccess) bufs.push_back(*ptr);
     return e;
   }
@@ -227,6 +268,7 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
     }
   } guard{p};
   p->device = dev;
+  p->stream = st;
   RFD_CUDA(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, dev));
   p->n = n;
   p->batch = batch;
@@ -238,15 +280,15 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   const int64_t total = n * batch;
   const size_t rr = size_t(p->r) * p->r;
 
-  RFD_CUDA(dalloc(&p->pts, size_t(total)));
-  RFD_CUDA(dalloc(&p->omega4, size_t(m)));
-  RFD_CUDA(dalloc(&p->nu, size_t(m)));
-  RFD_CUDA(dalloc(&p->G, rr * batch));
-  RFD_CUDA(dalloc(&p->C, rr * batch));
-  RFD_CUDA(dalloc(&p->flags, size_t(4)));
+  RFD_CUDA(dalloc(&p->pts, size_t(total), st));
+  RFD_CUDA(dalloc(&p->omega4, size_t(m), st));
+  RFD_CUDA(dalloc(&p->nu, size_t(m), st));
+  RFD_CUDA(dalloc(&p->G, rr * batch, st));
+  RFD_CUDA(dalloc(&p->C, rr * batch, st));
+  RFD_CUDA(dalloc(&p->flags, size_t(4), st));
   RFD_CUDA(cudaMemsetAsync(p->flags, 0, 4 * sizeof(int), st));
 
-  TempBuffers tmp;
+  TempBuffers tmp(st);
   const float* dev_xyz = points;
   if (!is_device_pointer(points)) {
     float* staged = nullptr;
@@ -258,11 +300,21 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   rfd::launch_pack_points(dev_xyz, p->pts, total, st);
   rfd::launch_freq(p->omega4, p->nu, p->flags, m, seed, eps, RFD_TRUNCATION_R, cached_c_r(), st);
 
-  // a4: Gram.
-  const rfd::GramGeom gg = rfd::gram_geometry(m, n, batch, p->sms);
-  float* gpart = nullptr;
-  RFD_CUDA(tmp.alloc(&gpart, rfd::gram_partial_elems(gg, batch)));
-  rfd::launch_gram(p->pts, p->omega4, m, n, batch, gg, gpart, p->G, st);
+  // a4: Gram -- tensor cores (tcgen05, fp16 hi/lo split) unless the SIMT
+  // kernel is requested for A/B comparison (RFD_GRAM=simt).
+  const char* gram_env = getenv("RFD_GRAM");
+  const bool gram_simt = gram_env && strcmp(gram_env, "simt") == 0;
+  if (gram_simt) {
+    const rfd::GramGeom gg = rfd::gram_geometry(m, n, batch, p->sms);
+    float* gpart = nullptr;
+    RFD_CUDA(tmp.alloc(&gpart, rfd::gram_partial_elems(gg, batch)));
+    rfd::launch_gram(p->pts, p->omega4, m, n, batch, gg, gpart, p->G, st);
+  } else {
+    const rfd::GramGeom gg = rfd::gram_tc_geometry(m, n, batch, p->sms);
+    float* gpart = nullptr;
+    RFD_CUDA(tmp.alloc(&gpart, rfd::gram_tc_partial_elems(gg, batch)));
+    rfd::launch_gram_tc(p->pts, p->omega4, m, n, batch, gg, gpart, p->G, st);
+  }
 
   // a5: core, scaling exponent first.
   double *Z = nullptr, *P0 = nullptr, *P1 = nullptr, *E0 = nullptr, *E1 = nullptr;
@@ -295,19 +347,16 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   return RFD_OK;
 }
 
-rfd_status ensure_workspace(rfd_plan* p, int d) {
+rfd_status ensure_workspace(rfd_plan* p, int d, cudaStream_t st) {
   if (p->ws_d >= d) return RFD_OK;
-  cudaFree(p->s_partial);
-  cudaFree(p->S);
-  cudaFree(p->Y);
-  p->s_partial = nullptr;
-  p->S = nullptr;
-  p->Y = nullptr;
+  dfree(p->s_partial, st);
+  dfree(p->S, st);
+  dfree(p->Y, st);
   p->ws_d = 0;
   const size_t part = size_t(p->batch) * p->pg.chunks * p->r * 16;
-  RFD_CUDA(dalloc(&p->s_partial, part));
-  RFD_CUDA(dalloc(&p->S, size_t(p->batch) * p->r * d));
-  RFD_CUDA(dalloc(&p->Y, size_t(p->batch) * p->r * d));
+  RFD_CUDA(dalloc(&p->s_partial, part, st));
+  RFD_CUDA(dalloc(&p->S, size_t(p->batch) * p->r * d, st));
+  RFD_CUDA(dalloc(&p->Y, size_t(p->batch) * p->r * d, st));
   p->ws_d = d;
   return RFD_OK;
 }
@@ -318,7 +367,8 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
   if (d < 1) return fail(RFD_EINVAL, "d must be >= 1");
   if (reinterpret_cast<uintptr_t>(F) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0)
     return fail(RFD_EINVAL, "F/out must be 16-byte aligned");
-  rfd_status rs = ensure_workspace(p, d);
+  p->stream = st;
+  rfd_status rs = ensure_workspace(p, d, st);
   if (rs != RFD_OK) return rs;
   for (int c0 = 0; c0 < d; c0 += 16) {
     const int dc = (d - c0 < 16) ? d - c0 : 16;
@@ -371,10 +421,9 @@ rfd_status rfd_integrate_host(rfd_plan* plan, const float* F_host, int32_t d, fl
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t elems = size_t(plan->batch) * plan->n * d;
   if (plan->stage_elems < elems) {
-    cudaFree(plan->stage);
-    plan->stage = nullptr;
+    dfree(plan->stage, st);
     plan->stage_elems = 0;
-    RFD_CUDA(dalloc(&plan->stage, elems));
+    RFD_CUDA(dalloc(&plan->stage, elems, st));
     plan->stage_elems = elems;
   }
   RFD_CUDA(cudaMemcpyAsync(plan->stage, F_host, elems * sizeof(float), cudaMemcpyHostToDevice, st));

@@ -50,6 +50,12 @@ size_t gram_partial_elems(const GramGeom& g, int batch);
 void launch_gram(const float4* pts, const float4* omega4, int m, int64_t n,
                  int batch, const GramGeom& g, float* partial, double* G,
                  cudaStream_t s);
+// Tensor-core Gram (k_gram_tc.cu): GramGeom.ntiles holds the number of units.
+GramGeom gram_tc_geometry(int m, int64_t n, int batch, int sms);
+size_t gram_tc_partial_elems(const GramGeom& g, int batch);
+void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n,
+                    int batch, const GramGeom& g, float* partial, double* G,
+                    cudaStream_t s);
 
 // ---------------------------------------------------------------- core
 // Z_b = lambda D^1/2 G D^1/2 (symmetric route) or lambda G D; writes the
