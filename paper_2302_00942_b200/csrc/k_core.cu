@@ -13,8 +13,8 @@
 // Sec. 0.1 item 2).  The oracle instead takes the top-right block of
 // scipy's expm of the augmented 2r x 2r matrix: a different algorithm.
 //
-// Dense fp64 GEMMs: 64 x 64 tiles, 256 threads x (4 x 4) outputs, batched
-// over clouds via blockIdx.z.
+// Dense fp64 GEMMs on the fp64 tensor cores (DMMA), batched over clouds via
+// blockIdx.z.
 #include <math.h>
 
 #include "rfd_internal.h"
@@ -23,7 +23,6 @@ namespace rfd {
 namespace {
 
 constexpr int kTaylor = 12;
-constexpr double kTheta = 0.5;
 
 __device__ __forceinline__ double dweight(const double* nu, int a) { return nu[a >> 1]; }
 
@@ -40,30 +39,27 @@ __global__ void core_prep_kernel(const double* __restrict__ G, const double* __r
   Z[int64_t(b) * r * r + e] = sym ? lambda * sqrt(da) * g * sqrt(dc) : lambda * g * dc;
 }
 
-__global__ void core_norm_kernel(const double* __restrict__ Z, int r, int* __restrict__ smax) {
-  // s_b = smallest s >= 0 with ||Z_b||_1 / 2^s <= kTheta (max column abs sum).
-  const int b = blockIdx.x;
+__global__ void core_norm_kernel(const double* __restrict__ Z, int r,
+                                 unsigned long long* __restrict__ norm_bits) {
+  // ||Z_b||_1 = max column abs sum; block (32 columns x 8 row groups), the
+  // max over blocks and clouds via atomicMax on the (non-negative) fp64 bits.
+  const int b = blockIdx.y;
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31), rg = threadIdx.x >> 5;
   const double* Zb = Z + int64_t(b) * r * r;
-  double best = 0.0;
-  for (int c = threadIdx.x; c < r; c += blockDim.x) {
-    double col = 0.0;
-    for (int a = 0; a < r; ++a) col += fabs(Zb[int64_t(a) * r + c]);
-    best = fmax(best, col);
-  }
-  __shared__ double red[256];
-  red[threadIdx.x] = best;
+  double col = 0.0;
+  if (c < r)
+    for (int a = rg; a < r; a += 8) col += fabs(Zb[int64_t(a) * r + c]);
+  __shared__ double red[8][33];
+  red[rg][threadIdx.x & 31] = col;
   __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const double nrm = red[0];
-    int s = 0;
-    if (!isfinite(nrm)) s = 1 << 20;
-    else
-      while (ldexp(nrm, -s) > kTheta && s < 1000) ++s;
-    atomicMax(smax, s);
+  if (threadIdx.x < 32) {
+    double sum = 0.0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) sum += red[g][threadIdx.x];
+    if (!isfinite(sum)) sum = __longlong_as_double(0x7FF0000000000000LL);  // +inf
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum = fmax(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+    if (threadIdx.x == 0) atomicMax(norm_bits, (unsigned long long)__double_as_longlong(sum));
   }
 }
 
@@ -84,9 +80,20 @@ struct GemmJobs {
   GemmJob job[2];
 };
 
-constexpr int kT = 64, kBK = 16;
+// fp64 tensor-core GEMM (DMMA, mma.sync m8n8k4 f64): CTA tile 32 x 64,
+// 4 warps side by side (each 32 x 16 = 4 x 2 fragments), K staged 16 at a
+// time through shared memory (padded strides: conflict-free fragment loads).
+constexpr int kBM = 32, kBN = 64, kBK = 16;
+constexpr int kSA = kBK + 4;   // A tile row stride (doubles)
+constexpr int kSB = kBN + 4;   // B tile row stride (doubles)
 
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128)
 dgemm_kernel(GemmJobs jobs, int njobs, int r) {
   const int jb = blockIdx.z % njobs, b = blockIdx.z / njobs;
   const GemmJob J = (jb == 0) ? jobs.job[0] : jobs.job[1];
@@ -94,46 +101,58 @@ dgemm_kernel(GemmJobs jobs, int njobs, int r) {
   const double* __restrict__ A = J.A + off;
   const double* __restrict__ B = J.B + off;
   double* __restrict__ C = J.C + off;
-  __shared__ double As[kBK][kT + 1];
-  __shared__ double Bs[kBK][kT];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int i0 = blockIdx.y * kT, j0 = blockIdx.x * kT;
-  double acc[4][4] = {};
+  __shared__ double As[kBM * kSA];
+  __shared__ double Bs[kBK * kSB];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = lane >> 2, tig = lane & 3;
+  const int i0 = blockIdx.y * kBM, j0 = blockIdx.x * kBN;
+  double acc[4][2][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+
   for (int k0 = 0; k0 < r; k0 += kBK) {
+    // A tile 32 x 16 (4 per thread), B tile 16 x 64 (8 per thread)
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
-      const int e = tid + 256 * l;
-      const int row = e / kBK, kk = e % kBK;
+      const int e = tid + 128 * l, row = e >> 4, kk = e & 15;
       const int gi = i0 + row, gk = k0 + kk;
       double v = 0.0;
       if (gi < r && gk < r) v = A[int64_t(gi) * r + gk] + (gi == gk ? J.sigma : 0.0);
-      As[kk][row] = v;
-      const int kb = e / kT, col = e % kT;
-      const int gkb = k0 + kb, gj = j0 + col;
-      Bs[kb][col] = (gkb < r && gj < r) ? B[int64_t(gkb) * r + gj] : 0.0;
+      As[row * kSA + kk] = v;
+    }
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      const int e = tid + 128 * l, kk = e >> 6, col = e & 63;
+      const int gk = k0 + kk, gj = j0 + col;
+      Bs[kk * kSB + col] = (gk < r && gj < r) ? B[int64_t(gk) * r + gj] : 0.0;
     }
     __syncthreads();
 #pragma unroll
-    for (int kk = 0; kk < kBK; ++kk) {
-      double a[4], bb[4];
+    for (int k4 = 0; k4 < kBK; k4 += 4) {
+      double af[4], bf[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+      for (int mi = 0; mi < 4; ++mi) af[mi] = As[(mi * 8 + grp) * kSA + k4 + tig];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bb[j] = Bs[kk][tx + 16 * j];
+      for (int ni = 0; ni < 2; ++ni) bf[ni] = Bs[(k4 + tig) * kSB + warp * 16 + ni * 8 + grp];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
+        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gi = i0 + ty + 16 * i, gj = j0 + tx + 16 * j;
-      if (gi < r && gj < r) C[int64_t(gi) * r + gj] = J.alpha * acc[i][j] + (gi == gj ? J.gamma : 0.0);
-    }
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gi = i0 + mi * 8 + grp, gj = j0 + warp * 16 + ni * 8 + 2 * tig + h;
+        if (gi < r && gj < r)
+          C[int64_t(gi) * r + gj] = J.alpha * acc[mi][ni][h] + (gi == gj ? J.gamma : 0.0);
+      }
 }
 
 __global__ void core_finalize_kernel(const double* __restrict__ P, const double* __restrict__ nu,
@@ -153,14 +172,15 @@ __global__ void core_finalize_kernel(const double* __restrict__ P, const double*
 
 void gemm(const GemmJobs& jobs, int njobs, int r, int batch, cudaStream_t s) {
   LaunchScope L("rfd_core_dgemm", s);
-  const int t = (r + kT - 1) / kT;
-  dgemm_kernel<<<dim3(t, t, njobs * batch), 256, 0, s>>>(jobs, njobs, r);
+  const dim3 grid((r + kBN - 1) / kBN, (r + kBM - 1) / kBM, njobs * batch);
+  dgemm_kernel<<<grid, 128, 0, s>>>(jobs, njobs, r);
 }
 
 }  // namespace
 
 void launch_core_prep(const double* G, const double* nu, const int* flags, double lambda,
-                      int m, int batch, double* Z, int* smax, cudaStream_t s) {
+                      int m, int batch, double* Z, unsigned long long* norm_bits,
+                      cudaStream_t s) {
   const int r = 2 * m;
   const int64_t rr = int64_t(r) * r;
   {
@@ -170,7 +190,7 @@ void launch_core_prep(const double* G, const double* nu, const int* flags, doubl
   }
   {
     LaunchScope L("rfd_core_norm", s);
-    core_norm_kernel<<<batch, 256, 0, s>>>(Z, r, smax);
+    core_norm_kernel<<<dim3((r + 31) / 32, batch), 256, 0, s>>>(Z, r, norm_bits);
   }
 }
 

@@ -28,7 +28,8 @@ __device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
   return c;
 }
 
-__global__ void freq_kernel(float4* __restrict__ omega4, double* __restrict__ nu,
+__global__ void freq_kernel(float4* __restrict__ omega4, float4* __restrict__ omega_rad4,
+                            double* __restrict__ nu,
                             int* __restrict__ flags, int m, uint64_t seed,
                             double eps, double R, double c_r) {
   const uint2 key = make_uint2(uint32_t(seed & 0xffffffffu), uint32_t(seed >> 32));
@@ -53,6 +54,10 @@ __global__ void freq_kernel(float4* __restrict__ omega4, double* __restrict__ nu
     if (!ok) atomicOr(flags, 2);
     const float wx = float(z0), wy = float(z1), wz = float(z2);
     omega4[k] = make_float4(wx, wy, wz, 0.0f);
+    // 2 pi omega rounded once from fp64: the tensor-core passes evaluate
+    // sincos(2 pi omega . x) as MUFU sin/cos of (2 pi omega) . x in radians.
+    omega_rad4[k] = make_float4(float(two_pi * double(wx)), float(two_pi * double(wy)),
+                                float(two_pi * double(wz)), 0.0f);
     // tau: product of 1-D sinc factors; factor 2 eps at w = 0.
     const double wc[3] = {double(wx), double(wy), double(wz)};
     double tau = 1.0, sq = 0.0;
@@ -78,10 +83,10 @@ __global__ void pack_kernel(const float* __restrict__ xyz, float4* __restrict__ 
 
 }  // namespace
 
-void launch_freq(float4* omega4, double* nu, int* flags, int m, uint64_t seed,
-                 double eps, double R, double c_r, cudaStream_t s) {
+void launch_freq(float4* omega4, float4* omega_rad4, double* nu, int* flags, int m,
+                 uint64_t seed, double eps, double R, double c_r, cudaStream_t s) {
   LaunchScope L("rfd_freq", s);
-  freq_kernel<<<1, 256, 0, s>>>(omega4, nu, flags, m, seed, eps, R, c_r);
+  freq_kernel<<<1, 256, 0, s>>>(omega4, omega_rad4, nu, flags, m, seed, eps, R, c_r);
 }
 
 void launch_pack_points(const float* xyz, float4* pts, int64_t total, cudaStream_t s) {

@@ -96,13 +96,10 @@ __host__ __device__ inline int gram_units(int T, int u_want, GramUnit* out) {
   return u;
 }
 
-__device__ __forceinline__ void sincos_turns(float4 w, float4 x, float& c, float& s) {
+__device__ __forceinline__ void sincos_rad(float4 w, float4 x, float& c, float& s) {
+  // w = fp32(2 pi omega): the argument in radians; MUFU reduces it in turns.
   const float t = fmaf(w.z, x.z, fmaf(w.y, x.y, w.x * x.x));
-  // u = t - rint(t) with the 1.5 * 2^23 trick (exact for |t| < 2^22): two FMA-
-  // pipe adds instead of an XU-pipe FRND.
-  const float r = (t + 12582912.0f) - 12582912.0f;
-  const float u = t - r;
-  __sincosf(6.28318530717958647f * u, &s, &c);
+  __sincosf(t, &s, &c);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -189,7 +186,7 @@ gram_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4
       if (i >= nloc) break;
       float c[8], sn[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sincos_turns(w[i], xt[j * 8 + q], c[j], sn[j]);
+      for (int j = 0; j < 8; ++j) sincos_rad(w[i], xt[j * 8 + q], c[j], sn[j]);
       if (base + q * 8 + 8 > p1) {
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -219,27 +216,31 @@ gram_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4
     tc::fence_proxy_async_smem();
     tc::tc_fence_before();
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {
+      // Warp-uniform issue (descriptors in uniform registers), one elected lane.
       tc::tc_fence_after();
+      if (tc::elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < kStepPts / 16; ++kk) {
-        const uint32_t koff = uint32_t(kk) * 2 * kLBO;
+        for (int kk = 0; kk < kStepPts / 16; ++kk) {
+          const uint32_t koff = uint32_t(kk) * 2 * kLBO;
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          if (g >= ngrp) break;
-          const uint64_t aH = tc::make_sdesc(hi_base + a_off[g] + koff, kLBO, kSBO);
-          const uint64_t aL = tc::make_sdesc(lo_base + a_off[g] + koff, kLBO, kSBO);
-          const uint64_t bH = tc::make_sdesc(hi_base + b_off[g] + koff, kLBO, kSBO);
-          const uint64_t bL = tc::make_sdesc(lo_base + b_off[g] + koff, kLBO, kSBO);
-          const uint32_t d = tmem + uint32_t(slot * 256 + g * 128);
-          // The first MMA of an epoch starts its TMEM slot afresh.
-          const uint32_t acc0 = ((t % kEpoch) > 0 || kk > 0) ? 1u : 0u;
-          tc::mma_f16(d, aH, bH, idesc[g], acc0);
-          tc::mma_f16(d, aH, bL, idesc[g], 1u);
-          tc::mma_f16(d, aL, bH, idesc[g], 1u);
+          for (int g = 0; g < 2; ++g) {
+            if (g >= ngrp) break;
+            const uint64_t aH = tc::make_sdesc(hi_base + a_off[g] + koff, kLBO, kSBO);
+            const uint64_t aL = tc::make_sdesc(lo_base + a_off[g] + koff, kLBO, kSBO);
+            const uint64_t bH = tc::make_sdesc(hi_base + b_off[g] + koff, kLBO, kSBO);
+            const uint64_t bL = tc::make_sdesc(lo_base + b_off[g] + koff, kLBO, kSBO);
+            const uint32_t d = tmem + uint32_t(slot * 256 + g * 128);
+            // The first MMA of an epoch starts its TMEM slot afresh.
+            const uint32_t acc0 = ((t % kEpoch) > 0 || kk > 0) ? 1u : 0u;
+            tc::mma_f16(d, aH, bH, idesc[g], acc0);
+            tc::mma_f16(d, aH, bL, idesc[g], 1u);
+            tc::mma_f16(d, aL, bH, idesc[g], 1u);
+          }
         }
+        tc::mma_commit(&mma_bar[s]);
       }
-      tc::mma_commit(&mma_bar[s]);
+      __syncwarp();
     }
     // A new epoch started on the other TMEM slot: move the finished slot into
     // the fp32 registers (round-to-nearest adds) while this step's MMAs run.

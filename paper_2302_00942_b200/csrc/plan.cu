@@ -98,10 +98,11 @@ struct rfd_plan {
   // owned device state
   float4* pts = nullptr;      // batch*n
   float4* omega4 = nullptr;   // m
+  float4* omega_rad4 = nullptr;  // m: fp32(2 pi omega) for the tensor-core kernels
   double* nu = nullptr;       // m
   double* G = nullptr;        // batch*r*r (interleaved)
   double* C = nullptr;        // batch*r*r (interleaved)
-  int* flags = nullptr;       // [0] nu/sampler flags, [2] s_max, [3] overflow
+  int* flags = nullptr;       // [0] nu/sampler flags, [2..3] ||Z||_1 bits, [4] overflow
   // integrate workspace (grows with d)
   int ws_d = 0;
   float* s_partial = nullptr; // batch*chunks*r*16
@@ -218,6 +219,7 @@ void free_plan(rfd_plan* p) {
   cudaStreamSynchronize(s);
   dfree(p->pts, s);
   dfree(p->omega4, s);
+  dfree(p->omega_rad4, s);
   dfree(p->nu, s);
   dfree(p->G, s);
   dfree(p->C, s);
@@ -282,11 +284,12 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
 
   RFD_CUDA(dalloc(&p->pts, size_t(total), st));
   RFD_CUDA(dalloc(&p->omega4, size_t(m), st));
+  RFD_CUDA(dalloc(&p->omega_rad4, size_t(m), st));
   RFD_CUDA(dalloc(&p->nu, size_t(m), st));
   RFD_CUDA(dalloc(&p->G, rr * batch, st));
   RFD_CUDA(dalloc(&p->C, rr * batch, st));
-  RFD_CUDA(dalloc(&p->flags, size_t(4), st));
-  RFD_CUDA(cudaMemsetAsync(p->flags, 0, 4 * sizeof(int), st));
+  RFD_CUDA(dalloc(&p->flags, size_t(8), st));
+  RFD_CUDA(cudaMemsetAsync(p->flags, 0, 8 * sizeof(int), st));
 
   TempBuffers tmp(st);
   const float* dev_xyz = points;
@@ -298,7 +301,7 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
     dev_xyz = staged;
   }
   rfd::launch_pack_points(dev_xyz, p->pts, total, st);
-  rfd::launch_freq(p->omega4, p->nu, p->flags, m, seed, eps, RFD_TRUNCATION_R, cached_c_r(), st);
+  rfd::launch_freq(p->omega4, p->omega_rad4, p->nu, p->flags, m, seed, eps, RFD_TRUNCATION_R, cached_c_r(), st);
 
   // a4: Gram -- tensor cores (tcgen05, fp16 hi/lo split) unless the SIMT
   // kernel is requested for A/B comparison (RFD_GRAM=simt).
@@ -313,7 +316,7 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
     const rfd::GramGeom gg = rfd::gram_tc_geometry(m, n, batch, p->sms);
     float* gpart = nullptr;
     RFD_CUDA(tmp.alloc(&gpart, rfd::gram_tc_partial_elems(gg, batch)));
-    rfd::launch_gram_tc(p->pts, p->omega4, m, n, batch, gg, gpart, p->G, st);
+    rfd::launch_gram_tc(p->pts, p->omega_rad4, m, n, batch, gg, gpart, p->G, st);
   }
 
   // a5: core, scaling exponent first.
@@ -323,22 +326,29 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   RFD_CUDA(tmp.alloc(&P1, rr * batch));
   RFD_CUDA(tmp.alloc(&E0, rr * batch));
   RFD_CUDA(tmp.alloc(&E1, rr * batch));
-  rfd::launch_core_prep(p->G, p->nu, p->flags, lambda, m, batch, Z, p->flags + 2, st);
+  rfd::launch_core_prep(p->G, p->nu, p->flags, lambda, m, batch, Z,
+                        reinterpret_cast<unsigned long long*>(p->flags + 2), st);
   RFD_CUDA(cudaGetLastError());
-  int hflags[4] = {0, 0, 0, 0};
+  int hflags[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   RFD_CUDA(cudaMemcpyAsync(hflags, p->flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
   RFD_CUDA(cudaStreamSynchronize(st));
   if (hflags[0] & 2)
     return fail(RFD_ERANGE, "frequency sampler exhausted its attempts (R too small?)");
-  if (hflags[2] > 200) return fail(RFD_ERANGE, "core: ||lambda G D|| is not finite or too large");
+  double znorm;
+  memcpy(&znorm, hflags + 2, sizeof(double));
+  // Scaling exponent: smallest s >= 0 with ||Z||_1 / 2^s <= 1/2.
+  if (!isfinite(znorm) || znorm > 1e60)
+    return fail(RFD_ERANGE, "core: ||lambda G D|| is not finite or too large");
+  int s_scale = 0;
+  while (ldexp(znorm, -s_scale) > 0.5) ++s_scale;
   p->symmetric = (hflags[0] & 1) ? 0 : 1;
-  p->scaling = hflags[2];
+  p->scaling = s_scale;
   rfd::launch_core_eval(Z, p->nu, p->flags, lambda, m, batch, p->scaling, P0, P1, E0, E1, p->C,
-                        p->flags + 3, st);
+                        p->flags + 4, st);
   RFD_CUDA(cudaGetLastError());
   RFD_CUDA(cudaMemcpyAsync(hflags, p->flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
   RFD_CUDA(cudaStreamSynchronize(st));
-  if (hflags[3])
+  if (hflags[4])
     return fail(RFD_ERANGE, "core: exp(lambda W~) overflows (lambda > 0 or negative nu)");
 
   p->pg = rfd::pass_geometry(m, n, batch, p->sms);
@@ -353,7 +363,8 @@ rfd_status ensure_workspace(rfd_plan* p, int d, cudaStream_t st) {
   dfree(p->S, st);
   dfree(p->Y, st);
   p->ws_d = 0;
-  const size_t part = size_t(p->batch) * p->pg.chunks * p->r * 16;
+  const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
+  const size_t part = size_t(p->batch) * (p->pg.chunks > ranges ? p->pg.chunks : ranges) * p->r * 16;
   RFD_CUDA(dalloc(&p->s_partial, part, st));
   RFD_CUDA(dalloc(&p->S, size_t(p->batch) * p->r * d, st));
   RFD_CUDA(dalloc(&p->Y, size_t(p->batch) * p->r * d, st));
@@ -370,17 +381,40 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
   p->stream = st;
   rfd_status rs = ensure_workspace(p, d, st);
   if (rs != RFD_OK) return rs;
+  // a6 on the tensor cores unless the SIMT kernel is requested (RFD_PASS1=simt,
+  // A/B comparison only).
+  static const bool p1_simt = [] {
+    const char* e = getenv("RFD_PASS1");
+    return e && strcmp(e, "simt") == 0;
+  }();
+  const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
   for (int c0 = 0; c0 < d; c0 += 16) {
     const int dc = (d - c0 < 16) ? d - c0 : 16;
-    rfd::launch_pass1(p->pts, p->omega4, p->m, p->n, p->batch, p->pg, F, d, c0, dc, p->s_partial,
-                      st);
-    rfd::launch_reduce_S(p->s_partial, p->m, p->batch, p->pg.chunks, d, c0, dc, p->S, st);
+    if (p1_simt) {
+      rfd::launch_pass1(p->pts, p->omega4, p->m, p->n, p->batch, p->pg, F, d, c0, dc,
+                        p->s_partial, st);
+      rfd::launch_reduce_S(p->s_partial, p->m, p->batch, p->pg.chunks, d, c0, dc, p->S, st);
+    } else {
+      rfd::launch_pass1_tc(p->pts, p->omega_rad4, p->m, p->n, p->batch, ranges, F, d, c0, dc,
+                           p->s_partial, st);
+      rfd::launch_reduce_S(p->s_partial, p->m, p->batch, ranges, d, c0, dc, p->S, st);
+    }
   }
   rfd::launch_core_apply(p->C, p->S, p->m, p->batch, d, p->Y, st);
+  // a8 on the tensor cores unless the SIMT kernel is requested (RFD_PASS2=simt,
+  // A/B comparison only).
+  static const bool p2_simt = [] {
+    const char* e = getenv("RFD_PASS2");
+    return e && strcmp(e, "simt") == 0;
+  }();
   for (int c0 = 0; c0 < d; c0 += 16) {
     const int dc = (d - c0 < 16) ? d - c0 : 16;
-    rfd::launch_pass2(p->pts, p->omega4, p->m, p->n, p->batch, p->pg, p->Y, F, out, d, c0, dc,
-                      st);
+    if (p2_simt)
+      rfd::launch_pass2(p->pts, p->omega4, p->m, p->n, p->batch, p->pg, p->Y, F, out, d, c0, dc,
+                        st);
+    else
+      rfd::launch_pass2_tc(p->pts, p->omega_rad4, p->m, p->n, p->batch, p->sms, p->Y, F, out, d, c0,
+                           dc, st);
   }
   RFD_CUDA(cudaGetLastError());
   p->last_d = d;

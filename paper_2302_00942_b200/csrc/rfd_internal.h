@@ -28,10 +28,10 @@ struct LaunchScope {
 };
 
 // ---------------------------------------------------------------- K0 freq
-// omega4[k] = (wx, wy, wz, 0) fp32, nu[k] fp64; flags[0] |= 1 if some nu <= 0,
-// flags[0] |= 2 if the sampler ran out of attempts.
-void launch_freq(float4* omega4, double* nu, int* flags, int m, uint64_t seed,
-                 double eps, double R, double c_r, cudaStream_t s);
+// omega4[k] = (wx, wy, wz, 0) fp32, omega_rad4[k] = fp32(2 pi omega_k), nu[k]
+// fp64; flags[0] |= 1 if some nu <= 0, |= 2 if the sampler ran out of attempts.
+void launch_freq(float4* omega4, float4* omega_rad4, double* nu, int* flags, int m,
+                 uint64_t seed, double eps, double R, double c_r, cudaStream_t s);
 
 // ---------------------------------------------------------------- pack
 void launch_pack_points(const float* xyz, float4* pts, int64_t total, cudaStream_t s);
@@ -58,11 +58,11 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n,
                     cudaStream_t s);
 
 // ---------------------------------------------------------------- core
-// Z_b = lambda D^1/2 G D^1/2 (symmetric route) or lambda G D; writes the
-// 1-norm based scaling exponent to *smax (atomicMax over the batch).
+// Z_b = lambda D^1/2 G D^1/2 (symmetric route) or lambda G D; atomicMax of
+// max_b ||Z_b||_1 (fp64 bits) into *norm_bits (zeroed by the caller).
 void launch_core_prep(const double* G, const double* nu, const int* flags,
-                      double lambda, int m, int batch, double* Z, int* smax,
-                      cudaStream_t s);
+                      double lambda, int m, int batch, double* Z,
+                      unsigned long long* norm_bits, cudaStream_t s);
 // Taylor (degree kTaylor) of phi1 and exp at Z / 2^s, then s doublings,
 // then C^ = lambda D^1/2 P D^1/2 (or lambda D P); flags[1] = 1 on overflow.
 void launch_core_eval(const double* Z, const double* nu, const int* flags,
@@ -92,5 +92,17 @@ void launch_core_apply(const double* C, const double* S, int m, int batch,
 void launch_pass2(const float4* pts, const float4* omega4, int m, int64_t n,
                   int batch, const PassGeom& g, const float* Y, const float* F,
                   float* out, int d, int c0, int dc, cudaStream_t s);
+
+// Tensor-core pass 2 (k_pass2_tc.cu): dc <= 16 columns per launch.
+size_t pass2_tc_smem(int m);
+void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
+                     int sms, const float* Y, const float* F, float* out, int d, int c0, int dc,
+                     cudaStream_t s);
+
+// Tensor-core pass 1 (k_pass1_tc.cu): partial[b][range][2m][dc].
+int pass1_tc_ranges(int m, int64_t n, int batch, int sms);
+void launch_pass1_tc(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
+                     int ranges, const float* F, int d, int c0, int dc, float* partial,
+                     cudaStream_t s);
 
 }  // namespace rfd
