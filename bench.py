@@ -42,48 +42,84 @@ UNIT = "points*dims/s"
 
 
 def peaks():
-    p = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "src": "fallback (B200_PROFILING.md)"}
+    p = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "bf16_tflops": 1590.0,
+         "src": "fallback (B200_PROFILING.md)"}
     if os.path.exists(PEAKS_PATH):
         with open(PEAKS_PATH) as f:
             j = json.load(f)
-        p.update({k: j[k] for k in ("hbm_gbs", "sm_max_mhz") if k in j})
+        p.update({k: j[k] for k in ("hbm_gbs", "sm_max_mhz", "bf16_tflops") if k in j})
         p["src"] = "measured (MEASURED_PEAKS.json)"
     return p
 
 
 # ------------------------------------------------------------------ work model
+# Peaks: FP32 FMA pipe and MUFU from the B200 unit counts at
+# sm_max_mhz; dense fp16 tensor = the measured bf16 burst (same rate for fp16),
+# tf32 = half of it (the guide's nominal 1.1 vs 2.25 PFLOP/s ratio).
 def kernel_work(name, N, m, d):
-    """Algorithmic work of one launch: (FMA, MUFU, bytes)."""
+    """Algorithmic work of one launch: dict of {fma, mufu, bytes, tensor_flop, tensor_kind}.
+
+    Algorithmic = what the method needs, not what the kernel
+    executes: the 3-product hi/lo splits, masked tile halves, range reduction
+    and loop control count against achieved efficiency, not the roofline.
+    """
     r = 2 * m
-    if name == "rfd_gram_partial":      # G = Phi^T Phi, upper triangle + features
-        return N * r * (r + 1) / 2 + 3.0 * N * m, 2.0 * N * m, 16.0 * N
-    if name == "rfd_pass1":             # S = Phi^T F
-        return 2.0 * N * m * min(d, 16) + 3.0 * N * m, 2.0 * N * m, N * (16 + 4 * min(d, 16))
-    if name == "rfd_pass2":             # out = F + Phi Y
-        return 2.0 * N * m * min(d, 16) + 3.0 * N * m, 2.0 * N * m, N * (16 + 8 * min(d, 16))
-    return None
+    dc = min(d, 16)
+    if name in ("rfd_gram_partial", "rfd_gram_tc"):   # G = Phi^T Phi (upper triangle)
+        w = dict(fma=N * r * (r + 1) / 2 + 3.0 * N * m, mufu=2.0 * N * m, bytes=16.0 * N)
+        if name == "rfd_gram_tc":
+            w.update(tensor_flop=2.0 * N * r * (r + 1) / 2, tensor_kind="f16")
+        return w
+    if name in ("rfd_pass1", "rfd_pass1_tc"):           # S = Phi^T F
+        w = dict(fma=2.0 * N * m * dc + 3.0 * N * m, mufu=2.0 * N * m, bytes=N * (16 + 4 * dc))
+    elif name in ("rfd_pass2", "rfd_pass2_tc"):         # out = F + Phi Y
+        w = dict(fma=2.0 * N * m * dc + 3.0 * N * m, mufu=2.0 * N * m, bytes=N * (16 + 8 * dc))
+    else:
+        return None
+    if name.endswith("_tc"):
+        w.update(tensor_flop=2.0 * 2.0 * N * m * dc, tensor_kind="tf32")
+    return w
+
+
+def peaks_of(pk):
+    clk = pk["sm_max_mhz"] * 1e6
+    bf16 = pk.get("bf16_tflops", 1590.0) * 1e12
+    return {"fma": SMS * FMA_PER_CLK * clk, "mufu": SMS * MUFU_PER_CLK * clk,
+            "hbm": pk["hbm_gbs"] * 1e9, "f16": bf16, "tf32": bf16 / 2}
 
 
 def roofline_of(name, N, m, d, ms_per_launch, pk):
+    """Roofline of one kernel: the slowest of its algorithmic HBM bytes, tensor
+    flops (tensor-core kernels: the contraction runs there) or FP32 FMA (SIMT
+    kernels), and MUFU work, each at its peak."""
     w = kernel_work(name, N, m, d)
     if w is None or ms_per_launch <= 0:
         return None
-    fma, mufu, byts = w
-    clk = pk["sm_max_mhz"] * 1e6
-    fma_peak = SMS * FMA_PER_CLK * clk
-    mufu_peak = SMS * MUFU_PER_CLK * clk
+    P = peaks_of(pk)
     t = ms_per_launch * 1e-3
-    t_fma, t_mufu, t_hbm = fma / fma_peak, mufu / mufu_peak, byts / (pk["hbm_gbs"] * 1e9)
-    bound = max((t_fma, "alu"), (t_mufu, "sfu"), (t_hbm, "hbm"))
-    if bound[1] == "hbm":
-        return {"bound": "hbm", "achieved": byts / t / 1e9, "peak": pk["hbm_gbs"],
-                "unit": "GB/s", "frac": t_hbm / t, "traffic": None}
-    if bound[1] == "alu":
-        return {"bound": "alu", "achieved": 2 * fma / t / 1e12, "peak": 2 * fma_peak / 1e12,
-                "unit": "TFLOP/s", "frac": t_fma / t, "traffic": None,
-                "peak_note": "fp32 FMA pipe: 148 SM x 128 FMA/clk x %.0f MHz (derived)" % pk["sm_max_mhz"]}
-    return {"bound": "sfu", "achieved": mufu / t / 1e12, "peak": mufu_peak / 1e12,
-            "unit": "Tops/s", "frac": t_mufu / t, "traffic": None}
+    terms = {"hbm": w["bytes"] / P["hbm"], "sfu": w["mufu"] / P["mufu"]}
+    if "tensor_flop" in w:
+        terms["tensor"] = w["tensor_flop"] / P[w["tensor_kind"]]
+        terms["alu"] = 3.0 * N * m / P["fma"]          # projections only
+    else:
+        terms["alu"] = w["fma"] / P["fma"]
+    bound = max(terms, key=terms.get)
+    t_roof = terms[bound]
+    out = {"bound": bound, "frac": t_roof / t, "traffic": None,
+           "terms_ms": {k: v * 1e3 for k, v in terms.items()}}
+    if bound == "hbm":
+        out.update(achieved=w["bytes"] / t / 1e9, peak=P["hbm"] / 1e9, unit="GB/s")
+    elif bound == "tensor":
+        out.update(achieved=w["tensor_flop"] / t / 1e12, peak=P[w["tensor_kind"]] / 1e12,
+                   unit="TFLOP/s", peak_note="dense %s tensor: measured bf16 burst%s"
+                   % (w["tensor_kind"], " / 2 (tf32 nominal ratio)" if w["tensor_kind"] == "tf32" else ""))
+    elif bound == "alu":
+        out.update(achieved=2 * w["fma"] / t / 1e12, peak=2 * P["fma"] / 1e12, unit="TFLOP/s",
+                   peak_note="fp32 FMA pipe: 148 SM x 128 FMA/clk x %.0f MHz (derived)" % pk["sm_max_mhz"])
+    else:
+        out.update(achieved=w["mufu"] / t / 1e12, peak=P["mufu"] / 1e12, unit="Tops/s",
+                   peak_note="MUFU: 148 SM x 16/clk x %.0f MHz (derived)" % pk["sm_max_mhz"])
+    return out
 
 
 # ------------------------------------------------------------------ clocks
@@ -295,16 +331,22 @@ def run_rfd(args, rank, world, local, pg):
         rl = roofline_of(name, N, m, d, tms / cnt, pk)
         ikern[name] = {"ms_per_launch": tms / cnt, "share": tms / itotal,
                        "roofline_frac": rl["frac"] if rl else None}
-    # integrate roofline (north star: slower of HBM bytes and FMA+SFU work)
+    # integrate roofline (north star: slower of HBM bytes and FMA+SFU work;
+    # SURVEY Sec. 8(d)).  Headline: the contraction counted as FP32 FMA.  Because
+    # the contraction runs on the tensor cores, the stricter max(HBM, tensor,
+    # MUFU) roofline is reported beside it.
+    P = peaks_of(pk)
     fma_i = N * (4.0 * m * d + 6.0 * m)
     mufu_i = 4.0 * N * m
     byts_i = N * (24.0 + 12.0 * d)
-    clk = pk["sm_max_mhz"] * 1e6
-    t_roof = max(fma_i / (SMS * FMA_PER_CLK * clk), mufu_i / (SMS * MUFU_PER_CLK * clk),
-                 byts_i / (pk["hbm_gbs"] * 1e9))
+    tc_i = 2.0 * 4.0 * N * m * d
+    t_roof = max(fma_i / P["fma"], mufu_i / P["mufu"], byts_i / P["hbm"])
+    t_strict = max(tc_i / P["tf32"], mufu_i / P["mufu"], byts_i / P["hbm"])
     integ = {"value": N * d * world / (ims * 1e-3), "unit": UNIT, "ms_per_call": ims,
              "roofline_ms": t_roof * 1e3, "roofline_frac": t_roof / (ims * 1e-3),
              "roofline_bound": "fp32 FMA pipe (4md+6m FMA/pt at 148x128/clk, %.0f MHz)" % pk["sm_max_mhz"],
+             "strict_roofline_ms": t_strict * 1e3, "strict_roofline_frac": t_strict / (ims * 1e-3),
+             "strict_roofline_bound": "MUFU (4m sin/cos per pt at 148x16/clk) vs tf32 tensor vs HBM",
              "hbm_gbs_achieved": byts_i / (ims * 1e-3) / 1e9, "kernels": ikern}
     return dict(N=N, m=m, d=d, ms_step=ms_step, launches=launches, roofline=roof,
                 kernels=kernels, integrate=integ, e2e=e2e, clocks=sampler.summary(), params=p)

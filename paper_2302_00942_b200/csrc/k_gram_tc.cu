@@ -25,7 +25,8 @@ namespace {
 
 constexpr int kBlk = 128;           // features per block (64 frequencies)
 constexpr int kStepPts = 64;        // points per K-step (4 MMA K-slices of 16)
-constexpr int kThreads = 512;       // 16 warps
+constexpr int kProducers = 512;     // 16 feature-producer warps
+constexpr int kThreads = 544;       // + 1 MMA-issue warp (warp 16)
 constexpr int kMaxLocal = 3;        // feature blocks per unit
 // Per operand (Hi or Lo), per block: 128 rows x 64 points x 2 B = 16 KB.
 constexpr int kBlkBytes = kBlk * kStepPts * 2;
@@ -109,7 +110,7 @@ gram_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t mma_bar[kStages];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ float4 xs[2][kStepPts];
+  __shared__ float4 xs[2][kStepPts + kStepPts / 8];  // padded: point p at p + p/8
 
   const int unit = blockIdx.x, ch = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -125,10 +126,10 @@ gram_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4
   const int64_t p0 = int64_t(ch) * chunk;
   const int64_t p1 = min(p0 + chunk, n);
   const float4* cloud = pts + int64_t(b) * n;
-  // xs holds a step's points transposed (point q*8 + j at j*8 + q) so that
-  // the 8 point groups of a warp read 8 consecutive 16-byte words.
+  // xs holds a step's points with one float4 of padding per 8 (point p at
+  // p + p/8): the point groups of an 8-lane phase hit distinct banks.
   if (tid < kStepPts)
-    xs[0][(tid & 7) * 8 + (tid >> 3)] =
+    xs[0][tid + (tid >> 3)] =
         (p0 + tid < p1) ? __ldg(cloud + p0 + tid) : make_float4(0.f, 0.f, 0.f, 0.f);
   tc::tc_fence_before();
   __syncthreads();
@@ -171,6 +172,16 @@ gram_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4
   const int ncols = (ngrp == 2) ? 256 : 128 * U.nb[0];
   const bool drains = quarter * 64 < ncols;
   const uint32_t lane_base = tmem + (uint32_t(lg * 32) << 16) + uint32_t(quarter * 64);
+  auto drain = [&](int dslot) {
+    if (!drains || tid >= kProducers) return;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float v[32];
+      tc::tmem_ld32(lane_base + uint32_t(dslot * 256 + c * 32), v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[c * 32 + j] += v[j];
+    }
+  };
 
   const int nsteps = int((p1 - p0 + kStepPts - 1) / kStepPts);
   for (int t = 0; t < nsteps; ++t) {
@@ -181,12 +192,19 @@ gram_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4
     const uint32_t lo_base = hi_base + kMaxLocal * kBlkBytes;
     const int64_t base = p0 + int64_t(t) * kStepPts;
     const float4* xt = xs[t & 1];
+    // Next step's points: load now (the global-memory latency hides behind
+    // this step's feature generation), store to shared memory at the end.
+    float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tid < kStepPts) {
+      const int64_t pn = base + kStepPts + tid;
+      if (pn < p1) xn = __ldg(cloud + pn);
+    }
 #pragma unroll
     for (int i = 0; i < kMaxLocal; ++i) {
-      if (i >= nloc) break;
+      if (i >= nloc || tid >= kProducers) break;
       float c[8], sn[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sincos_rad(w[i], xt[j * 8 + q], c[j], sn[j]);
+      for (int j = 0; j < 8; ++j) sincos_rad(w[i], xt[q * 9 + j], c[j], sn[j]);
       if (base + q * 8 + 8 > p1) {
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -207,17 +225,14 @@ gram_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4
       tc::st_shared_v4(hi_base + ob + off_second, sh[0], sh[1], sh[2], sh[3]);
       tc::st_shared_v4(lo_base + ob + off_second, sl[0], sl[1], sl[2], sl[3]);
     }
-    // Prefetch the next step's points (read after this step's barrier).
-    if (tid < kStepPts) {
-      const int64_t pn = base + kStepPts + tid;
-      xs[(t + 1) & 1][(tid & 7) * 8 + (tid >> 3)] =
-          (pn < p1) ? __ldg(cloud + pn) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    // The next step's points become visible after this step's barrier.
+    if (tid < kStepPts) xs[(t + 1) & 1][tid + (tid >> 3)] = xn;
     tc::fence_proxy_async_smem();
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 0) {
-      // Warp-uniform issue (descriptors in uniform registers), one elected lane.
+    if (warp == kProducers / 32) {
+      // MMA warp: warp-uniform issue (descriptors in uniform registers), one
+      // elected lane; the producer warps go straight on to the next step.
       tc::tc_fence_after();
       if (tc::elect_one()) {
 #pragma unroll
@@ -242,42 +257,27 @@ gram_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4
       }
       __syncwarp();
     }
-    // A new epoch started on the other TMEM slot: move the finished slot into
-    // the fp32 registers (round-to-nearest adds) while this step's MMAs run.
-    if (t % kEpoch == 0 && t > 0) {
-      tc::mbar_wait(&mma_bar[(t - 1) % kStages], ((t - 1) / kStages) & 1);
+    // One step into epoch e+1, epoch e (the other TMEM slot) is complete --
+    // the wait at the top of this step covered step t-2, its last MMA -- so
+    // move it into the fp32 registers (round-to-nearest adds).
+    if (t % kEpoch == 1 && t > kEpoch) {
       tc::tc_fence_after();
-      if (drains) {
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          float v[32];
-          tc::tmem_ld32(lane_base + uint32_t((slot ^ 1) * 256 + c * 32), v);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) acc[c * 32 + j] += v[j];
-        }
-      }
+      drain(slot ^ 1);
       tc::tc_fence_before();
     }
   }
   if (nsteps > 0) {
     tc::mbar_wait(&mma_bar[(nsteps - 1) % kStages], ((nsteps - 1) / kStages) & 1);
     tc::tc_fence_after();
-    if (drains) {
-      const int slot = ((nsteps - 1) / kEpoch) & 1;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        float v[32];
-        tc::tmem_ld32(lane_base + uint32_t(slot * 256 + c * 32), v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[c * 32 + j] += v[j];
-      }
-    }
+    const int last_e = (nsteps - 1) / kEpoch;
+    if (last_e >= 1 && (nsteps - 1) % kEpoch == 0) drain((last_e - 1) & 1);
+    drain(last_e & 1);
   }
 
   // partial[b][ch][unit][col (256)][row (128)] fp32 (rows contiguous).
   float* out = partial + ((int64_t(b) * chunks + ch) * nunits + unit) * (256 * 128);
   const int row = lg * 32 + lane;
-  if (drains) {
+  if (drains && tid < kProducers) {
 #pragma unroll
     for (int j = 0; j < 64; ++j) out[int64_t(quarter * 64 + j) * 128 + row] = acc[j];
   }
