@@ -23,7 +23,8 @@ LIB = os.path.join(HERE, "lib", "librfd.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-         "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
+         "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"] + \
+    (["-DRFD_GRAM_CHECK"] if os.environ.get("RFD_GRAM_CHECK") == "1" else [])
 
 
 def nvcc():

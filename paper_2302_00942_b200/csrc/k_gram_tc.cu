@@ -2,367 +2,754 @@
 // row a4; B^T A of PAPER.md:337, 355 without D).  Plan-time.
 //
 // G is a dense contraction over points (N x r by N x r), so it runs on
-// tcgen05: each CTA owns a "unit" of one or two 128 x 128 tiles of the upper
-// triangle of G (a 128 x 256 accumulator in TMEM) and a chunk of points.  Per
-// K-step of 32 points the CTA's 8 warps regenerate the feature rows of the
-// unit's 128-feature blocks (a3: omega.x in turns, MUFU sin/cos) straight into
-// shared memory as an fp16 hi/lo split, x = hi + lo (|x - hi - lo| <=
-// 2^-22 |x| + 2^-25), and one thread issues
-//     D += Hi_A Hi_B^T + Hi_A Lo_B^T + Lo_A Hi_B^T
-// (tcgen05.mma kind::f16, M = 128, N = 128/256, K = 16, fp32 accumulate): the
-// dropped Lo Lo^T term is below 2^-22, so the tile carries fp32-level
-// products (DESIGN.md Sec. 6 "Gram precision").  Two shared-memory stages:
-// feature generation of step t+1 overlaps the MMAs of step t; a
-// tcgen05.commit -> mbarrier releases each stage.
+// tcgen05.  Features are grouped in blocks of 64 frequencies; inside a block
+// the 128 rows are [cos of the 64 frequencies; sin of the same 64] (the
+// reduce kernel maps them back to the interleaved internal order).  A *unit*
+// is one A block (the accumulator rows) against one or two B blocks (two
+// 128 x 128 tiles, one 128 x 256 accumulator); the units cover the upper
+// triangle of the block grid (the leftover tiles of the last block column
+// are taken transposed, e.g. (3, [1, 3]) for T = 4).  Per K-step of 32 points:
 //
-// K2 (gram_tc_reduce): fixed-order fp64 sum of the chunk partials -> G,
-// mirrored to the lower triangle.  Deterministic.
+//   * the MMA warp bulk-copies chunks of 8 steps' points into a shared-memory
+//     ring (cp.async.bulk, mbarrier complete_tx), independent of the MMAs;
+//   * 16 producer warps regenerate the step's feature values (a3: omega.x in
+//     radians, one projection and one MUFU sin/cos pair per frequency and
+//     point), split each as x = hi + lo in fp16 (|x - hi - lo| <= 2^-22 |x| +
+//     2^-25) and store them in shared memory (canonical K-major, no swizzle);
+//   * one elected lane of the MMA warp issues per 16-point K-slice
+//         D += A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T
+//     (tcgen05.mma kind::f16, A and B from shared memory, M = 128, N = 256
+//     over both tiles, fp32 accumulate in TMEM).  On a diagonal tile the B
+//     copy of the block holds 2 lo and the third product is skipped:
+//     A_hi B_hi^T + A_hi (2 B_lo)^T = P + 2X, and G = (D + D^T) / 2.
+//
+// Measured on B200 (tools/microbench): the tensor core's shared-memory
+// operand reads do not slow down under ~100 B/cycle of concurrent STS, so
+// both operands come from shared memory and all of TMEM holds accumulators.
+//
+// Precision: the tensor core's fp32 accumulator is not round-to-nearest
+// (measured: the error grows with the number of accumulating MMAs; G and C^
+// leave the 1e-4 gate at 2048 points per accumulation on cfg 3), so D
+// accumulates for an *epoch* of 16 K-steps (512 points); the producer warps
+// then add it into a second TMEM accumulator L (tcgen05.ld, round-to-nearest
+// fp32 adds, tcgen05.st: ~530 cycles per 128 x 256 drain, measured) while the
+// MMA warp waits.  At the end of a unit segment L + D goes to a per-segment
+// partial; K2 (gram_tc_reduce) sums the partials in a fixed order in fp64 --
+// deterministic.
+//
+// Scheduling: one persistent CTA per SM.  The work items (cloud, unit, K-step)
+// are laid out linearly and cut into contiguous CTA ranges of equal *cost*,
+// so a CTA's range spans one or a few unit segments and no wave is left
+// partly empty.
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <vector>
+
 #include "rfd_internal.h"
 #include "tc_ptx.cuh"
 
 namespace rfd {
 namespace {
 
-constexpr int kBlk = 128;           // features per block (64 frequencies)
-constexpr int kStepPts = 64;        // points per K-step (4 MMA K-slices of 16)
-constexpr int kProducers = 512;     // 16 feature-producer warps
-constexpr int kThreads = 544;       // + 1 MMA-issue warp (warp 16)
-constexpr int kMaxLocal = 3;        // feature blocks per unit
-// Per operand (Hi or Lo), per block: 128 rows x 64 points x 2 B = 16 KB.
-constexpr int kBlkBytes = kBlk * kStepPts * 2;
-constexpr int kStageBytes = 2 * kMaxLocal * kBlkBytes;  // Hi + Lo: 96 KB
+// Debug bounds checks (compile with -DRFD_GRAM_CHECK): trap on the first
+// out-of-range shared/global access, naming it.
+#ifdef RFD_GRAM_CHECK
+__device__ int g_check_count;
+#define RFD_CHECK(cond, what, a, b)                                                      \
+  do {                                                                                   \
+    if (!(cond) && atomicAdd(&g_check_count, 1) < 8)                                     \
+      printf("gram check failed: %s (%lld, %lld) cta %d warp %d lane %d\n", what,       \
+             (long long)(a), (long long)(b), blockIdx.x, threadIdx.x / 32, threadIdx.x % 32); \
+  } while (0)
+// bounded wait: report (barrier tag, step) after ~2^26 probes, then give up
+__device__ __forceinline__ void dbg_wait(uint64_t* bar, uint32_t par, int tag, int it) {
+  for (long long i = 0; !tc::mbar_try_wait(bar, par); ++i)
+    if (i == (1LL << 22)) {
+      if (threadIdx.x % 32 == 0)
+        printf("gram wait stuck: tag %d step %d cta %d warp %d state %llx\n", tag, it, blockIdx.x,
+               threadIdx.x / 32, (unsigned long long)*reinterpret_cast<volatile uint64_t*>(bar));
+      return;
+    }
+}
+#define RFD_WAIT(bar, par, tag, it) dbg_wait((bar), (par), (tag), (it))
+#else
+#define RFD_WAIT(bar, par, tag, it) tc::mbar_wait((bar), (par))
+#define RFD_CHECK(cond, what, a, b) \
+  do {                              \
+  } while (0)
+#endif
+
+constexpr int kBlk = 128;           // feature rows per block
+constexpr int kFreqs = 64;          // frequencies per block
+constexpr int kStep = 64;           // points per K-step (4 MMA K-slices of 16)
 constexpr int kStages = 2;
-// K-steps per TMEM accumulation epoch: the tensor core accumulates at most
-// kEpoch * 12 MMA updates in fp32 before the sum moves to registers, which
-// bounds the accumulator's round-toward-zero bias.
-constexpr int kEpoch = 8;
+constexpr int kProducerWarps = 16;
+constexpr int kMmaWarp = kProducerWarps;        // MMA issue
+constexpr int kLoadWarp = kProducerWarps + 1;   // point loads
+constexpr int kThreads = (kProducerWarps + 2) * 32;
+constexpr int kEpoch = 8;           // K-steps per TMEM accumulation epoch (power of 2)
+constexpr int kMaxCtas = 160;
+// Shared memory per stage (canonical K-major fp16 operands, 16 KB each):
+//   [B hi: slot 0 rows | slot 1 rows][B lo: slot 0 | slot 1][A hi][A lo]
+// (the N = 256 B operand is one 256-row matrix).  A hi is unused when the A
+// block is a B block (its descriptor points at that slot's B hi).
+constexpr uint32_t kOpBytes = kBlk * kStep * 2;   // 16 KB
+constexpr uint32_t kBHi = 0, kBLo = 2 * kOpBytes, kAHi = 4 * kOpBytes, kALo = 5 * kOpBytes;
+constexpr uint32_t kStageBytes = 6 * kOpBytes;    // 96 KB
 // Canonical K-major layout (no swizzle): offset(row, k) = (row/8)*kSBO +
 // (k/8)*kLBO + (row%8)*16 + (k%8)*2.
 constexpr uint32_t kLBO = 128;
-constexpr uint32_t kSBO = (kStepPts / 8) * 128;  // 1024
+constexpr uint32_t kSBO = (kStep / 8) * 128;      // 1024
+// Point ring: kChunks chunks of kChunkSteps K-steps, refilled as soon as the
+// producers are done with a chunk (no dependence on MMA completion).
+constexpr int kChunkSteps = 4;
+constexpr int kChunks = 4;
+// Points in the Gram layout: groups of 8 points, 128 B each: x[8] | y[8] |
+// z[8] | pad[8] (packed FP32 pairs load straight into register pairs);
+// each cloud padded with zero groups to whole K-steps.
+constexpr uint32_t kGroupBytes = 128;
+constexpr uint32_t kStepBytes = (kStep / 8) * kGroupBytes;    // 1 KB
+constexpr uint32_t kChunkBytes = kChunkSteps * kStepBytes;    // 4 KB
+constexpr int kMaxFreqs = 512;                               // RFD_MAX_M
+constexpr int kRingOff = kStages * int(kStageBytes);
+constexpr int kOmegaOff = kRingOff + kChunks * int(kChunkBytes);
+constexpr int kSmemBytes = kOmegaOff + kMaxFreqs * 16;  // 216 KB
+// TMEM columns: epoch accumulator D [0, 256), long-term sum L [256, 512).
+constexpr uint32_t kColL = 256;
 
 struct GramUnit {
-  int ngrp;
-  int a_blk[2];   // global feature block of the A rows of group g
-  int b_blk[2];   // first global block of the B rows of group g
-  int nb[2];      // B blocks (1 or 2) -> N = 128 nb
-  int nloc;       // distinct global blocks, local order
-  int loc[kMaxLocal];
+  int a;     // A block (accumulator rows)
+  int nb;    // tiles (1 or 2)
+  int b[2];  // B block of tile tau
 };
 
-__host__ __device__ inline int local_of(const GramUnit& U, int blk) {
-  for (int i = 0; i < U.nloc; ++i)
-    if (U.loc[i] == blk) return i;
-  return 0;
-}
-
-__host__ __device__ inline void add_loc(GramUnit& U, int blk) {
-  for (int i = 0; i < U.nloc; ++i)
-    if (U.loc[i] == blk) return;
-  U.loc[U.nloc++] = blk;
-}
-
-// Enumerate units for T feature blocks: all pair units (i, [j, j+1]) row by
-// row, then the row-end single tiles (i, T-1) two at a time.
-__host__ __device__ inline int gram_units(int T, int u_want, GramUnit* out) {
+// Units covering the upper triangle of the T x T block grid: (i, [j, j+1])
+// for j = i, i+2, ... while j+1 < T; the leftover tiles (i, T-1), (T-i) odd,
+// paired as transposed tiles (T-1, [i1, i2]).
+__host__ __device__ inline int gram_units(int T, int want, GramUnit* out) {
   int u = 0;
   for (int i = 0; i < T; ++i)
     for (int j = i; j + 1 < T; j += 2) {
-      if (u == u_want && out) {
-        GramUnit U{};
-        U.ngrp = 1;
-        U.a_blk[0] = i; U.b_blk[0] = j; U.nb[0] = 2;
-        add_loc(U, j); add_loc(U, j + 1); add_loc(U, i);
-        *out = U;
-      }
+      if (u == want) *out = GramUnit{i, 2, {j, j + 1}};
       ++u;
     }
-  int singles[16];
-  int ns = 0;
-  for (int i = 0; i < T; ++i)
-    if ((T - i) % 2 == 1) singles[ns++] = i;
-  for (int s = 0; s < ns; s += 2) {
-    if (u == u_want && out) {
-      GramUnit U{};
-      U.ngrp = (s + 1 < ns) ? 2 : 1;
-      for (int g = 0; g < U.ngrp; ++g) {
-        U.a_blk[g] = singles[s + g]; U.b_blk[g] = T - 1; U.nb[g] = 1;
-      }
-      add_loc(U, T - 1);
-      for (int g = 0; g < U.ngrp; ++g) add_loc(U, U.a_blk[g]);
-      *out = U;
+  int first = -1;
+  for (int i = 0; i < T; ++i) {
+    if ((T - i) % 2 == 0) continue;
+    if (first < 0) {
+      first = i;
+      continue;
     }
+    if (u == want) *out = GramUnit{T - 1, 2, {first, i}};
+    ++u;
+    first = -1;
+  }
+  if (first >= 0) {
+    if (u == want) *out = GramUnit{T - 1, 1, {first, first}};
     ++u;
   }
   return u;
 }
 
-__device__ __forceinline__ void sincos_rad(float4 w, float4 x, float& c, float& s) {
-  // w = fp32(2 pi omega): the argument in radians; MUFU reduces it in turns.
-  const float t = fmaf(w.z, x.z, fmaf(w.y, x.y, w.x * x.x));
-  __sincosf(t, &s, &c);
+// Work partition, passed by value (<= 1.4 KB of kernel parameters).
+struct Sched {
+  int G;          // CTAs
+  int T;          // feature blocks
+  int U;          // units per cloud
+  int batch;
+  int64_t S;      // K-steps per unit per cloud
+  int64_t start[kMaxCtas + 1];  // first linear item (cloud*U + unit)*S + step of each CTA
+};
+
+
+// Producer-warp drain of a finished epoch: columns [64 q, 64 q + 64) of the
+// warp's 32 TMEM lanes.  L = D (first epoch of a segment) or L += D
+// (round-to-nearest fp32); on the segment's last epoch L + D goes to the
+// segment partial (row-major [128][256] fp32) instead.  Arrives on acce once
+// D has been read.
+__device__ __forceinline__ void drain_epoch(uint32_t tm_lane, int q, int lane, int nb, bool first,
+                                            bool last, float* row_out, uint64_t* acce_bar,
+                                            bool skip = false) {
+  tc::tc_fence_after();
+  if (q * 64 < nb * 128 && !skip) {
+    float4* o = reinterpret_cast<float4*>(row_out + q * 64);
+    RFD_CHECK(nb == 1 || nb == 2, "nb", nb, q);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const uint32_t col = uint32_t(q * 64 + h * 16);
+      float v[16];
+      tc::tmem_ld16(tm_lane + col, v);
+      if (!first) {
+        float w[16];
+        tc::tmem_ld16(tm_lane + kColL + col, w);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] += w[j];
+      }
+      if (last) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          o[4 * h + j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      } else {
+        uint32_t u[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) u[j] = __float_as_uint(v[j]);
+        tc::tmem_st16(tm_lane + kColL + col, u);
+      }
+    }
+    tc::tmem_st_wait();
+  }
+  tc::tc_fence_before();
+  __syncwarp();
+  if (lane == 0) tc::mbar_arrive(acce_bar);  // D is free again
 }
 
+// Diagnostics: per-step timestamps of CTA 0 (mode 3).
+__device__ long long g_trace[4096][4];
+
+// kMode (diagnostics only, RFD_GRAM_MODE): 0 = normal, 1 = no MMAs issued,
+// 2 = no feature generation (the pipeline still runs; results are wrong).
+template <int kMode>
 __global__ void __launch_bounds__(kThreads, 1)
-gram_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4, int m,
-               int64_t n, int T, int nunits, int chunks, int64_t chunk,
-               float* __restrict__ partial) {
+gram_tc_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict__ omega4, int m,
+               int64_t n, const __grid_constant__ Sched sc, float* __restrict__ partial) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t mma_bar[kStages];
-  __shared__ uint32_t tmem_base_sh;
-  __shared__ float4 xs[2][kStepPts + kStepPts / 8];  // padded: point p at p + p/8
+  __shared__ uint64_t full_bar[kStages], empty_bar[kStages], pts_bar[kChunks], pts_empty[kChunks];
+  __shared__ uint64_t accf_bar, acce_bar;
+  __shared__ uint32_t tmem_sh;
 
-  const int unit = blockIdx.x, ch = blockIdx.y, b = blockIdx.z;
+  const int cta = blockIdx.x;
+  const int64_t L0 = sc.start[cta], L1 = sc.start[cta + 1];
+  if (L0 >= L1) return;
+  const int nsteps = int(L1 - L0);
+  const int Si = int(sc.S);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  GramUnit U;
-  gram_units(T, unit, &U);
-  const int nloc = U.nloc, ngrp = U.ngrp;
+  const uint32_t sbase = tc::smem_addr(smem);
 
-  if (warp == 0) tc::tmem_alloc<512>(&tmem_base_sh);
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) tc::mbar_init(&mma_bar[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&full_bar[s], kProducerWarps);
+      tc::mbar_init(&empty_bar[s], 1);
+    }
+    for (int c = 0; c < kChunks; ++c) {
+      tc::mbar_init(&pts_bar[c], 1);
+      tc::mbar_init(&pts_empty[c], kProducerWarps);
+    }
+    tc::mbar_init(&accf_bar, 1);
+    tc::mbar_init(&acce_bar, kProducerWarps);
     tc::mbar_fence_init();
   }
-  const int64_t p0 = int64_t(ch) * chunk;
-  const int64_t p1 = min(p0 + chunk, n);
-  const float4* cloud = pts + int64_t(b) * n;
-  // xs holds a step's points with one float4 of padding per 8 (point p at
-  // p + p/8): the point groups of an 8-lane phase hit distinct banks.
-  if (tid < kStepPts)
-    xs[0][tid + (tid >> 3)] =
-        (p0 + tid < p1) ? __ldg(cloud + p0 + tid) : make_float4(0.f, 0.f, 0.f, 0.f);
+  {  // omega table (rows of padding frequencies >= m are zero)
+    float4* om_s = reinterpret_cast<float4*>(smem + kOmegaOff);
+    for (int k = tid; k < sc.T * kFreqs; k += kThreads)
+      om_s[k] = (k < m) ? __ldg(omega4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  const uint32_t tmem = tmem_base_sh;
-  const uint32_t sbase = tc::smem_addr(smem);
+  const uint32_t tmem = tmem_sh;
 
-  // Tasks: each thread owns one frequency fl (0..63) of every local block and
-  // one point group q (8 points).  Lane bits: [1:0] -> fl % 4, [2] -> q & 1,
-  // [4:3] -> q >> 1; warps take consecutive groups of 4 frequencies.  Lanes
-  // with odd q store their sin row first, so each 8-lane phase of a 16-byte
-  // store covers all 8 rows of a core matrix: no bank conflicts.
-  const int q = (((lane >> 3) & 3) << 1) | ((lane >> 2) & 1);
-  const int fl = 4 * warp + (lane & 3), odd = q & 1;
-  float4 w[kMaxLocal];
-#pragma unroll
-  for (int i = 0; i < kMaxLocal; ++i) {
-    const int k = (i < nloc) ? U.loc[i] * 64 + fl : m;
-    w[i] = (k < m) ? omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  const uint32_t grp_off = uint32_t((2 * fl) / 8) * kSBO + uint32_t(q) * kLBO;
-  const uint32_t off_first = grp_off + uint32_t((2 * fl + odd) % 8) * 16;
-  const uint32_t off_second = grp_off + uint32_t((2 * fl + 1 - odd) % 8) * 16;
+  // Step walk (all 32-bit): unit segment bu = cloud * U + unit; the CTA's
+  // steps of a segment are it in [seg_lo, seg_hi).
+  const int bu0 = int(L0 / sc.S), t0 = int(L0 - int64_t(bu0) * sc.S);
+  const int hi0 = int(min(L1, int64_t(bu0 + 1) * sc.S) - L0);
 
-  // MMA operand offsets (thread 0): local block of A rows / first B rows.
-  uint32_t a_off[2] = {0, 0}, b_off[2] = {0, 0}, idesc[2];
-#pragma unroll
-  for (int g = 0; g < 2; ++g) {
-    a_off[g] = uint32_t(local_of(U, U.a_blk[g])) * kBlkBytes;
-    b_off[g] = uint32_t(local_of(U, U.b_blk[g])) * kBlkBytes;
-    idesc[g] = tc::make_idesc(0, 128, 128 * U.nb[g]);
-  }
-
-  // fp32 register accumulators: TMEM lane group warp % 4, column quarter
-  // warp / 4 (64 of the 256 accumulator columns).
-  const int lg = warp & 3, quarter = warp >> 2;
-  float acc[64];
-#pragma unroll
-  for (int j = 0; j < 64; ++j) acc[j] = 0.0f;
-  const int ncols = (ngrp == 2) ? 256 : 128 * U.nb[0];
-  const bool drains = quarter * 64 < ncols;
-  const uint32_t lane_base = tmem + (uint32_t(lg * 32) << 16) + uint32_t(quarter * 64);
-  auto drain = [&](int dslot) {
-    if (!drains || tid >= kProducers) return;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      float v[32];
-      tc::tmem_ld32(lane_base + uint32_t(dslot * 256 + c * 32), v);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) acc[c * 32 + j] += v[j];
-    }
-  };
-
-  const int nsteps = int((p1 - p0 + kStepPts - 1) / kStepPts);
-  for (int t = 0; t < nsteps; ++t) {
-    const int s = t % kStages;
-    const int slot = (t / kEpoch) & 1;
-    if (t >= kStages) tc::mbar_wait(&mma_bar[s], ((t - kStages) / kStages) & 1);
-    const uint32_t hi_base = sbase + s * kStageBytes;
-    const uint32_t lo_base = hi_base + kMaxLocal * kBlkBytes;
-    const int64_t base = p0 + int64_t(t) * kStepPts;
-    const float4* xt = xs[t & 1];
-    // Next step's points: load now (the global-memory latency hides behind
-    // this step's feature generation), store to shared memory at the end.
-    float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (tid < kStepPts) {
-      const int64_t pn = base + kStepPts + tid;
-      if (pn < p1) xn = __ldg(cloud + pn);
-    }
-#pragma unroll
-    for (int i = 0; i < kMaxLocal; ++i) {
-      if (i >= nloc || tid >= kProducers) break;
-      float c[8], sn[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) sincos_rad(w[i], xt[q * 9 + j], c[j], sn[j]);
-      if (base + q * 8 + 8 > p1) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (base + q * 8 + j >= p1) { c[j] = 0.f; sn[j] = 0.f; }
-      }
-      uint32_t fh[4], fl_[4], sh[4], sl[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        uint32_t chh, cll, shh, sll;
-        tc::split_f16x2(c[2 * j], c[2 * j + 1], chh, cll);
-        tc::split_f16x2(sn[2 * j], sn[2 * j + 1], shh, sll);
-        fh[j] = odd ? shh : chh;  fl_[j] = odd ? sll : cll;
-        sh[j] = odd ? chh : shh;  sl[j] = odd ? cll : sll;
-      }
-      const uint32_t ob = uint32_t(i) * kBlkBytes;
-      tc::st_shared_v4(hi_base + ob + off_first, fh[0], fh[1], fh[2], fh[3]);
-      tc::st_shared_v4(lo_base + ob + off_first, fl_[0], fl_[1], fl_[2], fl_[3]);
-      tc::st_shared_v4(hi_base + ob + off_second, sh[0], sh[1], sh[2], sh[3]);
-      tc::st_shared_v4(lo_base + ob + off_second, sl[0], sl[1], sl[2], sl[3]);
-    }
-    // The next step's points become visible after this step's barrier.
-    if (tid < kStepPts) xs[(t + 1) & 1][tid + (tid >> 3)] = xn;
-    tc::fence_proxy_async_smem();
-    tc::tc_fence_before();
-    __syncthreads();
-    if (warp == kProducers / 32) {
-      // MMA warp: warp-uniform issue (descriptors in uniform registers), one
-      // elected lane; the producer warps go straight on to the next step.
-      tc::tc_fence_after();
-      if (tc::elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < kStepPts / 16; ++kk) {
-          const uint32_t koff = uint32_t(kk) * 2 * kLBO;
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            if (g >= ngrp) break;
-            const uint64_t aH = tc::make_sdesc(hi_base + a_off[g] + koff, kLBO, kSBO);
-            const uint64_t aL = tc::make_sdesc(lo_base + a_off[g] + koff, kLBO, kSBO);
-            const uint64_t bH = tc::make_sdesc(hi_base + b_off[g] + koff, kLBO, kSBO);
-            const uint64_t bL = tc::make_sdesc(lo_base + b_off[g] + koff, kLBO, kSBO);
-            const uint32_t d = tmem + uint32_t(slot * 256 + g * 128);
-            // The first MMA of an epoch starts its TMEM slot afresh.
-            const uint32_t acc0 = ((t % kEpoch) > 0 || kk > 0) ? 1u : 0u;
-            tc::mma_f16(d, aH, bH, idesc[g], acc0);
-            tc::mma_f16(d, aH, bL, idesc[g], 1u);
-            tc::mma_f16(d, aL, bH, idesc[g], 1u);
+  if (warp == kLoadWarp) {
+    // ============================================ point loads
+    // Chunk ch = CTA steps [4 ch, 4 ch + 4) into ring slot ch % kChunks: one
+    // bulk copy (cp.async.bulk, mbarrier complete_tx) per run of steps inside
+    // one unit segment (contiguous groups), independent of the MMAs.
+    const int nchunks = (nsteps + kChunkSteps - 1) / kChunkSteps;
+    const int64_t cloud_bytes = int64_t(Si) * kStepBytes;
+    int l_bu = bu0, l_t = t0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      // a ring slot is refilled once the producers are done with its previous
+      // chunk (pts_empty: one phase per use of the slot -- waiting on a stage
+      // barrier instead could alias phases two uses apart)
+      if (ch >= kChunks) RFD_WAIT(&pts_empty[ch % kChunks], uint32_t(ch / kChunks - 1) & 1u, 1, ch);
+      const int i0 = ch * kChunkSteps, i1 = min(nsteps, i0 + kChunkSteps);
+      uint64_t* bar = &pts_bar[ch % kChunks];
+      unsigned char* dst = smem + kRingOff + (ch % kChunks) * kChunkBytes;
+      if (lane == 0) {
+        // arm first (arrive + expect the chunk's bytes), then copy
+        tc::mbar_arrive_expect_tx(bar, uint32_t(i1 - i0) * kStepBytes);
+        for (int i = i0; i < i1;) {
+          const int run = min(i1 - i, Si - l_t);
+          RFD_CHECK(l_bu / sc.U < sc.batch && l_t + run <= Si && (i - i0 + run) <= kChunkSteps,
+                    "bulk", l_bu, l_t);
+          tc::bulk_g2s(dst + (i - i0) * kStepBytes,
+                       gpts + int64_t(l_bu / sc.U) * cloud_bytes + int64_t(l_t) * kStepBytes,
+                       uint32_t(run) * kStepBytes, bar);
+          i += run;
+          l_t += run;
+          if (l_t == Si) {
+            l_t = 0;
+            ++l_bu;
           }
         }
-        tc::mma_commit(&mma_bar[s]);
       }
       __syncwarp();
     }
-    // One step into epoch e+1, epoch e (the other TMEM slot) is complete --
-    // the wait at the top of this step covered step t-2, its last MMA -- so
-    // move it into the fp32 registers (round-to-nearest adds).
-    if (t % kEpoch == 1 && t > kEpoch) {
+  } else if (warp == kMmaWarp) {
+    // ============================================ MMA issue
+    // The whole warp walks the steps (warp-uniform state: descriptors live in
+    // uniform registers); one elected lane issues each tcgen05 op.
+    int m_lo = 0, m_hi = hi0, m_bu = bu0, epoch = 0;
+    // unit shape: nb - 1 | diag slot 0 << 1 | diag slot 1 << 2 | A is a B slot << 3
+    auto unit_bits = [&](int u) {
+      GramUnit X;
+      gram_units(sc.T, u, &X);
+      const int d0 = X.b[0] == X.a, d1 = X.nb > 1 && X.b[1] == X.a;
+      return (X.nb - 1) | (d0 << 1) | (d1 << 2);
+    };
+    int ub = unit_bits(m_bu % sc.U);
+    for (int it = 0; it < nsteps; ++it) {
+      const int s = it % kStages;
+      const int k = it - m_lo;
+      const bool efirst = (k & (kEpoch - 1)) == 0;
+      const bool elast = ((k + 1) & (kEpoch - 1)) == 0 || it + 1 == m_hi;
+      if (kMode == 4 && cta == 0 && it < 4096 && lane == 0) g_trace[it][0] = clock64();
+      if (efirst && epoch > 0) RFD_WAIT(&acce_bar, uint32_t(epoch - 1) & 1u, 2, it);
+      if (kMode == 4 && cta == 0 && it < 4096 && lane == 0) g_trace[it][1] = clock64();
+      RFD_WAIT(&full_bar[s], uint32_t(it / kStages) & 1u, 3, it);
+      if (kMode == 4 && cta == 0 && it < 4096 && lane == 0) g_trace[it][2] = clock64();
       tc::tc_fence_after();
-      drain(slot ^ 1);
-      tc::tc_fence_before();
-    }
-  }
-  if (nsteps > 0) {
-    tc::mbar_wait(&mma_bar[(nsteps - 1) % kStages], ((nsteps - 1) / kStages) & 1);
-    tc::tc_fence_after();
-    const int last_e = (nsteps - 1) / kEpoch;
-    if (last_e >= 1 && (nsteps - 1) % kEpoch == 0) drain((last_e - 1) & 1);
-    drain(last_e & 1);
-  }
-
-  // partial[b][ch][unit][col (256)][row (128)] fp32 (rows contiguous).
-  float* out = partial + ((int64_t(b) * chunks + ch) * nunits + unit) * (256 * 128);
-  const int row = lg * 32 + lane;
-  if (drains && tid < kProducers) {
+      __syncwarp();
+      const uint32_t stage = sbase + uint32_t(s) * kStageBytes;
+      const int nb = (ub & 1) + 1;
+      const bool d0 = (ub >> 1) & 1, d1 = (ub >> 2) & 1;
+      // A hi aliases the diagonal slot's B hi
+      const uint32_t a_hi = stage + (d0 ? kBHi : (d1 ? kBHi + kOpBytes : kAHi));
+      const uint32_t a_lo = stage + kALo;
+      const uint32_t idesc_n = tc::make_idesc(0, 128, 128 * nb);
+      const uint32_t idesc_1 = tc::make_idesc(0, 128, 128);
+      if (tc::elect_one()) {
 #pragma unroll
-    for (int j = 0; j < 64; ++j) out[int64_t(quarter * 64 + j) * 128 + row] = acc[j];
+        for (int kk = 0; kk < kStep / 16; ++kk) {
+          const uint32_t ko = uint32_t(kk) * 2u * kLBO;
+          const uint64_t ahi = tc::make_sdesc(a_hi + ko, kLBO, kSBO);
+          const uint64_t alo = tc::make_sdesc(a_lo + ko, kLBO, kSBO);
+          const uint64_t bhi = tc::make_sdesc(stage + kBHi + ko, kLBO, kSBO);
+          const uint64_t blo = tc::make_sdesc(stage + kBLo + ko, kLBO, kSBO);
+          const uint32_t acc0 = (efirst && kk == 0) ? 0u : 1u;
+          if (kMode != 1 && kMode != 3) {
+            tc::mma_f16(tmem, ahi, bhi, idesc_n, acc0);
+            tc::mma_f16(tmem, ahi, blo, idesc_n, 1u);
+            if (!d0 && !d1) {
+              tc::mma_f16(tmem, alo, bhi, idesc_n, 1u);
+            } else if (nb == 2) {  // the off-diagonal tile only
+              const uint32_t t = d0 ? 1u : 0u;
+              tc::mma_f16(tmem + 128u * t, alo,
+                          tc::make_sdesc(stage + kBHi + t * kOpBytes + ko, kLBO, kSBO), idesc_1,
+                          1u);
+            }
+          }
+        }
+        tc::mma_commit(&empty_bar[s]);
+        if (elast) tc::mma_commit(&accf_bar);
+      }
+      __syncwarp();
+      if (kMode == 4 && cta == 0 && it < 4096 && lane == 0) g_trace[it][3] = clock64();
+      if (elast) ++epoch;
+      if (it + 1 == m_hi && it + 1 < nsteps) {
+        ++m_bu;
+        m_lo = it + 1;
+        m_hi = min(nsteps, it + 1 + Si);
+        ub = unit_bits(m_bu % sc.U);
+      }
+    }
+  } else {
+    // ============================================ producers (+ drains)
+    const unsigned char* ring = smem + kRingOff;
+    const float4* om_s = reinterpret_cast<const float4*>(smem + kOmegaOff);
+    // Task = (frequency f of a block, 8-point group q): cos row f and sin row
+    // 64 + f for 8 points.  Warp w: q = w % 8, frequencies 32 (w / 8) + lane:
+    // the point loads are warp-wide broadcasts and an 8-lane store phase
+    // covers the 8 rows of one core matrix (no bank conflicts).  Every warp
+    // does one task of every local block per step.
+    const int q = warp & 7, f = 32 * (warp >> 3) + lane;
+    const uint32_t off_c = uint32_t(f >> 3) * kSBO + uint32_t(q) * kLBO + uint32_t(f & 7) * 16u;
+    const uint32_t off_s = off_c + 8u * kSBO;  // row 64 + f
+    const int lg = warp & 3, qd = warp >> 2;   // drain: TMEM lane group, column quarter
+    const uint32_t lane_field = uint32_t(32 * lg) << 16;
+    const int rho = 32 * lg + lane;
+
+    // Local blocks of the current unit, in task order: the A block first, then
+    // the B-only blocks.  Packed per local block i (8 bits): block (4 bits),
+    // bit 4: stored as B slot, bit 5: which slot, bit 6: stored as A.
+    int nloc = 1, locs = 0;
+    auto setup_unit = [&](int u) {
+      GramUnit U;
+      gram_units(sc.T, u, &U);
+      const bool dd0 = U.b[0] == U.a, dd1 = U.nb > 1 && U.b[1] == U.a;
+      locs = U.a | 0x40 | (dd0 ? 0x10 : (dd1 ? 0x30 : 0));
+      nloc = 1;
+      for (int tau = 0; tau < U.nb; ++tau)
+        if (U.b[tau] != U.a) locs |= (U.b[tau] | 0x10 | (tau << 5)) << (8 * nloc++);
+      return U.nb;
+    };
+    // Epochs awaiting their drain, oldest first (-1: none); info = segment id
+    // | (nb - 1) << 28 | first epoch of its segment << 29 | last << 30; last0/1
+    // = the epoch's last step.
+    int pend0 = -1, pend1 = -1, info0 = 0, info1 = 0, last0 = 0, last1 = 0;
+    auto drain0 = [&]() {
+      RFD_CHECK((info0 & 0x0FFFFFFF) < sc.G + sc.batch * sc.U, "seg", info0, pend0);
+      drain_epoch(tmem + lane_field, qd, lane, ((info0 >> 28) & 1) + 1, (info0 >> 29) & 1,
+                  (info0 >> 30) & 1,
+                  partial + (int64_t(info0 & 0x0FFFFFFF) * 128 + rho) * 256, &acce_bar,
+                  kMode == 5);
+      pend0 = pend1;
+      info0 = info1;
+      last0 = last1;
+      pend1 = -1;
+    };
+
+    const int tail = int(n - int64_t(Si - 1) * kStep);  // points of a unit's last step
+    int bu = bu0, seg_lo = 0, seg_hi = hi0, tail_it = Si - 1 - t0;
+    int nb = setup_unit(bu % sc.U);
+    int epoch = 0;
+    // Every wait is on ONE barrier (a thread parked in try_wait wakes on that
+    // barrier only).
+    for (int it = 0; it < nsteps; ++it) {
+      if (it == seg_hi) {
+        ++bu;
+        seg_lo = it;
+        seg_hi = min(nsteps, it + Si);
+        tail_it = it + Si - 1;
+        nb = setup_unit(bu % sc.U);
+      }
+      const int k = it - seg_lo;
+      const bool elast = ((k + 1) & (kEpoch - 1)) == 0 || it + 1 == seg_hi;
+      const int s = it % kStages;
+      const uint32_t ph = uint32_t(it / kStages) & 1u;
+      const int ch = it / kChunkSteps;
+      // drain the pending epoch right before a step whose stage needs an MMA
+      // of a later epoch (the MMA warp waits for the drain before that epoch)
+      while (pend0 >= 0 && it - kStages > last0) {
+        RFD_WAIT(&accf_bar, uint32_t(pend0) & 1u, 4, it);
+        __syncwarp();
+        drain0();
+      }
+      if (kMode == 3 && cta == 0 && it < 4096 && lane == 0 && warp == 5) g_trace[it][0] = clock64();
+      if (it >= kStages) RFD_WAIT(&empty_bar[s], ph ^ 1u, 5, it);
+      if (it % kChunkSteps == 0 || it == 0)  // a chunk's points arrive together
+        RFD_WAIT(&pts_bar[ch % kChunks], uint32_t(ch / kChunks) & 1u, 6, it);
+      __syncwarp();
+      if (kMode == 3 && cta == 0 && it < 4096 && lane == 0 && warp == 5) g_trace[it][1] = clock64();
+      const int cnt = (it == tail_it) ? tail : kStep;
+      const float* grp = reinterpret_cast<const float*>(
+          ring + (ch % kChunks) * kChunkBytes + (it % kChunkSteps) * kStepBytes + q * kGroupBytes);
+      float X[8], Y[8], Z[8];
+#pragma unroll
+      for (int j = 0; j < 8; j += 4) {
+        *reinterpret_cast<float4*>(X + j) = *reinterpret_cast<const float4*>(grp + j);
+        *reinterpret_cast<float4*>(Y + j) = *reinterpret_cast<const float4*>(grp + 8 + j);
+        *reinterpret_cast<float4*>(Z + j) = *reinterpret_cast<const float4*>(grp + 16 + j);
+      }
+      const uint32_t stage = sbase + uint32_t(s) * kStageBytes;
+      RFD_CHECK(stage + kStageBytes <= sbase + kRingOff, "stage", s, it);
+      RFD_CHECK((const unsigned char*)grp >= ring && (const unsigned char*)grp + 128 <= ring + kChunks * kChunkBytes, "ring", ch, it);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        if (i >= nloc || kMode == 2 || kMode == 4) break;
+        RFD_CHECK((locs >> (8 * i) & 15) < sc.T, "block", locs, i);
+        const int li = locs >> (8 * i);
+        const float4 wi = om_s[(li & 15) * kFreqs + f];
+        const float2 wx = make_float2(wi.x, wi.x), wy = make_float2(wi.y, wi.y),
+                     wz = make_float2(wi.z, wi.z);
+        // theta for two points per packed FP32 op (sm_100 FFMA2)
+        float c[8], sn[8];
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          const float2 th = __ffma2_rn(wz, make_float2(Z[j], Z[j + 1]),
+                                       __ffma2_rn(wy, make_float2(Y[j], Y[j + 1]),
+                                                  __fmul2_rn(wx, make_float2(X[j], X[j + 1]))));
+          __sincosf(th.x, &sn[j], &c[j]);
+          __sincosf(th.y, &sn[j + 1], &c[j + 1]);
+        }
+        if (cnt < kStep) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (q * 8 + j >= cnt) c[j] = sn[j] = 0.0f;
+        }
+        uint32_t ch_[4], cl[4], sh[4], sl[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          tc::split_f16x2_v2(make_float2(c[2 * j], c[2 * j + 1]), ch_[j], cl[j]);
+          tc::split_f16x2_v2(make_float2(sn[2 * j], sn[2 * j + 1]), sh[j], sl[j]);
+        }
+        if (li & 0x10) {  // B slot
+          const uint32_t sb = stage + uint32_t((li >> 5) & 1) * kOpBytes;
+          tc::st_shared_v4(sb + kBHi + off_c, ch_[0], ch_[1], ch_[2], ch_[3]);
+          tc::st_shared_v4(sb + kBHi + off_s, sh[0], sh[1], sh[2], sh[3]);
+          if (li & 0x40) {
+            // diagonal tile: A lo = lo, B lo = 2 lo (exact in fp16)
+            tc::st_shared_v4(stage + kALo + off_c, cl[0], cl[1], cl[2], cl[3]);
+            tc::st_shared_v4(stage + kALo + off_s, sl[0], sl[1], sl[2], sl[3]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              __half2 h = *reinterpret_cast<__half2*>(&cl[j]);
+              h = __hadd2(h, h);
+              cl[j] = *reinterpret_cast<uint32_t*>(&h);
+              h = *reinterpret_cast<__half2*>(&sl[j]);
+              h = __hadd2(h, h);
+              sl[j] = *reinterpret_cast<uint32_t*>(&h);
+            }
+          }
+          tc::st_shared_v4(sb + kBLo + off_c, cl[0], cl[1], cl[2], cl[3]);
+          tc::st_shared_v4(sb + kBLo + off_s, sl[0], sl[1], sl[2], sl[3]);
+        } else {  // A only
+          tc::st_shared_v4(stage + kAHi + off_c, ch_[0], ch_[1], ch_[2], ch_[3]);
+          tc::st_shared_v4(stage + kAHi + off_s, sh[0], sh[1], sh[2], sh[3]);
+          tc::st_shared_v4(stage + kALo + off_c, cl[0], cl[1], cl[2], cl[3]);
+          tc::st_shared_v4(stage + kALo + off_s, sl[0], sl[1], sl[2], sl[3]);
+        }
+      }
+      if (kMode == 3 && cta == 0 && it < 4096 && lane == 0 && warp == 5) g_trace[it][2] = clock64();
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tc::mbar_arrive(&full_bar[s]);
+        if (it % kChunkSteps == kChunkSteps - 1 || it == nsteps - 1)
+          tc::mbar_arrive(&pts_empty[ch % kChunks]);  // done with this chunk's points
+      }
+      if (kMode == 3 && cta == 0 && it < 4096 && lane == 0 && warp == 5) g_trace[it][3] = clock64();
+      if (elast) {
+        if (pend1 >= 0) {  // queue full: the oldest epoch's MMAs are all issued
+          RFD_WAIT(&accf_bar, uint32_t(pend0) & 1u, 7, it);
+          __syncwarp();
+          drain0();
+        }
+        const int info = (cta + bu) | ((nb - 1) << 28) | (k < kEpoch ? (1 << 29) : 0) |
+                         (it + 1 == seg_hi ? (1 << 30) : 0);
+        if (pend0 < 0) {
+          pend0 = epoch;
+          info0 = info;
+          last0 = it;
+        } else {
+          pend1 = epoch;
+          info1 = info;
+          last1 = it;
+        }
+        ++epoch;
+      }
+    }
+    while (pend0 >= 0) {
+      RFD_WAIT(&accf_bar, uint32_t(pend0) & 1u, 8, nsteps);
+      __syncwarp();
+      drain0();
+    }
   }
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
-__global__ void gram_tc_reduce_kernel(const float* __restrict__ partial, int r, int T, int nunits,
-                                      int chunks, double* __restrict__ G) {
-  // grid: (128*128/256, upper tiles, batch); tile t enumerates (ti <= tj).
-  const int b = blockIdx.z;
-  int t = blockIdx.y, ti = 0, row = T;
-  while (t >= row) { t -= row; ++ti; --row; }
-  const int tj = ti + t;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const int lr = e & 127, lc = e >> 7;  // row-fastest: coalesced partial reads
-  if (ti == tj && lr > lc) return;      // diagonal tile: upper half, mirrored
-  const int a = ti * kBlk + lr, c = tj * kBlk + lc;
-  if (a >= r || c >= r) return;
-  // find the unit / accumulator column of tile (ti, tj)
-  int unit = 0, col = 0;
-  for (int u = 0; u < nunits; ++u) {
-    GramUnit U;
-    gram_units(T, u, &U);
-    for (int g = 0; g < U.ngrp; ++g)
-      if (U.a_blk[g] == ti && tj >= U.b_blk[g] && tj < U.b_blk[g] + U.nb[g]) {
-        unit = u;
-        col = g * 128 + (tj - U.b_blk[g]) * 128;
-      }
+// Points -> Gram layout (groups of 8: x[8] y[8] z[8] 0[8]), clouds padded
+// with zero groups to S K-steps.  One thread per (padded) point.
+__global__ void gram_pack_kernel(const float4* __restrict__ pts, int64_t n, int64_t per_cloud,
+                                 int64_t total, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i / per_cloud, p = i - b * per_cloud;
+    const float4 v = (p < n) ? __ldg(pts + b * n + p) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float* g = out + (i >> 3) * 32 + (i & 7);
+    g[0] = v.x;
+    g[8] = v.y;
+    g[16] = v.z;
+    g[24] = 0.0f;
   }
-  const int64_t stride = int64_t(nunits) * 256 * 128;
-  const float* src = partial + (int64_t(b) * chunks * nunits + unit) * (256 * 128) +
-                     int64_t(col + lc) * 128 + lr;
-  double sum = 0.0;
-  for (int k = 0; k < chunks; ++k) sum += double(src[k * stride]);
-  double* Gb = G + int64_t(b) * r * r;
-  Gb[int64_t(a) * r + c] = sum;
-  Gb[int64_t(c) * r + a] = sum;
+}
+
+// K2: G[b] (interleaved r x r, fp64) from the segment partials, fixed order.
+// grid: (16 chunks x upper tiles, batch); tile (bi <= bj) of the block grid.
+__global__ void __launch_bounds__(256)
+gram_tc_reduce_kernel(const float* __restrict__ partial, int m, const __grid_constant__ Sched sc,
+                      double* __restrict__ G) {
+  __shared__ int segs[kMaxCtas];
+  __shared__ int nseg_sh;
+  const int b = blockIdx.y;
+  const int T = sc.T, r = 2 * m;
+  int tile = blockIdx.x >> 4;
+  const int chunk = blockIdx.x & 15;
+  int bi = 0, row = T;
+  while (tile >= row) {
+    tile -= row;
+    ++bi;
+    --row;
+  }
+  const int bj = bi + tile;
+  // the unit and accumulator tile holding (bi, bj), directly or transposed
+  int unit = 0, tau = 0;
+  bool transposed = false, found = false;
+  for (int u = 0; u < sc.U && !found; ++u) {
+    GramUnit X;
+    gram_units(T, u, &X);
+    for (int t = 0; t < X.nb && !found; ++t) {
+      if (X.a == bi && X.b[t] == bj) {
+        unit = u; tau = t; transposed = false; found = true;
+      } else if (X.a == bj && X.b[t] == bi) {
+        unit = u; tau = t; transposed = true; found = true;
+      }
+    }
+  }
+  const int64_t bu = int64_t(b) * sc.U + unit;
+  if (threadIdx.x == 0) {
+    int ns = 0;
+    const int64_t lo = bu * sc.S, hi = (bu + 1) * sc.S;
+    for (int c = 0; c < sc.G; ++c)
+      if (sc.start[c] < sc.start[c + 1] && sc.start[c] < hi && sc.start[c + 1] > lo)
+        segs[ns++] = int(c + bu);
+    nseg_sh = ns;
+  }
+  __syncthreads();
+  const int nseg = nseg_sh;
+  const bool diag = (bi == bj);
+#pragma unroll 1
+  for (int i = 0; i < 4; ++i) {
+    const int e = chunk * 1024 + i * 256 + threadIdx.x;
+    const int rr = e >> 7, cc = e & 127;  // cc fastest: coalesced partial reads
+    const int fr = bi * kFreqs + (rr & 63), fc = bj * kFreqs + (cc & 63);
+    if (fr >= m || fc >= m) continue;
+    // partial[seg][row (128)][col (256)]; element (x, y) of tile tau at x*256 + tau*128 + y
+    const int64_t o1 = transposed ? int64_t(cc) * 256 + tau * 128 + rr
+                                  : int64_t(rr) * 256 + tau * 128 + cc;
+    const int64_t o2 = int64_t(cc) * 256 + tau * 128 + rr;
+    double s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < nseg; ++k) {
+      const float* P = partial + int64_t(segs[k]) * (256 * 128);
+      s1 += double(P[o1]);
+      if (diag) s2 += double(P[o2]);
+    }
+    const double v = diag ? 0.5 * (s1 + s2) : s1;
+    const int a = 2 * fr + (rr >> 6), c = 2 * fc + (cc >> 6);
+    double* Gb = G + int64_t(b) * r * r;
+    Gb[int64_t(a) * r + c] = v;
+    Gb[int64_t(c) * r + a] = v;
+  }
+}
+
+Sched make_sched(int m, int64_t n, int batch, int sms) {
+  Sched sc{};
+  sc.T = (m + kFreqs - 1) / kFreqs;
+  sc.U = gram_units(sc.T, -1, nullptr);
+  sc.batch = batch;
+  sc.S = (n + kStep - 1) / kStep;
+  const int64_t items = int64_t(batch) * sc.U * sc.S;
+  int G = std::min(sms, kMaxCtas);
+  if (int64_t(G) > items) G = int(items);
+  sc.G = G;
+  // cost of one K-step of each unit: max(MMA cycles, MUFU cycles)
+  std::vector<int64_t> wgt(sc.U), pw(sc.U + 1, 0);
+  for (int u = 0; u < sc.U; ++u) {
+    GramUnit X;
+    gram_units(sc.T, u, &X);
+    int prod = 0, nloc = 1;
+    for (int t = 0; t < X.nb; ++t) {
+      prod += (X.b[t] == X.a) ? 2 : 3;
+      if (X.b[t] != X.a) ++nloc;
+    }
+    wgt[u] = std::max<int64_t>(int64_t(prod) * 128, int64_t(nloc) * 256);
+    pw[u + 1] = pw[u] + wgt[u];
+  }
+  const int64_t Wc = sc.S * pw[sc.U];
+  const int64_t total = int64_t(batch) * Wc;
+  for (int c = 0; c <= G; ++c) {
+    const int64_t target = (c == G) ? total : int64_t((__int128)total * c / G);
+    const int64_t b = target / Wc, rem = target - b * Wc;
+    int u = 0;
+    while (u + 1 < sc.U && pw[u + 1] * sc.S <= rem) ++u;
+    const int64_t tt = (rem - pw[u] * sc.S + wgt[u] - 1) / wgt[u];
+    int64_t L = (b * sc.U + u) * sc.S + tt;
+    if (L > items) L = items;
+    sc.start[c] = L;
+  }
+  sc.start[G] = items;
+  return sc;
 }
 
 }  // namespace
 
 GramGeom gram_tc_geometry(int m, int64_t n, int batch, int sms) {
+  const Sched sc = make_sched(m, n, batch, sms);
   GramGeom g;
   g.r = 2 * m;
   g.tile = kBlk;
-  g.tiles1d = (g.r + kBlk - 1) / kBlk;
-  g.ntiles = gram_units(g.tiles1d, -1, nullptr);  // units
-  // One CTA per SM (full TMEM); about three waves of CTAs.
-  int64_t chunks = 1;
-  const int64_t want = (3LL * sms + int64_t(g.ntiles) * batch - 1) / (int64_t(g.ntiles) * batch);
-  if (want > chunks) chunks = want;
-  const int64_t maxc = (n + kStepPts - 1) / kStepPts;
-  if (chunks > maxc) chunks = maxc;
-  if (chunks < 1) chunks = 1;
-  int64_t chunk = (n + chunks - 1) / chunks;
-  chunk = (chunk + kStepPts - 1) / kStepPts * kStepPts;
-  g.chunk = chunk;
-  g.chunks = int((n + chunk - 1) / chunk);
+  g.tiles1d = sc.T;
+  g.ntiles = sc.U;   // units
+  g.chunks = sc.G;   // persistent CTAs
+  g.chunk = sc.S;    // K-steps per unit
   return g;
 }
 
+// one partial per (CTA, unit segment) -- segment id = cta + cloud * U + unit --
+// followed by the points in the Gram layout (S K-steps per cloud)
+static size_t gram_tc_partial_only(const GramGeom& g, int batch) {
+  return size_t(g.chunks + int64_t(batch) * g.ntiles) * 256 * 128;
+}
 size_t gram_tc_partial_elems(const GramGeom& g, int batch) {
-  return size_t(batch) * g.chunks * g.ntiles * 256 * 128;
+  return gram_tc_partial_only(g, batch) + size_t(batch) * size_t(g.chunk) * (kStepBytes / 4);
 }
 
 void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
                     const GramGeom& g, float* partial, double* G, cudaStream_t s) {
-  const int smem = kStages * kStageBytes;
+  // same partition as gram_tc_geometry (G = g.chunks CTAs)
+  const Sched sc = make_sched(m, n, batch, g.chunks);
   static bool configured = false;
+  static int mode = 0;
   if (!configured) {
-    cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(gram_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemBytes);
+    cudaFuncSetAttribute(gram_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemBytes);
+    cudaFuncSetAttribute(gram_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemBytes);
+    cudaFuncSetAttribute(gram_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemBytes);
+    cudaFuncSetAttribute(gram_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemBytes);
+    cudaFuncSetAttribute(gram_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemBytes);
+    const char* e = getenv("RFD_GRAM_MODE");  // diagnostics only
+    mode = e ? atoi(e) : 0;
     configured = true;
   }
+  float* gpts = partial + gram_tc_partial_only(g, batch);
+  {
+    LaunchScope L("rfd_gram_pack", s);
+    const int64_t per_cloud = int64_t(g.chunk) * kStep, total = per_cloud * batch;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    gram_pack_kernel<<<int(blocks), 256, 0, s>>>(pts, n, per_cloud, total, gpts);
+  }
+  const unsigned char* gp = reinterpret_cast<const unsigned char*>(gpts);
   {
     LaunchScope L("rfd_gram_tc", s);
-    gram_tc_kernel<<<dim3(g.ntiles, g.chunks, batch), kThreads, smem, s>>>(
-        pts, omega4, m, n, g.tiles1d, g.ntiles, g.chunks, g.chunk, partial);
+    if (mode == 1)
+      gram_tc_kernel<1><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
+    else if (mode == 2)
+      gram_tc_kernel<2><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
+    else if (mode == 5)
+      gram_tc_kernel<5><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
+    else if (mode == 3 || mode == 4) {
+      if (mode == 3)
+        gram_tc_kernel<3><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
+      else
+        gram_tc_kernel<4><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
+      static long long h[4096][4];
+      cudaMemcpyFromSymbol(h, g_trace, sizeof(h));
+      for (int i = 0; i < 64; ++i)
+        fprintf(stderr, "it %3d t0 %7lld t1 %7lld t2 %7lld t3 %7lld\n", i,
+                h[i][0] - h[0][0], h[i][1] - h[0][0], h[i][2] - h[0][0], h[i][3] - h[0][0]);
+    } else
+      gram_tc_kernel<0><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
   }
   {
     LaunchScope L("rfd_gram_reduce", s);
-    const int tiles = g.tiles1d * (g.tiles1d + 1) / 2;
-    gram_tc_reduce_kernel<<<dim3(kBlk * kBlk / 256, tiles, batch), 256, 0, s>>>(
-        partial, g.r, g.tiles1d, g.ntiles, g.chunks, G);
+    const int tiles = sc.T * (sc.T + 1) / 2;
+    gram_tc_reduce_kernel<<<dim3(16 * tiles, batch), 256, 0, s>>>(partial, m, sc, G);
   }
 }
 

@@ -1,3 +1,4 @@
+#include <stdio.h>
 // Host side of the C ABI (include/rfd.h): argument validation, the plan
 // object (device buffers it owns), launch sequencing, status codes, launch
 // counting and event-based per-kernel timing.  No arithmetic of the method
@@ -72,6 +73,16 @@ void launch_begin(const char*, cudaStream_t s) {
 }
 void launch_end(const char* name, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  // RFD_SYNC_CHECK=1 (debugging): synchronize after every launch and name the
+  // kernel that faulted.
+  static const bool sync_check = [] {
+    const char* e = getenv("RFD_SYNC_CHECK");
+    return e && e[0] == '1';
+  }();
+  if (sync_check) {
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) fprintf(stderr, "rfd: kernel %s failed: %s\n", name, cudaGetErrorString(e));
+  }
   if (t_open_event) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaEvent_t b = take_event();
