@@ -46,6 +46,7 @@ pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   __shared__ __align__(1024) unsigned char bsm[kStages][2 * kBBytes];
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages], dfull_bar[2], dempty_bar[2];
   __shared__ uint32_t tmem_sh;
+  __shared__ float4 xbuf[kProducerWarps][8];  // each producer warp's 8 points of the chunk
 
   const int ft = blockIdx.x, rg = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, lg = warp & 3;
@@ -87,12 +88,18 @@ pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       return (c < nchunks && pp < p1 && je < dc) ? __ldg(Fb + pp * d + c0 + je) : 0.0f;
     };
     float f_next = load_f(0);
+    // The warp's 8 points, prefetched one chunk ahead by lanes 0-7 (global
+    // latency off the critical path) and handed over through shared memory.
+    auto load_x = [&](int c) {
+      const int64_t pp = p0 + int64_t(c) * kChunk + q * 8 + (lane & 7);
+      return __ldg(cloud + (pp < p1 ? pp : p1 - 1));
+    };
+    float4 x_next = load_x(0);
     for (int c = 0; c < nchunks; ++c) {
       const uint32_t s = c % kStages, u = c / kStages;
       const float fv = f_next;
       f_next = load_f(c + 1);
       if (u >= 1) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
-      const int64_t base = p0 + int64_t(c) * kChunk;
       {
         uint32_t hi, lo;
         tc::split_tf32(fv, hi, lo);
@@ -102,20 +109,13 @@ pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       // Points beyond the range (clamped loads) meet zero columns of F^T, and
       // lanes beyond m are never written out: no masking of the features.
       uint32_t chi[8], clo[8], shi[8], slo[8];
-      float4 xv[8];
-      const int64_t pb = base + q * 8;
-      if (pb + 8 <= p1) {
-        const float4* xp = cloud + pb;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) xv[j] = __ldg(xp + j);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) xv[j] = __ldg(cloud + (pb + j < p1 ? pb + j : p1 - 1));
-      }
+      if (lane < 8) xbuf[warp][lane] = x_next;
+      __syncwarp();
+      if (c + 1 < nchunks) x_next = load_x(c + 1);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         float cs, sn;
-        sincos_rad(w, xv[j], cs, sn);
+        sincos_rad(w, xbuf[warp][j], cs, sn);
         tc::split_tf32_fast(cs, chi[j], clo[j]);
         tc::split_tf32_fast(sn, shi[j], slo[j]);
       }

@@ -2,13 +2,17 @@
 // a8; the "x + A(...)" of Eq. 13).
 //
 // Per tile of 128 points the contraction Phi_tile (128 x r) . Y (r x 16) runs
-// as tcgen05.mma kind::tf32 with the A operand in TMEM: the 8 producer warps
-// regenerate each point's feature row (a3: omega.x in turns, MUFU sin/cos)
-// and write it, split x = hi + lo in tf32 (|x - hi - lo| <= 2^-22 |x|),
-// straight into TMEM with tcgen05.st -- row = point = TMEM lane, so no
-// shared-memory traffic for A.  Y^T (split likewise) sits in shared memory as
-// the B operand.  Per 32-feature chunk one thread issues
-//     D += A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T   (M=128, N=16, K=8 x 4)
+// as tcgen05.mma kind::f16 with the A operand in TMEM: the 16 producer warps
+// regenerate each point's feature row (a3: omega.x in radians, MUFU sin/cos)
+// and write it, split x = hi + lo in fp16 (|x - hi - lo| <= 2^-22 |x| +
+// 2^-25), straight into TMEM with tcgen05.st -- row = point = TMEM lane, so
+// no shared-memory traffic for A.  Y^T, scaled per channel by a power of two
+// into fp16 range (max |Y_j| 2^e_j <= 2^14; undone exactly in the epilogue)
+// and split likewise, sits in shared memory as the B operand.  Per 128-feature
+// chunk one thread issues
+//     D += A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T   (M=128, N=16, K=16 x 8)
+// (kind::f16 takes K = 16 per instruction, half the instructions of tf32:
+// with N = 16 the instruction issue, not the tensor math, sets the pace)
 // into a double-buffered TMEM accumulator; chunk stages are released by
 // tcgen05.commit -> mbarrier, so feature generation of the next chunk
 // overlaps the MMAs.  The epilogue (TMEM -> registers, + F, store) of tile t
@@ -25,10 +29,10 @@ constexpr int kMmaWarp = 16;
 constexpr int kEpiWarp0 = 17;                 // warps 17..20: epilogue
 constexpr int kThreads = 21 * 32;
 constexpr int kTile = 128;      // points per tile (= TMEM lanes)
-constexpr int kChunkF = 64;     // features per chunk (32 frequencies)
+constexpr int kChunkF = 128;    // features per chunk (64 frequencies)
 constexpr int kStages = 3;
 constexpr uint32_t kColD = 0;   // accumulators: cols [0,16) and [16,32)
-constexpr uint32_t kColA = 32;  // stage s: hi at 32 + 128 s, lo at +64
+constexpr uint32_t kColA = 32;  // stage s: hi at 32 + 128 s (64 cols = 128 fp16), lo at +64
 constexpr uint32_t kLBO = 128;
 
 __device__ __forceinline__ void sincos_rad(float4 w, float4 x, float& c, float& s) {
@@ -50,12 +54,14 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int lg = warp & 3;
-  const int nch = (m + 31) / 32;       // chunks of 32 frequencies
+  const int nch = (m + 63) / 64;       // chunks of 64 frequencies
   const int kpad = nch * kChunkF;      // padded feature count
-  const uint32_t sbo = uint32_t(kpad / 4) * 128;
-  unsigned char* yb = smem;                          // B hi: 16 x kpad tf32
-  unsigned char* yl = smem + 16 * kpad * 4;          // B lo
-  float4* om = reinterpret_cast<float4*>(smem + 2 * 16 * kpad * 4);
+  const uint32_t sbo = uint32_t(kpad / 8) * 128;
+  unsigned char* yb = smem;                          // B hi: 16 x kpad fp16
+  unsigned char* yl = smem + 16 * kpad * 2;          // B lo
+  float4* om = reinterpret_cast<float4*>(smem + 2 * 16 * kpad * 2);
+  __shared__ unsigned int ymax_bits[16];
+  __shared__ float yscale_inv[16];
   const uint32_t yb_s = tc::smem_addr(yb), yl_s = tc::smem_addr(yl);
 
   if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
@@ -71,14 +77,14 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
     tc::mbar_init(&yready_bar, 1);
     tc::mbar_fence_init();
   }
-  for (int k = tid; k < nch * 32; k += kThreads)
+  for (int k = tid; k < nch * 64; k += kThreads)
     om[k] = (k < m) ? omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = tmem_sh;
   const uint32_t lane_field = uint32_t(lg * 32) << 16;
-  const uint32_t idesc = tc::make_idesc(2, 128, 16);
+  const uint32_t idesc = tc::make_idesc(0, 128, 16);
 
   const int64_t tpc = (n + kTile - 1) / kTile;
   const int64_t ntiles = tpc * batch;
@@ -91,15 +97,37 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   // reading the old Y has completed.
   auto load_y = [&](int b) {
     const float* Yb = Y + int64_t(b) * 2 * m * d;
+    // per-channel power-of-two scale: max |Y_j| 2^e_j in [2^13, 2^14)
+    if (tid < 16) ymax_bits[tid] = 0u;
+    __syncthreads();
+    for (int e = tid; e < 16 * 2 * m; e += kThreads) {
+      const int a = e >> 4, j = e & 15;
+      if (j < dc) atomicMax(&ymax_bits[j], __float_as_uint(fabsf(Yb[int64_t(a) * d + c0 + j])));
+    }
+    __syncthreads();
+    float scale = 1.0f;
+    if (tid < 16) {
+      const float mx = __uint_as_float(ymax_bits[tid]);
+      int ex = 0;
+      if (mx > 0.0f && isfinite(mx)) {
+        frexpf(mx, &ex);  // mx = f 2^ex, f in [0.5, 1)
+        scale = ldexpf(1.0f, 14 - ex);
+      }
+      yscale_inv[tid] = 1.0f / scale;  // exact (power of two)
+      ymax_bits[tid] = __float_as_uint(scale);
+    }
+    __syncthreads();
     for (int e = tid; e < 16 * kpad; e += kThreads) {
       const int a = e >> 4, j = e & 15;
-      const float val = (a < 2 * m && j < dc) ? Yb[int64_t(a) * d + c0 + j] : 0.0f;
-      uint32_t hi, lo;
-      tc::split_tf32(val, hi, lo);
-      const uint32_t off = uint32_t(j >> 3) * sbo + uint32_t(a >> 2) * kLBO +
-                           uint32_t(j & 7) * 16 + uint32_t(a & 3) * 4;
-      *reinterpret_cast<uint32_t*>(yb + off) = hi;
-      *reinterpret_cast<uint32_t*>(yl + off) = lo;
+      const float val = (a < 2 * m && j < dc)
+                            ? Yb[int64_t(a) * d + c0 + j] * __uint_as_float(ymax_bits[j])
+                            : 0.0f;
+      const __half h = __float2half_rn(val);
+      const __half l = __float2half_rn(val - __half2float(h));
+      const uint32_t off = uint32_t(j >> 3) * sbo + uint32_t(a >> 3) * kLBO +
+                           uint32_t(j & 7) * 16 + uint32_t(a & 7) * 2;
+      *reinterpret_cast<__half*>(yb + off) = h;
+      *reinterpret_cast<__half*>(yl + off) = l;
     }
     tc::fence_proxy_async_smem();
   };
@@ -121,8 +149,8 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
     }
     const uint32_t buf = it & 1;
     if (warp < kProducerWarps) {
-      // ---------------- producers: 8 frequencies per warp per chunk --------
-      const int q = warp >> 2;  // which 8 of the chunk's 32 frequencies
+      // ---------------- producers: 16 frequencies per thread per chunk -----
+      const int q = warp >> 2;  // which 16 of the chunk's 64 frequencies
       // This tile's point (prefetched during the previous tile) and the next's.
       if (tile == t_begin) {
         const int64_t i0 = base + lg * 32 + lane;
@@ -137,22 +165,21 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       for (int c = 0; c < nch; ++c) {
         const uint32_t gg = g + c, s = gg % kStages, u = gg / kStages;
         if (u >= 1) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
-        float v[16];
-        const int f0 = 32 * c + 8 * q;
-        // Frequencies beyond m (zero omega) meet zero rows of Y^T: no masking.
-#pragma unroll
-        for (int j = 0; j < 8; ++j) sincos_rad(om[f0 + j], x, v[2 * j], v[2 * j + 1]);
-        // interleaved features: 2j = cos (first output of sincos_turns), 2j+1 = sin
-        uint32_t hi[16], lo[16];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          // sincos_rad(w, x, c, s) writes c then s: v[2j] = cos, v[2j+1] = sin
-          tc::split_tf32_fast(v[2 * j], hi[2 * j], lo[2 * j]);
-          tc::split_tf32_fast(v[2 * j + 1], hi[2 * j + 1], lo[2 * j + 1]);
-        }
         const uint32_t acol = tmem + lane_field + kColA + 128 * s + 16 * q;
-        tc::tmem_st16(acol, hi);
-        tc::tmem_st16(acol + 64, lo);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // two halves of 8 frequencies (register pressure)
+          float v[16];
+          const int f0 = 64 * c + 16 * q + 8 * h;
+          // Frequencies beyond m (zero omega) meet zero rows of Y^T: no masking.
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sincos_rad(om[f0 + j], x, v[2 * j], v[2 * j + 1]);
+          // interleaved features (2j = cos, 2j+1 = sin): one fp16 pair per column
+          uint32_t hi[8], lo[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) tc::split_f16x2(v[2 * j], v[2 * j + 1], hi[j], lo[j]);
+          tc::tmem_st8(acol + 8 * h, hi);
+          tc::tmem_st8(acol + 64 + 8 * h, lo);
+        }
         tc::tmem_st_wait();
         tc::tc_fence_before();
         __syncwarp();
@@ -171,14 +198,14 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
         if (tc::elect_one()) {
           const uint32_t a0 = tmem + kColA + 128 * s;
 #pragma unroll
-          for (int kk = 0; kk < kChunkF / 8; ++kk) {
+          for (int kk = 0; kk < kChunkF / 16; ++kk) {
             // start-address field (bits 0-13, 16-byte units) advances by
-            // (c * 16 + 2 kk) core matrices of 128 B
-            const uint64_t adv = uint64_t(c * (kChunkF / 4) + 2 * kk) * (kLBO >> 4);
+            // (c * 8 + 2 kk) core matrices of 128 B
+            const uint64_t adv = uint64_t(c * (kChunkF / 8) + 2 * kk) * (kLBO >> 4);
             const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
-            tc::mma_tf32_ts(dcol, a0 + 8 * kk, bh0 + adv, idesc, acc);
-            tc::mma_tf32_ts(dcol, a0 + 8 * kk, bl0 + adv, idesc, 1u);
-            tc::mma_tf32_ts(dcol, a0 + 64 + 8 * kk, bh0 + adv, idesc, 1u);
+            tc::mma_f16_ts(dcol, a0 + 8 * kk, bh0 + adv, idesc, acc);
+            tc::mma_f16_ts(dcol, a0 + 8 * kk, bl0 + adv, idesc, 1u);
+            tc::mma_f16_ts(dcol, a0 + 64 + 8 * kk, bh0 + adv, idesc, 1u);
           }
           tc::mma_commit(&empty_bar[s]);
           if (c == nch - 1) tc::mma_commit(&dfull_bar[buf]);
@@ -213,6 +240,8 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&dempty_bar[buf]);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] *= yscale_inv[j];
       if (i < n) {
         float* Oi = out + idx * d + c0;
         if (vec) {
@@ -238,8 +267,8 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
 }  // namespace
 
 size_t pass2_tc_smem(int m) {
-  const int nch = (m + 31) / 32;
-  return size_t(2) * 16 * nch * kChunkF * 4 + size_t(nch * 32) * sizeof(float4);
+  const int nch = (m + 63) / 64;
+  return size_t(2) * 16 * nch * kChunkF * 2 + size_t(nch * 64) * sizeof(float4);
 }
 
 void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
