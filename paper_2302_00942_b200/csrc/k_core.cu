@@ -6,15 +6,20 @@
 // on the symmetric matrix Z = lambda D^1/2 G D^1/2 (similar to lambda G D),
 // C^ = lambda D^1/2 phi1(Z) D^1/2; otherwise on Z = lambda G D directly,
 // C^ = lambda D phi1(Z).  phi1 and exp are evaluated by scaling and
-// doubling: Z0 = Z / 2^s with ||Z0||_1 <= 1/2, Taylor of degree 12 by Horner
-// (P = sum_k Z0^k / (k+1)!, E = I + Z0 P), then s times
+// doubling: Z0 = Z / 2^s with ||Z0||_1 <= 2, Taylor of degree 20 of phi1
+// evaluated by Paterson-Stockmeyer (P = sum_k Z0^k / (k+1)! from the powers
+// Z0^2..Z0^5 and three Horner steps in Z0^5: 8 GEMMs instead of 20), E = I +
+// Z0 P, then s times
 //     P <- (E + I) P / 2   (phi1(2Y) = (e^Y + I) phi1(Y) / 2),   E <- E E.
+// Truncation: ||Z0||^21 / 22! < 2e-15 for phi1, ||Z0||^22 / 22! < 4e-15 for exp.
 // No inverse, no Cholesky: G is numerically singular in practice (SURVEY
 // Sec. 0.1 item 2).  The oracle instead takes the top-right block of
 // scipy's expm of the augmented 2r x 2r matrix: a different algorithm.
 //
-// Dense fp64 GEMMs on the fp64 tensor cores (DMMA), batched over clouds via
-// blockIdx.z.
+// Dense fp64 GEMMs on the fp64 tensor cores (DMMA, 64 FMA/clk/SM measured:
+// tools/microbench/dmma_rate.cu), batched over clouds via blockIdx.z, with a
+// 3-stage cp.async pipeline and a fused epilogue (scaled identity, sigma B and
+// up to four extra matrices: the Paterson-Stockmeyer combinations).
 #include <math.h>
 
 #include "rfd_internal.h"
@@ -22,7 +27,8 @@
 namespace rfd {
 namespace {
 
-constexpr int kTaylor = 12;
+constexpr int kTaylor = 20;   // Taylor degree of phi1
+constexpr int kPS = 5;        // Paterson-Stockmeyer block
 
 __device__ __forceinline__ double dweight(const double* nu, int a) { return nu[a >> 1]; }
 
@@ -63,86 +69,113 @@ __global__ void core_norm_kernel(const double* __restrict__ Z, int r,
   }
 }
 
-__global__ void scaled_identity_kernel(double* __restrict__ P, int r, double c) {
-  const int b = blockIdx.y;
-  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= int64_t(r) * r) return;
-  P[int64_t(b) * r * r + e] = (e / r == e % r) ? c : 0.0;
-}
 
 struct GemmJob {
   const double* A;  // r x r, per-batch stride r*r
   const double* B;
   double* C;
-  double alpha, sigma, gamma;  // C = alpha (A + sigma I) B + gamma I
+  // C = alpha (A + sigma I) B + gamma I + sum_i mc[i] M[i]
+  double alpha, sigma, gamma;
+  const double* M[4];
+  double mc[4];
+  int nm;
 };
 struct GemmJobs {
   GemmJob job[2];
 };
 
-// fp64 tensor-core GEMM (DMMA, mma.sync m8n8k4 f64): CTA tile 32 x 64,
-// 4 warps side by side (each 32 x 16 = 4 x 2 fragments), K staged 16 at a
-// time through shared memory (padded strides: conflict-free fragment loads).
-constexpr int kBM = 32, kBN = 64, kBK = 16;
-constexpr int kSA = kBK + 4;   // A tile row stride (doubles)
+// fp64 tensor-core GEMM (DMMA, mma.sync m8n8k4 f64): CTA tile 32 x 64, 4 warps
+// side by side (each 32 x 16 = 4 x 2 fragments), K in steps of 32 through a
+// 3-stage cp.async pipeline (padded strides: conflict-free fragment loads).
+constexpr int kBM = 32, kBN = 64, kBK = 32, kGStages = 3;
+constexpr int kSA = kBK + 4;   // A tile row stride (doubles): 8g + 2t banks, distinct
 constexpr int kSB = kBN + 4;   // B tile row stride (doubles)
+constexpr int kGemmSmem = kGStages * (kBM * kSA + kBK * kSB) * 8;
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 __global__ void __launch_bounds__(128)
 dgemm_kernel(GemmJobs jobs, int njobs, int r) {
+  extern __shared__ __align__(16) double gsm[];
   const int jb = blockIdx.z % njobs, b = blockIdx.z / njobs;
-  const GemmJob J = (jb == 0) ? jobs.job[0] : jobs.job[1];
+  const GemmJob& J = (jb == 0) ? jobs.job[0] : jobs.job[1];
   const int64_t off = int64_t(b) * r * r;
   const double* __restrict__ A = J.A + off;
   const double* __restrict__ B = J.B + off;
   double* __restrict__ C = J.C + off;
-  __shared__ double As[kBM * kSA];
-  __shared__ double Bs[kBK * kSB];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = lane >> 2, tig = lane & 3;
   const int i0 = blockIdx.y * kBM, j0 = blockIdx.x * kBN;
+  double* As = gsm;                                  // [stage][kBM][kSA]
+  double* Bs = gsm + kGStages * kBM * kSA;           // [stage][kBK][kSB]
+
+  auto load_tile = [&](int st, int k0) {
+    // A: 32 rows x 32 doubles = 512 chunks of 16 B; B: 32 x 64 = 1024 chunks
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int e = tid + 128 * l, row = e >> 4, kc = (e & 15) * 2;
+      const int gi = i0 + row, gk = k0 + kc;
+      const bool ok = gi < r && gk < r;
+      cp_async16(As + (st * kBM + row) * kSA + kc, ok ? A + int64_t(gi) * r + gk : A, ok);
+    }
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      const int e = tid + 128 * l, kk = e >> 5, col = (e & 31) * 2;
+      const int gk = k0 + kk, gj = j0 + col;
+      const bool ok = gk < r && gj < r;
+      cp_async16(Bs + (st * kBK + kk) * kSB + col, ok ? B + int64_t(gk) * r + gj : B, ok);
+    }
+  };
+
   double acc[4][2][2];
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
-  for (int k0 = 0; k0 < r; k0 += kBK) {
-    // A tile 32 x 16 (4 per thread), B tile 16 x 64 (8 per thread)
+  const int nk = (r + kBK - 1) / kBK;
 #pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      const int e = tid + 128 * l, row = e >> 4, kk = e & 15;
-      const int gi = i0 + row, gk = k0 + kk;
-      double v = 0.0;
-      if (gi < r && gk < r) v = A[int64_t(gi) * r + gk] + (gi == gk ? J.sigma : 0.0);
-      As[row * kSA + kk] = v;
-    }
-#pragma unroll
-    for (int l = 0; l < 8; ++l) {
-      const int e = tid + 128 * l, kk = e >> 6, col = e & 63;
-      const int gk = k0 + kk, gj = j0 + col;
-      Bs[kk * kSB + col] = (gk < r && gj < r) ? B[int64_t(gk) * r + gj] : 0.0;
-    }
+  for (int st = 0; st < kGStages - 1; ++st) {
+    if (st < nk) load_tile(st, st * kBK);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<kGStages - 2>();
     __syncthreads();
+    // prefetch tile kt + 2 into the stage freed by tile kt - 1
+    if (kt + kGStages - 1 < nk) load_tile((kt + kGStages - 1) % kGStages, (kt + kGStages - 1) * kBK);
+    cp_async_commit();
+    const double* as = As + (kt % kGStages) * kBM * kSA;
+    const double* bs = Bs + (kt % kGStages) * kBK * kSB;
 #pragma unroll
     for (int k4 = 0; k4 < kBK; k4 += 4) {
       double af[4], bf[2];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) af[mi] = As[(mi * 8 + grp) * kSA + k4 + tig];
+      for (int mi = 0; mi < 4; ++mi) af[mi] = as[(mi * 8 + grp) * kSA + k4 + tig];
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni) bf[ni] = Bs[(k4 + tig) * kSB + warp * 16 + ni * 8 + grp];
+      for (int ni = 0; ni < 2; ++ni) bf[ni] = bs[(k4 + tig) * kSB + warp * 16 + ni * 8 + grp];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
         for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -150,8 +183,13 @@ dgemm_kernel(GemmJobs jobs, int njobs, int r) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int gi = i0 + mi * 8 + grp, gj = j0 + warp * 16 + ni * 8 + 2 * tig + h;
-        if (gi < r && gj < r)
-          C[int64_t(gi) * r + gj] = J.alpha * acc[mi][ni][h] + (gi == gj ? J.gamma : 0.0);
+        if (gi < r && gj < r) {
+          const int64_t e = int64_t(gi) * r + gj;
+          double v = J.alpha * acc[mi][ni][h] + (gi == gj ? J.gamma : 0.0);
+          if (J.sigma != 0.0) v += J.alpha * J.sigma * B[e];
+          for (int t = 0; t < J.nm; ++t) v += J.mc[t] * J.M[t][off + e];
+          C[e] = v;
+        }
       }
 }
 
@@ -172,8 +210,33 @@ __global__ void core_finalize_kernel(const double* __restrict__ P, const double*
 
 void gemm(const GemmJobs& jobs, int njobs, int r, int batch, cudaStream_t s) {
   LaunchScope L("rfd_core_dgemm", s);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(dgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+    configured = true;
+  }
   const dim3 grid((r + kBN - 1) / kBN, (r + kBM - 1) / kBM, njobs * batch);
-  dgemm_kernel<<<grid, 128, 0, s>>>(jobs, njobs, r);
+  dgemm_kernel<<<grid, 128, kGemmSmem, s>>>(jobs, njobs, r);
+}
+
+GemmJob job(const double* A, const double* B, double* C, double alpha, double sigma = 0.0,
+            double gamma = 0.0) {
+  GemmJob j{};
+  j.A = A; j.B = B; j.C = C;
+  j.alpha = alpha; j.sigma = sigma; j.gamma = gamma;
+  j.nm = 0;
+  return j;
+}
+
+// T = sum_i mc[i] M[i] + gamma I (elementwise; the first Horner operand)
+__global__ void combo_kernel(double* __restrict__ T, const double* M0, const double* M1,
+                             const double* M2, const double* M3, double c0, double c1, double c2,
+                             double c3, double gamma, int r) {
+  const int b = blockIdx.y;
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= int64_t(r) * r) return;
+  const int64_t o = int64_t(b) * r * r + e;
+  T[o] = c0 * M0[o] + c1 * M1[o] + c2 * M2[o] + c3 * M3[o] + ((e / r == e % r) ? gamma : 0.0);
 }
 
 }  // namespace
@@ -195,42 +258,75 @@ void launch_core_prep(const double* G, const double* nu, const int* flags, doubl
 }
 
 void launch_core_eval(const double* Z, const double* nu, const int* flags, double lambda,
-                      int m, int batch, int s_scale, double* P0, double* P1, double* E0,
-                      double* E1, double* C, int* oflag, cudaStream_t s) {
+                      int m, int batch, int s_scale, double* work, double* C, int* oflag,
+                      cudaStream_t s) {
   const int r = 2 * m;
   const int64_t rr = int64_t(r) * r;
   const dim3 egrid(unsigned((rr + 255) / 256), batch);
-  const double alpha = ldexp(1.0, -s_scale);
-  // Taylor coefficients c_k = 1 / (k+1)!.
-  double coef[kTaylor + 1];
+  const double alpha = ldexp(1.0, -s_scale);  // Z0 = alpha Z
+  // Taylor coefficients of phi1: c_k = 1 / (k+1)!
+  double c[kTaylor + 1];
   double f = 1.0;
   for (int k = 0; k <= kTaylor; ++k) {
     f *= double(k + 1);
-    coef[k] = 1.0 / f;
+    c[k] = 1.0 / f;
+  }
+  const int64_t S = rr * batch;  // one matrix (all clouds)
+  double* Z2 = work;             // Z0^2 .. Z0^5
+  double* Z3 = work + S;
+  double* Z4 = work + 2 * S;
+  double* Z5 = work + 3 * S;
+  double* Ta = work + 4 * S;
+  double* Tb = work + 5 * S;
+  double* P = work + 6 * S;
+  double* E = work + 7 * S;
+  double* Pn = work + 8 * S;
+  double* En = work + 9 * S;
+  {  // powers: Z0^2 = a^2 Z Z; Z0^3 = a Z0^2 Z and Z0^4 = Z0^2 Z0^2 together; Z0^5 = a Z0^4 Z
+    GemmJobs j{};
+    j.job[0] = job(Z, Z, Z2, alpha * alpha);
+    gemm(j, 1, r, batch, s);
+    j.job[0] = job(Z2, Z, Z3, alpha);
+    j.job[1] = job(Z2, Z2, Z4, 1.0);
+    gemm(j, 2, r, batch, s);
+    j.job[0] = job(Z4, Z, Z5, alpha);
+    gemm(j, 1, r, batch, s);
+  }
+  // B_q = sum_{i<5} c_{5q+i} Z0^i  (Z0^1 = alpha Z); Horner in Z0^5 from the top:
+  // T = B_3 + c_20 Z0^5, then T <- Z0^5 T + B_q for q = 2, 1, 0.
+  {
+    LaunchScope L("rfd_core_combo", s);
+    combo_kernel<<<egrid, 256, 0, s>>>(Ta, Z, Z2, Z3, Z4, c[16] * alpha, c[17], c[18], c[19],
+                                       c[15], r);
   }
   {
-    LaunchScope L("rfd_core_identity", s);
-    scaled_identity_kernel<<<egrid, 256, 0, s>>>(P0, r, coef[kTaylor]);
+    // + c_20 Z0^5: fold into T via one more combo term (M = Z5)
+    LaunchScope L("rfd_core_combo", s);
+    combo_kernel<<<egrid, 256, 0, s>>>(Ta, Ta, Z5, Z5, Z5, 1.0, c[20], 0.0, 0.0, 0.0, r);
   }
-  double* P = P0;
-  double* Pn = P1;
-  for (int k = kTaylor - 1; k >= 0; --k) {  // P <- c_k I + Z0 P
+  double* T = Ta;
+  double* Tn = Tb;
+  for (int q = 2; q >= 0; --q) {
     GemmJobs j{};
-    j.job[0] = GemmJob{Z, P, Pn, alpha, 0.0, coef[k]};
+    GemmJob g = job(Z5, T, q == 0 ? P : Tn, 1.0, 0.0, c[kPS * q]);
+    g.nm = 4;
+    g.M[0] = Z; g.mc[0] = c[kPS * q + 1] * alpha;
+    g.M[1] = Z2; g.mc[1] = c[kPS * q + 2];
+    g.M[2] = Z3; g.mc[2] = c[kPS * q + 3];
+    g.M[3] = Z4; g.mc[3] = c[kPS * q + 4];
+    j.job[0] = g;
     gemm(j, 1, r, batch, s);
-    double* t = P; P = Pn; Pn = t;
+    double* t = T; T = Tn; Tn = t;
   }
   {  // E = I + Z0 P
     GemmJobs j{};
-    j.job[0] = GemmJob{Z, P, E0, alpha, 0.0, 1.0};
+    j.job[0] = job(Z, P, E, alpha, 0.0, 1.0);
     gemm(j, 1, r, batch, s);
   }
-  double* E = E0;
-  double* En = E1;
   for (int i = 0; i < s_scale; ++i) {  // P <- (E + I) P / 2 ; E <- E E
     GemmJobs j{};
-    j.job[0] = GemmJob{E, P, Pn, 0.5, 1.0, 0.0};
-    j.job[1] = GemmJob{E, E, En, 1.0, 0.0, 0.0};
+    j.job[0] = job(E, P, Pn, 0.5, 1.0, 0.0);
+    j.job[1] = job(E, E, En, 1.0, 0.0, 0.0);
     gemm(j, 2, r, batch, s);
     double* t = P; P = Pn; Pn = t;
     t = E; E = En; En = t;

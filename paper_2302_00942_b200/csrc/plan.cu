@@ -331,12 +331,9 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   }
 
   // a5: core, scaling exponent first.
-  double *Z = nullptr, *P0 = nullptr, *P1 = nullptr, *E0 = nullptr, *E1 = nullptr;
+  double *Z = nullptr, *work = nullptr;
   RFD_CUDA(tmp.alloc(&Z, rr * batch));
-  RFD_CUDA(tmp.alloc(&P0, rr * batch));
-  RFD_CUDA(tmp.alloc(&P1, rr * batch));
-  RFD_CUDA(tmp.alloc(&E0, rr * batch));
-  RFD_CUDA(tmp.alloc(&E1, rr * batch));
+  RFD_CUDA(tmp.alloc(&work, rr * batch * rfd::kCoreWork));
   rfd::launch_core_prep(p->G, p->nu, p->flags, lambda, m, batch, Z,
                         reinterpret_cast<unsigned long long*>(p->flags + 2), st);
   RFD_CUDA(cudaGetLastError());
@@ -347,14 +344,14 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
     return fail(RFD_ERANGE, "frequency sampler exhausted its attempts (R too small?)");
   double znorm;
   memcpy(&znorm, hflags + 2, sizeof(double));
-  // Scaling exponent: smallest s >= 0 with ||Z||_1 / 2^s <= 1/2.
+  // Scaling exponent: smallest s >= 0 with ||Z||_1 / 2^s <= kCoreTheta.
   if (!isfinite(znorm) || znorm > 1e60)
     return fail(RFD_ERANGE, "core: ||lambda G D|| is not finite or too large");
   int s_scale = 0;
-  while (ldexp(znorm, -s_scale) > 0.5) ++s_scale;
+  while (ldexp(znorm, -s_scale) > rfd::kCoreTheta) ++s_scale;
   p->symmetric = (hflags[0] & 1) ? 0 : 1;
   p->scaling = s_scale;
-  rfd::launch_core_eval(Z, p->nu, p->flags, lambda, m, batch, p->scaling, P0, P1, E0, E1, p->C,
+  rfd::launch_core_eval(Z, p->nu, p->flags, lambda, m, batch, p->scaling, work, p->C,
                         p->flags + 4, st);
   RFD_CUDA(cudaGetLastError());
   RFD_CUDA(cudaMemcpyAsync(hflags, p->flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));

@@ -63,11 +63,13 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n,
 void launch_core_prep(const double* G, const double* nu, const int* flags,
                       double lambda, int m, int batch, double* Z,
                       unsigned long long* norm_bits, cudaStream_t s);
-// Taylor (degree kTaylor) of phi1 and exp at Z / 2^s, then s doublings,
-// then C^ = lambda D^1/2 P D^1/2 (or lambda D P); flags[1] = 1 on overflow.
+// Taylor (degree 20, Paterson-Stockmeyer) of phi1 and exp at Z / 2^s
+// (||Z / 2^s||_1 <= kCoreTheta), then s doublings, then C^ = lambda D^1/2 P
+// D^1/2 (or lambda D P); oflag = 1 on overflow.  work: kCoreWork matrices.
+constexpr double kCoreTheta = 2.0;
+constexpr int kCoreWork = 10;
 void launch_core_eval(const double* Z, const double* nu, const int* flags,
-                      double lambda, int m, int batch, int s_scale,
-                      double* P0, double* P1, double* E0, double* E1,
+                      double lambda, int m, int batch, int s_scale, double* work,
                       double* C, int* oflag, cudaStream_t s);
 
 // ---------------------------------------------------------------- passes
