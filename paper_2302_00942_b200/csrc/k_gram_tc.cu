@@ -202,11 +202,11 @@ __device__ __forceinline__ void drain_epoch(uint32_t tm_lane, int q, int lane, i
   }
   tc::tc_fence_before();
   __syncwarp();
-  if (lane == 0) tc::mbar_arrive(acce_bar);  // D is free again
+  if (lane == 0 && acce_bar) tc::mbar_arrive(acce_bar);  // D is free again
 }
 
 // Diagnostics: per-step timestamps of CTA 0 (mode 3).
-__device__ long long g_trace[4096][4];
+__device__ long long g_trace[4096][8];
 
 // kMode (diagnostics only, RFD_GRAM_MODE): 0 = normal, 1 = no MMAs issued,
 // 2 = no feature generation (the pipeline still runs; results are wrong).
@@ -670,13 +670,475 @@ Sched make_sched(int m, int64_t n, int batch, int sms) {
   return sc;
 }
 
+
+// ============================================================== CTA pairs
+// Gram on CTA pairs (tcgen05 cta_group::2), used when there are >= 2 feature
+// blocks.  Super-blocks of 256 features (2 blocks); a *pair-tile* (I <= J) is
+// the 256 x 256 tile of super-blocks I and J, one MMA of M = N = 256 per
+// K-slice on the SM pair.  CTA c of the pair holds A rows = block 2I + c and
+// B rows = block 2J + c, so each SM generates half the features the tile
+// needs (on a diagonal pair-tile A = B: one block per SM) and reads half the
+// B operand -- twice the MMA work per generated feature of the 1-SM design.
+// Diagonal pair-tiles use the symmetric two-product form (B lo = 2 lo, G =
+// (D + D^T) / 2 over the 256 x 256 tile); off-diagonal ones three products.
+// Each CTA accumulates its 128 rows in its own TMEM (epoch D + long-term L, as
+// above) and writes them to the segment partial (256 x 256 per segment).
+// Barriers: full / acce live in the leader (rank 0), arrived on by both CTAs
+// (release at cluster scope); empty / accf are committed to both CTAs by the
+// leader's MMA (multicast); the point ring is per CTA.
+
+__host__ __device__ inline void pair_tile(int TS, int u, int& I, int& J) {
+  int i = 0, row = TS;
+  while (u >= row) {
+    u -= row;
+    ++i;
+    --row;
+  }
+  I = i;
+  J = i + u;
+}
+
+constexpr uint32_t kPAHi = 0, kPALo = kOpBytes, kPBHi = 2 * kOpBytes, kPBLo = 3 * kOpBytes;
+constexpr uint32_t kPStageBytes = 4 * kOpBytes;                 // 64 KB
+constexpr int kPStages = 3;
+// Epoch of the pair kernel: 16 K-steps (1024 points).  Used for >= 2 feature
+// blocks only (cfg 4: G, C^, Delta errors stay <= ~1.5e-5);
+// the 1-SM kernel (small m, e.g. the 2048-point clouds of cfg 3) keeps 512.
+constexpr int kPEpoch = 16;
+constexpr int kPRingOff = kPStages * int(kPStageBytes);          // 192 KB
+constexpr int kPOmegaOff = kPRingOff + kChunks * int(kChunkBytes);
+constexpr int kPSmemBytes = kPOmegaOff + kMaxFreqs * 16;         // 216 KB
+
+template <bool kTrace>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict__ omega4, int m,
+                 int64_t n, const __grid_constant__ Sched sc, float* __restrict__ partial) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t full_bar[kPStages], empty_bar[kPStages], pts_bar[kChunks],
+      pts_empty[kChunks];
+  __shared__ uint64_t accf_bar, acce_bar;
+  __shared__ uint32_t tmem_sh;
+
+  const uint32_t rank = tc::cluster_rank();
+  const int pair = blockIdx.x >> 1;
+  const int64_t L0 = sc.start[pair], L1 = sc.start[pair + 1];
+  if (L0 >= L1) return;  // both CTAs of the pair
+  const int nsteps = int(L1 - L0);
+  const int Si = int(sc.S);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbase = tc::smem_addr(smem);
+
+  if (tid == 0) {
+    // full / acce: the CTA's 16 warps, plus (leader) the follower's relay
+    for (int s = 0; s < kPStages; ++s) {
+      tc::mbar_init(&full_bar[s], kProducerWarps + (rank == 0 ? 1 : 0));
+      tc::mbar_init(&empty_bar[s], 1);
+    }
+    for (int c = 0; c < kChunks; ++c) {
+      tc::mbar_init(&pts_bar[c], 1);
+      tc::mbar_init(&pts_empty[c], kProducerWarps);
+    }
+    tc::mbar_init(&accf_bar, 1);
+    tc::mbar_init(&acce_bar, kProducerWarps + (rank == 0 ? 1 : 0));
+    tc::mbar_fence_init();
+  }
+  {  // omega table (rows of padding frequencies >= m are zero)
+    float4* om_s = reinterpret_cast<float4*>(smem + kPOmegaOff);
+    for (int k = tid; k < 2 * sc.T * kFreqs; k += kThreads)
+      om_s[k] = (k < m) ? __ldg(omega4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (warp == 0) tc::tmem_alloc_pair<512>(&tmem_sh);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+
+  const int bu0 = int(L0 / sc.S), t0 = int(L0 - int64_t(bu0) * sc.S);
+  const int hi0 = int(min(L1, int64_t(bu0 + 1) * sc.S) - L0);
+
+  if (warp == kLoadWarp) {
+    // ============================================ point loads (per CTA)
+    const int nchunks = (nsteps + kChunkSteps - 1) / kChunkSteps;
+    const int64_t cloud_bytes = int64_t(Si) * kStepBytes;
+    int l_bu = bu0, l_t = t0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      if (ch >= kChunks) tc::mbar_wait(&pts_empty[ch % kChunks], uint32_t(ch / kChunks - 1) & 1u);
+      const int i0 = ch * kChunkSteps, i1 = min(nsteps, i0 + kChunkSteps);
+      uint64_t* bar = &pts_bar[ch % kChunks];
+      unsigned char* dst = smem + kPRingOff + (ch % kChunks) * kChunkBytes;
+      if (lane == 0) {
+        tc::mbar_arrive_expect_tx(bar, uint32_t(i1 - i0) * kStepBytes);
+        for (int i = i0; i < i1;) {
+          const int run = min(i1 - i, Si - l_t);
+          tc::bulk_g2s(dst + (i - i0) * kStepBytes,
+                       gpts + int64_t(l_bu / sc.U) * cloud_bytes + int64_t(l_t) * kStepBytes,
+                       uint32_t(run) * kStepBytes, bar);
+          i += run;
+          l_t += run;
+          if (l_t == Si) {
+            l_t = 0;
+            ++l_bu;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp == kMmaWarp) {
+    // ============================================ MMA issue (leader) / relay (follower)
+    if (rank == 1) {
+      // Relay: the follower's producers and drains arrive on its local full /
+      // acce barriers (release at CTA scope: cheap); one thread forwards each
+      // completed phase to the leader with ONE release at cluster scope (that
+      // arrive compiles to MEMBAR.GPU + L1 invalidate: too costly per warp).
+      if (lane == 0) {
+        int n_epochs = 0;  // the epochs of this CTA's step range: ceil(len / E) per segment
+        for (int lo = 0, hi = hi0; lo < nsteps; lo = hi, hi = min(nsteps, hi + Si))
+          n_epochs += (hi - lo + kPEpoch - 1) / kPEpoch;
+        const uint32_t full_lead0 = tc::mapa(&full_bar[0], 0);
+        const uint32_t acce_lead = tc::mapa(&acce_bar, 0);
+        int fi = 0, ei = 0;
+        while (fi < nsteps || ei < n_epochs) {
+          bool moved = false;
+          if (fi < nsteps &&
+              tc::mbar_test_wait(&full_bar[fi % kPStages], uint32_t(fi / kPStages) & 1u)) {
+            tc::mbar_arrive_cluster(full_lead0 + 8u * uint32_t(fi % kPStages));
+            ++fi;
+            moved = true;
+          }
+          if (ei < n_epochs && tc::mbar_test_wait(&acce_bar, uint32_t(ei) & 1u)) {
+            tc::mbar_arrive_cluster(acce_lead);
+            ++ei;
+            moved = true;
+          }
+          if (!moved) __nanosleep(32);
+        }
+      }
+      __syncwarp();
+    } else {
+      const uint32_t idesc = tc::make_idesc(0, 256, 256);
+      int m_lo = 0, m_hi = hi0, m_bu = bu0, epoch = 0;
+      auto is_diag = [&](int u) {
+        int I, J;
+        pair_tile(sc.T, u, I, J);
+        return I == J;
+      };
+      bool diag = is_diag(m_bu % sc.U);
+      for (int it = 0; it < nsteps; ++it) {
+        const int s = it % kPStages;
+        const int k = it - m_lo;
+        const bool efirst = (k & (kPEpoch - 1)) == 0;
+        const bool elast = ((k + 1) & (kPEpoch - 1)) == 0 || it + 1 == m_hi;
+        if (efirst && epoch > 0) tc::mbar_wait_cluster(&acce_bar, uint32_t(epoch - 1) & 1u);
+        if (kTrace && blockIdx.x == 0 && it < 4096 && lane == 0) g_trace[it][0] = clock64();
+        tc::mbar_wait_cluster(&full_bar[s], uint32_t(it / kPStages) & 1u);
+        if (kTrace && blockIdx.x == 0 && it < 4096 && lane == 0) g_trace[it][1] = clock64();
+        tc::tc_fence_after();
+        __syncwarp();
+        const uint32_t stage = sbase + uint32_t(s) * kPStageBytes;
+        if (tc::elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < kStep / 16; ++kk) {
+            const uint32_t ko = uint32_t(kk) * 2u * kLBO;
+            const uint64_t ahi = tc::make_sdesc(stage + kPAHi + ko, kLBO, kSBO);
+            const uint64_t blo = tc::make_sdesc(stage + kPBLo + ko, kLBO, kSBO);
+            const uint32_t acc0 = (efirst && kk == 0) ? 0u : 1u;
+            if (diag) {  // A = B = H:  D += H H^T + H (2L)^T
+              tc::mma_f16_pair(tmem, ahi, ahi, idesc, acc0);
+              tc::mma_f16_pair(tmem, ahi, blo, idesc, 1u);
+            } else {
+              const uint64_t alo = tc::make_sdesc(stage + kPALo + ko, kLBO, kSBO);
+              const uint64_t bhi = tc::make_sdesc(stage + kPBHi + ko, kLBO, kSBO);
+              tc::mma_f16_pair(tmem, ahi, bhi, idesc, acc0);
+              tc::mma_f16_pair(tmem, ahi, blo, idesc, 1u);
+              tc::mma_f16_pair(tmem, alo, bhi, idesc, 1u);
+            }
+          }
+          tc::mma_commit_pair(&empty_bar[s]);
+          if (elast) tc::mma_commit_pair(&accf_bar);
+        }
+        __syncwarp();
+        if (elast) ++epoch;
+        if (it + 1 == m_hi && it + 1 < nsteps) {
+          ++m_bu;
+          m_lo = it + 1;
+          m_hi = min(nsteps, it + 1 + Si);
+          diag = is_diag(m_bu % sc.U);
+        }
+      }
+    }
+  } else {
+    // ============================================ producers (+ drains)
+    const unsigned char* ring = smem + kPRingOff;
+    const float4* om_s = reinterpret_cast<const float4*>(smem + kPOmegaOff);
+    const int q = warp & 7, f = 32 * (warp >> 3) + lane;
+    const uint32_t off_c = uint32_t(f >> 3) * kSBO + uint32_t(q) * kLBO + uint32_t(f & 7) * 16u;
+    const uint32_t off_s = off_c + 8u * kSBO;  // row 64 + f
+    const int lg = warp & 3, qd = warp >> 2;
+    const uint32_t lane_field = uint32_t(32 * lg) << 16;
+    const int rho = 32 * lg + lane;
+    // blocks of this CTA: A = 2I + rank, B = 2J + rank (diag: the same block)
+    int blkA = 0, blkB = 0;
+    bool diag = true;
+    auto setup_unit = [&](int u) {
+      int I, J;
+      pair_tile(sc.T, u, I, J);
+      blkA = 2 * I + int(rank);
+      blkB = 2 * J + int(rank);
+      diag = I == J;
+    };
+    int pend0 = -1, pend1 = -1, info0 = 0, info1 = 0, last0 = 0, last1 = 0;
+    auto drain0 = [&]() {
+      drain_epoch(tmem + lane_field, qd, lane, 2, (info0 >> 29) & 1, (info0 >> 30) & 1,
+                  partial + (int64_t(info0 & 0x0FFFFFFF) * 256 + 128 * rank + rho) * 256,
+                  nullptr, false);
+      if (lane == 0) tc::mbar_arrive(&acce_bar);  // leader: counted; follower: relayed
+      pend0 = pend1;
+      info0 = info1;
+      last0 = last1;
+      pend1 = -1;
+    };
+    const int tail = int(n - int64_t(Si - 1) * kStep);
+    int bu = bu0, seg_lo = 0, seg_hi = hi0, tail_it = Si - 1 - t0;
+    setup_unit(bu % sc.U);
+    int epoch = 0;
+    for (int it = 0; it < nsteps; ++it) {
+      if (it == seg_hi) {
+        ++bu;
+        seg_lo = it;
+        seg_hi = min(nsteps, it + Si);
+        tail_it = it + Si - 1;
+        setup_unit(bu % sc.U);
+      }
+      const int k = it - seg_lo;
+      const bool elast = ((k + 1) & (kPEpoch - 1)) == 0 || it + 1 == seg_hi;
+      const int s = it % kPStages;
+      const uint32_t ph = uint32_t(it / kPStages) & 1u;
+      const int ch = it / kChunkSteps;
+      // drain as soon as the epoch's MMAs are complete (non-parking probe), and
+      // at the latest before a step whose stage needs a later epoch's MMA
+      while (pend0 >= 0) {
+        if (it - kPStages > last0)
+          tc::mbar_wait(&accf_bar, uint32_t(pend0) & 1u);
+        else if (!__any_sync(0xffffffffu, tc::mbar_test_wait(&accf_bar, uint32_t(pend0) & 1u)))
+          break;
+        __syncwarp();
+        drain0();
+      }
+      if (kTrace && blockIdx.x == 0 && it < 4096 && tid == 160) g_trace[it][2] = clock64();
+      if (it >= kPStages) tc::mbar_wait(&empty_bar[s], ph ^ 1u);
+      if (it % kChunkSteps == 0 || it == 0)
+        tc::mbar_wait(&pts_bar[ch % kChunks], uint32_t(ch / kChunks) & 1u);
+      __syncwarp();
+      if (kTrace && blockIdx.x == 0 && it < 4096 && tid == 160) g_trace[it][3] = clock64();
+      const int cnt = (it == tail_it) ? tail : kStep;
+      const float* grp = reinterpret_cast<const float*>(
+          ring + (ch % kChunks) * kChunkBytes + (it % kChunkSteps) * kStepBytes + q * kGroupBytes);
+      float X[8], Y[8], Z[8];
+#pragma unroll
+      for (int j = 0; j < 8; j += 4) {
+        *reinterpret_cast<float4*>(X + j) = *reinterpret_cast<const float4*>(grp + j);
+        *reinterpret_cast<float4*>(Y + j) = *reinterpret_cast<const float4*>(grp + 8 + j);
+        *reinterpret_cast<float4*>(Z + j) = *reinterpret_cast<const float4*>(grp + 16 + j);
+      }
+      const uint32_t stage = sbase + uint32_t(s) * kPStageBytes;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        if (i == 1 && diag) break;
+        const int blk = (i == 0) ? blkA : blkB;
+        const float4 wi = om_s[blk * kFreqs + f];
+        const float2 wx = make_float2(wi.x, wi.x), wy = make_float2(wi.y, wi.y),
+                     wz = make_float2(wi.z, wi.z);
+        float c[8], sn[8];
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          const float2 th = __ffma2_rn(wz, make_float2(Z[j], Z[j + 1]),
+                                       __ffma2_rn(wy, make_float2(Y[j], Y[j + 1]),
+                                                  __fmul2_rn(wx, make_float2(X[j], X[j + 1]))));
+          __sincosf(th.x, &sn[j], &c[j]);
+          __sincosf(th.y, &sn[j + 1], &c[j + 1]);
+        }
+        if (cnt < kStep) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (q * 8 + j >= cnt) c[j] = sn[j] = 0.0f;
+        }
+        uint32_t ch_[4], cl[4], sh[4], sl[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          tc::split_f16x2_v2(make_float2(c[2 * j], c[2 * j + 1]), ch_[j], cl[j]);
+          tc::split_f16x2_v2(make_float2(sn[2 * j], sn[2 * j + 1]), sh[j], sl[j]);
+        }
+        const uint32_t hiR = stage + ((i == 0) ? kPAHi : kPBHi);
+        tc::st_shared_v4(hiR + off_c, ch_[0], ch_[1], ch_[2], ch_[3]);
+        tc::st_shared_v4(hiR + off_s, sh[0], sh[1], sh[2], sh[3]);
+        if (diag) {  // B lo = 2 lo (exact in fp16); no A lo
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            __half2 h = *reinterpret_cast<__half2*>(&cl[j]);
+            h = __hadd2(h, h);
+            cl[j] = *reinterpret_cast<uint32_t*>(&h);
+            h = *reinterpret_cast<__half2*>(&sl[j]);
+            h = __hadd2(h, h);
+            sl[j] = *reinterpret_cast<uint32_t*>(&h);
+          }
+        }
+        const uint32_t loR = stage + ((i == 0 && !diag) ? kPALo : kPBLo);
+        tc::st_shared_v4(loR + off_c, cl[0], cl[1], cl[2], cl[3]);
+        tc::st_shared_v4(loR + off_s, sl[0], sl[1], sl[2], sl[3]);
+      }
+      if (kTrace && blockIdx.x == 0 && it < 4096 && tid == 160) g_trace[it][4] = clock64();
+      // a second, mid-step probe: the MMA warp idles until the drain is done
+      if (pend0 >= 0 && __any_sync(0xffffffffu, tc::mbar_test_wait(&accf_bar, uint32_t(pend0) & 1u))) {
+        __syncwarp();
+        drain0();
+      }
+      if (kTrace && blockIdx.x == 0 && it < 4096 && tid == 160) g_trace[it][5] = clock64();
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (kTrace && blockIdx.x == 0 && it < 4096 && tid == 160) g_trace[it][6] = clock64();
+      if (lane == 0) {
+        tc::mbar_arrive(&full_bar[s]);  // leader: counted; follower: relayed
+        if (it % kChunkSteps == kChunkSteps - 1 || it == nsteps - 1)
+          tc::mbar_arrive(&pts_empty[ch % kChunks]);
+      }
+      if (elast) {
+        if (pend1 >= 0) {
+          tc::mbar_wait(&accf_bar, uint32_t(pend0) & 1u);
+          __syncwarp();
+          drain0();
+        }
+        const int info = (pair + bu) | (k < kPEpoch ? (1 << 29) : 0) |
+                         (it + 1 == seg_hi ? (1 << 30) : 0);
+        if (pend0 < 0) {
+          pend0 = epoch;
+          info0 = info;
+          last0 = it;
+        } else {
+          pend1 = epoch;
+          info1 = info;
+          last1 = it;
+        }
+        ++epoch;
+      }
+    }
+    while (pend0 >= 0) {
+      tc::mbar_wait(&accf_bar, uint32_t(pend0) & 1u);
+      __syncwarp();
+      drain0();
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  if (warp == 0) tc::tmem_dealloc_pair<512>(tmem);
+}
+
+// K2 (pairs): G[b] from the pair-tile partials (256 x 256 per segment).
+__global__ void __launch_bounds__(256)
+gram_pair_reduce_kernel(const float* __restrict__ partial, int m, const __grid_constant__ Sched sc,
+                        double* __restrict__ G) {
+  __shared__ int segs[kMaxCtas];
+  __shared__ int nseg_sh;
+  const int b = blockIdx.y;
+  const int T = 2 * sc.T, r = 2 * m;  // 128-feature blocks
+  int tile = blockIdx.x >> 4;
+  const int chunk = blockIdx.x & 15;
+  int bi = 0, row = T;
+  while (tile >= row) {
+    tile -= row;
+    ++bi;
+    --row;
+  }
+  const int bj = bi + tile;
+  const int I = bi >> 1, J = bj >> 1;
+  // pair-tile index of (I, J), I <= J
+  int unit = 0;
+  for (int i = 0; i < I; ++i) unit += sc.T - i;
+  unit += J - I;
+  const int64_t bu = int64_t(b) * sc.U + unit;
+  if (threadIdx.x == 0) {
+    int ns = 0;
+    const int64_t lo = bu * sc.S, hi = (bu + 1) * sc.S;
+    for (int c = 0; c < sc.G; ++c)
+      if (sc.start[c] < sc.start[c + 1] && sc.start[c] < hi && sc.start[c + 1] > lo)
+        segs[ns++] = int(c + bu);
+    nseg_sh = ns;
+  }
+  __syncthreads();
+  const int nseg = nseg_sh;
+  const bool diag = (I == J);
+  const int ro = 128 * (bi & 1), co = 128 * (bj & 1);
+#pragma unroll 1
+  for (int i = 0; i < 4; ++i) {
+    const int e = chunk * 1024 + i * 256 + threadIdx.x;
+    const int rr = e >> 7, cc = e & 127;
+    const int fr = bi * kFreqs + (rr & 63), fc = bj * kFreqs + (cc & 63);
+    if (fr >= m || fc >= m) continue;
+    const int64_t o1 = int64_t(ro + rr) * 256 + co + cc;
+    const int64_t o2 = int64_t(co + cc) * 256 + ro + rr;
+    double s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < nseg; ++k) {
+      const float* P = partial + int64_t(segs[k]) * (256 * 256);
+      s1 += double(P[o1]);
+      if (diag) s2 += double(P[o2]);
+    }
+    const double v = diag ? 0.5 * (s1 + s2) : s1;
+    const int a = 2 * fr + (rr >> 6), c = 2 * fc + (cc >> 6);
+    double* Gb = G + int64_t(b) * r * r;
+    Gb[int64_t(a) * r + c] = v;
+    Gb[int64_t(c) * r + a] = v;
+  }
+}
+
+Sched make_pair_sched(int m, int64_t n, int batch, int sms) {
+  Sched sc{};
+  const int T = (m + kFreqs - 1) / kFreqs;
+  sc.T = (T + 1) / 2;  // super-blocks
+  sc.U = sc.T * (sc.T + 1) / 2;
+  sc.batch = batch;
+  sc.S = (n + kStep - 1) / kStep;
+  const int64_t items = int64_t(batch) * sc.U * sc.S;
+  int G = std::min(sms, 2 * kMaxCtas) / 2;
+  if (int64_t(G) > items) G = int(items);
+  sc.G = G;
+  // cost of one K-step: diagonal 8 pair-MMAs, off-diagonal 12 (x 128 cycles)
+  std::vector<int64_t> wgt(sc.U), pw(sc.U + 1, 0);
+  for (int u = 0; u < sc.U; ++u) {
+    int I, J;
+    pair_tile(sc.T, u, I, J);
+    wgt[u] = (I == J) ? 2 : 3;
+    pw[u + 1] = pw[u] + wgt[u];
+  }
+  const int64_t Wc = sc.S * pw[sc.U];
+  const int64_t total = int64_t(batch) * Wc;
+  for (int c = 0; c <= G; ++c) {
+    const int64_t target = (c == G) ? total : int64_t((__int128)total * c / G);
+    const int64_t b = target / Wc, rem = target - b * Wc;
+    int u = 0;
+    while (u + 1 < sc.U && pw[u + 1] * sc.S <= rem) ++u;
+    const int64_t tt = (rem - pw[u] * sc.S + wgt[u] - 1) / wgt[u];
+    int64_t L = (b * sc.U + u) * sc.S + tt;
+    if (L > items) L = items;
+    sc.start[c] = L;
+  }
+  sc.start[G] = items;
+  return sc;
+}
+
+bool use_pairs(int m) {
+  const char* e = getenv("RFD_GRAM_PAIRS");  // "0": the 1-SM kernel (A/B comparison)
+  return (m + kFreqs - 1) / kFreqs >= 2 && !(e && e[0] == '0');
+}
+
 }  // namespace
 
 GramGeom gram_tc_geometry(int m, int64_t n, int batch, int sms) {
-  const Sched sc = make_sched(m, n, batch, sms);
+  const bool pairs = use_pairs(m);
+  const Sched sc = pairs ? make_pair_sched(m, n, batch, sms) : make_sched(m, n, batch, sms);
   GramGeom g;
   g.r = 2 * m;
-  g.tile = kBlk;
+  g.tile = pairs ? 2 * kBlk : kBlk;  // 256: CTA-pair path
   g.tiles1d = sc.T;
   g.ntiles = sc.U;   // units
   g.chunks = sc.G;   // persistent CTAs
@@ -687,7 +1149,7 @@ GramGeom gram_tc_geometry(int m, int64_t n, int batch, int sms) {
 // one partial per (CTA, unit segment) -- segment id = cta + cloud * U + unit --
 // followed by the points in the Gram layout (S K-steps per cloud)
 static size_t gram_tc_partial_only(const GramGeom& g, int batch) {
-  return size_t(g.chunks + int64_t(batch) * g.ntiles) * 256 * 128;
+  return size_t(g.chunks + int64_t(batch) * g.ntiles) * 256 * g.tile;
 }
 size_t gram_tc_partial_elems(const GramGeom& g, int batch) {
   return gram_tc_partial_only(g, batch) + size_t(batch) * size_t(g.chunk) * (kStepBytes / 4);
@@ -695,8 +1157,10 @@ size_t gram_tc_partial_elems(const GramGeom& g, int batch) {
 
 void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
                     const GramGeom& g, float* partial, double* G, cudaStream_t s) {
-  // same partition as gram_tc_geometry (G = g.chunks CTAs)
-  const Sched sc = make_sched(m, n, batch, g.chunks);
+  const bool pairs = g.tile == 2 * kBlk;
+  // same partition as gram_tc_geometry (G = g.chunks CTAs or CTA pairs)
+  const Sched sc = pairs ? make_pair_sched(m, n, batch, 2 * g.chunks)
+                         : make_sched(m, n, batch, g.chunks);
   static bool configured = false;
   static int mode = 0;
   if (!configured) {
@@ -712,6 +1176,10 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, i
                          kSmemBytes);
     cudaFuncSetAttribute(gram_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSmemBytes);
+    cudaFuncSetAttribute(gram_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kPSmemBytes);
+    cudaFuncSetAttribute(gram_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kPSmemBytes);
     const char* e = getenv("RFD_GRAM_MODE");  // diagnostics only
     mode = e ? atoi(e) : 0;
     configured = true;
@@ -725,6 +1193,28 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, i
     gram_pack_kernel<<<int(blocks), 256, 0, s>>>(pts, n, per_cloud, total, gpts);
   }
   const unsigned char* gp = reinterpret_cast<const unsigned char*>(gpts);
+  if (pairs) {
+    {
+      LaunchScope L("rfd_gram_tc", s);
+      if (mode == 6) {
+        gram_pair_kernel<true><<<2 * sc.G, kThreads, kPSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
+        static long long h[4096][8];
+        cudaMemcpyFromSymbol(h, g_trace, sizeof(h));
+        for (int i = 0; i < 40; ++i)
+          fprintf(stderr, "it %3d mma_wait %7lld go %7lld | prod top %7lld go %7lld comp %7lld probe %7lld fence %7lld\n", i,
+                  h[i][0] - h[0][2], h[i][1] - h[0][2], h[i][2] - h[0][2], h[i][3] - h[0][2],
+                  h[i][4] - h[0][2], h[i][5] - h[0][2], h[i][6] - h[0][2]);
+      } else {
+        gram_pair_kernel<false><<<2 * sc.G, kThreads, kPSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
+      }
+    }
+    {
+      LaunchScope L("rfd_gram_reduce", s);
+      const int T = 2 * sc.T, tiles = T * (T + 1) / 2;
+      gram_pair_reduce_kernel<<<dim3(16 * tiles, batch), 256, 0, s>>>(partial, m, sc, G);
+    }
+    return;
+  }
   {
     LaunchScope L("rfd_gram_tc", s);
     if (mode == 1)
@@ -738,7 +1228,7 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, i
         gram_tc_kernel<3><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
       else
         gram_tc_kernel<4><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
-      static long long h[4096][4];
+      static long long h[4096][8];
       cudaMemcpyFromSymbol(h, g_trace, sizeof(h));
       for (int i = 0; i < 64; ++i)
         fprintf(stderr, "it %3d t0 %7lld t1 %7lld t2 %7lld t3 %7lld\n", i,
