@@ -2,18 +2,24 @@
 // first bracket "B^T x" of Eq. 13).
 //
 // A CTA owns a tile of 128 frequencies (TMEM lanes) and a contiguous range of
-// points (the contraction dimension K).  Per chunk of 32 points the 16
+// points (the contraction dimension K).  Per chunk of 64 points the 16
 // producer warps regenerate cos and sin of omega_k . x for their lane's
-// frequency (a3) and write them, split x = hi + lo in tf32, straight into
-// TMEM as two A operands (cos rows, sin rows); F's chunk, split likewise, is
-// the B operand in shared memory (16 channels x 32 points, K-major).  One
-// elected lane issues
+// frequency (a3) and write them, split x = hi + lo in fp16 (|x - hi - lo| <=
+// 2^-22 |x| + 2^-25), straight into TMEM as the A operands (cos rows, sin
+// rows).  F's chunk is the B operand in shared memory (16 channels x 64
+// points, K-major), scaled per channel by a power of two into fp16 range
+// (max_i |F_ij| 2^e_j in [2^13, 2^14); undone exactly on the partial sums)
+// and split likewise.  One elected lane issues
 //     D_cos += C_hi F_hi^T + C_hi F_lo^T + C_lo F_hi^T,  D_sin likewise
-// (tcgen05.mma kind::tf32, M = 128, N = 16, K = 8 x 4).  The tensor core's
-// fp32 accumulator is not round-to-nearest, so D accumulates for an epoch of
-// 8 chunks (256 points) in one of two TMEM buffers and 4 drain warps move it
-// into fp32 registers; at the end each lane writes its frequency's 2 x 16
-// partial sums.  K5 then reduces the partials in a fixed order in fp64.
+// (tcgen05.mma kind::f16, M = 128, N = 16, K = 16 x 4).  With N = 16 the
+// instruction count paces the tensor core, and kind::f16 needs half the
+// instructions of kind::tf32 per point.  The fp32 accumulator of the tensor
+// core is not round-to-nearest, so D accumulates for an epoch of 8 chunks (512
+// points) in one of two TMEM buffers and 4 drain warps move it into fp32
+// registers; at the end each lane writes its frequency's 2 x 16 partial sums.
+// K5 then reduces the partials in a fixed order in fp64.
+//
+// The channel scales come from a column max-|F| pre-pass (one read of F).
 #include "rfd_internal.h"
 #include "tc_ptx.cuh"
 
@@ -23,15 +29,16 @@ namespace {
 constexpr int kProducerWarps = 16;  // 4 per TMEM lane group
 constexpr int kMmaWarp = 16;
 constexpr int kThreads = 21 * 32;   // + MMA warp + 4 drain warps (17..20)
-constexpr int kChunk = 32;          // points per chunk
+constexpr int kChunk = 64;          // points per chunk
 constexpr int kStages = 3;
 constexpr int kEpoch = 8;           // chunks per TMEM accumulation epoch
 // TMEM columns: D buffers (cos 16 + sin 16) at 0 and 32; stage s at
-// 64 + 128 s: [cos_hi 32 | cos_lo 32 | sin_hi 32 | sin_lo 32].
+// 64 + 128 s: [cos_hi 32 | cos_lo 32 | sin_hi 32 | sin_lo 32], two fp16
+// points per column.
 constexpr uint32_t kColA = 64;
 constexpr uint32_t kLBO = 128;
-constexpr uint32_t kSBO = (kChunk / 4) * 128;   // B: 8-channel groups
-constexpr int kBBytes = 16 * kChunk * 4;        // one B operand (hi or lo)
+constexpr uint32_t kSBO = (kChunk / 8) * 128;   // B: 8-channel groups
+constexpr int kBBytes = 16 * kChunk * 2;        // one fp16 B operand (hi or lo)
 
 __device__ __forceinline__ void sincos_rad(float4 w, float4 x, float& c, float& s) {
   // w = fp32(2 pi omega): the argument in radians; MUFU reduces it in turns.
@@ -39,14 +46,73 @@ __device__ __forceinline__ void sincos_rad(float4 w, float4 x, float& c, float& 
   __sincosf(t, &s, &c);
 }
 
+// max_i |F[i, j]| for every column j over all rows of all clouds, as fp32
+// bits (atomicMax on non-negative floats orders like their bit patterns: the
+// result is order-independent).  F is read once as float4s: with a grid
+// stride that is a multiple of d/4 (d % 4 == 0) each thread stays on the same
+// 4 columns; otherwise element-wise.
+constexpr int kColmaxThreads = 256;
+__global__ void __launch_bounds__(kColmaxThreads)
+colmax_kernel(const float* __restrict__ F, int64_t rows, int d, unsigned int* __restrict__ maxbits) {
+  extern __shared__ unsigned int smax[];  // d
+  for (int j = threadIdx.x; j < d; j += blockDim.x) smax[j] = 0u;
+  __syncthreads();
+  const int64_t total = rows * d;
+  const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if ((d & 3) == 0) {
+    const int q = d >> 2;                        // float4s per row
+    const int64_t stride = (nthreads / q) * q;   // keeps (k mod q) fixed per thread
+    const int64_t n4 = total >> 2;
+    float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t < stride) {
+      const float4* F4 = reinterpret_cast<const float4*>(F);
+      int64_t k = t;
+      for (; k + 3 * stride < n4; k += 4 * stride) {  // 4 loads in flight
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(F4 + k + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          mx.x = fmaxf(mx.x, fabsf(v[u].x));
+          mx.y = fmaxf(mx.y, fabsf(v[u].y));
+          mx.z = fmaxf(mx.z, fabsf(v[u].z));
+          mx.w = fmaxf(mx.w, fabsf(v[u].w));
+        }
+      }
+      for (; k < n4; k += stride) {
+        const float4 v = __ldg(F4 + k);
+        mx.x = fmaxf(mx.x, fabsf(v.x));
+        mx.y = fmaxf(mx.y, fabsf(v.y));
+        mx.z = fmaxf(mx.z, fabsf(v.z));
+        mx.w = fmaxf(mx.w, fabsf(v.w));
+      }
+      const int j = int(t % q) * 4;
+      if (mx.x > 0.f) atomicMax(smax + j, __float_as_uint(mx.x));
+      if (mx.y > 0.f) atomicMax(smax + j + 1, __float_as_uint(mx.y));
+      if (mx.z > 0.f) atomicMax(smax + j + 2, __float_as_uint(mx.z));
+      if (mx.w > 0.f) atomicMax(smax + j + 3, __float_as_uint(mx.w));
+    }
+  } else {
+    for (int64_t k = t; k < total; k += nthreads) {
+      const float v = fabsf(__ldg(F + k));
+      if (v > 0.f) atomicMax(smax + int(k % d), __float_as_uint(v));
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < d; j += blockDim.x)
+    if (smax[j]) atomicMax(maxbits + j, smax[j]);
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
 pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4, int m,
                 int64_t n, int ranges, const float* __restrict__ F, int d, int c0, int dc,
-                float* __restrict__ partial) {
+                const unsigned int* __restrict__ maxbits, float* __restrict__ partial) {
   __shared__ __align__(1024) unsigned char bsm[kStages][2 * kBBytes];
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages], dfull_bar[2], dempty_bar[2];
   __shared__ uint32_t tmem_sh;
-  __shared__ float4 xbuf[kProducerWarps][8];  // each producer warp's 8 points of the chunk
+  __shared__ float4 xbuf[kProducerWarps][16];  // each producer warp's 16 points of the chunk
+  __shared__ float fscale[16], fscale_inv[16];
 
   const int ft = blockIdx.x, rg = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, lg = warp & 3;
@@ -67,6 +133,20 @@ pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
     }
     tc::mbar_fence_init();
   }
+  if (tid >= 32 && tid < 48) {
+    // channel scale 2^e_j with max |F_j| 2^e_j in [2^13, 2^14) (1 for a zero
+    // or non-finite channel)
+    const int j = tid - 32;
+    const float mx = (j < dc) ? __uint_as_float(maxbits[c0 + j]) : 0.0f;
+    float scale = 1.0f;
+    if (mx > 0.0f && isfinite(mx)) {
+      int ex = 0;
+      frexpf(mx, &ex);  // mx in [2^(ex-1), 2^ex)
+      scale = ldexpf(1.0f, min(126, max(-126, 14 - ex)));  // 2^+-126: normal, exact inverse
+    }
+    fscale[j] = scale;
+    fscale_inv[j] = 1.0f / scale;  // exact: a power of two
+  }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -75,55 +155,72 @@ pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   const int f = ft * 128 + lg * 32 + lane;  // this lane's frequency
 
   if (warp < kProducerWarps) {
-    // ---------------- producers: 8 points per warp per chunk ---------------
-    const int q = warp >> 2;  // which 8 of the chunk's 32 points
+    // ---------------- producers: 16 points per warp per chunk --------------
+    const int q = warp >> 2;  // which 16 of the chunk's 64 points
     const float4 w = (f < m) ? omega4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
-    // B operand element of this lane: (channel j, point p) of each chunk;
-    // F is prefetched one chunk ahead (it streams from HBM).
-    const int e = warp * 32 + lane, pe = e >> 4, je = e & 15;
-    const uint32_t boff = uint32_t(je >> 3) * kSBO + uint32_t(pe >> 2) * kLBO +
-                          uint32_t(je & 7) * 16 + uint32_t(pe & 3) * 4;
+    // B operand elements of this lane: channels je, je + 1 of point pe of each
+    // chunk; F is prefetched one chunk ahead (it streams from HBM).
+    const int e = warp * 32 + lane, pe = e >> 3, je = (e & 7) * 2;
+    const uint32_t boff = uint32_t(je >> 3) * kSBO + uint32_t(pe >> 3) * kLBO +
+                          uint32_t(je & 7) * 16 + uint32_t(pe & 7) * 2;
+    const float sc0 = fscale[je], sc1 = fscale[je + 1];
     auto load_f = [&](int c) {
       const int64_t pp = p0 + int64_t(c) * kChunk + pe;
-      return (c < nchunks && pp < p1 && je < dc) ? __ldg(Fb + pp * d + c0 + je) : 0.0f;
+      float2 v = make_float2(0.f, 0.f);
+      if (c < nchunks && pp < p1) {
+        const float* Fi = Fb + pp * d + c0 + je;
+        if (je < dc) v.x = __ldg(Fi);
+        if (je + 1 < dc) v.y = __ldg(Fi + 1);
+      }
+      return v;
     };
-    float f_next = load_f(0);
-    // The warp's 8 points, prefetched one chunk ahead by lanes 0-7 (global
+    float2 f_next = load_f(0);
+    // The warp's 16 points, prefetched one chunk ahead by lanes 0-15 (global
     // latency off the critical path) and handed over through shared memory.
     auto load_x = [&](int c) {
-      const int64_t pp = p0 + int64_t(c) * kChunk + q * 8 + (lane & 7);
+      const int64_t pp = p0 + int64_t(c) * kChunk + q * 16 + (lane & 15);
       return __ldg(cloud + (pp < p1 ? pp : p1 - 1));
     };
     float4 x_next = load_x(0);
     for (int c = 0; c < nchunks; ++c) {
       const uint32_t s = c % kStages, u = c / kStages;
-      const float fv = f_next;
+      const float2 fv = f_next;
       f_next = load_f(c + 1);
       if (u >= 1) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
       {
-        uint32_t hi, lo;
-        tc::split_tf32(fv, hi, lo);
-        *reinterpret_cast<uint32_t*>(&bsm[s][boff]) = hi;
-        *reinterpret_cast<uint32_t*>(&bsm[s][kBBytes + boff]) = lo;
+        // rows je and je + 1 (channels) of column pe (point)
+        const float a0 = fv.x * sc0, a1 = fv.y * sc1;
+        const __half h0 = __float2half_rn(a0), h1 = __float2half_rn(a1);
+        const __half l0 = __float2half_rn(a0 - __half2float(h0));
+        const __half l1 = __float2half_rn(a1 - __half2float(h1));
+        *reinterpret_cast<__half*>(&bsm[s][boff]) = h0;
+        *reinterpret_cast<__half*>(&bsm[s][boff + 16]) = h1;
+        *reinterpret_cast<__half*>(&bsm[s][kBBytes + boff]) = l0;
+        *reinterpret_cast<__half*>(&bsm[s][kBBytes + boff + 16]) = l1;
       }
       // Points beyond the range (clamped loads) meet zero columns of F^T, and
       // lanes beyond m are never written out: no masking of the features.
-      uint32_t chi[8], clo[8], shi[8], slo[8];
-      if (lane < 8) xbuf[warp][lane] = x_next;
+      if (lane < 16) xbuf[warp][lane] = x_next;
       __syncwarp();
       if (c + 1 < nchunks) x_next = load_x(c + 1);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        float cs, sn;
-        sincos_rad(w, xbuf[warp][j], cs, sn);
-        tc::split_tf32_fast(cs, chi[j], clo[j]);
-        tc::split_tf32_fast(sn, shi[j], slo[j]);
-      }
       const uint32_t a = tmem + lane_field + kColA + 128 * s + 8 * q;
-      tc::tmem_st8(a, chi);
-      tc::tmem_st8(a + 32, clo);
-      tc::tmem_st8(a + 64, shi);
-      tc::tmem_st8(a + 96, slo);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // two halves of 8 points (register pressure)
+        float cs[8], sn[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sincos_rad(w, xbuf[warp][8 * h + j], cs[j], sn[j]);
+        uint32_t chi[4], clo[4], shi[4], slo[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          tc::split_f16x2(cs[2 * j], cs[2 * j + 1], chi[j], clo[j]);
+          tc::split_f16x2(sn[2 * j], sn[2 * j + 1], shi[j], slo[j]);
+        }
+        const uint32_t ah = a + 4 * h;
+        tc::tmem_st4(ah, chi[0], chi[1], chi[2], chi[3]);
+        tc::tmem_st4(ah + 32, clo[0], clo[1], clo[2], clo[3]);
+        tc::tmem_st4(ah + 64, shi[0], shi[1], shi[2], shi[3]);
+        tc::tmem_st4(ah + 96, slo[0], slo[1], slo[2], slo[3]);
+      }
       tc::tmem_st_wait();
       tc::fence_proxy_async_smem();
       tc::tc_fence_before();
@@ -132,7 +229,7 @@ pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
     }
   } else if (warp == kMmaWarp) {
     // ---------------- MMA issue: warp-uniform loop, one elected lane -------
-    const uint32_t idesc = tc::make_idesc(2, 128, 16);
+    const uint32_t idesc = tc::make_idesc(0, 128, 16);
     for (int c = 0; c < nchunks; ++c) {
       const uint32_t s = c % kStages, u = c / kStages;
       const int e = c / kEpoch;
@@ -146,15 +243,15 @@ pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
         const uint32_t a0 = tmem + kColA + 128 * s;
         const uint32_t dcos = tmem + 32 * buf, dsin = dcos + 16;
 #pragma unroll
-        for (int kk = 0; kk < kChunk / 8; ++kk) {
+        for (int kk = 0; kk < kChunk / 16; ++kk) {
           const uint64_t adv = uint64_t(2 * kk) * (kLBO >> 4);
           const uint32_t acc = (c % kEpoch > 0 || kk > 0) ? 1u : 0u;
-          tc::mma_tf32_ts(dcos, a0 + 8 * kk, bh + adv, idesc, acc);
-          tc::mma_tf32_ts(dcos, a0 + 8 * kk, bl + adv, idesc, 1u);
-          tc::mma_tf32_ts(dcos, a0 + 32 + 8 * kk, bh + adv, idesc, 1u);
-          tc::mma_tf32_ts(dsin, a0 + 64 + 8 * kk, bh + adv, idesc, acc);
-          tc::mma_tf32_ts(dsin, a0 + 64 + 8 * kk, bl + adv, idesc, 1u);
-          tc::mma_tf32_ts(dsin, a0 + 96 + 8 * kk, bh + adv, idesc, 1u);
+          tc::mma_f16_ts(dcos, a0 + 8 * kk, bh + adv, idesc, acc);
+          tc::mma_f16_ts(dcos, a0 + 8 * kk, bl + adv, idesc, 1u);
+          tc::mma_f16_ts(dcos, a0 + 32 + 8 * kk, bh + adv, idesc, 1u);
+          tc::mma_f16_ts(dsin, a0 + 64 + 8 * kk, bh + adv, idesc, acc);
+          tc::mma_f16_ts(dsin, a0 + 64 + 8 * kk, bl + adv, idesc, 1u);
+          tc::mma_f16_ts(dsin, a0 + 96 + 8 * kk, bh + adv, idesc, 1u);
         }
         tc::mma_commit(&empty_bar[s]);
         if (c % kEpoch == kEpoch - 1 || c == nchunks - 1) tc::mma_commit(&dfull_bar[buf]);
@@ -185,8 +282,8 @@ pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         if (j < dc) {
-          out[int64_t(2 * f) * dc + j] = acc[j];
-          out[int64_t(2 * f + 1) * dc + j] = acc[16 + j];
+          out[int64_t(2 * f) * dc + j] = acc[j] * fscale_inv[j];
+          out[int64_t(2 * f + 1) * dc + j] = acc[16 + j] * fscale_inv[j];
         }
       }
     }
@@ -207,12 +304,25 @@ int pass1_tc_ranges(int m, int64_t n, int batch, int sms) {
   return int(ranges);
 }
 
+void launch_colmax(const float* F, int64_t rows, int d, unsigned int* maxbits, cudaStream_t s) {
+  LaunchScope L("rfd_colmax", s);
+  cudaMemsetAsync(maxbits, 0, size_t(d) * sizeof(unsigned int), s);
+  const size_t smem = size_t(d) * sizeof(unsigned int);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(colmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  int64_t blocks = (rows * d / 4 + kColmaxThreads - 1) / kColmaxThreads;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  colmax_kernel<<<int(blocks), kColmaxThreads, smem, s>>>(F, rows, d, maxbits);
+}
+
 void launch_pass1_tc(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
-                     int ranges, const float* F, int d, int c0, int dc, float* partial,
-                     cudaStream_t s) {
+                     int ranges, const float* F, int d, int c0, int dc,
+                     const unsigned int* maxbits, float* partial, cudaStream_t s) {
   LaunchScope L("rfd_pass1_tc", s);
   const dim3 grid((m + 127) / 128, ranges, batch);
-  pass1_tc_kernel<<<grid, kThreads, 0, s>>>(pts, omega4, m, n, ranges, F, d, c0, dc, partial);
+  pass1_tc_kernel<<<grid, kThreads, 0, s>>>(pts, omega4, m, n, ranges, F, d, c0, dc, maxbits,
+                                           partial);
 }
 
 }  // namespace rfd
