@@ -74,11 +74,23 @@ __global__ void freq_kernel(float4* __restrict__ omega4, float4* __restrict__ om
   }
 }
 
+// pts: float4 (x, y, z, 0) per point.  pts16: per cloud, groups of 16 points
+// as [x0..x15 | y0..y15 | z0..z15] (pass 1 reads a group with 12 16-byte
+// copies and pairs neighbouring points in packed FP32 math); the tail group is
+// zero-padded (the buffer is cleared first when n % 16 != 0).
 __global__ void pack_kernel(const float* __restrict__ xyz, float4* __restrict__ pts,
-                            int64_t total) {
+                            float* __restrict__ pts16, int64_t n, int64_t total) {
+  const int64_t gpc = (n + 15) / 16;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
-       i += int64_t(gridDim.x) * blockDim.x)
-    pts[i] = make_float4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], 0.0f);
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const float x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+    pts[i] = make_float4(x, y, z, 0.0f);
+    const int64_t b = i / n, k = i - b * n;
+    float* g = pts16 + (b * gpc + k / 16) * 48 + (k & 15);
+    g[0] = x;
+    g[16] = y;
+    g[32] = z;
+  }
 }
 
 }  // namespace
@@ -89,12 +101,15 @@ void launch_freq(float4* omega4, float4* omega_rad4, double* nu, int* flags, int
   freq_kernel<<<1, 256, 0, s>>>(omega4, omega_rad4, nu, flags, m, seed, eps, R, c_r);
 }
 
-void launch_pack_points(const float* xyz, float4* pts, int64_t total, cudaStream_t s) {
+void launch_pack_points(const float* xyz, float4* pts, float* pts16, int64_t n, int batch,
+                        cudaStream_t s) {
   LaunchScope L("rfd_pack_points", s);
+  const int64_t total = n * batch;
+  if (n % 16 != 0) cudaMemsetAsync(pts16, 0, size_t(batch) * ((n + 15) / 16) * 48 * sizeof(float), s);
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  pack_kernel<<<int(blocks), 256, 0, s>>>(xyz, pts, total);
+  pack_kernel<<<int(blocks), 256, 0, s>>>(xyz, pts, pts16, n, total);
 }
 
 }  // namespace rfd

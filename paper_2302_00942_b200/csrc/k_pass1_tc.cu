@@ -40,12 +40,6 @@ constexpr uint32_t kLBO = 128;
 constexpr uint32_t kSBO = (kChunk / 8) * 128;   // B: 8-channel groups
 constexpr int kBBytes = 16 * kChunk * 2;        // one fp16 B operand (hi or lo)
 
-__device__ __forceinline__ void sincos_rad(float4 w, float4 x, float& c, float& s) {
-  // w = fp32(2 pi omega): the argument in radians; MUFU reduces it in turns.
-  const float t = fmaf(w.z, x.z, fmaf(w.y, x.y, w.x * x.x));
-  __sincosf(t, &s, &c);
-}
-
 // max_i |F[i, j]| for every column j over all rows of all clouds, as fp32
 // bits (atomicMax on non-negative floats orders like their bit patterns: the
 // result is order-independent).  F is read once as float4s: with a grid
@@ -105,20 +99,25 @@ colmax_kernel(const float* __restrict__ F, int64_t rows, int d, unsigned int* __
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4, int m,
+pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omega4, int m,
                 int64_t n, int ranges, const float* __restrict__ F, int d, int c0, int dc,
                 const unsigned int* __restrict__ maxbits, float* __restrict__ partial) {
   __shared__ __align__(1024) unsigned char bsm[kStages][2 * kBBytes];
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages], dfull_bar[2], dempty_bar[2];
   __shared__ uint32_t tmem_sh;
-  __shared__ float4 xbuf[kProducerWarps][16];  // each producer warp's 16 points of the chunk
+  // each producer warp's 16 points of a chunk as [x0..15 | y0..15 | z0..15],
+  // 3 chunks deep (cp.async ring)
+  __shared__ __align__(16) float xbuf[3][kProducerWarps][48];
   __shared__ float fscale[16], fscale_inv[16];
 
   const int ft = blockIdx.x, rg = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, lg = warp & 3;
-  const int64_t p0 = n * rg / ranges, p1 = n * (rg + 1) / ranges;
-  const int nchunks = int((p1 - p0 + kChunk - 1) / kChunk);
-  const float4* cloud = pts + int64_t(b) * n;
+  // ranges are whole chunks; only a cloud's last chunk is partial
+  const int64_t cpc = (n + kChunk - 1) / kChunk, gpc = (n + 15) / 16;
+  const int64_t ch0 = cpc * rg / ranges, ch1 = cpc * (rg + 1) / ranges;
+  const int64_t p0 = ch0 * kChunk;
+  const int nchunks = int(ch1 - ch0);
+  const float* cloud16 = pts16 + int64_t(b) * gpc * 48;
   const float* Fb = F + int64_t(b) * n * d;
 
   if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
@@ -158,57 +157,93 @@ pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
     // ---------------- producers: 16 points per warp per chunk --------------
     const int q = warp >> 2;  // which 16 of the chunk's 64 points
     const float4 w = (f < m) ? omega4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
-    // B operand elements of this lane: channels je, je + 1 of point pe of each
-    // chunk; F is prefetched one chunk ahead (it streams from HBM).
-    const int e = warp * 32 + lane, pe = e >> 3, je = (e & 7) * 2;
-    const uint32_t boff = uint32_t(je >> 3) * kSBO + uint32_t(pe >> 3) * kLBO +
-                          uint32_t(je & 7) * 16 + uint32_t(pe & 7) * 2;
-    const float sc0 = fscale[je], sc1 = fscale[je + 1];
-    auto load_f = [&](int c) {
-      const int64_t pp = p0 + int64_t(c) * kChunk + pe;
+    const float2 wx = make_float2(w.x, w.x), wy = make_float2(w.y, w.y), wz = make_float2(w.z, w.z);
+    // B operand elements of this lane: channel je of points 2 pe, 2 pe + 1 of
+    // each chunk (one 32-bit word of the K-major core matrix); F is prefetched
+    // one chunk ahead (it streams from HBM).  Pointers and counters advance
+    // per chunk (no 64-bit index arithmetic in the loop).
+    const int e = warp * 32 + lane, je = e & 15, pe = e >> 4;
+    const uint32_t boff = uint32_t(je >> 3) * kSBO + uint32_t(pe >> 2) * kLBO +
+                          uint32_t(je & 7) * 16 + uint32_t(pe & 3) * 4;
+    const uint32_t b_s = tc::smem_addr(&bsm[0][0]) + boff;
+    const float sc = fscale[je];
+    const bool jok = je < dc;
+    const float* fptr = Fb + (p0 + 2 * pe) * d + c0 + je;
+    const int64_t fstep = int64_t(kChunk) * d;
+    const int64_t frem0 = n - (p0 + 2 * pe);
+    int frem = int(frem0 > 0x7fffffff ? 0x7fffffff : frem0);  // points left from the first
+    auto load_f = [&]() {
       float2 v = make_float2(0.f, 0.f);
-      if (c < nchunks && pp < p1) {
-        const float* Fi = Fb + pp * d + c0 + je;
-        if (je < dc) v.x = __ldg(Fi);
-        if (je + 1 < dc) v.y = __ldg(Fi + 1);
+      if (jok && frem > 0) {
+        v.x = __ldg(fptr);
+        if (frem > 1) v.y = __ldg(fptr + d);
       }
+      fptr += fstep;
+      frem -= kChunk;
       return v;
     };
-    float2 f_next = load_f(0);
-    // The warp's 16 points, prefetched one chunk ahead by lanes 0-15 (global
-    // latency off the critical path) and handed over through shared memory.
-    auto load_x = [&](int c) {
-      const int64_t pp = p0 + int64_t(c) * kChunk + q * 16 + (lane & 15);
-      return __ldg(cloud + (pp < p1 ? pp : p1 - 1));
+    float2 f_next = load_f();
+    // The warp's 16 points (one SoA group, 192 B), copied two chunks ahead by
+    // lanes 0-11 straight into shared memory (cp.async: global latency off the
+    // critical path).  Groups past the cloud's end repeat its last group
+    // (finite values that meet zero F).
+    const float* xsrc = cloud16 + ((ch0 * (kChunk / 16) + q) * 48 + 4 * lane);
+    const float* xlast = cloud16 + ((gpc - 1) * 48 + 4 * lane);
+    const int64_t xrem0 = gpc - (ch0 * (kChunk / 16) + q);
+    int xrem = int(xrem0 > 0x7fffffff ? 0x7fffffff : xrem0);  // groups left
+    constexpr uint32_t kRing = kProducerWarps * 48 * 4;           // bytes per ring slot
+    const uint32_t x_s = tc::smem_addr(&xbuf[0][warp][0]);
+    uint32_t xw = 0;
+    auto load_x = [&](bool valid) {
+      if (lane < 12 && valid) tc::cp_async16(x_s + xw * kRing + 16 * lane, xrem > 0 ? xsrc : xlast);
+      tc::cp_async_commit();  // one group per chunk, empty past the end
+      xsrc += 48 * (kChunk / 16);
+      xrem -= kChunk / 16;
+      xw = (xw == 2) ? 0 : xw + 1;
     };
-    float4 x_next = load_x(0);
+    load_x(nchunks > 0);
+    load_x(nchunks > 1);
+    const uint32_t empty_s = tc::smem_addr(&empty_bar[0]), full_s = tc::smem_addr(&full_bar[0]);
+    uint32_t s = 0, u = 0, xr = 0;  // stage, its round, ring slot read
     for (int c = 0; c < nchunks; ++c) {
-      const uint32_t s = c % kStages, u = c / kStages;
       const float2 fv = f_next;
-      f_next = load_f(c + 1);
-      if (u >= 1) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
+      f_next = load_f();
+      load_x(c + 2 < nchunks);  // the slot chunk c - 1 read (ordered by its __syncwarp)
+      if (u >= 1) tc::mbar_wait(empty_s + 8 * s, (u - 1) & 1);
       {
-        // rows je and je + 1 (channels) of column pe (point)
-        const float a0 = fv.x * sc0, a1 = fv.y * sc1;
-        const __half h0 = __float2half_rn(a0), h1 = __float2half_rn(a1);
-        const __half l0 = __float2half_rn(a0 - __half2float(h0));
-        const __half l1 = __float2half_rn(a1 - __half2float(h1));
-        *reinterpret_cast<__half*>(&bsm[s][boff]) = h0;
-        *reinterpret_cast<__half*>(&bsm[s][boff + 16]) = h1;
-        *reinterpret_cast<__half*>(&bsm[s][kBBytes + boff]) = l0;
-        *reinterpret_cast<__half*>(&bsm[s][kBBytes + boff + 16]) = l1;
+        uint32_t hi, lo;
+        tc::split_f16x2(fv.x * sc, fv.y * sc, hi, lo);
+        tc::st_shared_u32(b_s + s * (2 * kBBytes), hi);
+        tc::st_shared_u32(b_s + s * (2 * kBBytes) + kBBytes, lo);
       }
-      // Points beyond the range (clamped loads) meet zero columns of F^T, and
-      // lanes beyond m are never written out: no masking of the features.
-      if (lane < 16) xbuf[warp][lane] = x_next;
+      // Points beyond the cloud meet zero columns of F^T, and lanes beyond m
+      // are never written out: no masking of the features.
+      tc::cp_async_wait<2>();  // chunk c's group (c + 1, c + 2 may be in flight)
       __syncwarp();
-      if (c + 1 < nchunks) x_next = load_x(c + 1);
+      const float* xs = &xbuf[0][warp][0] + xr * (kProducerWarps * 48);
+      xr = (xr == 2) ? 0 : xr + 1;
       const uint32_t a = tmem + lane_field + kColA + 128 * s + 8 * q;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {  // two halves of 8 points (register pressure)
         float cs[8], sn[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) sincos_rad(w, xbuf[warp][8 * h + j], cs[j], sn[j]);
+        for (int j = 0; j < 8; j += 4) {
+          // omega . x for 4 points in packed FP32 (2 points per instruction),
+          // the same operation order as fmaf(wz, z, fmaf(wy, y, wx * x))
+          const float4 X = *reinterpret_cast<const float4*>(xs + 8 * h + j);
+          const float4 Y = *reinterpret_cast<const float4*>(xs + 16 + 8 * h + j);
+          const float4 Z = *reinterpret_cast<const float4*>(xs + 32 + 8 * h + j);
+          float2 t0 = __fmul2_rn(wx, make_float2(X.x, X.y));
+          float2 t1 = __fmul2_rn(wx, make_float2(X.z, X.w));
+          t0 = __ffma2_rn(wy, make_float2(Y.x, Y.y), t0);
+          t1 = __ffma2_rn(wy, make_float2(Y.z, Y.w), t1);
+          t0 = __ffma2_rn(wz, make_float2(Z.x, Z.y), t0);
+          t1 = __ffma2_rn(wz, make_float2(Z.z, Z.w), t1);
+          __sincosf(t0.x, &sn[j], &cs[j]);
+          __sincosf(t0.y, &sn[j + 1], &cs[j + 1]);
+          __sincosf(t1.x, &sn[j + 2], &cs[j + 2]);
+          __sincosf(t1.y, &sn[j + 3], &cs[j + 3]);
+        }
         uint32_t chi[4], clo[4], shi[4], slo[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -225,7 +260,11 @@ pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       tc::fence_proxy_async_smem();
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&full_bar[s]);
+      if (lane == 0) tc::mbar_arrive(full_s + 8 * s);
+      if (++s == kStages) {
+        s = 0;
+        ++u;
+      }
     }
   } else if (warp == kMmaWarp) {
     // ---------------- MMA issue: warp-uniform loop, one elected lane -------
@@ -296,6 +335,7 @@ pass1_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
 }  // namespace
 
 int pass1_tc_ranges(int m, int64_t n, int batch, int sms) {
+  // ranges of whole chunks: about one CTA per SM
   const int ftiles = (m + 127) / 128;
   int64_t ranges = (int64_t(sms) + int64_t(ftiles) * batch - 1) / (int64_t(ftiles) * batch);
   const int64_t maxr = (n + kChunk - 1) / kChunk;
@@ -316,12 +356,12 @@ void launch_colmax(const float* F, int64_t rows, int d, unsigned int* maxbits, c
   colmax_kernel<<<int(blocks), kColmaxThreads, smem, s>>>(F, rows, d, maxbits);
 }
 
-void launch_pass1_tc(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
+void launch_pass1_tc(const float* pts16, const float4* omega4, int m, int64_t n, int batch,
                      int ranges, const float* F, int d, int c0, int dc,
                      const unsigned int* maxbits, float* partial, cudaStream_t s) {
   LaunchScope L("rfd_pass1_tc", s);
   const dim3 grid((m + 127) / 128, ranges, batch);
-  pass1_tc_kernel<<<grid, kThreads, 0, s>>>(pts, omega4, m, n, ranges, F, d, c0, dc, maxbits,
+  pass1_tc_kernel<<<grid, kThreads, 0, s>>>(pts16, omega4, m, n, ranges, F, d, c0, dc, maxbits,
                                            partial);
 }
 

@@ -108,6 +108,7 @@ struct rfd_plan {
   rfd::PassGeom pg{};
   // owned device state
   float4* pts = nullptr;      // batch*n
+  float* pts16 = nullptr;     // batch*ceil(n/16)*48: SoA groups of 16 points (pass 1)
   float4* omega4 = nullptr;   // m
   float4* omega_rad4 = nullptr;  // m: fp32(2 pi omega) for the tensor-core kernels
   double* nu = nullptr;       // m
@@ -230,6 +231,7 @@ void free_plan(rfd_plan* p) {
   cudaStream_t s = p->stream;
   cudaStreamSynchronize(s);
   dfree(p->pts, s);
+  dfree(p->pts16, s);
   dfree(p->omega4, s);
   dfree(p->omega_rad4, s);
   dfree(p->nu, s);
@@ -296,6 +298,7 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   const size_t rr = size_t(p->r) * p->r;
 
   RFD_CUDA(dalloc(&p->pts, size_t(total), st));
+  RFD_CUDA(dalloc(&p->pts16, size_t(batch) * size_t((n + 15) / 16) * 48, st));
   RFD_CUDA(dalloc(&p->omega4, size_t(m), st));
   RFD_CUDA(dalloc(&p->omega_rad4, size_t(m), st));
   RFD_CUDA(dalloc(&p->nu, size_t(m), st));
@@ -313,7 +316,7 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
                              cudaMemcpyHostToDevice, st));
     dev_xyz = staged;
   }
-  rfd::launch_pack_points(dev_xyz, p->pts, total, st);
+  rfd::launch_pack_points(dev_xyz, p->pts, p->pts16, n, batch, st);
   rfd::launch_freq(p->omega4, p->omega_rad4, p->nu, p->flags, m, seed, eps, RFD_TRUNCATION_R, cached_c_r(), st);
 
   // a4: Gram -- tensor cores (tcgen05, fp16 hi/lo split) unless the SIMT
@@ -408,7 +411,7 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
                         p->s_partial, st);
       rfd::launch_reduce_S(p->s_partial, p->m, p->batch, p->pg.chunks, d, c0, dc, p->S, st);
     } else {
-      rfd::launch_pass1_tc(p->pts, p->omega_rad4, p->m, p->n, p->batch, ranges, F, d, c0, dc,
+      rfd::launch_pass1_tc(p->pts16, p->omega_rad4, p->m, p->n, p->batch, ranges, F, d, c0, dc,
                            p->fmax, p->s_partial, st);
       rfd::launch_reduce_S(p->s_partial, p->m, p->batch, ranges, d, c0, dc, p->S, st);
     }

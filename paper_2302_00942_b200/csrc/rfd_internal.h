@@ -34,7 +34,8 @@ void launch_freq(float4* omega4, float4* omega_rad4, double* nu, int* flags, int
                  uint64_t seed, double eps, double R, double c_r, cudaStream_t s);
 
 // ---------------------------------------------------------------- pack
-void launch_pack_points(const float* xyz, float4* pts, int64_t total, cudaStream_t s);
+void launch_pack_points(const float* xyz, float4* pts, float* pts16, int64_t n, int batch,
+                        cudaStream_t s);
 
 // ---------------------------------------------------------------- Gram
 struct GramGeom {
@@ -103,7 +104,7 @@ void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, 
 
 // Tensor-core pass 1 (k_pass1_tc.cu): partial[b][range][2m][dc].
 int pass1_tc_ranges(int m, int64_t n, int batch, int sms);
-void launch_pass1_tc(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
+void launch_pass1_tc(const float* pts16, const float4* omega4, int m, int64_t n, int batch,
                      int ranges, const float* F, int d, int c0, int dc,
                      const unsigned int* maxbits, float* partial, cudaStream_t s);
 // max_i |F[i, j]| per column (fp32 bits) for pass 1's fp16 channel scaling.

@@ -33,7 +33,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// The same on a precomputed shared-memory address (hot loops).
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 // ---------------------------------------------------------------- fences
+// 16-byte global -> shared copy that bypasses the registers (LDGSTS): the
+// consumer waits on the group, not on a register scoreboard.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -124,25 +149,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 // ---------------------------------------------------------------- splits
 // x = hi + lo with hi = fp16(x), lo = fp16(x - hi): |x - hi - lo| <= 2^-22 |x|
 // (+ 2^-25 absolute in fp16's subnormal range).  Packs two values per word.
+// The residual x - hi (exact in fp32) is one mixed-precision FMA per value,
+// fma.rn.f32.f16 (hi * -1 + x, sm_100: FHFMA reads the fp16 half in place):
+// 4 instructions per 2 values instead of unpack + subtract.
 __device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
-  const __half2 h = __floats2half2_rn(a, b);
-  const float2 hf = __half22float2(h);
-  const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
-  hi = *reinterpret_cast<const uint32_t*>(&h);
-  lo = *reinterpret_cast<const uint32_t*>(&l);
+  asm("{\n\t.reg .f16 h0, h1, m1;\n\t.reg .f32 r0, r1;\n\t"
+      "cvt.rn.f16x2.f32 %0, %3, %2;\n\t"
+      "mov.b32 {h0, h1}, %0;\n\t"
+      "mov.b16 m1, 0xBC00;\n\t"
+      "fma.rn.f32.f16 r0, h0, m1, %2;\n\t"
+      "fma.rn.f32.f16 r1, h1, m1, %3;\n\t"
+      "cvt.rn.f16x2.f32 %1, r1, r0;\n\t}"
+      : "=r"(hi), "=r"(lo)
+      : "f"(a), "f"(b));
 }
 
-// The same split for a packed pair, subtracting with one packed FP32 op
-// (sm_100 FADD2): 5 instructions per 2 values.
 __device__ __forceinline__ void split_f16x2_v2(float2 v, uint32_t& hi, uint32_t& lo) {
-  const __half2 h = __floats2half2_rn(v.x, v.y);
-  const float2 hf = __half22float2(h);
-  const float2 d = __fadd2_rn(v, make_float2(-hf.x, -hf.y));
-  const __half2 l = __floats2half2_rn(d.x, d.y);
-  hi = *reinterpret_cast<const uint32_t*>(&h);
-  lo = *reinterpret_cast<const uint32_t*>(&l);
+  split_f16x2(v.x, v.y, hi, lo);
 }
 
+__device__ __forceinline__ void st_shared_u32(uint32_t addr, uint32_t a) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(a) : "memory");
+}
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                              uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),

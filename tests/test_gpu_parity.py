@@ -144,6 +144,27 @@ def test_ragged_shapes_parity(n, m, d):
     _check_against_oracle(plan, out, x, F, p)
 
 
+def test_field_column_scales_parity():
+    # Pass 1 scales each channel of F by a power of two into fp16 range
+    # (pass 1): columns spanning 1e-30 .. 1e30, a zero column and
+    # a column with one nonzero entry must each meet the tolerance on their own.
+    n, m = 3000, 64
+    x = _sphere(n, 5)
+    g = np.random.default_rng(6).standard_normal((n, 6))
+    scales = np.array([1e-30, 1e-6, 1.0, 1e6, 1e30, 0.0])
+    F = (g * scales).astype(np.float32)
+    F[:, 5] = 0.0
+    F[1234, 5] = 3.0
+    p = dict(name="column scales", eps=0.05, lam=-0.8, m=m, seed=21)
+    plan, out = _run_single(x, F, p)
+    ref = orf.Plan(x, p["eps"], p["lam"], p["m"], p["seed"]).apply(F.astype(np.float64))
+    for c in range(6):
+        e_out = relerr(out[:, c], ref["out"][:, c])
+        e_del = relerr(out[:, c] - F[:, c].astype(np.float64), ref["out"][:, c] - F[:, c])
+        print("column", c, "%.2e %.2e" % (e_out, e_del))
+        assert e_out <= TOL and e_del <= TOL, (c, e_out, e_del)
+
+
 @pytest.mark.parametrize("n,m,seed,lam", [(1000, 40, 11, -0.8), (3001, 96, 14, -0.3),
                                           (2000, 128, 13, 0.05)])
 def test_negative_nu_nonsymmetric_route(n, m, seed, lam):

@@ -1,6 +1,8 @@
-# Full round measurement: tests, default bench (with cpu_baseline + e2e), reference arm,
-# ncu launch list of the bench command, ncu --set full of the top kernels.
+# Full round measurement: GPU tests, smoke, default bench (cpu_baseline + e2e),
+# reference arm, ncu launch list of the bench command, ncu --set full of the
+# top kernels.  Outputs under gpurun_out/.
 mkdir -p gpurun_out
+python -c "from paper_2302_00942_b200 import build; build.build()" > gpurun_out/build.log 2>&1
 timeout 900 python -m pytest tests -m gpu -q -s > gpurun_out/gpu_tests.log 2>&1; echo tests rc $?
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc $?
 nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv -lms 200 > gpurun_out/clocks.csv 2>&1 &
@@ -11,4 +13,4 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 C="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 600 $C > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $C > gpurun_out/ncu_launches.log 2>&1; echo launches rc $?
 C2="python tools/profile_step.py"
-timeout 300 $C2 > gpurun_out/plain2.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"gram_tc_kernel|pass1_tc|pass2_tc" -c 3 -o gpurun_out/full $C2 > gpurun_out/ncu_full.log 2>&1; echo full rc $?
+timeout 300 $C2 > gpurun_out/plain2.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"gram_pair_kernel|pass1_tc|pass2_tc|dgemm" -c 4 -o gpurun_out/full $C2 > gpurun_out/ncu_full.log 2>&1; echo full rc $?
