@@ -35,12 +35,6 @@ constexpr uint32_t kColD = 0;   // accumulators: cols [0,16) and [16,32)
 constexpr uint32_t kColA = 32;  // stage s: hi at 32 + 128 s (64 cols = 128 fp16), lo at +64
 constexpr uint32_t kLBO = 128;
 
-__device__ __forceinline__ void sincos_rad(float4 w, float4 x, float& c, float& s) {
-  // w = fp32(2 pi omega): the argument in radians; MUFU reduces it in turns.
-  const float t = fmaf(w.z, x.z, fmaf(w.y, x.y, w.x * x.x));
-  __sincosf(t, &s, &c);
-}
-
 __global__ void __launch_bounds__(kThreads, 1)
 pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4, int m, int64_t n,
                 int batch, const float* __restrict__ Y, const float* F, float* out, int d, int c0,
@@ -59,7 +53,10 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   const uint32_t sbo = uint32_t(kpad / 8) * 128;
   unsigned char* yb = smem;                          // B hi: 16 x kpad fp16
   unsigned char* yl = smem + 16 * kpad * 2;          // B lo
-  float4* om = reinterpret_cast<float4*>(smem + 2 * 16 * kpad * 2);
+  // omega (radians) as SoA: x components of all frequencies, then y, then z
+  float* ox = reinterpret_cast<float*>(smem + 2 * 16 * kpad * 2);
+  float* oy = ox + nch * 64;
+  float* oz = oy + nch * 64;
   __shared__ unsigned int ymax_bits[16];
   __shared__ float yscale_inv[16];
   const uint32_t yb_s = tc::smem_addr(yb), yl_s = tc::smem_addr(yl);
@@ -77,8 +74,12 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
     tc::mbar_init(&yready_bar, 1);
     tc::mbar_fence_init();
   }
-  for (int k = tid; k < nch * 64; k += kThreads)
-    om[k] = (k < m) ? omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k = tid; k < nch * 64; k += kThreads) {
+    const float4 w = (k < m) ? omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+    ox[k] = w.x;
+    oy[k] = w.y;
+    oz[k] = w.z;
+  }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -136,7 +137,17 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   // barrier, taken once all MMAs issued so far have completed.
   uint32_t g = 0, it = 0;
   int cur_b = -1;
-  float4 x_next = make_float4(0.f, 0.f, 0.f, 0.f);
+  // Each producer lane's point, copied one tile ahead into a private 2-slot
+  // shared-memory ring (cp.async: no register scoreboard on the global load).
+  __shared__ __align__(16) float4 xring[2][kProducerWarps][32];
+  auto copy_x = [&](int64_t t, int slot) {
+    const int bt = int(t / tpc);
+    const int64_t i = (t % tpc) * kTile + lg * 32 + lane;
+    // points past the cloud's end read its first point (finite; their rows
+    // of the output are never stored)
+    tc::cp_async16(tc::smem_addr(&xring[slot][warp][lane]), pts + int64_t(bt) * n + (i < n ? i : 0));
+    tc::cp_async_commit();
+  };
   for (int64_t tile = t_begin; tile < t_end; ++tile, ++it) {
     const int b = int(tile / tpc);
     const int64_t base = (tile % tpc) * kTile;
@@ -152,16 +163,12 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       // ---------------- producers: 16 frequencies per thread per chunk -----
       const int q = warp >> 2;  // which 16 of the chunk's 64 frequencies
       // This tile's point (prefetched during the previous tile) and the next's.
-      if (tile == t_begin) {
-        const int64_t i0 = base + lg * 32 + lane;
-        x_next = (i0 < n) ? pts[int64_t(b) * n + i0] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      const float4 x = x_next;
-      if (tile + 1 < t_end) {
-        const int bn = int((tile + 1) / tpc);
-        const int64_t in = ((tile + 1) % tpc) * kTile + lg * 32 + lane;
-        x_next = (in < n) ? pts[int64_t(bn) * n + in] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+      if (tile == t_begin) copy_x(tile, 0);
+      if (tile + 1 < t_end) copy_x(tile + 1, int(it + 1) & 1);
+      else tc::cp_async_commit();
+      tc::cp_async_wait<1>();  // this tile's copy
+      const float4 x = xring[it & 1][warp][lane];
+      const float2 xx = make_float2(x.x, x.x), xy = make_float2(x.y, x.y), xz = make_float2(x.z, x.z);
       for (int c = 0; c < nch; ++c) {
         const uint32_t gg = g + c, s = gg % kStages, u = gg / kStages;
         if (u >= 1) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
@@ -171,8 +178,24 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
           float v[16];
           const int f0 = 64 * c + 16 * q + 8 * h;
           // Frequencies beyond m (zero omega) meet zero rows of Y^T: no masking.
+          // omega . x for 2 frequencies per packed FP32 instruction, in the
+          // operation order of fmaf(wz, z, fmaf(wy, y, wx * x)).
 #pragma unroll
-          for (int j = 0; j < 8; ++j) sincos_rad(om[f0 + j], x, v[2 * j], v[2 * j + 1]);
+          for (int j = 0; j < 8; j += 4) {
+            const float4 WX = *reinterpret_cast<const float4*>(ox + f0 + j);
+            const float4 WY = *reinterpret_cast<const float4*>(oy + f0 + j);
+            const float4 WZ = *reinterpret_cast<const float4*>(oz + f0 + j);
+            float2 t0 = __fmul2_rn(make_float2(WX.x, WX.y), xx);
+            float2 t1 = __fmul2_rn(make_float2(WX.z, WX.w), xx);
+            t0 = __ffma2_rn(make_float2(WY.x, WY.y), xy, t0);
+            t1 = __ffma2_rn(make_float2(WY.z, WY.w), xy, t1);
+            t0 = __ffma2_rn(make_float2(WZ.x, WZ.y), xz, t0);
+            t1 = __ffma2_rn(make_float2(WZ.z, WZ.w), xz, t1);
+            __sincosf(t0.x, &v[2 * j + 1], &v[2 * j]);
+            __sincosf(t0.y, &v[2 * j + 3], &v[2 * j + 2]);
+            __sincosf(t1.x, &v[2 * j + 5], &v[2 * j + 4]);
+            __sincosf(t1.y, &v[2 * j + 7], &v[2 * j + 6]);
+          }
           // interleaved features (2j = cos, 2j+1 = sin): one fp16 pair per column
           uint32_t hi[8], lo[8];
 #pragma unroll
@@ -268,7 +291,7 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
 
 size_t pass2_tc_smem(int m) {
   const int nch = (m + 63) / 64;
-  return size_t(2) * 16 * nch * kChunkF * 2 + size_t(nch * 64) * sizeof(float4);
+  return size_t(2) * 16 * nch * kChunkF * 2 + size_t(nch * 64) * 3 * sizeof(float);
 }
 
 void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
