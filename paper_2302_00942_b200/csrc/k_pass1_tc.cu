@@ -2,24 +2,28 @@
 // first bracket "B^T x" of Eq. 13).
 //
 // A CTA owns a tile of 128 frequencies (TMEM lanes) and a contiguous range of
-// points (the contraction dimension K).  Per chunk of 64 points the 16
-// producer warps regenerate cos and sin of omega_k . x for their lane's
-// frequency (a3) and write them, split x = hi + lo in fp16 (|x - hi - lo| <=
-// 2^-22 |x| + 2^-25), straight into TMEM as the A operands (cos rows, sin
-// rows).  F's chunk is the B operand in shared memory (16 channels x 64
-// points, K-major), scaled per channel by a power of two into fp16 range
-// (max_i |F_ij| 2^e_j in [2^13, 2^14); undone exactly on the partial sums)
-// and split likewise.  One elected lane issues
-//     D_cos += C_hi F_hi^T + C_hi F_lo^T + C_lo F_hi^T,  D_sin likewise
-// (tcgen05.mma kind::f16, M = 128, N = 16, K = 16 x 4).  With N = 16 the
-// instruction count paces the tensor core, and kind::f16 needs half the
-// instructions of kind::tf32 per point.  The fp32 accumulator of the tensor
-// core is not round-to-nearest, so D accumulates for an epoch of 8 chunks (512
-// points) in one of two TMEM buffers and 4 drain warps move it into fp32
-// registers; at the end each lane writes its frequency's 2 x 16 partial sums.
-// K5 then reduces the partials in a fixed order in fp64.
+// whole chunks of 64 points (the contraction dimension K).  Warp roles:
 //
-// The channel scales come from a column max-|F| pre-pass (one read of F).
+//   * 16 producer warps regenerate cos and sin of omega_k . x for their
+//     lane's frequency (a3; 16 points per warp and chunk, read as one SoA
+//     group copied ahead with cp.async, arguments in packed FP32) and write
+//     them, split x = hi + lo in fp16 (|x - hi - lo| <= 2^-22 |x| + 2^-25),
+//     straight into TMEM as the A operands (cos rows, sin rows);
+//   * one elected lane of the MMA warp issues per chunk
+//         D_cos += C_hi F_hi^T + C_hi F_lo^T + C_lo F_hi^T,  D_sin likewise
+//     (tcgen05.mma kind::f16, M = 128, N = 16, K = 16 x 4: with N = 16 the
+//     instruction count paces the tensor core, and kind::f16 needs half the
+//     instructions of kind::tf32);
+//   * 4 F/drain warps stage F: per epoch of 8 chunks (512 points) they read
+//     the epoch's 512 x 16 block of F, scale each channel by a power of two
+//     into fp16 range (max |F_j| 2^e_j in [2^13, 2^14) over the epoch) and
+//     write it, split likewise, as the B operands of the epoch's 8 chunks
+//     (16 channels x 64 points, K-major, double-buffered by epoch).  The tensor
+//     core's fp32 accumulator is not round-to-nearest, so D accumulates for
+//     one epoch in one of two TMEM buffers; the same warps then move it into
+//     fp32 registers, undoing the epoch's scale exactly (x 2^-e_j).  At the
+//     end each lane writes its frequency's 2 x 16 partial sums; K5 reduces the
+//     partials in a fixed order in fp64.
 #include "rfd_internal.h"
 #include "tc_ptx.cuh"
 
@@ -28,87 +32,38 @@ namespace {
 
 constexpr int kProducerWarps = 16;  // 4 per TMEM lane group
 constexpr int kMmaWarp = 16;
-constexpr int kThreads = 21 * 32;   // + MMA warp + 4 drain warps (17..20)
-constexpr int kChunk = 64;          // points per chunk
+constexpr int kFWarp0 = 17;         // warps 17..20: F staging + drains
+constexpr int kThreads = 21 * 32;
+constexpr int kChunk = 64;          // points per chunk (16 per producer warp)
+constexpr int kArr = kChunk / 2;    // TMEM columns per A array (fp16 pairs)
 constexpr int kStages = 3;
 constexpr int kEpoch = 8;           // chunks per TMEM accumulation epoch
 // TMEM columns: D buffers (cos 16 + sin 16) at 0 and 32; stage s at
-// 64 + 128 s: [cos_hi 32 | cos_lo 32 | sin_hi 32 | sin_lo 32], two fp16
+// 64 + 128 s: [cos_hi | cos_lo | sin_hi | sin_lo], 32 columns each, two fp16
 // points per column.
 constexpr uint32_t kColA = 64;
 constexpr uint32_t kLBO = 128;
 constexpr uint32_t kSBO = (kChunk / 8) * 128;   // B: 8-channel groups
-constexpr int kBBytes = 16 * kChunk * 2;        // one fp16 B operand (hi or lo)
-
-// max_i |F[i, j]| for every column j over all rows of all clouds, as fp32
-// bits (atomicMax on non-negative floats orders like their bit patterns: the
-// result is order-independent).  F is read once as float4s: with a grid
-// stride that is a multiple of d/4 (d % 4 == 0) each thread stays on the same
-// 4 columns; otherwise element-wise.
-constexpr int kColmaxThreads = 256;
-__global__ void __launch_bounds__(kColmaxThreads)
-colmax_kernel(const float* __restrict__ F, int64_t rows, int d, unsigned int* __restrict__ maxbits) {
-  extern __shared__ unsigned int smax[];  // d
-  for (int j = threadIdx.x; j < d; j += blockDim.x) smax[j] = 0u;
-  __syncthreads();
-  const int64_t total = rows * d;
-  const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
-  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if ((d & 3) == 0) {
-    const int q = d >> 2;                        // float4s per row
-    const int64_t stride = (nthreads / q) * q;   // keeps (k mod q) fixed per thread
-    const int64_t n4 = total >> 2;
-    float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (t < stride) {
-      const float4* F4 = reinterpret_cast<const float4*>(F);
-      int64_t k = t;
-      for (; k + 3 * stride < n4; k += 4 * stride) {  // 4 loads in flight
-        float4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldg(F4 + k + u * stride);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          mx.x = fmaxf(mx.x, fabsf(v[u].x));
-          mx.y = fmaxf(mx.y, fabsf(v[u].y));
-          mx.z = fmaxf(mx.z, fabsf(v[u].z));
-          mx.w = fmaxf(mx.w, fabsf(v[u].w));
-        }
-      }
-      for (; k < n4; k += stride) {
-        const float4 v = __ldg(F4 + k);
-        mx.x = fmaxf(mx.x, fabsf(v.x));
-        mx.y = fmaxf(mx.y, fabsf(v.y));
-        mx.z = fmaxf(mx.z, fabsf(v.z));
-        mx.w = fmaxf(mx.w, fabsf(v.w));
-      }
-      const int j = int(t % q) * 4;
-      if (mx.x > 0.f) atomicMax(smax + j, __float_as_uint(mx.x));
-      if (mx.y > 0.f) atomicMax(smax + j + 1, __float_as_uint(mx.y));
-      if (mx.z > 0.f) atomicMax(smax + j + 2, __float_as_uint(mx.z));
-      if (mx.w > 0.f) atomicMax(smax + j + 3, __float_as_uint(mx.w));
-    }
-  } else {
-    for (int64_t k = t; k < total; k += nthreads) {
-      const float v = fabsf(__ldg(F + k));
-      if (v > 0.f) atomicMax(smax + int(k % d), __float_as_uint(v));
-    }
-  }
-  __syncthreads();
-  for (int j = threadIdx.x; j < d; j += blockDim.x)
-    if (smax[j]) atomicMax(maxbits + j, smax[j]);
-}
+constexpr int kBBytes = 16 * kChunk * 2;        // one fp16 B operand (hi or lo): 2 KB
+constexpr int kChunkB = 2 * kBBytes;            // hi + lo of one chunk
+constexpr int kEpochB = kEpoch * kChunkB;       // 32 KB per epoch buffer
+constexpr int kStageF = kEpoch * kChunk * 16 * 4;  // fp32 F block of one epoch: 32 KB
+constexpr int kSmem = 2 * kEpochB + kStageF;       // dynamic: B (2 epochs) + F staging
 
 __global__ void __launch_bounds__(kThreads, 1)
 pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omega4, int m,
                 int64_t n, int ranges, const float* __restrict__ F, int d, int c0, int dc,
-                const unsigned int* __restrict__ maxbits, float* __restrict__ partial) {
-  __shared__ __align__(1024) unsigned char bsm[kStages][2 * kBBytes];
-  __shared__ uint64_t full_bar[kStages], empty_bar[kStages], dfull_bar[2], dempty_bar[2];
+                float* __restrict__ partial) {
+  // [2 epochs][8 chunks][hi | lo] B operands, then the fp32 F staging block
+  extern __shared__ __align__(1024) unsigned char bsm[];
+  __shared__ uint64_t full_bar[kStages], empty_bar[kStages], dfull_bar[2], dempty_bar[2],
+      bready_bar[2];
   __shared__ uint32_t tmem_sh;
   // each producer warp's 16 points of a chunk as [x0..15 | y0..15 | z0..15],
   // 3 chunks deep (cp.async ring)
   __shared__ __align__(16) float xbuf[3][kProducerWarps][48];
-  __shared__ float fscale[16], fscale_inv[16];
+  __shared__ unsigned int fmax_part[2][4][16];  // per epoch buffer, F warp, channel (fp32 bits)
+  __shared__ float fscale_inv[2][16];        // per epoch buffer
 
   const int ft = blockIdx.x, rg = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, lg = warp & 3;
@@ -117,8 +72,8 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
   const int64_t ch0 = cpc * rg / ranges, ch1 = cpc * (rg + 1) / ranges;
   const int64_t p0 = ch0 * kChunk;
   const int nchunks = int(ch1 - ch0);
+  const int nepochs = (nchunks + kEpoch - 1) / kEpoch;
   const float* cloud16 = pts16 + int64_t(b) * gpc * 48;
-  const float* Fb = F + int64_t(b) * n * d;
 
   if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
   if (tid == 0) {
@@ -129,22 +84,9 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&dfull_bar[i], 1);
       tc::mbar_init(&dempty_bar[i], 4);
+      tc::mbar_init(&bready_bar[i], 4);
     }
     tc::mbar_fence_init();
-  }
-  if (tid >= 32 && tid < 48) {
-    // channel scale 2^e_j with max |F_j| 2^e_j in [2^13, 2^14) (1 for a zero
-    // or non-finite channel)
-    const int j = tid - 32;
-    const float mx = (j < dc) ? __uint_as_float(maxbits[c0 + j]) : 0.0f;
-    float scale = 1.0f;
-    if (mx > 0.0f && isfinite(mx)) {
-      int ex = 0;
-      frexpf(mx, &ex);  // mx in [2^(ex-1), 2^ex)
-      scale = ldexpf(1.0f, min(126, max(-126, 14 - ex)));  // 2^+-126: normal, exact inverse
-    }
-    fscale[j] = scale;
-    fscale_inv[j] = 1.0f / scale;  // exact: a power of two
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -155,38 +97,14 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
 
   if (warp < kProducerWarps) {
     // ---------------- producers: 16 points per warp per chunk --------------
-    const int q = warp >> 2;  // which 16 of the chunk's 64 points
+    const int q = warp >> 2;  // which 16 of the chunk's points
     const float4 w = (f < m) ? omega4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float2 wx = make_float2(w.x, w.x), wy = make_float2(w.y, w.y), wz = make_float2(w.z, w.z);
-    // B operand elements of this lane: channel je of points 2 pe, 2 pe + 1 of
-    // each chunk (one 32-bit word of the K-major core matrix); F is prefetched
-    // one chunk ahead (it streams from HBM).  Pointers and counters advance
-    // per chunk (no 64-bit index arithmetic in the loop).
-    const int e = warp * 32 + lane, je = e & 15, pe = e >> 4;
-    const uint32_t boff = uint32_t(je >> 3) * kSBO + uint32_t(pe >> 2) * kLBO +
-                          uint32_t(je & 7) * 16 + uint32_t(pe & 3) * 4;
-    const uint32_t b_s = tc::smem_addr(&bsm[0][0]) + boff;
-    const float sc = fscale[je];
-    const bool jok = je < dc;
-    const float* fptr = Fb + (p0 + 2 * pe) * d + c0 + je;
-    const int64_t fstep = int64_t(kChunk) * d;
-    const int64_t frem0 = n - (p0 + 2 * pe);
-    int frem = int(frem0 > 0x7fffffff ? 0x7fffffff : frem0);  // points left from the first
-    auto load_f = [&]() {
-      float2 v = make_float2(0.f, 0.f);
-      if (jok && frem > 0) {
-        v.x = __ldg(fptr);
-        if (frem > 1) v.y = __ldg(fptr + d);
-      }
-      fptr += fstep;
-      frem -= kChunk;
-      return v;
-    };
-    float2 f_next = load_f();
     // The warp's 16 points (one SoA group, 192 B), copied two chunks ahead by
     // lanes 0-11 straight into shared memory (cp.async: global latency off the
     // critical path).  Groups past the cloud's end repeat its last group
-    // (finite values that meet zero F).
+    // (finite values that meet zero F).  Pointers and counters advance per
+    // chunk (no 64-bit index arithmetic in the loop).
     const float* xsrc = cloud16 + ((ch0 * (kChunk / 16) + q) * 48 + 4 * lane);
     const float* xlast = cloud16 + ((gpc - 1) * 48 + 4 * lane);
     const int64_t xrem0 = gpc - (ch0 * (kChunk / 16) + q);
@@ -206,23 +124,15 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
     const uint32_t empty_s = tc::smem_addr(&empty_bar[0]), full_s = tc::smem_addr(&full_bar[0]);
     uint32_t s = 0, u = 0, xr = 0;  // stage, its round, ring slot read
     for (int c = 0; c < nchunks; ++c) {
-      const float2 fv = f_next;
-      f_next = load_f();
       load_x(c + 2 < nchunks);  // the slot chunk c - 1 read (ordered by its __syncwarp)
       if (u >= 1) tc::mbar_wait(empty_s + 8 * s, (u - 1) & 1);
-      {
-        uint32_t hi, lo;
-        tc::split_f16x2(fv.x * sc, fv.y * sc, hi, lo);
-        tc::st_shared_u32(b_s + s * (2 * kBBytes), hi);
-        tc::st_shared_u32(b_s + s * (2 * kBBytes) + kBBytes, lo);
-      }
       // Points beyond the cloud meet zero columns of F^T, and lanes beyond m
       // are never written out: no masking of the features.
       tc::cp_async_wait<2>();  // chunk c's group (c + 1, c + 2 may be in flight)
       __syncwarp();
       const float* xs = &xbuf[0][warp][0] + xr * (kProducerWarps * 48);
       xr = (xr == 2) ? 0 : xr + 1;
-      const uint32_t a = tmem + lane_field + kColA + 128 * s + 8 * q;
+      const uint32_t a = tmem + lane_field + kColA + 4 * kArr * s + 8 * q;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {  // two halves of 8 points (register pressure)
         float cs[8], sn[8];
@@ -252,12 +162,11 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
         }
         const uint32_t ah = a + 4 * h;
         tc::tmem_st4(ah, chi[0], chi[1], chi[2], chi[3]);
-        tc::tmem_st4(ah + 32, clo[0], clo[1], clo[2], clo[3]);
-        tc::tmem_st4(ah + 64, shi[0], shi[1], shi[2], shi[3]);
-        tc::tmem_st4(ah + 96, slo[0], slo[1], slo[2], slo[3]);
+        tc::tmem_st4(ah + kArr, clo[0], clo[1], clo[2], clo[3]);
+        tc::tmem_st4(ah + 2 * kArr, shi[0], shi[1], shi[2], shi[3]);
+        tc::tmem_st4(ah + 3 * kArr, slo[0], slo[1], slo[2], slo[3]);
       }
       tc::tmem_st_wait();
-      tc::fence_proxy_async_smem();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(full_s + 8 * s);
@@ -269,40 +178,116 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
   } else if (warp == kMmaWarp) {
     // ---------------- MMA issue: warp-uniform loop, one elected lane -------
     const uint32_t idesc = tc::make_idesc(0, 128, 16);
+    const uint32_t b_s = tc::smem_addr(bsm);
     for (int c = 0; c < nchunks; ++c) {
       const uint32_t s = c % kStages, u = c / kStages;
-      const int e = c / kEpoch;
+      const int e = c / kEpoch, ce = c % kEpoch;
       const uint32_t buf = e & 1;
-      if (c % kEpoch == 0 && e >= 2) tc::mbar_wait(&dempty_bar[buf], ((e - 2) >> 1) & 1);
+      if (ce == 0) {
+        if (e >= 2) tc::mbar_wait(&dempty_bar[buf], ((e - 2) >> 1) & 1);
+        tc::mbar_wait(&bready_bar[buf], (e >> 1) & 1);
+      }
       tc::mbar_wait(&full_bar[s], u & 1);
       tc::tc_fence_after();
       if (tc::elect_one()) {
-        const uint64_t bh = tc::make_sdesc(tc::smem_addr(&bsm[s][0]), kLBO, kSBO);
-        const uint64_t bl = tc::make_sdesc(tc::smem_addr(&bsm[s][kBBytes]), kLBO, kSBO);
-        const uint32_t a0 = tmem + kColA + 128 * s;
+        const uint32_t bc = b_s + buf * kEpochB + ce * kChunkB;
+        const uint64_t bh = tc::make_sdesc(bc, kLBO, kSBO);
+        const uint64_t bl = tc::make_sdesc(bc + kBBytes, kLBO, kSBO);
+        const uint32_t a0 = tmem + kColA + 4 * kArr * s;
         const uint32_t dcos = tmem + 32 * buf, dsin = dcos + 16;
 #pragma unroll
         for (int kk = 0; kk < kChunk / 16; ++kk) {
           const uint64_t adv = uint64_t(2 * kk) * (kLBO >> 4);
-          const uint32_t acc = (c % kEpoch > 0 || kk > 0) ? 1u : 0u;
+          const uint32_t acc = (ce > 0 || kk > 0) ? 1u : 0u;
           tc::mma_f16_ts(dcos, a0 + 8 * kk, bh + adv, idesc, acc);
           tc::mma_f16_ts(dcos, a0 + 8 * kk, bl + adv, idesc, 1u);
-          tc::mma_f16_ts(dcos, a0 + 32 + 8 * kk, bh + adv, idesc, 1u);
-          tc::mma_f16_ts(dsin, a0 + 64 + 8 * kk, bh + adv, idesc, acc);
-          tc::mma_f16_ts(dsin, a0 + 64 + 8 * kk, bl + adv, idesc, 1u);
-          tc::mma_f16_ts(dsin, a0 + 96 + 8 * kk, bh + adv, idesc, 1u);
+          tc::mma_f16_ts(dcos, a0 + kArr + 8 * kk, bh + adv, idesc, 1u);
+          tc::mma_f16_ts(dsin, a0 + 2 * kArr + 8 * kk, bh + adv, idesc, acc);
+          tc::mma_f16_ts(dsin, a0 + 2 * kArr + 8 * kk, bl + adv, idesc, 1u);
+          tc::mma_f16_ts(dsin, a0 + 3 * kArr + 8 * kk, bh + adv, idesc, 1u);
         }
         tc::mma_commit(&empty_bar[s]);
-        if (c % kEpoch == kEpoch - 1 || c == nchunks - 1) tc::mma_commit(&dfull_bar[buf]);
+        if (ce == kEpoch - 1 || c == nchunks - 1) tc::mma_commit(&dfull_bar[buf]);
       }
       __syncwarp();
     }
   } else {
-    // ---------------- drain warps: epochs -> fp32 registers -> partial ---
+    // ---------------- F staging + drains (4 warps, 128 threads) ----------
+    const int fw = warp - kFWarp0, t = fw * 32 + lane;
+    // Per epoch: the F block is copied into shared memory, then thread t
+    // converts channel je of the point pairs (2 pk, 2 pk + 1), pk = (t >> 4) +
+    // 8 i (one 32-bit word of the K-major B operand each).
+    const int je = t & 15, pk0 = t >> 4;
+    const float* Fb = F + int64_t(b) * n * d + c0;
+    const uint32_t b_s = tc::smem_addr(bsm);
+    const uint32_t fs_s = b_s + 2 * kEpochB;  // staging: [512 points][16 channels] fp32
+    const float* fstage = reinterpret_cast<const float*>(bsm + 2 * kEpochB);
+    const bool vec = (dc == 16) && (d % 4 == 0) && (c0 % 4 == 0);
+    // prepare the B operands of epoch e into buffer e & 1
+    auto stage_f = [&](int e) {
+      const int64_t q0 = p0 + int64_t(e) * (kEpoch * kChunk);  // first point of the epoch
+      const int ncs = min(kEpoch, nchunks - e * kEpoch);        // chunks of this epoch
+      const int npts = ncs * kChunk;
+      // the epoch's F block -> shared memory (cp.async, all in flight at once;
+      // rows past the cloud and channels past dc are zero-filled)
+      if (vec) {
+        for (int i = t; i < npts * 4; i += 128) {
+          const int p = i >> 2, cq = i & 3;
+          const bool ok = q0 + p < n;
+          tc::cp_async16_zf(fs_s + uint32_t(p * 64 + cq * 16),
+                            ok ? Fb + (q0 + p) * d + 4 * cq : Fb, ok ? 16u : 0u);
+        }
+      } else {
+        for (int i = t; i < npts * 16; i += 128) {
+          const int p = i >> 4, j = i & 15;
+          const bool ok = q0 + p < n && j < dc;
+          tc::cp_async4_zf(fs_s + uint32_t(i * 4), ok ? Fb + (q0 + p) * d + j : Fb, ok ? 4u : 0u);
+        }
+      }
+      tc::cp_async_commit();
+      tc::cp_async_wait<0>();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // per-channel max |F| over the epoch's points
+      float mx = 0.0f;
+      for (int p = pk0; p < npts; p += 8) mx = fmaxf(mx, fabsf(fstage[p * 16 + je]));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      if (lane < 16) fmax_part[e & 1][fw][lane] = __float_as_uint(mx);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const unsigned int(*fp)[16] = fmax_part[e & 1];
+      const float cm = fmaxf(fmaxf(__uint_as_float(fp[0][je]), __uint_as_float(fp[1][je])),
+                             fmaxf(__uint_as_float(fp[2][je]), __uint_as_float(fp[3][je])));
+      // scale 2^e_j with max |F_j| 2^e_j in [2^13, 2^14) (1 for a zero or
+      // non-finite channel; |e_j| <= 126 keeps both factors normal and exact)
+      float scale = 1.0f;
+      if (cm > 0.0f && isfinite(cm)) {
+        int ex = 0;
+        frexpf(cm, &ex);  // cm in [2^(ex-1), 2^ex)
+        scale = ldexpf(1.0f, min(126, max(-126, 14 - ex)));
+      }
+      if (t < 16) fscale_inv[e & 1][t] = 1.0f / scale;
+      // scaled, split, stored as 32-bit words (points 2 pk, 2 pk + 1)
+      const uint32_t eb = b_s + (e & 1) * kEpochB;
+      for (int pk = pk0; 2 * pk < npts; pk += 8) {
+        const int p = 2 * pk;
+        uint32_t hi, lo;
+        tc::split_f16x2(fstage[p * 16 + je] * scale, fstage[(p + 1) * 16 + je] * scale, hi, lo);
+        const int ce = p / kChunk, pc = p % kChunk;
+        const uint32_t off = uint32_t(ce) * kChunkB + uint32_t(je >> 3) * kSBO +
+                             uint32_t(pc >> 3) * kLBO + uint32_t(je & 7) * 16 + uint32_t(pc & 7) * 2;
+        tc::st_shared_u32(eb + off, hi);
+        tc::st_shared_u32(eb + off + kBBytes, lo);
+      }
+      // the staging block is rewritten by the next epoch's copies
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&bready_bar[e & 1]);
+    };
+    if (nepochs > 0) stage_f(0);
+    if (nepochs > 1) stage_f(1);
     float acc[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
-    const int nepochs = (nchunks + kEpoch - 1) / kEpoch;
     for (int e = 0; e < nepochs; ++e) {
       const uint32_t buf = e & 1;
       tc::mbar_wait(&dfull_bar[buf], (e >> 1) & 1);
@@ -313,7 +298,15 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&dempty_bar[buf]);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) acc[j] += v[j];
+      for (int j = 0; j < 16; ++j) {
+        const float inv = fscale_inv[buf][j];
+        acc[j] = fmaf(v[j], inv, acc[j]);  // v * 2^-e_j is exact: one rounding
+        acc[16 + j] = fmaf(v[16 + j], inv, acc[16 + j]);
+      }
+      // buffer e & 1 (B and scales) is free once epoch e's MMAs completed and
+      // all four warps have read its scales
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (e + 2 < nepochs) stage_f(e + 2);
     }
     if (f < m) {
       // partial[b][rg][2m][dc]: row 2f = cos, 2f + 1 = sin (interleaved order)
@@ -321,8 +314,8 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         if (j < dc) {
-          out[int64_t(2 * f) * dc + j] = acc[j] * fscale_inv[j];
-          out[int64_t(2 * f + 1) * dc + j] = acc[16 + j] * fscale_inv[j];
+          out[int64_t(2 * f) * dc + j] = acc[j];
+          out[int64_t(2 * f + 1) * dc + j] = acc[16 + j];
         }
       }
     }
@@ -344,25 +337,18 @@ int pass1_tc_ranges(int m, int64_t n, int batch, int sms) {
   return int(ranges);
 }
 
-void launch_colmax(const float* F, int64_t rows, int d, unsigned int* maxbits, cudaStream_t s) {
-  LaunchScope L("rfd_colmax", s);
-  cudaMemsetAsync(maxbits, 0, size_t(d) * sizeof(unsigned int), s);
-  const size_t smem = size_t(d) * sizeof(unsigned int);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(colmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  int64_t blocks = (rows * d / 4 + kColmaxThreads - 1) / kColmaxThreads;
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  if (blocks < 1) blocks = 1;
-  colmax_kernel<<<int(blocks), kColmaxThreads, smem, s>>>(F, rows, d, maxbits);
-}
-
 void launch_pass1_tc(const float* pts16, const float4* omega4, int m, int64_t n, int batch,
-                     int ranges, const float* F, int d, int c0, int dc,
-                     const unsigned int* maxbits, float* partial, cudaStream_t s) {
+                     int ranges, const float* F, int d, int c0, int dc, float* partial,
+                     cudaStream_t s) {
   LaunchScope L("rfd_pass1_tc", s);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(pass1_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    configured = true;
+  }
   const dim3 grid((m + 127) / 128, ranges, batch);
-  pass1_tc_kernel<<<grid, kThreads, 0, s>>>(pts16, omega4, m, n, ranges, F, d, c0, dc, maxbits,
-                                           partial);
+  pass1_tc_kernel<<<grid, kThreads, kSmem, s>>>(pts16, omega4, m, n, ranges, F, d, c0, dc,
+                                               partial);
 }
 
 }  // namespace rfd

@@ -109,22 +109,53 @@ __global__ void reduce_S_kernel(const float* __restrict__ partial, int r, int ch
   if (e >= r * dc) return;
   const int a = e / dc, j = e % dc;
   const float* src = partial + int64_t(b) * chunks * r * dc + e;
-  double sum = 0.0;
-  for (int ch = 0; ch < chunks; ++ch) sum += double(src[int64_t(ch) * r * dc]);
+  const int64_t st = int64_t(r) * dc;
+  // fixed order: 8 interleaved fp64 sums (8 loads in flight), then combined
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int ch = 0;
+  for (; ch + 8 <= chunks; ch += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (ch + u) * st);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] += double(v[u]);
+  }
+  for (int u = 0; ch < chunks; ++ch, ++u) acc[u] += double(__ldg(src + ch * st));
+  const double sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
   S[(int64_t(b) * r + a) * d + c0 + j] = sum;
 }
 
-__global__ void core_apply_kernel(const double* __restrict__ C, const double* __restrict__ S,
-                                  int r, int d, float* __restrict__ Y) {
+// Y = C^ S for 4 rows of C^ and 16 columns of S per CTA: 16 k-slices x 16
+// columns of threads, each summing k = slice (mod 16) for the 4 rows; the
+// slices are then added in a fixed order (deterministic).
+constexpr int kApplyRows = 4;
+__global__ void __launch_bounds__(256)
+core_apply_kernel(const double* __restrict__ C, const double* __restrict__ S, int r, int d,
+                  float* __restrict__ Y) {
+  __shared__ double red[16][kApplyRows][17];
   const int b = blockIdx.y;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= r * d) return;
-  const int a = e / d, c = e % d;
-  const double* Cr = C + (int64_t(b) * r + a) * r;
-  const double* Sb = S + int64_t(b) * r * d;
-  double acc = 0.0;
-  for (int k = 0; k < r; ++k) acc = fma(Cr[k], Sb[int64_t(k) * d + c], acc);
-  Y[(int64_t(b) * r + a) * d + c] = float(acc);
+  const int a0 = blockIdx.x * kApplyRows, c0 = blockIdx.z * 16;
+  const int slice = threadIdx.x >> 4, c = threadIdx.x & 15;
+  const bool cok = c0 + c < d;
+  const double* Cb = C + (int64_t(b) * r + a0) * r;
+  const double* Sb = S + int64_t(b) * r * d + c0 + c;
+  double acc[kApplyRows] = {0.0, 0.0, 0.0, 0.0};
+  for (int k = slice; k < r; k += 16) {
+    const double sv = cok ? __ldg(Sb + int64_t(k) * d) : 0.0;
+#pragma unroll
+    for (int i = 0; i < kApplyRows; ++i)
+      if (a0 + i < r) acc[i] = fma(__ldg(Cb + int64_t(i) * r + k), sv, acc[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < kApplyRows; ++i) red[slice][i][c] = acc[i];
+  __syncthreads();
+  if (threadIdx.x < kApplyRows * 16) {
+    const int i = threadIdx.x >> 4, cc = threadIdx.x & 15;
+    double sum = 0.0;
+#pragma unroll
+    for (int sl = 0; sl < 16; ++sl) sum += red[sl][i][cc];
+    if (a0 + i < r && c0 + cc < d) Y[(int64_t(b) * r + a0 + i) * d + c0 + cc] = float(sum);
+  }
 }
 
 template <int DC, int PPT>
@@ -306,7 +337,8 @@ void launch_core_apply(const double* C, const double* S, int m, int batch, int d
                        cudaStream_t s) {
   LaunchScope L("rfd_core_apply", s);
   const int r = 2 * m;
-  core_apply_kernel<<<dim3((r * d + 255) / 256, batch), 256, 0, s>>>(C, S, r, d, Y);
+  core_apply_kernel<<<dim3((r + kApplyRows - 1) / kApplyRows, batch, (d + 15) / 16), 256, 0, s>>>(
+      C, S, r, d, Y);
 }
 
 void launch_pass2(const float4* pts, const float4* omega4, int m, int64_t n, int batch,

@@ -118,7 +118,6 @@ struct rfd_plan {
   // integrate workspace (grows with d)
   int ws_d = 0;
   float* s_partial = nullptr; // batch*chunks*r*16
-  unsigned int* fmax = nullptr;  // ws_d: max |F| per column (fp32 bits), pass 1's scales
   double* S = nullptr;        // batch*r*d
   float* Y = nullptr;         // batch*r*d
   int last_d = 0;
@@ -239,7 +238,6 @@ void free_plan(rfd_plan* p) {
   dfree(p->C, s);
   dfree(p->flags, s);
   dfree(p->s_partial, s);
-  dfree(p->fmax, s);
   dfree(p->S, s);
   dfree(p->Y, s);
   dfree(p->stage, s);
@@ -373,14 +371,12 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
 rfd_status ensure_workspace(rfd_plan* p, int d, cudaStream_t st) {
   if (p->ws_d >= d) return RFD_OK;
   dfree(p->s_partial, st);
-  dfree(p->fmax, st);
   dfree(p->S, st);
   dfree(p->Y, st);
   p->ws_d = 0;
   const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
   const size_t part = size_t(p->batch) * (p->pg.chunks > ranges ? p->pg.chunks : ranges) * p->r * 16;
   RFD_CUDA(dalloc(&p->s_partial, part, st));
-  RFD_CUDA(dalloc(&p->fmax, size_t(d), st));
   RFD_CUDA(dalloc(&p->S, size_t(p->batch) * p->r * d, st));
   RFD_CUDA(dalloc(&p->Y, size_t(p->batch) * p->r * d, st));
   p->ws_d = d;
@@ -403,7 +399,6 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
     return e && strcmp(e, "simt") == 0;
   }();
   const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
-  if (!p1_simt) rfd::launch_colmax(F, p->n * p->batch, d, p->fmax, st);
   for (int c0 = 0; c0 < d; c0 += 16) {
     const int dc = (d - c0 < 16) ? d - c0 : 16;
     if (p1_simt) {
@@ -412,7 +407,7 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
       rfd::launch_reduce_S(p->s_partial, p->m, p->batch, p->pg.chunks, d, c0, dc, p->S, st);
     } else {
       rfd::launch_pass1_tc(p->pts16, p->omega_rad4, p->m, p->n, p->batch, ranges, F, d, c0, dc,
-                           p->fmax, p->s_partial, st);
+                           p->s_partial, st);
       rfd::launch_reduce_S(p->s_partial, p->m, p->batch, ranges, d, c0, dc, p->S, st);
     }
   }
