@@ -35,19 +35,25 @@ def main():
     rep = sys.argv[1]
     nsrc = int(sys.argv[sys.argv.index("--source") + 1]) if "--source" in sys.argv else 0
     r = ncu_csv(rep, "raw")
-    h, units, vals = r[0], r[1], r[2]
-    d = dict(zip(h, vals))
-    u = dict(zip(h, units))
-    print("kernel:", d.get("Kernel Name", "?")[:100])
-    for k in KEYS:
-        if k in d:
-            print("  %-75s %s %s" % (k, d[k], u.get(k, "")))
-    st = [(float(v), n) for n, v in d.items()
-          if "average_warps_issue_stalled" in n and "per_issue_active" in n and v]
-    print("  top stalls (warps per issue):")
-    for v, n in sorted(st, reverse=True)[:8]:
-        print("    %.3f %s" % (v, n.replace("smsp__average_warps_issue_stalled_", "").replace(
-            "_per_issue_active.ratio", "")))
+    h, units = r[0], r[1]
+    seen = set()
+    for vals in r[2:]:  # one block per distinct kernel (first launch of each)
+        d = dict(zip(h, vals))
+        u = dict(zip(h, units))
+        name = d.get("Kernel Name", "?")[:100]
+        if name in seen:
+            continue
+        seen.add(name)
+        print("kernel:", name)
+        for k in KEYS:
+            if k in d:
+                print("  %-75s %s %s" % (k, d[k], u.get(k, "")))
+        st = [(float(v), n) for n, v in d.items()
+              if "average_warps_issue_stalled" in n and "per_issue_active" in n and v]
+        print("  top stalls (warps per issue):")
+        for v, n in sorted(st, reverse=True)[:8]:
+            print("    %.3f %s" % (v, n.replace("smsp__average_warps_issue_stalled_", "").replace(
+                "_per_issue_active.ratio", "")))
     if nsrc:
         rows = ncu_csv(rep, "source", ["--print-source", "sass"])
         hdr = rows[1]

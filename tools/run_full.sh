@@ -13,4 +13,5 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 C="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 600 $C > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $C > gpurun_out/ncu_launches.log 2>&1; echo launches rc $?
 C2="python tools/profile_step.py"
-timeout 300 $C2 > gpurun_out/plain2.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"gram_pair_kernel|pass1_tc|pass2_tc|dgemm" -c 4 -o gpurun_out/full $C2 > gpurun_out/ncu_full.log 2>&1; echo full rc $?
+timeout 300 $C2 > gpurun_out/plain2.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"gram_pair_kernel|pass1_tc|pass2_tc" -c 3 -o gpurun_out/full $C2 > gpurun_out/ncu_full.log 2>&1; echo full rc $?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"dgemm" -c 1 -o gpurun_out/full2 $C2 > gpurun_out/ncu_full2.log 2>&1; echo full2 rc $?
