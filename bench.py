@@ -284,6 +284,23 @@ def run_rfd(args, rank, world, local, pg):
         plan.integrate(Fd, out=outd)
     iprof = rfd.profile_read()
     rfd.profile_enable(False)
+
+    # ---- re-parameterisation: nu + core on the stored G.
+    # The call reads back the scaling exponent and an overflow flag, so its
+    # time includes two device->host round trips.
+    rts = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        plan.reparam(p["eps"] * (1.0 + 0.25 * (i % 2)), p["lam"])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            rts.append(ev0.elapsed_time(ev1))
+    reparam = {"ms_per_call": float(np.median(rts)),
+               "plan_create_ms": ms_step - ims,
+               "note": "rfd_plan_reparam(eps, lambda) at cfg5: nu + core on the stored Gram "
+                       "(median of %d); plan_create_ms = step - integrate" % len(rts)}
     plan.close()
 
     # ---- end to end through the public API with host buffers
@@ -349,7 +366,8 @@ def run_rfd(args, rank, world, local, pg):
              "strict_roofline_bound": "MUFU (4m sin/cos per pt at 148x16/clk) vs tf32 tensor vs HBM",
              "hbm_gbs_achieved": byts_i / (ims * 1e-3) / 1e9, "kernels": ikern}
     return dict(N=N, m=m, d=d, ms_step=ms_step, launches=launches, roofline=roof,
-                kernels=kernels, integrate=integ, e2e=e2e, clocks=sampler.summary(), params=p)
+                kernels=kernels, integrate=integ, e2e=e2e, clocks=sampler.summary(), params=p,
+                reparam=reparam)
 
 
 def oracle_sample(n_sample, steps=1):
@@ -431,7 +449,7 @@ def main():
             "dtype": "f32", "data": "synthetic", "config": dict(cfg_desc, parallelism="dp%d (independent clouds)" % world),
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
             "gpu_launches": res["launches"], "clocks": res["clocks"],
-            "integrate": res["integrate"], "kernels": res["kernels"]}
+            "integrate": res["integrate"], "reparam": res["reparam"], "kernels": res["kernels"]}
     print(json.dumps(line))
 
 

@@ -91,6 +91,26 @@ rfd_status rfd_plan_create_batched(const float* points, int32_t batch,
                                    rfd_plan** plan_out);
 
 /*
+ * rfd_plan_reparam -- re-parameterise a plan to a new (eps, lambda) without
+ * recomputing the Gram matrix: G = Phi^T Phi
+ * depends only on the points and omega, so only nu
+ * (a2, eps enters through tau: PAPER.md:361-366) and the core C^ (a5,
+ * PAPER.md:333-339) are recomputed -- O(m + r^3) instead of O(N r^2).  The
+ * paper grid-searches lambda and eps per mesh.
+ *   plan    a plan from rfd_plan_create[_batched]; keeps omega, G, points.
+ *   eps     new epsilon (> 0, finite); lambda  new multiplier (finite).
+ * The result equals, bit for bit, a fresh rfd_plan_create with the same
+ * points, m, seed and the new (eps, lambda).  The new nu and C^ are written
+ * into the plan's existing buffers (CUDA graphs capturing rfd_integrate stay
+ * valid).  Must be ordered after earlier rfd_integrate calls on the plan
+ * (same stream).  Blocks the host (scaling exponent / overflow read-back).
+ * Errors: EINVAL (NULL plan, bad eps or lambda), ERANGE (core overflow),
+ * ENOMEM, ECUDA -- the plan is unchanged on any error.
+ */
+rfd_status rfd_plan_reparam(rfd_plan* plan, double eps, double lambda,
+                            rfd_stream stream);
+
+/*
  * rfd_integrate -- inference, Eq. 13 in bracket order:
  *   S = Phi^T F (a6), Y = C^ S (a7), out = F + Phi Y (a8).
  *   F    DEVICE, (batch x) N x d fp32.   out  DEVICE, same shape; may alias F.

@@ -285,6 +285,15 @@ class Plan:
         self.G = gram(self.X, self.omega)
         self.C = core(self.G, self.nu, lam)
 
+    def reparam(self, eps, lam):
+        """New (eps, lambda) on the stored G: G =
+        B^T A depends on the points and omega only, eps enters
+        through tau in nu, lambda through the core."""
+        self.eps, self.lam = eps, lam
+        self.nu = importance_weights(self.omega, eps, self.c_r)
+        self.C = core(self.G, self.nu, lam)
+        return self
+
     def apply(self, F, rows=None):
         """Inference (Eq. 13, bracket order).
 

@@ -28,13 +28,31 @@ __device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
   return c;
 }
 
+// a2: nu_k = tau(omega_k) / (m p(omega_k)) with tau the product of the 1-D
+// sinc factors sin(2 pi eps w) / (pi w) (2 eps at w = 0; reading A1) and p the
+// truncated standard normal pdf (2 pi)^{-3/2} e^{-|w|^2/2} / C_R (A6, A7).
+__device__ __forceinline__ double nu_of(float wx, float wy, float wz, double eps, int m,
+                                        double c_r) {
+  const double two_pi = 6.283185307179586;
+  const double pi = 3.141592653589793;
+  const double wc[3] = {double(wx), double(wy), double(wz)};
+  double tau = 1.0, sq = 0.0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double w = wc[c];
+    tau *= (w != 0.0) ? sin(two_pi * eps * w) / (pi * w) : 2.0 * eps;
+    sq += w * w;
+  }
+  const double p = exp(-0.5 * sq) / (15.749609945722419 * c_r);  // (2 pi)^{3/2}
+  return tau / (double(m) * p);
+}
+
 __global__ void freq_kernel(float4* __restrict__ omega4, float4* __restrict__ omega_rad4,
                             double* __restrict__ nu,
                             int* __restrict__ flags, int m, uint64_t seed,
                             double eps, double R, double c_r) {
   const uint2 key = make_uint2(uint32_t(seed & 0xffffffffu), uint32_t(seed >> 32));
   const double two_pi = 6.283185307179586;  // fl64(2 pi), as 2.0 * math.pi
-  const double pi = 3.141592653589793;
   for (int k = threadIdx.x; k < m; k += blockDim.x) {
     double z0 = 0.0, z1 = 0.0, z2 = 0.0;
     bool ok = false;
@@ -58,17 +76,19 @@ __global__ void freq_kernel(float4* __restrict__ omega4, float4* __restrict__ om
     // sincos(2 pi omega . x) as MUFU sin/cos of (2 pi omega) . x in radians.
     omega_rad4[k] = make_float4(float(two_pi * double(wx)), float(two_pi * double(wy)),
                                 float(two_pi * double(wz)), 0.0f);
-    // tau: product of 1-D sinc factors; factor 2 eps at w = 0.
-    const double wc[3] = {double(wx), double(wy), double(wz)};
-    double tau = 1.0, sq = 0.0;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double w = wc[c];
-      tau *= (w != 0.0) ? sin(two_pi * eps * w) / (pi * w) : 2.0 * eps;
-      sq += w * w;
-    }
-    const double p = exp(-0.5 * sq) / (15.749609945722419 * c_r);  // (2 pi)^{3/2}
-    const double v = tau / (double(m) * p);
+    const double v = nu_of(wx, wy, wz, eps, m, c_r);
+    nu[k] = v;
+    if (!(v > 0.0)) atomicOr(flags, 1);
+  }
+}
+
+// a2 alone, from the stored fp32 omega (re-parameterisation: nu depends on eps
+// only; bit-identical to freq_kernel's nu for the same omega and eps).
+__global__ void nu_kernel(const float4* __restrict__ omega4, double* __restrict__ nu,
+                          int* __restrict__ flags, int m, double eps, double c_r) {
+  for (int k = threadIdx.x; k < m; k += blockDim.x) {
+    const float4 w = omega4[k];
+    const double v = nu_of(w.x, w.y, w.z, eps, m, c_r);
     nu[k] = v;
     if (!(v > 0.0)) atomicOr(flags, 1);
   }
@@ -99,6 +119,12 @@ void launch_freq(float4* omega4, float4* omega_rad4, double* nu, int* flags, int
                  uint64_t seed, double eps, double R, double c_r, cudaStream_t s) {
   LaunchScope L("rfd_freq", s);
   freq_kernel<<<1, 256, 0, s>>>(omega4, omega_rad4, nu, flags, m, seed, eps, R, c_r);
+}
+
+void launch_nu(const float4* omega4, double* nu, int* flags, int m, double eps, double c_r,
+               cudaStream_t s) {
+  LaunchScope L("rfd_nu", s);
+  nu_kernel<<<1, 256, 0, s>>>(omega4, nu, flags, m, eps, c_r);
 }
 
 void launch_pack_points(const float* xyz, float4* pts, float* pts16, int64_t n, int batch,

@@ -259,6 +259,43 @@ struct TempBuffers {
   }
 };
 
+// a5 on the plan's G: C = lambda D phi1(lambda G D) for the given nu (its
+// sign flags in flags[0]); the scaling exponent is read back first.  Blocks
+// the host.  flags[2..4] are scratch.
+rfd_status core_impl(rfd_plan* p, const double* nu, int* flags, double lambda, double* C,
+                     int* scaling_out, int* symmetric_out, cudaStream_t st) {
+  const int m = p->m, batch = p->batch;
+  const size_t rr = size_t(p->r) * p->r;
+  TempBuffers tmp(st);
+  double *Z = nullptr, *work = nullptr;
+  RFD_CUDA(tmp.alloc(&Z, rr * batch));
+  RFD_CUDA(tmp.alloc(&work, rr * batch * rfd::kCoreWork));
+  rfd::launch_core_prep(p->G, nu, flags, lambda, m, batch, Z,
+                        reinterpret_cast<unsigned long long*>(flags + 2), st);
+  RFD_CUDA(cudaGetLastError());
+  int hflags[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  RFD_CUDA(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
+  RFD_CUDA(cudaStreamSynchronize(st));
+  if (hflags[0] & 2)
+    return fail(RFD_ERANGE, "frequency sampler exhausted its attempts (R too small?)");
+  double znorm;
+  memcpy(&znorm, hflags + 2, sizeof(double));
+  // Scaling exponent: smallest s >= 0 with ||Z||_1 / 2^s <= kCoreTheta.
+  if (!isfinite(znorm) || znorm > 1e60)
+    return fail(RFD_ERANGE, "core: ||lambda G D|| is not finite or too large");
+  int s_scale = 0;
+  while (ldexp(znorm, -s_scale) > rfd::kCoreTheta) ++s_scale;
+  rfd::launch_core_eval(Z, nu, flags, lambda, m, batch, s_scale, work, C, flags + 4, st);
+  RFD_CUDA(cudaGetLastError());
+  RFD_CUDA(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
+  RFD_CUDA(cudaStreamSynchronize(st));
+  if (hflags[4])
+    return fail(RFD_ERANGE, "core: exp(lambda W~) overflows (lambda > 0 or negative nu)");
+  *scaling_out = s_scale;
+  *symmetric_out = (hflags[0] & 1) ? 0 : 1;
+  return RFD_OK;
+}
+
 rfd_status create_impl(const float* points, int batch, int64_t n, double eps, double lambda,
                        int m, uint64_t seed, cudaStream_t st, rfd_plan** plan_out) {
   if (!plan_out) return fail(RFD_EINVAL, "plan_out is NULL");
@@ -333,38 +370,59 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
     rfd::launch_gram_tc(p->pts, p->omega_rad4, m, n, batch, gg, gpart, p->G, st);
   }
 
-  // a5: core, scaling exponent first.
-  double *Z = nullptr, *work = nullptr;
-  RFD_CUDA(tmp.alloc(&Z, rr * batch));
-  RFD_CUDA(tmp.alloc(&work, rr * batch * rfd::kCoreWork));
-  rfd::launch_core_prep(p->G, p->nu, p->flags, lambda, m, batch, Z,
-                        reinterpret_cast<unsigned long long*>(p->flags + 2), st);
-  RFD_CUDA(cudaGetLastError());
-  int hflags[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  RFD_CUDA(cudaMemcpyAsync(hflags, p->flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
-  RFD_CUDA(cudaStreamSynchronize(st));
-  if (hflags[0] & 2)
-    return fail(RFD_ERANGE, "frequency sampler exhausted its attempts (R too small?)");
-  double znorm;
-  memcpy(&znorm, hflags + 2, sizeof(double));
-  // Scaling exponent: smallest s >= 0 with ||Z||_1 / 2^s <= kCoreTheta.
-  if (!isfinite(znorm) || znorm > 1e60)
-    return fail(RFD_ERANGE, "core: ||lambda G D|| is not finite or too large");
-  int s_scale = 0;
-  while (ldexp(znorm, -s_scale) > rfd::kCoreTheta) ++s_scale;
-  p->symmetric = (hflags[0] & 1) ? 0 : 1;
-  p->scaling = s_scale;
-  rfd::launch_core_eval(Z, p->nu, p->flags, lambda, m, batch, p->scaling, work, p->C,
-                        p->flags + 4, st);
-  RFD_CUDA(cudaGetLastError());
-  RFD_CUDA(cudaMemcpyAsync(hflags, p->flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
-  RFD_CUDA(cudaStreamSynchronize(st));
-  if (hflags[4])
-    return fail(RFD_ERANGE, "core: exp(lambda W~) overflows (lambda > 0 or negative nu)");
+  // a5: core
+  {
+    int sc = 0, sym = 1;
+    const rfd_status cs = core_impl(p, p->nu, p->flags, lambda, p->C, &sc, &sym, st);
+    if (cs != RFD_OK) return cs;
+    p->scaling = sc;
+    p->symmetric = sym;
+  }
 
   p->pg = rfd::pass_geometry(m, n, batch, p->sms);
   guard.keep = true;
   *plan_out = p;
+  return RFD_OK;
+}
+
+// NEXT-4: new (eps, lambda) on the stored G (independent of both,
+// PAPER.md:337): a2 and a5 only.  Computed into fresh buffers and swapped in
+// on success, so the plan is untouched on error.  The results are copied into
+// the plan's existing buffers (device addresses unchanged: CUDA graphs that
+// captured rfd_integrate on this plan stay valid and see the new core).
+rfd_status reparam_impl(rfd_plan* p, double eps, double lambda, cudaStream_t st) {
+  if (!p) return fail(RFD_EINVAL, "plan is NULL");
+  if (!(eps > 0.0) || !isfinite(eps)) return fail(RFD_EINVAL, "eps must be finite and > 0");
+  if (!isfinite(lambda)) return fail(RFD_EINVAL, "lambda must be finite");
+  p->stream = st;
+  const size_t rr = size_t(p->r) * p->r;
+  double *nu = nullptr, *C = nullptr;
+  int* flags = nullptr;
+  struct Owned {
+    double **nu, **C;
+    int** flags;
+    cudaStream_t s;
+    ~Owned() {
+      dfree(*nu, s);
+      dfree(*C, s);
+      dfree(*flags, s);
+    }
+  } owned{&nu, &C, &flags, st};
+  RFD_CUDA(dalloc(&nu, size_t(p->m), st));
+  RFD_CUDA(dalloc(&C, rr * p->batch, st));
+  RFD_CUDA(dalloc(&flags, size_t(8), st));
+  RFD_CUDA(cudaMemsetAsync(flags, 0, 8 * sizeof(int), st));
+  rfd::launch_nu(p->omega4, nu, flags, p->m, eps, cached_c_r(), st);
+  int sc = 0, sym = 1;
+  const rfd_status cs = core_impl(p, nu, flags, lambda, C, &sc, &sym, st);
+  if (cs != RFD_OK) return cs;
+  RFD_CUDA(cudaMemcpyAsync(p->nu, nu, size_t(p->m) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  RFD_CUDA(cudaMemcpyAsync(p->C, C, rr * p->batch * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  RFD_CUDA(cudaMemcpyAsync(p->flags, flags, 8 * sizeof(int), cudaMemcpyDeviceToDevice, st));
+  p->eps = eps;
+  p->lambda = lambda;
+  p->scaling = sc;
+  p->symmetric = sym;
   return RFD_OK;
 }
 
@@ -451,6 +509,10 @@ rfd_status rfd_plan_create_batched(const float* points, int32_t batch, int64_t n
                                    rfd_plan** plan_out) {
   return create_impl(points, batch, n, eps, lambda, m, seed,
                      reinterpret_cast<cudaStream_t>(stream), plan_out);
+}
+
+rfd_status rfd_plan_reparam(rfd_plan* plan, double eps, double lambda, rfd_stream stream) {
+  return reparam_impl(plan, eps, lambda, reinterpret_cast<cudaStream_t>(stream));
 }
 
 rfd_status rfd_integrate(rfd_plan* plan, const float* F, int32_t d, float* out,

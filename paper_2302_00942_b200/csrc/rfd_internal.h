@@ -33,6 +33,11 @@ struct LaunchScope {
 void launch_freq(float4* omega4, float4* omega_rad4, double* nu, int* flags, int m,
                  uint64_t seed, double eps, double R, double c_r, cudaStream_t s);
 
+// a2 alone from the stored omega (re-parameterisation); flags[0] |= 1 if some
+// nu <= 0.
+void launch_nu(const float4* omega4, double* nu, int* flags, int m, double eps, double c_r,
+               cudaStream_t s);
+
 // ---------------------------------------------------------------- pack
 void launch_pack_points(const float* xyz, float4* pts, float* pts16, int64_t n, int batch,
                         cudaStream_t s);

@@ -165,6 +165,47 @@ def test_field_column_scales_parity():
         assert e_out <= TOL and e_del <= TOL, (c, e_out, e_del)
 
 
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_reparam_bitwise_equals_fresh_plan_and_oracle(cfg):
+    # NEXT-4: rfd_plan_reparam keeps G and recomputes nu and C^; the result is
+    # bit-identical to a fresh plan (same kernels, same inputs) and meets the
+    # oracle at the new parameters.
+    p, x, F = make_config(cfg)
+    xd, Fd = torch.from_numpy(x).cuda(), torch.from_numpy(F).cuda()
+    eps2, lam2 = p["eps"] * 1.5, p["lam"] * 0.5
+    plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
+    G0 = plan.export("gram")
+    plan.reparam(eps2, lam2)
+    fresh = rfd.Plan(xd, eps2, lam2, p["m"], p["seed"])
+    np.testing.assert_array_equal(plan.export("gram"), G0)
+    np.testing.assert_array_equal(plan.export("gram"), fresh.export("gram"))
+    np.testing.assert_array_equal(plan.export("nu"), fresh.export("nu"))
+    np.testing.assert_array_equal(plan.export("core"), fresh.export("core"))
+    assert plan.info()["eps"] == eps2 and plan.info()["lambda"] == lam2
+    assert plan.info()["scaling"] == fresh.info()["scaling"]
+    out = plan.integrate(Fd).cpu().numpy()
+    np.testing.assert_array_equal(out, fresh.integrate(Fd).cpu().numpy())
+    q = dict(p, eps=eps2, lam=lam2, name="reparam cfg%d" % cfg)
+    _check_against_oracle(plan, out, x, F, q)
+
+
+def test_reparam_errors_leave_plan_unchanged():
+    p, x, F = make_config(1)
+    xd, Fd = torch.from_numpy(x).cuda(), torch.from_numpy(F).cuda()
+    plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
+    before = plan.integrate(Fd).cpu().numpy()
+    C0 = plan.export("core")
+    for eps, lam in [(0.0, -0.5), (-1.0, -0.5), (float("nan"), -0.5), (0.1, float("inf"))]:
+        with pytest.raises(rfd.RFDError):
+            plan.reparam(eps, lam)
+    # overflow (large lambda > 0): ERANGE, plan unchanged
+    with pytest.raises(rfd.RFDError):
+        plan.reparam(p["eps"], 1e6)
+    np.testing.assert_array_equal(plan.export("core"), C0)
+    assert plan.info()["lambda"] == p["lam"]
+    np.testing.assert_array_equal(plan.integrate(Fd).cpu().numpy(), before)
+
+
 @pytest.mark.parametrize("n,m,seed,lam", [(1000, 40, 11, -0.8), (3001, 96, 14, -0.3),
                                           (2000, 128, 13, 0.05)])
 def test_negative_nu_nonsymmetric_route(n, m, seed, lam):

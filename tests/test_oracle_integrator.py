@@ -108,6 +108,24 @@ def test_semigroup_symmetry_linearity_permutation():
     np.testing.assert_allclose(pplan.apply(F[perm])["out"], a[perm], atol=1e-11)
 
 
+def test_reparam_keeps_gram_and_matches_dense():
+    # NEXT-4: G depends on the points and omega only; after a
+    # re-parameterisation the integrator must equal the dense exponential of
+    # the NEW low-rank W~ (an independent route) and a fresh plan.
+    X, rng = _cloud(400, seed=12)
+    F = rng.standard_normal((400, 2))
+    plan = rfd.Plan(X, 0.3, -0.7, 16, seed=6, c_r=C_R)
+    G0 = plan.G.copy()
+    plan.reparam(0.18, -1.3)
+    np.testing.assert_array_equal(plan.G, G0)
+    fresh = rfd.Plan(X, 0.18, -1.3, 16, seed=6, c_r=C_R)
+    np.testing.assert_array_equal(plan.nu, fresh.nu)
+    np.testing.assert_array_equal(plan.C, fresh.C)
+    out = plan.apply(F)["out"]
+    ref = dense.symmetric_expm_apply(_lowrank_dense(plan), -1.3, F)
+    assert np.abs(out - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
 def test_rows_subset_matches_full():
     X, rng = _cloud(500, seed=9)
     F = rng.standard_normal((500, 4))
