@@ -181,7 +181,7 @@ def test_reparam_bitwise_equals_fresh_plan_and_oracle(cfg):
     np.testing.assert_array_equal(plan.export("gram"), fresh.export("gram"))
     np.testing.assert_array_equal(plan.export("nu"), fresh.export("nu"))
     np.testing.assert_array_equal(plan.export("core"), fresh.export("core"))
-    assert plan.info()["eps"] == eps2 and plan.info()["lambda"] == lam2
+    assert plan.info()["eps"] == eps2 and plan.info()["lam"] == lam2
     assert plan.info()["scaling"] == fresh.info()["scaling"]
     out = plan.integrate(Fd).cpu().numpy()
     np.testing.assert_array_equal(out, fresh.integrate(Fd).cpu().numpy())
@@ -202,7 +202,7 @@ def test_reparam_errors_leave_plan_unchanged():
     with pytest.raises(rfd.RFDError):
         plan.reparam(p["eps"], 1e6)
     np.testing.assert_array_equal(plan.export("core"), C0)
-    assert plan.info()["lambda"] == p["lam"]
+    assert plan.info()["lam"] == p["lam"]
     np.testing.assert_array_equal(plan.integrate(Fd).cpu().numpy(), before)
 
 
