@@ -270,6 +270,35 @@ def core(G, nu, lam):
 
 
 # --------------------------------------------------------------------------
+# NEXT-3  spectrum
+# --------------------------------------------------------------------------
+def spectrum(G, nu, lam, n, k):
+    """The k smallest eigenvalues of K = exp(lam W~), W~ = Phi D Phi^T (N x N).
+
+    PAPER.md:609 (classification "using the eigenvectors of the kernel
+    matrix ... the k smallest eigenvalues"; low-rank route "as described in
+    [nakatsukasa2019lowrank]"): the nonzero eigenvalues of
+    A B^T = Phi D Phi^T are those of the 2m x 2m matrix B^T A = G D; each maps
+    through exp(lam .), and the N - 2m null directions give eigenvalue 1.
+    Reading (A19): for N < 2m, G D has 2m - N exact zero eigenvalues
+    beyond W~'s N; the 2m - N of smallest modulus are dropped.
+    """
+    G = np.asarray(G, np.float64)
+    r = G.shape[0]
+    d = np.concatenate([nu, nu]).astype(np.float64)
+    mu = np.linalg.eigvals(G * d[None, :])
+    scale = max(1.0, float(np.abs(mu).max()))
+    if np.abs(mu.imag).max() > 1e-8 * scale:  # SPEC.md:422
+        raise ValueError("G D has non-real eigenvalues")
+    mu = mu.real
+    if n < r:
+        mu = mu[np.argsort(np.abs(mu))[r - n:]]
+    vals = np.exp(lam * mu)
+    ones = np.ones(min(max(n - r, 0), k))
+    return np.sort(np.concatenate([vals, ones]))[:k]
+
+
+# --------------------------------------------------------------------------
 # plan + apply
 # --------------------------------------------------------------------------
 class Plan:
@@ -293,6 +322,10 @@ class Plan:
         self.nu = importance_weights(self.omega, eps, self.c_r)
         self.C = core(self.G, self.nu, lam)
         return self
+
+    def spectrum(self, k):
+        """k smallest eigenvalues of exp(lam W~) (NEXT-3; see ``spectrum``)."""
+        return spectrum(self.G, self.nu, self.lam, self.X.shape[0], k)
 
     def apply(self, F, rows=None):
         """Inference (Eq. 13, bracket order).

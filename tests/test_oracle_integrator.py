@@ -126,6 +126,32 @@ def test_reparam_keeps_gram_and_matches_dense():
     assert np.abs(out - ref).max() <= 1e-10 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("n,m,lam", [(150, 6, -0.8), (300, 16, -0.3), (10, 8, -0.6),
+                                     (40, 24, 0.3)])
+def test_spectrum_against_dense_eigendecomposition(n, m, lam):
+    # NEXT-3: the low-rank route equals the k smallest
+    # eigenvalues of the dense N x N exp(lam W~) (brute force), including
+    # N < 2m (reading A19) and lambda > 0.
+    X, rng = _cloud(n, seed=n + m)
+    plan = rfd.Plan(X, 0.3, lam, m, seed=9, c_r=C_R)
+    W = _lowrank_dense(plan)
+    ref = np.sort(np.exp(lam * np.linalg.eigvalsh(W)))
+    for k in (1, min(n, 5), n):
+        np.testing.assert_allclose(plan.spectrum(k), ref[:k], rtol=0, atol=1e-9 * ref.max())
+
+
+def test_spectrum_special_cases():
+    # lambda = 0: K = I; rank-1 A = B = e1, lambda > 0, k = 2,
+    # N >= 3 gives [1, 1] -- here through G = e1 e1^T, nu = 1.
+    X, _ = _cloud(50, seed=1)
+    plan = rfd.Plan(X, 0.3, 0.0, 8, seed=2, c_r=C_R)
+    np.testing.assert_array_equal(plan.spectrum(7), np.ones(7))
+    G = np.zeros((2, 2))
+    G[0, 0] = 1.0
+    np.testing.assert_array_equal(rfd.spectrum(G, np.array([1.0]), 0.7, 3, 2), [1.0, 1.0])
+    np.testing.assert_allclose(rfd.spectrum(G, np.array([1.0]), 0.7, 3, 3)[-1], math.exp(0.7))
+
+
 def test_rows_subset_matches_full():
     X, rng = _cloud(500, seed=9)
     F = rng.standard_normal((500, 4))
