@@ -297,6 +297,19 @@ def run_rfd(args, rank, world, local, pg):
         torch.cuda.synchronize()
         if i >= args.warmup:
             rts.append(ev0.elapsed_time(ev1))
+    # ---- spectrum: k = 32 smallest eigenvalues of exp(lambda W~)
+    sts = []
+    for i in range(2 + 3):
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        plan.spectrum(32)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if i >= 2:
+            sts.append(ev0.elapsed_time(ev1))
+    spectrum = {"ms_per_call": float(np.median(sts)), "k": 32,
+                "note": "rfd_plan_spectrum at cfg5 (r = 512): Householder tridiagonalisation "
+                        "of D^1/2 G D^1/2 in fp64 + bisection, median of 3"}
     reparam = {"ms_per_call": float(np.median(rts)),
                "plan_create_ms": ms_step - ims,
                "note": "rfd_plan_reparam(eps, lambda) at cfg5: nu + core on the stored Gram "
@@ -367,7 +380,7 @@ def run_rfd(args, rank, world, local, pg):
              "hbm_gbs_achieved": byts_i / (ims * 1e-3) / 1e9, "kernels": ikern}
     return dict(N=N, m=m, d=d, ms_step=ms_step, launches=launches, roofline=roof,
                 kernels=kernels, integrate=integ, e2e=e2e, clocks=sampler.summary(), params=p,
-                reparam=reparam)
+                reparam=reparam, spectrum=spectrum)
 
 
 def oracle_sample(n_sample, steps=1):
@@ -449,7 +462,7 @@ def main():
             "dtype": "f32", "data": "synthetic", "config": dict(cfg_desc, parallelism="dp%d (independent clouds)" % world),
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
             "gpu_launches": res["launches"], "clocks": res["clocks"],
-            "integrate": res["integrate"], "reparam": res["reparam"], "kernels": res["kernels"]}
+            "integrate": res["integrate"], "reparam": res["reparam"], "spectrum": res["spectrum"], "kernels": res["kernels"]}
     print(json.dumps(line))
 
 

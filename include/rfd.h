@@ -111,6 +111,23 @@ rfd_status rfd_plan_reparam(rfd_plan* plan, double eps, double lambda,
                             rfd_stream stream);
 
 /*
+ * rfd_plan_spectrum -- the k smallest eigenvalues of the kernel matrix
+ * K = exp(lambda W~), W~ = Phi D Phi^T (N x N, never formed), per cloud
+ * (classification features
+ * "the k smallest eigenvalues of the kernel matrix" via the low-rank
+ * decomposition).  The nonzero eigenvalues of Phi D Phi^T
+ * are those of G D (r x r); each maps through exp(lambda .), the N - r null
+ * directions give 1; for N < r the r - N eigenvalues of G D of smallest
+ * modulus (exact zeros) are dropped (A19).  O(r^3) fp64 on the
+ * plan's G: Householder tridiagonalisation of D^1/2 G D^1/2, then bisection.
+ *   k     1 <= k <= N eigenvalues per cloud, ascending.
+ *   out   batch x k fp64, HOST or DEVICE memory (cudaMemcpyDefault).
+ * Requires all nu > 0 (rfd_plan_info_t.symmetric == 1; otherwise EINVAL).
+ * Blocks the host until `out` is written.  Errors: EINVAL, ENOMEM, ECUDA.
+ */
+rfd_status rfd_plan_spectrum(rfd_plan* plan, int32_t k, double* out, rfd_stream stream);
+
+/*
  * rfd_integrate -- inference, Eq. 13 in bracket order:
  *   S = Phi^T F (a6), Y = C^ S (a7), out = F + Phi Y (a8).
  *   F    DEVICE, (batch x) N x d fp32.   out  DEVICE, same shape; may alias F.

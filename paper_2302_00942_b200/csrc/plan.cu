@@ -426,6 +426,33 @@ rfd_status reparam_impl(rfd_plan* p, double eps, double lambda, cudaStream_t st)
   return RFD_OK;
 }
 
+// NEXT-3: the k smallest eigenvalues of exp(lambda W~) per cloud from the
+// plan's G and nu (symmetric route: all nu > 0).
+rfd_status spectrum_impl(rfd_plan* p, int k, double* out, cudaStream_t st) {
+  if (!p) return fail(RFD_EINVAL, "plan is NULL");
+  if (!out) return fail(RFD_EINVAL, "out is NULL");
+  if (k < 1 || int64_t(k) > p->n) return fail(RFD_EINVAL, "k must be in [1, n]");
+  if (!p->symmetric)
+    return fail(RFD_EINVAL, "spectrum needs all nu > 0 (symmetric route D^1/2 G D^1/2)");
+  p->stream = st;
+  const int r = p->r, B = p->batch;
+  TempBuffers tmp(st);
+  double *W = nullptr, *P = nullptr, *dg = nullptr, *of = nullptr, *mu = nullptr, *o = nullptr;
+  unsigned int* bar = nullptr;
+  RFD_CUDA(tmp.alloc(&W, size_t(B) * r * r));
+  RFD_CUDA(tmp.alloc(&P, size_t(B) * r));
+  RFD_CUDA(tmp.alloc(&dg, size_t(B) * r));
+  RFD_CUDA(tmp.alloc(&of, size_t(B) * r));
+  RFD_CUDA(tmp.alloc(&mu, size_t(B) * r));
+  RFD_CUDA(tmp.alloc(&o, size_t(B) * k));
+  RFD_CUDA(tmp.alloc(&bar, size_t(2)));
+  RFD_CUDA(rfd::launch_spectrum(p->G, p->nu, p->m, B, p->n, p->lambda, k, W, P, dg, of, mu, bar,
+                                o, st));
+  RFD_CUDA(cudaMemcpyAsync(out, o, size_t(B) * k * sizeof(double), cudaMemcpyDefault, st));
+  RFD_CUDA(cudaStreamSynchronize(st));
+  return RFD_OK;
+}
+
 rfd_status ensure_workspace(rfd_plan* p, int d, cudaStream_t st) {
   if (p->ws_d >= d) return RFD_OK;
   dfree(p->s_partial, st);
@@ -513,6 +540,10 @@ rfd_status rfd_plan_create_batched(const float* points, int32_t batch, int64_t n
 
 rfd_status rfd_plan_reparam(rfd_plan* plan, double eps, double lambda, rfd_stream stream) {
   return reparam_impl(plan, eps, lambda, reinterpret_cast<cudaStream_t>(stream));
+}
+
+rfd_status rfd_plan_spectrum(rfd_plan* plan, int32_t k, double* out, rfd_stream stream) {
+  return spectrum_impl(plan, k, out, reinterpret_cast<cudaStream_t>(stream));
 }
 
 rfd_status rfd_integrate(rfd_plan* plan, const float* F, int32_t d, float* out,

@@ -78,6 +78,16 @@ void launch_core_eval(const double* Z, const double* nu, const int* flags,
                       double lambda, int m, int batch, int s_scale, double* work,
                       double* C, int* oflag, cudaStream_t s);
 
+// ---------------------------------------------------------------- spectrum
+// NEXT-3 (k_spectrum.cu): k smallest eigenvalues of exp(lambda W~) per cloud.
+// Workspaces: W batch*r*r, P/diag/off/mu batch*r doubles, bar 2 uints,
+// out batch*k doubles (device).
+int spectrum_group(int r);
+cudaError_t launch_spectrum(const double* G, const double* nu, int m, int batch, int64_t n,
+                            double lambda, int k, double* W, double* P, double* diag,
+                            double* off, double* mu, unsigned int* bar, double* out,
+                            cudaStream_t s);
+
 // ---------------------------------------------------------------- passes
 struct PassGeom {
   int fblocks;    // ceil(m / 32)

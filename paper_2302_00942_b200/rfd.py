@@ -23,7 +23,8 @@ RFD_MAX_M = 512
 FIELDS = {"omega": 0, "nu": 1, "gram": 2, "core": 3, "S": 4, "Y": 5}
 
 # Every symbol include/rfd.h declares (checked by tests/test_abi.py).
-EXPORTED = ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_reparam", "rfd_integrate",
+EXPORTED = ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_reparam",
+            "rfd_plan_spectrum", "rfd_integrate",
             "rfd_integrate_host", "rfd_destroy", "rfd_last_error", "rfd_plan_info",
             "rfd_plan_export", "rfd_launch_count", "rfd_profile_enable",
             "rfd_profile_read")
@@ -65,6 +66,7 @@ def load_library(path=LIB_PATH):
     lib.rfd_plan_create.argtypes = [vp, i64, dbl, dbl, i32, u64, vp, pp]
     lib.rfd_plan_create_batched.argtypes = [vp, i32, i64, dbl, dbl, i32, u64, vp, pp]
     lib.rfd_plan_reparam.argtypes = [vp, dbl, dbl, vp]
+    lib.rfd_plan_spectrum.argtypes = [vp, i32, vp, vp]
     lib.rfd_integrate.argtypes = [vp, vp, i32, vp, vp]
     lib.rfd_integrate_host.argtypes = [vp, vp, i32, vp, vp]
     lib.rfd_destroy.argtypes = [vp]
@@ -76,7 +78,8 @@ def load_library(path=LIB_PATH):
     lib.rfd_profile_enable.argtypes = [ctypes.c_int]
     lib.rfd_profile_read.argtypes = [ctypes.POINTER(ProfileEntry), i32]
     lib.rfd_profile_read.restype = i32
-    for name in ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_reparam", "rfd_integrate",
+    for name in ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_reparam",
+                 "rfd_plan_spectrum", "rfd_integrate",
                  "rfd_integrate_host", "rfd_plan_info", "rfd_plan_export",
                  "rfd_profile_enable"):
         getattr(lib, name).restype = ctypes.c_int
@@ -169,6 +172,14 @@ class Plan:
                                                _stream_handle(stream)))
         self.eps, self.lam = float(eps), float(lam)
         return self
+
+    def spectrum(self, k, stream=None):
+        """k smallest eigenvalues of exp(lambda W~) per cloud (NEXT-3), numpy fp64
+        of shape (k,) or (B, k)."""
+        out = np.empty((self.batch, max(int(k), 1)), np.float64)  # k < 1: the ABI rejects it
+        _check(load_library().rfd_plan_spectrum(self._h, int(k), _ptr(out),
+                                                _stream_handle(stream)))
+        return out[0] if self.batch == 1 else out
 
     # -- inference -----------------------------------------------------------
     def _field_dims(self, F):

@@ -206,6 +206,45 @@ def test_reparam_errors_leave_plan_unchanged():
     np.testing.assert_array_equal(plan.integrate(Fd).cpu().numpy(), before)
 
 
+@pytest.mark.parametrize("cfg,k", [(1, 32), (2, 64), (4, 200), (1, 1024)])
+def test_spectrum_matches_oracle(cfg, k):
+    # NEXT-3: k smallest eigenvalues of exp(lambda W~) (GPU: Householder
+    # tridiagonalisation of D^1/2 G D^1/2 + bisection; oracle: general
+    # eigenvalues of its own G D).  Values lie in (0, 1] for lambda < 0;
+    # gate 1e-4 absolute (the G parity gate carried through exp).
+    p, x, F = make_config(cfg)
+    plan = rfd.Plan(torch.from_numpy(x).cuda(), p["eps"], p["lam"], p["m"], p["seed"])
+    got = plan.spectrum(k)
+    ref = orf.Plan(x, p["eps"], p["lam"], p["m"], p["seed"]).spectrum(k)
+    err = float(np.abs(got - ref).max())
+    print("spectrum cfg%d k=%d max abs err %.2e" % (cfg, k, err))
+    assert got.shape == (k,)
+    assert np.all(np.diff(got) >= 0)
+    assert err <= 1e-4
+
+
+def test_spectrum_batched_and_small_clouds():
+    # cfg-3-like batch (r = 64 per cloud) and clouds with N < r.
+    rng = np.random.default_rng(3)
+    for n, m, B in [(300, 32, 8), (20, 16, 3)]:
+        x = rng.random((B, n, 3), dtype=np.float32)
+        plan = rfd.Plan(torch.from_numpy(x).cuda(), 0.1, -2.0, m, 5)
+        k = min(n, 16)
+        got = plan.spectrum(k)
+        assert got.shape == (B, k)
+        for b in range(B):
+            ref = orf.Plan(x[b], 0.1, -2.0, m, 5).spectrum(k)
+            assert float(np.abs(got[b] - ref).max()) <= 1e-4, (n, m, b)
+
+
+def test_spectrum_errors():
+    p, x, F = make_config(1)
+    plan = rfd.Plan(torch.from_numpy(x).cuda(), p["eps"], p["lam"], p["m"], p["seed"])
+    for k in (0, -1, x.shape[0] + 1):
+        with pytest.raises(rfd.RFDError):
+            plan.spectrum(k)
+
+
 @pytest.mark.parametrize("n,m,seed,lam", [(1000, 40, 11, -0.8), (3001, 96, 14, -0.3),
                                           (2000, 128, 13, 0.05)])
 def test_negative_nu_nonsymmetric_route(n, m, seed, lam):
