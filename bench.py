@@ -383,6 +383,91 @@ def run_rfd(args, rank, world, local, pg):
                 reparam=reparam, spectrum=spectrum)
 
 
+def config_legs(args, pk):
+    """SURVEY 8(d) per-config timing: integrate at cfgs 1, 2, 4 (median of
+    timed calls) against each config's roofline, the cfg-3 reuse loop (50
+    applications over 256 clouds, plain and CUDA-graph captured), and the
+    eps-independence check at cfg 5."""
+    import torch
+    from paper_2302_00942_b200 import rfd
+    P = peaks_of(pk)
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def roof(N, m, d):
+        t = max(2.0 * 4.0 * N * m * d / P["tf32"], 4.0 * N * m / P["mufu"],
+                N * (24.0 + 12.0 * d) / P["hbm"])
+        return t * 1e3
+
+    def timed(fn, reps):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            ev0.record(stream)
+            fn()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(ev0.elapsed_time(ev1))
+        return float(np.median(ts)), float(np.percentile(ts, 10)), float(np.percentile(ts, 90))
+
+    out = {}
+    for cfg in (1, 2, 4):
+        p, x, F = make_config(cfg)
+        xd, Fd = torch.from_numpy(x).cuda(), torch.from_numpy(F).cuda()
+        od = torch.empty_like(Fd)
+        plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
+        med, p10, p90 = timed(lambda: plan.integrate(Fd, out=od), 200)
+        N, m, d = p["n"], p["m"], p["d"]
+        rl = roof(N, m, d)
+        out["cfg%d" % cfg] = {"integrate_us": med * 1e3, "p10_us": p10 * 1e3, "p90_us": p90 * 1e3,
+                              "value": N * d / (med * 1e-3), "unit": UNIT,
+                              "strict_roofline_us": rl * 1e3, "strict_roofline_frac": rl / med}
+        plan.close()
+    # cfg 3: 50 applications back to back on device-resident vectors
+    p, x, V = make_config(3)
+    xd = torch.from_numpy(x).cuda()
+    plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
+    Vd = torch.from_numpy(V).cuda()
+    outs = torch.empty_like(Vd)
+    A = p["applications"]
+
+    def loop():
+        for t in range(A):
+            plan.integrate(Vd[t], out=outs[t])
+    med, p10, p90 = timed(loop, 10)
+    s2 = torch.cuda.Stream()
+    s2.wait_stream(stream)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s2):
+        plan.integrate(Vd[0], out=outs[0])
+        with torch.cuda.graph(g, stream=s2):
+            for t in range(A):
+                plan.integrate(Vd[t], out=outs[t], stream=s2)
+    torch.cuda.synchronize()
+    gmed, gp10, gp90 = timed(g.replay, 10)
+    Ntot = p["clouds"] * p["n"]
+    rl = roof(Ntot, p["m"], 1) * A
+    out["cfg3_reuse_loop"] = {"applications": A, "clouds": p["clouds"], "plain_ms": med,
+                              "graph_ms": gmed, "graph_p10_ms": gp10, "graph_p90_ms": gp90,
+                              "us_per_application_graph": gmed * 1e3 / A,
+                              "strict_roofline_ms": rl, "strict_roofline_frac_graph": rl / gmed}
+    plan.close()
+    del Vd, outs, g
+    # eps-independence at cfg 5 (same plan re-parameterised: identical G)
+    p, x, F = make_config(5)
+    xd, Fd = torch.from_numpy(x).cuda(), torch.from_numpy(F).cuda()
+    od = torch.empty_like(Fd)
+    plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
+    t_a = timed(lambda: plan.integrate(Fd, out=od), 10)[0]
+    plan.reparam(0.1, p["lam"])
+    t_b = timed(lambda: plan.integrate(Fd, out=od), 10)[0]
+    out["cfg5_eps_independence"] = {"eps_0.01_ms": t_a, "eps_0.1_ms": t_b}
+    plan.close()
+    return out
+
+
 def oracle_sample(n_sample, steps=1):
     """The oracle as it stands on a bounded sample of cfg 5 (first n_sample
     points of the same generator recipe): plan + apply, all rows."""
@@ -412,6 +497,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 20)
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config legs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -449,6 +535,9 @@ def main():
     res = run_rfd(args, rank, world, local, pg)
     if rank != 0:
         return
+    legs = None
+    if world == 1 and not args.no_configs:
+        legs = config_legs(args, peaks())
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         _, cval, cdt = oracle_sample(args.cpu_sample)
@@ -462,7 +551,8 @@ def main():
             "dtype": "f32", "data": "synthetic", "config": dict(cfg_desc, parallelism="dp%d (independent clouds)" % world),
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
             "gpu_launches": res["launches"], "clocks": res["clocks"],
-            "integrate": res["integrate"], "reparam": res["reparam"], "spectrum": res["spectrum"], "kernels": res["kernels"]}
+            "integrate": res["integrate"], "reparam": res["reparam"], "spectrum": res["spectrum"], "configs": legs,
+            "kernels": res["kernels"]}
     print(json.dumps(line))
 
 

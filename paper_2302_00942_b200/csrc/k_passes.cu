@@ -102,59 +102,84 @@ pass1_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4, 
   }
 }
 
-__global__ void reduce_S_kernel(const float* __restrict__ partial, int r, int chunks, int d,
-                                int c0, int dc, double* __restrict__ S) {
-  const int b = blockIdx.y;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= r * dc) return;
-  const int a = e / dc, j = e % dc;
-  const float* src = partial + int64_t(b) * chunks * r * dc + e;
-  const int64_t st = int64_t(r) * dc;
-  // fixed order: 8 interleaved fp64 sums (8 loads in flight), then combined
-  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  int ch = 0;
-  for (; ch + 8 <= chunks; ch += 8) {
-    float v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (ch + u) * st);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] += double(v[u]);
-  }
-  for (int u = 0; ch < chunks; ++ch, ++u) acc[u] += double(__ldg(src + ch * st));
-  const double sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-  S[(int64_t(b) * r + a) * d + c0 + j] = sum;
-}
-
-// Y = C^ S for 4 rows of C^ and 16 columns of S per CTA: 16 k-slices x 16
-// columns of threads, each summing k = slice (mod 16) for the 4 rows; the
-// slices are then added in a fixed order (deterministic).
-constexpr int kApplyRows = 4;
+// S[b] = sum over the `chunks` partials, fp64, in a fixed order: each CTA
+// takes 32 consecutive elements x 8 chunk slices (slice l sums chunks l, l + 8,
+// ... in order, 8 loads in flight), then the 8 slice sums are added in order.
 __global__ void __launch_bounds__(256)
-core_apply_kernel(const double* __restrict__ C, const double* __restrict__ S, int r, int d,
-                  float* __restrict__ Y) {
-  __shared__ double red[16][kApplyRows][17];
+reduce_S_kernel(const float* __restrict__ partial, int r, int chunks, int d, int c0, int dc,
+                double* __restrict__ S) {
+  __shared__ double red[8][33];
   const int b = blockIdx.y;
-  const int a0 = blockIdx.x * kApplyRows, c0 = blockIdx.z * 16;
-  const int slice = threadIdx.x >> 4, c = threadIdx.x & 15;
-  const bool cok = c0 + c < d;
-  const double* Cb = C + (int64_t(b) * r + a0) * r;
-  const double* Sb = S + int64_t(b) * r * d + c0 + c;
-  double acc[kApplyRows] = {0.0, 0.0, 0.0, 0.0};
-  for (int k = slice; k < r; k += 16) {
-    const double sv = cok ? __ldg(Sb + int64_t(k) * d) : 0.0;
+  const int el = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + el;
+  const int64_t st = int64_t(r) * dc;
+  double acc = 0.0;
+  if (e < r * dc) {
+    const float* src = partial + int64_t(b) * chunks * st + e;
+    int ch = sl;
+    for (; ch + 56 < chunks; ch += 64) {
+      float v[8];
 #pragma unroll
-    for (int i = 0; i < kApplyRows; ++i)
-      if (a0 + i < r) acc[i] = fma(__ldg(Cb + int64_t(i) * r + k), sv, acc[i]);
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (ch + 8 * u) * st);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += double(v[u]);
+    }
+    for (; ch < chunks; ch += 8) acc += double(__ldg(src + ch * st));
   }
-#pragma unroll
-  for (int i = 0; i < kApplyRows; ++i) red[slice][i][c] = acc[i];
+  red[sl][el] = acc;
   __syncthreads();
-  if (threadIdx.x < kApplyRows * 16) {
-    const int i = threadIdx.x >> 4, cc = threadIdx.x & 15;
+  if (sl == 0 && e < r * dc) {
     double sum = 0.0;
 #pragma unroll
-    for (int sl = 0; sl < 16; ++sl) sum += red[sl][i][cc];
-    if (a0 + i < r && c0 + cc < d) Y[(int64_t(b) * r + a0 + i) * d + c0 + cc] = float(sum);
+    for (int l = 0; l < 8; ++l) sum += red[l][el];
+    const int a = e / dc, j = e % dc;
+    S[(int64_t(b) * r + a) * d + c0 + j] = sum;
+  }
+}
+
+// Y = C^ S: a CTA takes 8 x rpw rows of one cloud's C^ (rpw rows per warp;
+// small r: the whole cloud in one CTA) and a chunk of <= 16 columns; the chunk
+// of S is staged transposed in shared memory (St[j][k]: conflict-free reads),
+// lanes split k (k = lane + 32 i), then a butterfly reduction per column
+// (fixed order: deterministic).
+__global__ void __launch_bounds__(256)
+core_apply_kernel(const double* __restrict__ C, const double* __restrict__ S, int r, int d,
+                  int rpw, float* __restrict__ Y) {
+  extern __shared__ double St[];  // [dc][r]
+  const int b = blockIdx.y, c0 = blockIdx.z * 16;
+  const int dc = min(16, d - c0);
+  const double* Sb = S + int64_t(b) * r * d + c0;
+  for (int i = threadIdx.x; i < dc * r; i += 256) {
+    const int k = i / dc, j = i - k * dc;
+    St[j * r + k] = Sb[int64_t(k) * d + j];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = 0; t < rpw; ++t) {
+    const int a = (blockIdx.x * 8 + warp) * rpw + t;
+    if (a >= r) break;
+    const double* Ca = C + (int64_t(b) * r + a) * r;
+    double acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+#pragma unroll 4
+    for (int k = lane; k < r; k += 32) {
+      const double c = __ldg(Ca + k);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < dc) acc[j] = fma(c, St[j * r + k], acc[j]);
+    }
+    double v = 0.0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j < dc) {
+        double x = acc[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (j == lane) v = x;
+      }
+    }
+    if (lane < dc) Y[(int64_t(b) * r + a) * d + c0 + lane] = float(v);
   }
 }
 
@@ -329,16 +354,28 @@ void launch_reduce_S(const float* partial, int m, int batch, int chunks, int d, 
                      double* S, cudaStream_t s) {
   LaunchScope L("rfd_reduce_S", s);
   const int r = 2 * m;
-  reduce_S_kernel<<<dim3((r * dc + 255) / 256, batch), 256, 0, s>>>(partial, r, chunks, d, c0,
-                                                                     dc, S);
+  reduce_S_kernel<<<dim3((r * dc + 31) / 32, batch), 256, 0, s>>>(partial, r, chunks, d, c0, dc,
+                                                                   S);
 }
 
 void launch_core_apply(const double* C, const double* S, int m, int batch, int d, float* Y,
                        cudaStream_t s) {
   LaunchScope L("rfd_core_apply", s);
   const int r = 2 * m;
-  core_apply_kernel<<<dim3((r + kApplyRows - 1) / kApplyRows, batch, (d + 15) / 16), 256, 0, s>>>(
-      C, S, r, d, Y);
+  const size_t smem = size_t(16) * r * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(core_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         16 * 1024 * int(sizeof(double)));  // r <= 2 RFD_MAX_M = 1024
+    configured = true;
+  }
+  // rows per warp: 1 while that leaves < ~2 CTAs per SM, more for many small
+  // clouds (at most the whole cloud in one CTA)
+  int64_t rpw64 = (int64_t(r) * batch) / (8 * 148 * 2);
+  if (rpw64 > (r + 7) / 8) rpw64 = (r + 7) / 8;
+  const int rpw = rpw64 < 1 ? 1 : int(rpw64);
+  core_apply_kernel<<<dim3((r + 8 * rpw - 1) / (8 * rpw), batch, (d + 15) / 16), 256, smem, s>>>(
+      C, S, r, d, rpw, Y);
 }
 
 void launch_pass2(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
