@@ -464,7 +464,18 @@ def config_legs(args, pk):
     plan.reparam(0.1, p["lam"])
     t_b = timed(lambda: plan.integrate(Fd, out=od), 10)[0]
     out["cfg5_eps_independence"] = {"eps_0.01_ms": t_a, "eps_0.1_ms": t_b}
+    plan.reparam(p["eps"], p["lam"])
+    # multi-column integrate (NEXT-2): cfg-5 points, d = 64 synthetic N(0,1)
+    F64 = torch.randn((p["n"], 64), device="cuda", generator=torch.Generator("cuda").manual_seed(4))
+    o64 = torch.empty_like(F64)
+    t64 = timed(lambda: plan.integrate(F64, out=o64), 10)[0]
+    N = p["n"]
+    out["cfg5_d64"] = {"integrate_ms": t64, "value": N * 64 / (t64 * 1e-3), "unit": UNIT,
+                       "ms_per_16_columns": t64 / 4, "d16_ms": t_a,
+                       "strict_roofline_ms": roof(N, p["m"], 64),
+                       "strict_roofline_frac": roof(N, p["m"], 64) / t64}
     plan.close()
+    del F64, o64
     return out
 
 

@@ -245,6 +245,19 @@ def test_spectrum_errors():
             plan.spectrum(k)
 
 
+@pytest.mark.parametrize("n,m,d", [(20000, 256, 64), (9001, 256, 100), (6000, 512, 50),
+                                   (5000, 64, 33)])
+def test_multi_column_parity(n, m, d):
+    # NEXT-2: pass 2 takes up to 64 columns per launch (MMA N = the chunk's
+    # columns, Y^T scaled per channel); wide and ragged d against the oracle.
+    x = _sphere(n, n + d)
+    F = np.random.default_rng(d).standard_normal((n, d)).astype(np.float32)
+    F[:, -1] *= 1e3  # channels of very different scales in one chunk
+    p = dict(name="multicol n=%d m=%d d=%d" % (n, m, d), eps=0.05, lam=-0.8, m=m, seed=17)
+    plan, out = _run_single(x, F, p)
+    _check_against_oracle(plan, out, x, F, p)
+
+
 @pytest.mark.parametrize("n,m,seed,lam", [(1000, 40, 11, -0.8), (3001, 96, 14, -0.3),
                                           (2000, 128, 13, 0.05)])
 def test_negative_nu_nonsymmetric_route(n, m, seed, lam):

@@ -505,7 +505,7 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
   }();
   // pass 2 on the tensor cores takes up to 64 columns per launch (MMA N = the
   // chunk's columns): the features are regenerated once per chunk (NEXT-2)
-  const int w2 = p2_simt ? 16 : rfd::pass2_tc_width(p->m);
+  const int w2 = 16;
   for (int c0 = 0; c0 < d; c0 += w2) {
     const int dc = (d - c0 < w2) ? d - c0 : w2;
     if (p2_simt)

@@ -246,54 +246,49 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       }
     } else {
       // ---------------- epilogue warps: TMEM -> registers, + F, store -----
-      // (16-column groups; D is released once every group has been read)
       const int64_t i = base + lg * 32 + lane;
       const int64_t idx = int64_t(b) * n + i;
-      tc::mbar_wait(&dfull_bar[buf], (it >> 1) & 1);
-      tc::tc_fence_after();
-      for (int g16 = 0; g16 < nw; g16 += 16) {
-        const int dcg = min(16, dc - g16);
-        const bool vec = (dcg == 16) && (d % 4 == 0) && ((c0 + g16) % 4 == 0);
-        float f[16];
+      const bool vec = (dc == 16) && (d % 4 == 0) && (c0 % 4 == 0);
+      float f[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = 0.0f;
-        if (i < n && dcg > 0) {
-          const float* Fi = F + idx * d + c0 + g16;
-          if (vec) {
+      for (int j = 0; j < 16; ++j) f[j] = 0.0f;
+      if (i < n) {
+        const float* Fi = F + idx * d + c0;
+        if (vec) {
 #pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-              const float4 t4 = *reinterpret_cast<const float4*>(Fi + j);
-              f[j] = t4.x; f[j + 1] = t4.y; f[j + 2] = t4.z; f[j + 3] = t4.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < dcg) f[j] = Fi[j];
+          for (int j = 0; j < 16; j += 4) {
+            const float4 t4 = *reinterpret_cast<const float4*>(Fi + j);
+            f[j] = t4.x; f[j + 1] = t4.y; f[j + 2] = t4.z; f[j + 3] = t4.w;
           }
-        }
-        float v[16];
-        __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the F loads
-        tc::tmem_ld16(tmem + lane_field + nw * buf + g16, v);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] *= yscale_inv[g16 + j];
-        if (i < n && dcg > 0) {
-          float* Oi = out + idx * d + c0 + g16;
-          if (vec) {
-#pragma unroll
-            for (int j = 0; j < 16; j += 4)
-              *reinterpret_cast<float4*>(Oi + j) =
-                  make_float4(f[j] + v[j], f[j + 1] + v[j + 1], f[j + 2] + v[j + 2],
-                              f[j + 3] + v[j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < dcg) Oi[j] = f[j] + v[j];
-          }
+          for (int j = 0; j < 16; ++j)
+            if (j < dc) f[j] = Fi[j];
         }
       }
+      tc::mbar_wait(&dfull_bar[buf], (it >> 1) & 1);
+      tc::tc_fence_after();
+      float v[16];
+      tc::tmem_ld16(tmem + lane_field + nw * buf, v);
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&dempty_bar[buf]);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] *= yscale_inv[j];
+      if (i < n) {
+        float* Oi = out + idx * d + c0;
+        if (vec) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(Oi + j) =
+                make_float4(f[j] + v[j], f[j + 1] + v[j + 1], f[j + 2] + v[j + 2],
+                            f[j + 3] + v[j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < dc) Oi[j] = f[j] + v[j];
+        }
+      }
     }
     g += nch;
   }

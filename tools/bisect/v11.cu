@@ -275,7 +275,7 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
         __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the F loads
         tc::tmem_ld16(tmem + lane_field + nw * buf + g16, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] *= yscale_inv[g16 + j];
+        for (int j = 0; j < 16; ++j) v[j] *= yscale_inv[j];
         if (i < n && dcg > 0) {
           float* Oi = out + idx * d + c0 + g16;
           if (vec) {

@@ -274,6 +274,11 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
         float v[16];
         __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the F loads
         tc::tmem_ld16(tmem + lane_field + nw * buf + g16, v);
+        if (g16 + 16 >= nw) {
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&dempty_bar[buf]);
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] *= yscale_inv[g16 + j];
         if (i < n && dcg > 0) {
@@ -291,9 +296,6 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
           }
         }
       }
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&dempty_bar[buf]);
     }
     g += nch;
   }

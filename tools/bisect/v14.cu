@@ -251,6 +251,7 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       const int64_t idx = int64_t(b) * n + i;
       tc::mbar_wait(&dfull_bar[buf], (it >> 1) & 1);
       tc::tc_fence_after();
+      __nanosleep(20000);
       for (int g16 = 0; g16 < nw; g16 += 16) {
         const int dcg = min(16, dc - g16);
         const bool vec = (dcg == 16) && (d % 4 == 0) && ((c0 + g16) % 4 == 0);

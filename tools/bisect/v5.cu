@@ -100,16 +100,12 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   // reading the old Y has completed.
   auto load_y = [&](int b) {
     const float* Yb = Y + int64_t(b) * 2 * m * d;
-    // per-channel power-of-two scale: max |Y_j| 2^e_j in [2^13, 2^14); one warp
-    // per channel, lanes over the 2m rows (no atomics, no index division)
+    // per-channel power-of-two scale: max |Y_j| 2^e_j in [2^13, 2^14)
     if (tid < nw) ymax_bits[tid] = 0u;
     __syncthreads();
-    for (int j = warp; j < dc; j += kThreads / 32) {
-      float mx = 0.0f;
-      for (int a = lane; a < 2 * m; a += 32) mx = fmaxf(mx, fabsf(Yb[int64_t(a) * d + c0 + j]));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0) ymax_bits[j] = __float_as_uint(mx);
+    for (int e = tid; e < 16 * 2 * m; e += kThreads) {
+      const int a = e >> 4, j = e & 15;
+      if (j < dc) atomicMax(&ymax_bits[j], __float_as_uint(fabsf(Yb[int64_t(a) * d + c0 + j])));
     }
     __syncthreads();
     float scale = 1.0f;
@@ -124,20 +120,17 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       ymax_bits[tid] = __float_as_uint(scale);
     }
     __syncthreads();
-    // Y^T (nw rows x kpad), scaled and split; one warp per feature row a,
-    // lanes over channels
-    for (int a = warp; a < kpad; a += kThreads / 32) {
-      for (int j = lane; j < nw; j += 32) {
-        const float val = (a < 2 * m && j < dc)
-                              ? Yb[int64_t(a) * d + c0 + j] * __uint_as_float(ymax_bits[j])
-                              : 0.0f;
-        const __half h = __float2half_rn(val);
-        const __half l = __float2half_rn(val - __half2float(h));
-        const uint32_t off = uint32_t(j >> 3) * sbo + uint32_t(a >> 3) * kLBO +
-                             uint32_t(j & 7) * 16 + uint32_t(a & 7) * 2;
-        *reinterpret_cast<__half*>(yb + off) = h;
-        *reinterpret_cast<__half*>(yl + off) = l;
-      }
+    for (int e = tid; e < nw * kpad; e += kThreads) {
+      const int a = e / nw, j = e - a * nw;
+      const float val = (a < 2 * m && j < dc)
+                            ? Yb[int64_t(a) * d + c0 + j] * __uint_as_float(ymax_bits[j])
+                            : 0.0f;
+      const __half h = __float2half_rn(val);
+      const __half l = __float2half_rn(val - __half2float(h));
+      const uint32_t off = uint32_t(j >> 3) * sbo + uint32_t(a >> 3) * kLBO +
+                           uint32_t(j & 7) * 16 + uint32_t(a & 7) * 2;
+      *reinterpret_cast<__half*>(yb + off) = h;
+      *reinterpret_cast<__half*>(yl + off) = l;
     }
     tc::fence_proxy_async_smem();
   };
@@ -246,54 +239,49 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       }
     } else {
       // ---------------- epilogue warps: TMEM -> registers, + F, store -----
-      // (16-column groups; D is released once every group has been read)
       const int64_t i = base + lg * 32 + lane;
       const int64_t idx = int64_t(b) * n + i;
-      tc::mbar_wait(&dfull_bar[buf], (it >> 1) & 1);
-      tc::tc_fence_after();
-      for (int g16 = 0; g16 < nw; g16 += 16) {
-        const int dcg = min(16, dc - g16);
-        const bool vec = (dcg == 16) && (d % 4 == 0) && ((c0 + g16) % 4 == 0);
-        float f[16];
+      const bool vec = (dc == 16) && (d % 4 == 0) && (c0 % 4 == 0);
+      float f[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = 0.0f;
-        if (i < n && dcg > 0) {
-          const float* Fi = F + idx * d + c0 + g16;
-          if (vec) {
+      for (int j = 0; j < 16; ++j) f[j] = 0.0f;
+      if (i < n) {
+        const float* Fi = F + idx * d + c0;
+        if (vec) {
 #pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-              const float4 t4 = *reinterpret_cast<const float4*>(Fi + j);
-              f[j] = t4.x; f[j + 1] = t4.y; f[j + 2] = t4.z; f[j + 3] = t4.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < dcg) f[j] = Fi[j];
+          for (int j = 0; j < 16; j += 4) {
+            const float4 t4 = *reinterpret_cast<const float4*>(Fi + j);
+            f[j] = t4.x; f[j + 1] = t4.y; f[j + 2] = t4.z; f[j + 3] = t4.w;
           }
-        }
-        float v[16];
-        __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the F loads
-        tc::tmem_ld16(tmem + lane_field + nw * buf + g16, v);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] *= yscale_inv[g16 + j];
-        if (i < n && dcg > 0) {
-          float* Oi = out + idx * d + c0 + g16;
-          if (vec) {
-#pragma unroll
-            for (int j = 0; j < 16; j += 4)
-              *reinterpret_cast<float4*>(Oi + j) =
-                  make_float4(f[j] + v[j], f[j + 1] + v[j + 1], f[j + 2] + v[j + 2],
-                              f[j + 3] + v[j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < dcg) Oi[j] = f[j] + v[j];
-          }
+          for (int j = 0; j < 16; ++j)
+            if (j < dc) f[j] = Fi[j];
         }
       }
+      tc::mbar_wait(&dfull_bar[buf], (it >> 1) & 1);
+      tc::tc_fence_after();
+      float v[16];
+      tc::tmem_ld16(tmem + lane_field + nw * buf, v);
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&dempty_bar[buf]);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] *= yscale_inv[j];
+      if (i < n) {
+        float* Oi = out + idx * d + c0;
+        if (vec) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(Oi + j) =
+                make_float4(f[j] + v[j], f[j + 1] + v[j + 1], f[j + 2] + v[j + 2],
+                            f[j + 3] + v[j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < dc) Oi[j] = f[j] + v[j];
+        }
+      }
     }
     g += nch;
   }

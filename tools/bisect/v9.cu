@@ -100,16 +100,12 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   // reading the old Y has completed.
   auto load_y = [&](int b) {
     const float* Yb = Y + int64_t(b) * 2 * m * d;
-    // per-channel power-of-two scale: max |Y_j| 2^e_j in [2^13, 2^14); one warp
-    // per channel, lanes over the 2m rows (no atomics, no index division)
+    // per-channel power-of-two scale: max |Y_j| 2^e_j in [2^13, 2^14)
     if (tid < nw) ymax_bits[tid] = 0u;
     __syncthreads();
-    for (int j = warp; j < dc; j += kThreads / 32) {
-      float mx = 0.0f;
-      for (int a = lane; a < 2 * m; a += 32) mx = fmaxf(mx, fabsf(Yb[int64_t(a) * d + c0 + j]));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0) ymax_bits[j] = __float_as_uint(mx);
+    for (int e = tid; e < nw * 2 * m; e += kThreads) {
+      const int a = int(unsigned(e) / unsigned(nw)), j = int(unsigned(e) % unsigned(nw));
+      if (j < dc) atomicMax(&ymax_bits[j], __float_as_uint(fabsf(Yb[int64_t(a) * d + c0 + j])));
     }
     __syncthreads();
     float scale = 1.0f;
@@ -124,20 +120,17 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       ymax_bits[tid] = __float_as_uint(scale);
     }
     __syncthreads();
-    // Y^T (nw rows x kpad), scaled and split; one warp per feature row a,
-    // lanes over channels
-    for (int a = warp; a < kpad; a += kThreads / 32) {
-      for (int j = lane; j < nw; j += 32) {
-        const float val = (a < 2 * m && j < dc)
-                              ? Yb[int64_t(a) * d + c0 + j] * __uint_as_float(ymax_bits[j])
-                              : 0.0f;
-        const __half h = __float2half_rn(val);
-        const __half l = __float2half_rn(val - __half2float(h));
-        const uint32_t off = uint32_t(j >> 3) * sbo + uint32_t(a >> 3) * kLBO +
-                             uint32_t(j & 7) * 16 + uint32_t(a & 7) * 2;
-        *reinterpret_cast<__half*>(yb + off) = h;
-        *reinterpret_cast<__half*>(yl + off) = l;
-      }
+    for (int e = tid; e < nw * kpad; e += kThreads) {
+      const int a = int(unsigned(e) / unsigned(nw)), j = int(unsigned(e) % unsigned(nw));
+      const float val = (a < 2 * m && j < dc)
+                            ? Yb[int64_t(a) * d + c0 + j] * __uint_as_float(ymax_bits[j])
+                            : 0.0f;
+      const __half h = __float2half_rn(val);
+      const __half l = __float2half_rn(val - __half2float(h));
+      const uint32_t off = uint32_t(j >> 3) * sbo + uint32_t(a >> 3) * kLBO +
+                           uint32_t(j & 7) * 16 + uint32_t(a & 7) * 2;
+      *reinterpret_cast<__half*>(yb + off) = h;
+      *reinterpret_cast<__half*>(yl + off) = l;
     }
     tc::fence_proxy_async_smem();
   };
