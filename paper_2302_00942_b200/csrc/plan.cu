@@ -460,7 +460,9 @@ rfd_status ensure_workspace(rfd_plan* p, int d, cudaStream_t st) {
   dfree(p->Y, st);
   p->ws_d = 0;
   const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
-  const size_t part = size_t(p->batch) * (p->pg.chunks > ranges ? p->pg.chunks : ranges) * p->r * 16;
+  // pass-1 partials: (chunks or ranges) x r x (column chunk <= 64)
+  const size_t part = size_t(p->batch) * (p->pg.chunks > ranges ? p->pg.chunks : ranges) * p->r *
+                      size_t(d < 64 ? d : 64);
   RFD_CUDA(dalloc(&p->s_partial, part, st));
   RFD_CUDA(dalloc(&p->S, size_t(p->batch) * p->r * d, st));
   RFD_CUDA(dalloc(&p->Y, size_t(p->batch) * p->r * d, st));
@@ -484,8 +486,11 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
     return e && strcmp(e, "simt") == 0;
   }();
   const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
-  for (int c0 = 0; c0 < d; c0 += 16) {
-    const int dc = (d - c0 < 16) ? d - c0 : 16;
+  // pass 1 on the tensor cores takes up to 64 columns per launch (MMA N = the
+  // chunk's columns): the features are regenerated once per chunk (NEXT-2)
+  const int w1 = p1_simt ? 16 : 64;
+  for (int c0 = 0; c0 < d; c0 += w1) {
+    const int dc = (d - c0 < w1) ? d - c0 : w1;
     if (p1_simt) {
       rfd::launch_pass1(p->pts, p->omega4, p->m, p->n, p->batch, p->pg, F, d, c0, dc,
                         p->s_partial, st);

@@ -1,0 +1,439 @@
+// K4 on the tensor cores -- pass 1, S = Phi^T F (the
+// first bracket "B^T x" of Eq. 13), for a chunk of up to 64
+// columns of F per launch (NEXT-2: the features are generated once for all the
+// chunk's columns).
+//
+// A CTA owns a tile of 128 frequencies (TMEM lanes) and a contiguous range of
+// whole chunks of 64 points (the contraction dimension K).  Warp roles:
+//
+//   * 16 producer warps regenerate cos and sin of omega_k . x for their
+//     lane's frequency (a3; 16 points per warp and chunk, read as one SoA
+//     group copied ahead with cp.async, arguments in packed FP32) and write
+//     them, split x = hi + lo in fp16 (|x - hi - lo| <= 2^-22 |x| + 2^-25),
+//     straight into TMEM as the A operands (cos rows, sin rows);
+//   * one elected lane of the MMA warp issues per chunk
+//         D_cos += C_hi F_hi^T + C_hi F_lo^T + C_lo F_hi^T,  D_sin likewise
+//     (tcgen05.mma kind::f16, M = 128, N = 16 NC, K = 16 x 4);
+//   * 4 F/drain warps stage F: per epoch of E chunks they copy the epoch's
+//     F block into shared memory (cp.async), scale each channel by a power of
+//     two into fp16 range (max |F_j| 2^e_j in [2^13, 2^14) over the epoch) and
+//     write it, split likewise, as the B operands of the epoch's chunks
+//     (N channels x 64 points, K-major, double-buffered by epoch).  The tensor
+//     core's fp32 accumulator is not round-to-nearest, so D accumulates one
+//     epoch only; the same warps then add it, scaled back exactly (x 2^-e_j),
+//     into a long-term fp32 sum L in TMEM (round-to-nearest FFMA), and at the
+//     end write L as the CTA's 2 x N partial sums per frequency.  K5 reduces
+//     the partials in a fixed order in fp64.
+//
+// TMEM: D [0, 2N) (cos N | sin N), L [2N, 4N), A stages at 4N + 128 s.
+#include "rfd_internal.h"
+#include "tc_ptx.cuh"
+
+namespace rfd {
+namespace {
+
+constexpr int kProducerWarps = 16;  // 4 per TMEM lane group
+constexpr int kMmaWarp = 16;
+constexpr int kFWarp0 = 17;         // warps 17..20: F staging + drains
+constexpr int kThreads = 21 * 32;
+constexpr int kChunk = 64;          // points per chunk (16 per producer warp)
+constexpr int kArr = kChunk / 2;    // TMEM columns per A array (fp16 pairs)
+constexpr uint32_t kLBO = 128;
+constexpr uint32_t kSBO = (kChunk / 8) * 128;   // B: 8-channel groups
+
+// NC == 1 (d <= 16, the common case): D double-buffered (two epochs in
+// flight, no MMA stall at a drain) and the long-term sums in the drain warps'
+// registers.  NC >= 2: one D buffer and the long-term sums L in TMEM (2N
+// registers per lane would not fit).
+template <int NC>
+struct P1 {
+  static constexpr int N = 16 * NC;                          // MMA N: channels
+  static constexpr bool kRegAcc = NC == 1;
+  static constexpr int kStages = (512 - 4 * N) / 128 < 3 ? (512 - 4 * N) / 128 : 3;
+  static constexpr int kEpoch = NC <= 2 ? 8 : 4;             // chunks per epoch
+  // TMEM: NC == 1: D buffers at 0 and 2N; NC >= 2: D at 0, L at 2N
+  static constexpr uint32_t kColL = 2 * N, kColA = 4 * N;
+  static constexpr int kBBytes = N * kChunk * 2;             // one fp16 B operand
+  static constexpr int kChunkB = 2 * kBBytes;                // hi + lo
+  static constexpr int kEpochB = kEpoch * kChunkB;
+  static constexpr int kStageF = kEpoch * kChunk * N * 4;    // fp32 F block
+  static constexpr int kSmem = 2 * kEpochB + kStageF;
+};
+
+template <int NC>
+__global__ void __launch_bounds__(kThreads, 1)
+pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omega4, int m,
+                int64_t n, int ranges, const float* __restrict__ F, int d, int c0, int dc,
+                float* __restrict__ partial) {
+  using C = P1<NC>;
+  constexpr int N = C::N, kStages = C::kStages, kEpoch = C::kEpoch;
+  // [2 epochs][E chunks][hi | lo] B operands, then the fp32 F staging block
+  extern __shared__ __align__(1024) unsigned char bsm[];
+  __shared__ uint64_t full_bar[kStages], empty_bar[kStages], dfull_bar[2], dempty_bar[2],
+      bready_bar[2];
+  __shared__ uint32_t tmem_sh;
+  // each producer warp's 16 points of a chunk as [x0..15 | y0..15 | z0..15],
+  // 3 chunks deep (cp.async ring)
+  __shared__ __align__(16) float xbuf[3][kProducerWarps][48];
+  __shared__ float fmax_part[128];
+  __shared__ float fscale_inv[2][N];  // per epoch buffer
+
+  const int ft = blockIdx.x, rg = blockIdx.y, b = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, lg = warp & 3;
+  // ranges are whole chunks; only a cloud's last chunk is partial
+  const int64_t cpc = (n + kChunk - 1) / kChunk, gpc = (n + 15) / 16;
+  const int64_t ch0 = cpc * rg / ranges, ch1 = cpc * (rg + 1) / ranges;
+  const int64_t p0 = ch0 * kChunk;
+  const int nchunks = int(ch1 - ch0);
+  const int nepochs = (nchunks + kEpoch - 1) / kEpoch;
+  const float* cloud16 = pts16 + int64_t(b) * gpc * 48;
+
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&full_bar[s], kProducerWarps);
+      tc::mbar_init(&empty_bar[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&dfull_bar[i], 1);
+      tc::mbar_init(&dempty_bar[i], 4);
+      tc::mbar_init(&bready_bar[i], 4);
+    }
+    tc::mbar_fence_init();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+  const uint32_t lane_field = uint32_t(lg * 32) << 16;
+  const int f = ft * 128 + lg * 32 + lane;  // this lane's frequency
+
+  if (warp < kProducerWarps) {
+    // ---------------- producers: 16 points per warp per chunk --------------
+    const int q = warp >> 2;  // which 16 of the chunk's points
+    const float4 w = (f < m) ? omega4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float2 wx = make_float2(w.x, w.x), wy = make_float2(w.y, w.y), wz = make_float2(w.z, w.z);
+    // The warp's 16 points (one SoA group, 192 B), copied two chunks ahead by
+    // lanes 0-11 straight into shared memory (cp.async: global latency off the
+    // critical path).  Groups past the cloud's end repeat its last group
+    // (finite values that meet zero F).  Pointers and counters advance per
+    // chunk (no 64-bit index arithmetic in the loop).
+    const float* xsrc = cloud16 + ((ch0 * (kChunk / 16) + q) * 48 + 4 * lane);
+    const float* xlast = cloud16 + ((gpc - 1) * 48 + 4 * lane);
+    const int64_t xrem0 = gpc - (ch0 * (kChunk / 16) + q);
+    int xrem = int(xrem0 > 0x7fffffff ? 0x7fffffff : xrem0);  // groups left
+    constexpr uint32_t kRing = kProducerWarps * 48 * 4;           // bytes per ring slot
+    const uint32_t x_s = tc::smem_addr(&xbuf[0][warp][0]);
+    uint32_t xw = 0;
+    auto load_x = [&](bool valid) {
+      if (lane < 12 && valid) tc::cp_async16(x_s + xw * kRing + 16 * lane, xrem > 0 ? xsrc : xlast);
+      tc::cp_async_commit();  // one group per chunk, empty past the end
+      xsrc += 48 * (kChunk / 16);
+      xrem -= kChunk / 16;
+      xw = (xw == 2) ? 0 : xw + 1;
+    };
+    load_x(nchunks > 0);
+    load_x(nchunks > 1);
+    const uint32_t empty_s = tc::smem_addr(&empty_bar[0]), full_s = tc::smem_addr(&full_bar[0]);
+    uint32_t s = 0, u = 0, xr = 0;  // stage, its round, ring slot read
+    for (int c = 0; c < nchunks; ++c) {
+      load_x(c + 2 < nchunks);  // the slot chunk c - 1 read (ordered by its __syncwarp)
+      if (u >= 1) tc::mbar_wait(empty_s + 8 * s, (u - 1) & 1);
+      // Points beyond the cloud meet zero columns of F^T, and lanes beyond m
+      // are never written out: no masking of the features.
+      tc::cp_async_wait<2>();  // chunk c's group (c + 1, c + 2 may be in flight)
+      __syncwarp();
+      const float* xs = &xbuf[0][warp][0] + xr * (kProducerWarps * 48);
+      xr = (xr == 2) ? 0 : xr + 1;
+      const uint32_t a = tmem + lane_field + C::kColA + 4 * kArr * s + 8 * q;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // two halves of 8 points (register pressure)
+        float cs[8], sn[8];
+#pragma unroll
+        for (int j = 0; j < 8; j += 4) {
+          // omega . x for 4 points in packed FP32 (2 points per instruction),
+          // the same operation order as fmaf(wz, z, fmaf(wy, y, wx * x))
+          const float4 X = *reinterpret_cast<const float4*>(xs + 8 * h + j);
+          const float4 Y = *reinterpret_cast<const float4*>(xs + 16 + 8 * h + j);
+          const float4 Z = *reinterpret_cast<const float4*>(xs + 32 + 8 * h + j);
+          float2 t0 = __fmul2_rn(wx, make_float2(X.x, X.y));
+          float2 t1 = __fmul2_rn(wx, make_float2(X.z, X.w));
+          t0 = __ffma2_rn(wy, make_float2(Y.x, Y.y), t0);
+          t1 = __ffma2_rn(wy, make_float2(Y.z, Y.w), t1);
+          t0 = __ffma2_rn(wz, make_float2(Z.x, Z.y), t0);
+          t1 = __ffma2_rn(wz, make_float2(Z.z, Z.w), t1);
+          __sincosf(t0.x, &sn[j], &cs[j]);
+          __sincosf(t0.y, &sn[j + 1], &cs[j + 1]);
+          __sincosf(t1.x, &sn[j + 2], &cs[j + 2]);
+          __sincosf(t1.y, &sn[j + 3], &cs[j + 3]);
+        }
+        uint32_t chi[4], clo[4], shi[4], slo[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          tc::split_f16x2(cs[2 * j], cs[2 * j + 1], chi[j], clo[j]);
+          tc::split_f16x2(sn[2 * j], sn[2 * j + 1], shi[j], slo[j]);
+        }
+        const uint32_t ah = a + 4 * h;
+        tc::tmem_st4(ah, chi[0], chi[1], chi[2], chi[3]);
+        tc::tmem_st4(ah + kArr, clo[0], clo[1], clo[2], clo[3]);
+        tc::tmem_st4(ah + 2 * kArr, shi[0], shi[1], shi[2], shi[3]);
+        tc::tmem_st4(ah + 3 * kArr, slo[0], slo[1], slo[2], slo[3]);
+      }
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(full_s + 8 * s);
+      if (++s == kStages) {
+        s = 0;
+        ++u;
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ---------------- MMA issue: warp-uniform loop, one elected lane -------
+    const uint32_t idesc = tc::make_idesc(0, 128, N);
+    const uint32_t b_s = tc::smem_addr(bsm);
+    for (int c = 0; c < nchunks; ++c) {
+      const uint32_t s = c % kStages, u = c / kStages;
+      const int e = c / kEpoch, ce = c % kEpoch;
+      // D buffer of this epoch: e & 1 (double-buffered) or 0 (single)
+      const uint32_t db = C::kRegAcc ? uint32_t(e & 1) : 0u;
+      if (ce == 0) {
+        if (C::kRegAcc) {
+          if (e >= 2) tc::mbar_wait(&dempty_bar[db], ((e - 2) >> 1) & 1);
+        } else if (e >= 1) {
+          tc::mbar_wait(&dempty_bar[0], (e - 1) & 1);  // D drained into L
+        }
+        tc::mbar_wait(&bready_bar[e & 1], (e >> 1) & 1);
+      }
+      tc::mbar_wait(&full_bar[s], u & 1);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t bc = b_s + (e & 1) * C::kEpochB + ce * C::kChunkB;
+        const uint64_t bh = tc::make_sdesc(bc, kLBO, kSBO);
+        const uint64_t bl = tc::make_sdesc(bc + C::kBBytes, kLBO, kSBO);
+        const uint32_t a0 = tmem + C::kColA + 4 * kArr * s;
+        const uint32_t dcos = tmem + 2 * N * db, dsin = dcos + N;
+#pragma unroll
+        for (int kk = 0; kk < kChunk / 16; ++kk) {
+          const uint64_t adv = uint64_t(2 * kk) * (kLBO >> 4);
+          const uint32_t acc = (ce > 0 || kk > 0) ? 1u : 0u;
+          tc::mma_f16_ts(dcos, a0 + 8 * kk, bh + adv, idesc, acc);
+          tc::mma_f16_ts(dcos, a0 + 8 * kk, bl + adv, idesc, 1u);
+          tc::mma_f16_ts(dcos, a0 + kArr + 8 * kk, bh + adv, idesc, 1u);
+          tc::mma_f16_ts(dsin, a0 + 2 * kArr + 8 * kk, bh + adv, idesc, acc);
+          tc::mma_f16_ts(dsin, a0 + 2 * kArr + 8 * kk, bl + adv, idesc, 1u);
+          tc::mma_f16_ts(dsin, a0 + 3 * kArr + 8 * kk, bh + adv, idesc, 1u);
+        }
+        tc::mma_commit(&empty_bar[s]);
+        if (ce == kEpoch - 1 || c == nchunks - 1) tc::mma_commit(&dfull_bar[db]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- F staging + drains (4 warps, 128 threads) ----------
+    const int fw = warp - kFWarp0, t = fw * 32 + lane;
+    const float* Fb = F + int64_t(b) * n * d + c0;
+    const uint32_t b_s = tc::smem_addr(bsm);
+    const uint32_t fs_s = b_s + 2 * C::kEpochB;  // staging: [E*64 points][N channels] fp32
+    const float* fstage = reinterpret_cast<const float*>(bsm + 2 * C::kEpochB);
+    const bool vec = (dc == N) && (d % 4 == 0) && (c0 % 4 == 0);
+    // Per epoch: the F block is copied into shared memory, the per-channel
+    // maxima taken, and thread t converts channel (t % N) of point pairs
+    // (one 32-bit word of the K-major B operand each).
+    auto stage_f = [&](int e) {
+      const int64_t q0 = p0 + int64_t(e) * (kEpoch * kChunk);  // first point of the epoch
+      const int ncs = min(kEpoch, nchunks - e * kEpoch);        // chunks of this epoch
+      const int npts = ncs * kChunk;
+      // the epoch's F block -> shared memory (cp.async, all in flight at once;
+      // rows past the cloud and channels past dc are zero-filled)
+      if (vec) {
+        for (int i = t; i < npts * (N / 4); i += 128) {
+          const int p = i / (N / 4), cq = i % (N / 4);
+          const bool ok = q0 + p < n;
+          tc::cp_async16_zf(fs_s + uint32_t(p * N * 4 + cq * 16),
+                            ok ? Fb + (q0 + p) * d + 4 * cq : Fb, ok ? 16u : 0u);
+        }
+      } else {
+        for (int i = t; i < npts * N; i += 128) {
+          const int p = i / N, j = i % N;
+          const bool ok = q0 + p < n && j < dc;
+          tc::cp_async4_zf(fs_s + uint32_t(i * 4), ok ? Fb + (q0 + p) * d + j : Fb, ok ? 4u : 0u);
+        }
+      }
+      tc::cp_async_commit();
+      tc::cp_async_wait<0>();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // per-channel max |F| over the epoch: thread t takes channel t % N, points
+      // t / N, t / N + 128 / N, ...; then the 128 / N partial maxima per channel
+      {
+        const int j = t % N;
+        float mx = 0.0f;
+        for (int p = t / N; p < npts; p += 128 / N) mx = fmaxf(mx, fabsf(fstage[p * N + j]));
+        fmax_part[t] = mx;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (t < N) {
+        float cm = 0.0f;
+        for (int k = t; k < 128; k += N) cm = fmaxf(cm, fmax_part[k]);
+        // scale 2^e_j with max |F_j| 2^e_j in [2^13, 2^14) (1 for a zero or
+        // non-finite channel; |e_j| <= 126 keeps both factors normal, exact)
+        float scale = 1.0f;
+        if (cm > 0.0f && isfinite(cm)) {
+          int ex = 0;
+          frexpf(cm, &ex);  // cm in [2^(ex-1), 2^ex)
+          scale = ldexpf(1.0f, min(126, max(-126, 14 - ex)));
+        }
+        fmax_part[t] = scale;  // read back as the scale below
+        fscale_inv[e & 1][t] = 1.0f / scale;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // scaled, split, stored as 32-bit words: channel j, points (2 pk, 2 pk + 1)
+      const uint32_t eb = b_s + (e & 1) * C::kEpochB;
+      for (int i = t; i < N * (npts / 2); i += 128) {
+        const int j = i % N, pk = i / N, p = 2 * pk;
+        const float sc = fmax_part[j];
+        uint32_t hi, lo;
+        tc::split_f16x2(fstage[p * N + j] * sc, fstage[(p + 1) * N + j] * sc, hi, lo);
+        const int ce = p / kChunk, pc = p % kChunk;
+        const uint32_t off = uint32_t(ce) * C::kChunkB + uint32_t(j >> 3) * kSBO +
+                             uint32_t(pc >> 3) * kLBO + uint32_t(j & 7) * 16 + uint32_t(pc & 7) * 2;
+        tc::st_shared_u32(eb + off, hi);
+        tc::st_shared_u32(eb + off + C::kBBytes, lo);
+      }
+      // the staging block and fmax_part are rewritten by the next epoch
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&bready_bar[e & 1]);
+    };
+    if (nepochs > 0) stage_f(0);
+    if (nepochs > 1) stage_f(1);
+    const uint32_t tl = tmem + lane_field;
+    float* out = partial + (int64_t(b) * ranges + rg) * int64_t(2 * m) * dc;
+    if constexpr (C::kRegAcc) {
+      // N = 16: epochs -> fp32 registers (x 2^-e_j), two D buffers
+      float acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
+      for (int e = 0; e < nepochs; ++e) {
+        const uint32_t buf = e & 1;
+        tc::mbar_wait(&dfull_bar[buf], (e >> 1) & 1);
+        tc::tc_fence_after();
+        float v[32];
+        tc::tmem_ld32(tl + 32 * buf, v);
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&dempty_bar[buf]);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float inv = fscale_inv[buf][j];
+          acc[j] = fmaf(v[j], inv, acc[j]);  // v * 2^-e_j is exact: one rounding
+          acc[16 + j] = fmaf(v[16 + j], inv, acc[16 + j]);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (e + 2 < nepochs) stage_f(e + 2);
+      }
+      if (f < m) {
+        // partial[b][rg][2m][dc]: row 2f = cos, 2f + 1 = sin (interleaved order)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j < dc) {
+            out[int64_t(2 * f) * dc + j] = acc[j];
+            out[int64_t(2 * f + 1) * dc + j] = acc[16 + j];
+          }
+        }
+      }
+    } else {
+      for (int e = 0; e < nepochs; ++e) {
+        const uint32_t buf = e & 1;
+        tc::mbar_wait(&dfull_bar[0], e & 1);
+        tc::tc_fence_after();
+        // L (+)= D x 2^-e_j, 32 columns per round (cos channels, then sin)
+#pragma unroll 1
+        for (int c = 0; c < 2 * N; c += 32) {
+          float v[32], l[32];
+          tc::tmem_ld32(tl + c, v);
+          if (e > 0) tc::tmem_ld32(tl + C::kColL + c, l);
+          uint32_t o[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float inv = fscale_inv[buf][(c + j) % N];
+            o[j] = __float_as_uint(e > 0 ? fmaf(v[j], inv, l[j]) : v[j] * inv);
+          }
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) tc::tmem_st8(tl + C::kColL + c + j, o + j);
+        }
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&dempty_bar[0]);
+        // buffer e & 1 (B and scales) is free once epoch e's MMAs completed
+        // and all four warps have read its scales
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (e + 2 < nepochs) stage_f(e + 2);
+      }
+      // L -> partial[b][rg][2m][dc]: row 2f = cos, 2f + 1 = sin (interleaved)
+#pragma unroll 1
+      for (int c = 0; c < 2 * N; c += 32) {
+        float l[32];
+        if (nepochs > 0) {
+          tc::tc_fence_after();
+          tc::tmem_ld32(tl + C::kColL + c, l);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) l[j] = 0.0f;
+        }
+        if (f < m) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = c + j, ch = col % N, sin_row = col / N;
+            if (ch < dc) out[int64_t(2 * f + sin_row) * dc + ch] = l[j];
+          }
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+template <int NC>
+void launch_nc(dim3 grid, cudaStream_t s, const float* pts16, const float4* omega4, int m,
+               int64_t n, int ranges, const float* F, int d, int c0, int dc, float* partial) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(pass1_tc_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         P1<NC>::kSmem);
+    configured = true;
+  }
+  pass1_tc_kernel<NC><<<grid, kThreads, P1<NC>::kSmem, s>>>(pts16, omega4, m, n, ranges, F, d, c0,
+                                                           dc, partial);
+}
+
+}  // namespace
+
+int pass1_tc_ranges(int m, int64_t n, int batch, int sms) {
+  // ranges of whole chunks: about one CTA per SM
+  const int ftiles = (m + 127) / 128;
+  int64_t ranges = (int64_t(sms) + int64_t(ftiles) * batch - 1) / (int64_t(ftiles) * batch);
+  const int64_t maxr = (n + kChunk - 1) / kChunk;
+  if (ranges > maxr) ranges = maxr;
+  if (ranges < 1) ranges = 1;
+  return int(ranges);
+}
+
+void launch_pass1_tc(const float* pts16, const float4* omega4, int m, int64_t n, int batch,
+                     int ranges, const float* F, int d, int c0, int dc, float* partial,
+                     cudaStream_t s) {
+  LaunchScope L("rfd_pass1_tc", s);
+  const dim3 grid((m + 127) / 128, ranges, batch);
+  switch ((dc + 15) / 16) {
+    case 1: launch_nc<1>(grid, s, pts16, omega4, m, n, ranges, F, d, c0, dc, partial); break;
+    case 2: launch_nc<2>(grid, s, pts16, omega4, m, n, ranges, F, d, c0, dc, partial); break;
+    case 3: launch_nc<3>(grid, s, pts16, omega4, m, n, ranges, F, d, c0, dc, partial); break;
+    default: launch_nc<4>(grid, s, pts16, omega4, m, n, ranges, F, d, c0, dc, partial); break;
+  }
+}
+
+}  // namespace rfd
