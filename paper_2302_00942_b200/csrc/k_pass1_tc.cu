@@ -53,7 +53,8 @@ struct P1 {
   static constexpr int kBBytes = N * kChunk * 2;             // one fp16 B operand
   static constexpr int kChunkB = 2 * kBBytes;                // hi + lo
   static constexpr int kEpochB = kEpoch * kChunkB;
-  static constexpr int kStageF = kEpoch * kChunk * N * 4;    // fp32 F block
+  static constexpr int kRowF = N + 4;                        // staging row stride (floats)
+  static constexpr int kStageF = kEpoch * kChunk * kRowF * 4;  // fp32 F block
   static constexpr int kSmem = 2 * kEpochB + kStageF;
 };
 
@@ -238,14 +239,15 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
         for (int i = t; i < npts * (N / 4); i += 128) {
           const int p = i / (N / 4), cq = i % (N / 4);
           const bool ok = q0 + p < n;
-          tc::cp_async16_zf(fs_s + uint32_t(p * N * 4 + cq * 16),
+          tc::cp_async16_zf(fs_s + uint32_t(p * C::kRowF * 4 + cq * 16),
                             ok ? Fb + (q0 + p) * d + 4 * cq : Fb, ok ? 16u : 0u);
         }
       } else {
         for (int i = t; i < npts * N; i += 128) {
           const int p = i / N, j = i % N;
           const bool ok = q0 + p < n && j < dc;
-          tc::cp_async4_zf(fs_s + uint32_t(i * 4), ok ? Fb + (q0 + p) * d + j : Fb, ok ? 4u : 0u);
+          tc::cp_async4_zf(fs_s + uint32_t((p * C::kRowF + j) * 4), ok ? Fb + (q0 + p) * d + j : Fb,
+                           ok ? 4u : 0u);
         }
       }
       tc::cp_async_commit();
@@ -254,10 +256,17 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
       // per-channel max |F| over the epoch: thread t takes channel t % N, points
       // t / N, t / N + 128 / N, ...; then the 128 / N partial maxima per channel
       {
-        const int j = t % N;
-        float mx = 0.0f;
-        for (int p = t / N; p < npts; p += 128 / N) mx = fmaxf(mx, fabsf(fstage[p * N + j]));
-        fmax_part[t] = mx;
+        const int j = t % N, st = 128 / N;
+        float m0 = 0.0f, m1 = 0.0f, m2 = 0.0f, m3 = 0.0f;  // 4 loads in flight
+        int p = t / N;
+        for (; p + 3 * st < npts; p += 4 * st) {
+          m0 = fmaxf(m0, fabsf(fstage[p * C::kRowF + j]));
+          m1 = fmaxf(m1, fabsf(fstage[(p + st) * C::kRowF + j]));
+          m2 = fmaxf(m2, fabsf(fstage[(p + 2 * st) * C::kRowF + j]));
+          m3 = fmaxf(m3, fabsf(fstage[(p + 3 * st) * C::kRowF + j]));
+        }
+        for (; p < npts; p += st) m0 = fmaxf(m0, fabsf(fstage[p * C::kRowF + j]));
+        fmax_part[t] = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (t < N) {
@@ -275,18 +284,29 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
         fscale_inv[e & 1][t] = 1.0f / scale;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      // scaled, split, stored as 32-bit words: channel j, points (2 pk, 2 pk + 1)
+      // scaled, split, stored as 32-bit words: channel j, points (2 pk, 2 pk + 1).
+      // Lane (jl, pl) = (lane >> 2, lane & 3) takes channel 8 jh + jl and pair
+      // 4 pkh + pl: the 32 lanes hit 32 distinct banks on the B stores (4 jl +
+      // pl) and on the staging reads (row stride N + 4).  Warp fw takes the
+      // channel groups jh = fw, fw + 4, ...
       const uint32_t eb = b_s + (e & 1) * C::kEpochB;
-      for (int i = t; i < N * (npts / 2); i += 128) {
-        const int j = i % N, pk = i / N, p = 2 * pk;
+      const int jl = lane >> 2, pl = lane & 3;
+      for (int jh = fw; jh < N / 8; jh += 4) {
+        const int j = 8 * jh + jl;
         const float sc = fmax_part[j];
-        uint32_t hi, lo;
-        tc::split_f16x2(fstage[p * N + j] * sc, fstage[(p + 1) * N + j] * sc, hi, lo);
-        const int ce = p / kChunk, pc = p % kChunk;
-        const uint32_t off = uint32_t(ce) * C::kChunkB + uint32_t(j >> 3) * kSBO +
-                             uint32_t(pc >> 3) * kLBO + uint32_t(j & 7) * 16 + uint32_t(pc & 7) * 2;
-        tc::st_shared_u32(eb + off, hi);
-        tc::st_shared_u32(eb + off + C::kBBytes, lo);
+        const uint32_t jo = uint32_t(jh) * kSBO + uint32_t(jl) * 16;
+#pragma unroll 4
+        for (int pkh = 0; pkh < npts / 8; ++pkh) {
+          const int p = 8 * pkh + 2 * pl;  // even point of the pair
+          uint32_t hi, lo;
+          tc::split_f16x2(fstage[p * C::kRowF + j] * sc, fstage[(p + 1) * C::kRowF + j] * sc, hi,
+                          lo);
+          const int ce = p / kChunk, pc = p % kChunk;
+          const uint32_t off = uint32_t(ce) * C::kChunkB + jo + uint32_t(pc >> 3) * kLBO +
+                               uint32_t(pc & 7) * 2;
+          tc::st_shared_u32(eb + off, hi);
+          tc::st_shared_u32(eb + off + C::kBBytes, lo);
+        }
       }
       // the staging block and fmax_part are rewritten by the next epoch
       asm volatile("bar.sync 1, 128;" ::: "memory");
