@@ -662,6 +662,329 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
 }
 
 
+// ---------------------------------------------------------------- small m
+// m <= 64 leaves most of the 128 TMEM lanes of a frequency tile idle.  The
+// packed kernel gives each group of 128 / R lanes (R = 4 for m <= 32, 2 for
+// m <= 64) its own *segment* (cloud, point range): lane group g computes the
+// features of segment g's points, and B stacks the R segments' F chunks as
+// 16-column blocks (N = 16 R).  Row block g of D against column block g is
+// segment g's sum; the off-diagonal blocks are never read.  d <= 16.
+template <int R>
+struct PK {
+  static constexpr int N = 16 * R;
+  static constexpr int kStages = R == 4 ? 2 : 3;
+  static constexpr int kEpoch = R == 4 ? 4 : 8;
+  static constexpr uint32_t kColA = 4 * N;                  // D buffers at 0 and 2N
+  static constexpr int kBBytes = N * kChunk * 2;
+  static constexpr int kChunkB = 2 * kBBytes;
+  static constexpr int kEpochB = kEpoch * kChunkB;
+  static constexpr int kStageF = kEpoch * kChunk * N * 4;   // [points][N] fp32
+  static constexpr int kSmem = 2 * kEpochB + kStageF;
+};
+
+template <int R>
+__global__ void __launch_bounds__(kThreads, 1)
+pass1_tc_packed(const float* __restrict__ pts16, const float4* __restrict__ omega4, int m,
+                int64_t n, int batch, int ranges, const float* __restrict__ F, int d, int c0,
+                int dc, float* __restrict__ partial) {
+  using C = PK<R>;
+  constexpr int N = C::N, kStages = C::kStages, kEpoch = C::kEpoch, kGroupsPerSeg = 4 / R;
+  extern __shared__ __align__(1024) unsigned char bsm[];
+  __shared__ uint64_t full_bar[kStages], empty_bar[kStages], dfull_bar[2], dempty_bar[2],
+      bready_bar[2];
+  __shared__ uint32_t tmem_sh;
+  __shared__ __align__(16) float xbuf[3][kProducerWarps][48];
+  __shared__ float fscale[N];
+  __shared__ float fscale_inv[2][N];
+  __shared__ float fmax_part[128];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, lg = warp & 3;
+  const int64_t cpc = (n + kChunk - 1) / kChunk, gpc = (n + 15) / 16;
+  const int64_t nseg = int64_t(batch) * ranges;
+  // segment g of this CTA: cloud sb[g], chunks [sc0[g], sc0[g] + snc[g])
+  // (shared memory: every role reads them, registers are scarce)
+  __shared__ int sb[R], snc[R];
+  __shared__ long long sc0[R];
+  int nchunks = 0;
+#pragma unroll
+  for (int g = 0; g < R; ++g) {
+    const int64_t sg = int64_t(blockIdx.x) * R + g;
+    int nc = 0;
+    if (sg < nseg) {
+      const int rg = int(sg % ranges);
+      const int64_t a = cpc * rg / ranges;
+      nc = int(cpc * (rg + 1) / ranges - a);
+      if (tid == 0) {
+        sb[g] = int(sg / ranges);
+        sc0[g] = a;
+      }
+    } else if (tid == 0) {
+      sb[g] = 0;
+      sc0[g] = 0;
+    }
+    if (tid == 0) snc[g] = nc;
+    nchunks = max(nchunks, nc);
+  }
+  const int nepochs = (nchunks + kEpoch - 1) / kEpoch;
+
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&full_bar[s], kProducerWarps);
+      tc::mbar_init(&empty_bar[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&dfull_bar[i], 1);
+      tc::mbar_init(&dempty_bar[i], 4);
+      tc::mbar_init(&bready_bar[i], 4);
+    }
+    tc::mbar_fence_init();
+  }
+  // B buffers and the staging block start at zero: only the R dc real
+  // columns are ever written (the others stay zero for the whole kernel)
+  for (int i = tid; i < C::kSmem / 16; i += kThreads)
+    reinterpret_cast<float4*>(bsm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  tc::fence_proxy_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+  const uint32_t lane_field = uint32_t(lg * 32) << 16;
+  const int g_me = lg / kGroupsPerSeg;                          // this lane group's segment
+  const int f = (lg % kGroupsPerSeg) * 32 + lane;               // this lane's frequency
+
+  if (warp < kProducerWarps) {
+    // ---------------- producers (as pass1_tc_kernel16), per segment -------
+    const int q = warp >> 2;
+    const float4 w = (f < m) ? omega4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float2 wx = make_float2(w.x, w.x), wy = make_float2(w.y, w.y), wz = make_float2(w.z, w.z);
+    const float* cloud16 = pts16 + int64_t(sb[g_me]) * gpc * 48;
+    const float* xsrc = cloud16 + ((sc0[g_me] * (kChunk / 16) + q) * 48 + 4 * lane);
+    const float* xlast = cloud16 + ((gpc - 1) * 48 + 4 * lane);
+    const int64_t xrem0 = gpc - (sc0[g_me] * (kChunk / 16) + q);
+    int xrem = int(xrem0 > 0x7fffffff ? 0x7fffffff : xrem0);
+    constexpr uint32_t kRing = kProducerWarps * 48 * 4;
+    const uint32_t x_s = tc::smem_addr(&xbuf[0][warp][0]);
+    uint32_t xw = 0;
+    auto load_x = [&](bool valid) {
+      if (lane < 12 && valid) tc::cp_async16(x_s + xw * kRing + 16 * lane, xrem > 0 ? xsrc : xlast);
+      tc::cp_async_commit();
+      xsrc += 48 * (kChunk / 16);
+      xrem -= kChunk / 16;
+      xw = (xw == 2) ? 0 : xw + 1;
+    };
+    load_x(nchunks > 0);
+    load_x(nchunks > 1);
+    const uint32_t empty_s = tc::smem_addr(&empty_bar[0]), full_s = tc::smem_addr(&full_bar[0]);
+    uint32_t s = 0, u = 0, xr = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      load_x(c + 2 < nchunks);
+      if (u >= 1) tc::mbar_wait(empty_s + 8 * s, (u - 1) & 1);
+      // chunks past the segment (or the cloud) repeat finite points; their
+      // F rows are zero
+      tc::cp_async_wait<2>();
+      __syncwarp();
+      const float* xs = &xbuf[0][warp][0] + xr * (kProducerWarps * 48);
+      xr = (xr == 2) ? 0 : xr + 1;
+      const uint32_t a = tmem + lane_field + C::kColA + 4 * kArr * s + 8 * q;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float cs[8], sn[8];
+#pragma unroll
+        for (int j = 0; j < 8; j += 4) {
+          const float4 X = *reinterpret_cast<const float4*>(xs + 8 * h + j);
+          const float4 Y = *reinterpret_cast<const float4*>(xs + 16 + 8 * h + j);
+          const float4 Z = *reinterpret_cast<const float4*>(xs + 32 + 8 * h + j);
+          float2 t0 = __fmul2_rn(wx, make_float2(X.x, X.y));
+          float2 t1 = __fmul2_rn(wx, make_float2(X.z, X.w));
+          t0 = __ffma2_rn(wy, make_float2(Y.x, Y.y), t0);
+          t1 = __ffma2_rn(wy, make_float2(Y.z, Y.w), t1);
+          t0 = __ffma2_rn(wz, make_float2(Z.x, Z.y), t0);
+          t1 = __ffma2_rn(wz, make_float2(Z.z, Z.w), t1);
+          __sincosf(t0.x, &sn[j], &cs[j]);
+          __sincosf(t0.y, &sn[j + 1], &cs[j + 1]);
+          __sincosf(t1.x, &sn[j + 2], &cs[j + 2]);
+          __sincosf(t1.y, &sn[j + 3], &cs[j + 3]);
+        }
+        uint32_t chi[4], clo[4], shi[4], slo[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          tc::split_f16x2(cs[2 * j], cs[2 * j + 1], chi[j], clo[j]);
+          tc::split_f16x2(sn[2 * j], sn[2 * j + 1], shi[j], slo[j]);
+        }
+        const uint32_t ah = a + 4 * h;
+        tc::tmem_st4(ah, chi[0], chi[1], chi[2], chi[3]);
+        tc::tmem_st4(ah + kArr, clo[0], clo[1], clo[2], clo[3]);
+        tc::tmem_st4(ah + 2 * kArr, shi[0], shi[1], shi[2], shi[3]);
+        tc::tmem_st4(ah + 3 * kArr, slo[0], slo[1], slo[2], slo[3]);
+      }
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(full_s + 8 * s);
+      if (++s == kStages) {
+        s = 0;
+        ++u;
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ---------------- MMA issue: N = 16 R, two D buffers -------------------
+    const uint32_t idesc = tc::make_idesc(0, 128, N);
+    const uint32_t b_s = tc::smem_addr(bsm);
+    for (int c = 0; c < nchunks; ++c) {
+      const uint32_t s = c % kStages, u = c / kStages;
+      const int e = c / kEpoch, ce = c % kEpoch;
+      const uint32_t buf = e & 1;
+      if (ce == 0) {
+        if (e >= 2) tc::mbar_wait(&dempty_bar[buf], ((e - 2) >> 1) & 1);
+        tc::mbar_wait(&bready_bar[buf], (e >> 1) & 1);
+      }
+      tc::mbar_wait(&full_bar[s], u & 1);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t bc = b_s + buf * C::kEpochB + ce * C::kChunkB;
+        const uint64_t bh = tc::make_sdesc(bc, kLBO, kSBO);
+        const uint64_t bl = tc::make_sdesc(bc + C::kBBytes, kLBO, kSBO);
+        const uint32_t a0 = tmem + C::kColA + 4 * kArr * s;
+        const uint32_t dcos = tmem + 2 * N * buf, dsin = dcos + N;
+#pragma unroll
+        for (int kk = 0; kk < kChunk / 16; ++kk) {
+          const uint64_t adv = uint64_t(2 * kk) * (kLBO >> 4);
+          const uint32_t acc = (ce > 0 || kk > 0) ? 1u : 0u;
+          tc::mma_f16_ts(dcos, a0 + 8 * kk, bh + adv, idesc, acc);
+          tc::mma_f16_ts(dcos, a0 + 8 * kk, bl + adv, idesc, 1u);
+          tc::mma_f16_ts(dcos, a0 + kArr + 8 * kk, bh + adv, idesc, 1u);
+          tc::mma_f16_ts(dsin, a0 + 2 * kArr + 8 * kk, bh + adv, idesc, acc);
+          tc::mma_f16_ts(dsin, a0 + 2 * kArr + 8 * kk, bl + adv, idesc, 1u);
+          tc::mma_f16_ts(dsin, a0 + 3 * kArr + 8 * kk, bh + adv, idesc, 1u);
+        }
+        tc::mma_commit(&empty_bar[s]);
+        if (ce == kEpoch - 1 || c == nchunks - 1) tc::mma_commit(&dfull_bar[buf]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- F staging + drains (4 warps, 128 threads) ----------
+    const int fw = warp - kFWarp0, t = fw * 32 + lane;
+    const uint32_t b_s = tc::smem_addr(bsm);
+    const uint32_t fs_s = b_s + 2 * C::kEpochB;  // staging [E*64 points][N] fp32
+    const float* fstage = reinterpret_cast<const float*>(bsm + 2 * C::kEpochB);
+    const int ncol = R * dc;                     // real columns: 16 g + j, j < dc
+    auto stage_f = [&](int e) {
+      const int npts = min(kEpoch, nchunks - e * kEpoch) * kChunk;
+      for (int i = t; i < npts * ncol; i += 128) {
+        const int p = i / ncol, cc = i % ncol, g = cc / dc, j = cc % dc;
+        const int64_t cl = int64_t(e) * kEpoch * kChunk + p;  // point of segment g
+        const int64_t pp = sc0[g] * kChunk + cl;
+        const bool ok = cl < int64_t(snc[g]) * kChunk && pp < n;
+        const float* src = F + (int64_t(sb[g]) * n + (ok ? pp : 0)) * d + c0 + j;
+        tc::cp_async4_zf(fs_s + uint32_t((p * N + 16 * g + j) * 4), src, ok ? 4u : 0u);
+      }
+      tc::cp_async_commit();
+      tc::cp_async_wait<0>();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // per-column max |F| over the epoch (real columns; the rest keep scale 1)
+      {
+        const int cc = t % ncol, g = cc / dc, j = cc % dc, st = 128 / ncol;
+        float mx = 0.0f;
+        if (t < st * ncol)
+          for (int p = t / ncol; p < npts; p += st) mx = fmaxf(mx, fabsf(fstage[p * N + 16 * g + j]));
+        fmax_part[t] = mx;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (t < N) {
+        const int g = t / 16, j = t % 16;
+        float scale = 1.0f;
+        if (j < dc) {
+          const int cc = g * dc + j, st = 128 / ncol;
+          float cm = 0.0f;
+          for (int k = cc; k < st * ncol; k += ncol) cm = fmaxf(cm, fmax_part[k]);
+          if (cm > 0.0f && isfinite(cm)) {
+            int ex = 0;
+            frexpf(cm, &ex);
+            scale = ldexpf(1.0f, min(126, max(-126, 14 - ex)));
+          }
+        }
+        fscale[t] = scale;
+        fscale_inv[e & 1][t] = 1.0f / scale;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const uint32_t eb = b_s + (e & 1) * C::kEpochB;
+      for (int i = t; i < ncol * (npts / 2); i += 128) {
+        const int cc = i % ncol, pk = i / ncol, p = 2 * pk;
+        const int col = 16 * (cc / dc) + cc % dc;
+        const float sc = fscale[col];
+        uint32_t hi, lo;
+        tc::split_f16x2(fstage[p * N + col] * sc, fstage[(p + 1) * N + col] * sc, hi, lo);
+        const int ce = p / kChunk, pc = p % kChunk;
+        const uint32_t off = uint32_t(ce) * C::kChunkB + uint32_t(col >> 3) * kSBO +
+                             uint32_t(pc >> 3) * kLBO + uint32_t(col & 7) * 16 + uint32_t(pc & 7) * 2;
+        tc::st_shared_u32(eb + off, hi);
+        tc::st_shared_u32(eb + off + C::kBBytes, lo);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&bready_bar[e & 1]);
+    };
+    if (nepochs > 0) stage_f(0);
+    if (nepochs > 1) stage_f(1);
+    // drains: lane group lg reads its segment's blocks (cos 16 g, sin N + 16 g)
+    float acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
+    const uint32_t tl = tmem + lane_field + 16 * g_me;
+    for (int e = 0; e < nepochs; ++e) {
+      const uint32_t buf = e & 1;
+      tc::mbar_wait(&dfull_bar[buf], (e >> 1) & 1);
+      tc::tc_fence_after();
+      float vc[16], vs[16];
+      tc::tmem_ld16(tl + 2 * N * buf, vc);
+      tc::tmem_ld16(tl + 2 * N * buf + N, vs);
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&dempty_bar[buf]);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float inv = fscale_inv[buf][16 * g_me + j];
+        acc[j] = fmaf(vc[j], inv, acc[j]);
+        acc[16 + j] = fmaf(vs[j], inv, acc[16 + j]);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (e + 2 < nepochs) stage_f(e + 2);
+    }
+    const int64_t sg = int64_t(blockIdx.x) * R + g_me;
+    if (f < m && sg < nseg) {
+      const int b = int(sg / ranges), rg = int(sg % ranges);
+      float* out = partial + (int64_t(b) * ranges + rg) * int64_t(2 * m) * dc;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < dc) {
+          out[int64_t(2 * f) * dc + j] = acc[j];
+          out[int64_t(2 * f + 1) * dc + j] = acc[16 + j];
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+template <int R>
+void launch_packed(cudaStream_t s, const float* pts16, const float4* omega4, int m, int64_t n,
+                   int batch, int ranges, const float* F, int d, int c0, int dc, float* partial) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(pass1_tc_packed<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         PK<R>::kSmem);
+    configured = true;
+  }
+  const int64_t ctas = (int64_t(batch) * ranges + R - 1) / R;
+  pass1_tc_packed<R><<<unsigned(ctas), kThreads, PK<R>::kSmem, s>>>(pts16, omega4, m, n, batch,
+                                                                   ranges, F, d, c0, dc, partial);
+}
+
 template <int NC>
 void launch_nc(dim3 grid, cudaStream_t s, const float* pts16, const float4* omega4, int m,
                int64_t n, int ranges, const float* F, int d, int c0, int dc, float* partial) {
@@ -677,10 +1000,22 @@ void launch_nc(dim3 grid, cudaStream_t s, const float* pts16, const float4* omeg
 
 }  // namespace
 
+// Segments per CTA of the packed small-m kernel: R = 4 (m <= 32) or 2
+// (m <= 64) when there are enough chunks to keep every SM busy with R of them
+// (>= 2 per segment); otherwise 1 (one CTA per frequency tile and range).
+int pass1_pack(int m, int64_t n, int batch, int sms) {
+  const int R = m <= 32 ? 4 : (m <= 64 ? 2 : 1);
+  const int64_t chunks = int64_t(batch) * ((n + kChunk - 1) / kChunk);
+  return (R > 1 && chunks >= int64_t(sms) * R * 2) ? R : 1;
+}
+
 int pass1_tc_ranges(int m, int64_t n, int batch, int sms) {
-  // ranges of whole chunks: about one CTA per SM
+  // ranges of whole chunks: about one CTA per SM (packed: R segments per CTA)
   const int ftiles = (m + 127) / 128;
-  int64_t ranges = (int64_t(sms) + int64_t(ftiles) * batch - 1) / (int64_t(ftiles) * batch);
+  const int R = pass1_pack(m, n, batch, sms);
+  int64_t ranges = (R > 1)
+                       ? int64_t(sms) * R / batch
+                       : (int64_t(sms) + int64_t(ftiles) * batch - 1) / (int64_t(ftiles) * batch);
   const int64_t maxr = (n + kChunk - 1) / kChunk;
   if (ranges > maxr) ranges = maxr;
   if (ranges < 1) ranges = 1;
@@ -688,10 +1023,18 @@ int pass1_tc_ranges(int m, int64_t n, int batch, int sms) {
 }
 
 void launch_pass1_tc(const float* pts16, const float4* omega4, int m, int64_t n, int batch,
-                     int ranges, const float* F, int d, int c0, int dc, float* partial,
+                     int sms, int ranges, const float* F, int d, int c0, int dc, float* partial,
                      cudaStream_t s) {
   LaunchScope L("rfd_pass1_tc", s);
   const dim3 grid((m + 127) / 128, ranges, batch);
+  const int R = pass1_pack(m, n, batch, sms);
+  if (dc <= 16 && R > 1) {  // packed segments (small m)
+    if (R == 4)
+      launch_packed<4>(s, pts16, omega4, m, n, batch, ranges, F, d, c0, dc, partial);
+    else
+      launch_packed<2>(s, pts16, omega4, m, n, batch, ranges, F, d, c0, dc, partial);
+    return;
+  }
   switch ((dc + 15) / 16) {
     case 1: {
       static bool configured = false;

@@ -496,7 +496,7 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
                         p->s_partial, st);
       rfd::launch_reduce_S(p->s_partial, p->m, p->batch, p->pg.chunks, d, c0, dc, p->S, st);
     } else {
-      rfd::launch_pass1_tc(p->pts16, p->omega_rad4, p->m, p->n, p->batch, ranges, F, d, c0, dc,
+      rfd::launch_pass1_tc(p->pts16, p->omega_rad4, p->m, p->n, p->batch, p->sms, ranges, F, d, c0, dc,
                            p->s_partial, st);
       rfd::launch_reduce_S(p->s_partial, p->m, p->batch, ranges, d, c0, dc, p->S, st);
     }

@@ -122,7 +122,7 @@ void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, 
 // Tensor-core pass 1 (k_pass1_tc.cu): partial[b][range][2m][dc].
 int pass1_tc_ranges(int m, int64_t n, int batch, int sms);
 void launch_pass1_tc(const float* pts16, const float4* omega4, int m, int64_t n, int batch,
-                     int ranges, const float* F, int d, int c0, int dc, float* partial,
+                     int sms, int ranges, const float* F, int d, int c0, int dc, float* partial,
                      cudaStream_t s);
 
 }  // namespace rfd
