@@ -29,7 +29,6 @@ constexpr int kMmaWarp = 16;
 constexpr int kEpiWarp0 = 17;                 // warps 17..20: epilogue
 constexpr int kThreads = 21 * 32;
 constexpr int kTile = 128;      // points per tile (= TMEM lanes)
-constexpr int kChunkF = 128;    // features per chunk (64 frequencies)
 constexpr int kStages = 3;
 // TMEM columns: accumulators [0, nw) and [nw, 2 nw) (nw = the launch's column
 // width, a multiple of 16, <= 64); stage s: hi at 2 nw + 128 s (64 cols = 128
@@ -37,10 +36,18 @@ constexpr int kStages = 3;
 constexpr uint32_t kLBO = 128;
 constexpr size_t kPass2MaxSmem = 200 * 1024;
 
+// KF = features per K-chunk: 128 (64 frequencies) or, for m <= 32, 64 (32
+// frequencies: no chunk half filled with padding frequencies).
+template <int KF>
 __global__ void __launch_bounds__(kThreads, 1)
 pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4, int m, int64_t n,
                 int batch, const float* __restrict__ Y, const float* F, float* out, int d, int c0,
-                int dc, int nw) {
+                int dc, int nw, const float* __restrict__ part, int ranges,
+                const double* __restrict__ C, double* __restrict__ S_out, float* __restrict__ Y_out) {
+  // part != nullptr: fused a7 -- each CTA sums the cloud's pass-1 partials
+  // (S, fp64, fixed order) and forms Y = C^ S itself (small r: no separate
+  // reduce / apply launches); the CTA holding the cloud's first tile also
+  // writes S and Y to the plan (export).
   // F and out may alias (in place): each epilogue thread reads F_i before
   // writing out_i.
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -50,15 +57,20 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int lg = warp & 3;
-  const int nch = (m + 63) / 64;       // chunks of 64 frequencies
-  const int kpad = nch * kChunkF;      // padded feature count
+  constexpr int kChunkF = KF, kFpc = KF / 2;  // features / frequencies per chunk
+  const int nch = (m + kFpc - 1) / kFpc;       // chunks
+  const int kpad = nch * kChunkF;              // padded feature count
   const uint32_t sbo = uint32_t(kpad / 8) * 128;
   unsigned char* yb = smem;                          // B hi: 16 x kpad fp16
   unsigned char* yl = smem + nw * kpad * 2;          // B lo
   // omega (radians) as SoA: x components of all frequencies, then y, then z
   float* ox = reinterpret_cast<float*>(smem + 2 * nw * kpad * 2);
-  float* oy = ox + nch * 64;
-  float* oz = oy + nch * 64;
+  float* oy = ox + nch * kFpc;
+  float* oz = oy + nch * kFpc;
+  // fused a7: S_b (fp64 [2m][dc]) and Y_b (fp32 [2m][dc]) after the omegas
+  double* Ss = reinterpret_cast<double*>(oz + nch * kFpc);
+  float* Ys = reinterpret_cast<float*>(Ss + 2 * m * dc);
+  const bool fuse = part != nullptr;
   __shared__ unsigned int ymax_bits[64];
   __shared__ float yscale_inv[64];
   const uint32_t kColA = 2 * nw;
@@ -77,7 +89,7 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
     tc::mbar_init(&yready_bar, 1);
     tc::mbar_fence_init();
   }
-  for (int k = tid; k < nch * 64; k += kThreads) {
+  for (int k = tid; k < nch * kFpc; k += kThreads) {
     const float4 w = (k < m) ? omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
     ox[k] = w.x;
     oy[k] = w.y;
@@ -98,15 +110,62 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   // Y_b^T as the B operand; the CTA's tiles are contiguous, so the cloud
   // changes rarely.  (Re)loads run under a full-CTA barrier after every MMA
   // reading the old Y has completed.
-  auto load_y = [&](int b) {
+  auto load_y = [&](int b, bool owner) {
+    const int r = 2 * m;
     const float* Yb = Y + int64_t(b) * 2 * m * d;
+    int ystride = d, ycol = c0;  // Y element (a, j) at Yb[a * ystride + ycol + j]
+    if (fuse) {
+      // S = sum over the ranges' partials, in range order (fp64)
+      const float* pb = part + int64_t(b) * ranges * r * dc;
+      for (int e = tid; e < r * dc; e += kThreads) {
+        double acc = 0.0;
+        for (int rg = 0; rg < ranges; ++rg) acc += double(__ldg(pb + int64_t(rg) * r * dc + e));
+        Ss[e] = acc;
+      }
+      __syncthreads();
+      // Y = C^ S: a warp per row a, lanes over k, butterfly per column
+      for (int a = warp; a < r; a += kThreads / 32) {
+        const double* Ca = C + (int64_t(b) * r + a) * r;
+        for (int j0 = 0; j0 < dc; j0 += 16) {  // column groups of 16
+          double acc[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+          for (int k = lane; k < r; k += 32) {
+            const double cv = __ldg(Ca + k);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j0 + j < dc) acc[j] = fma(cv, Ss[k * dc + j0 + j], acc[j]);
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j0 + j < dc) {
+              double x = acc[j];
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+              if (lane == 0) Ys[a * dc + j0 + j] = float(x);
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (owner)
+        for (int e = tid; e < r * dc; e += kThreads) {
+          const int a = e / dc, j = e - (e / dc) * dc;
+          S_out[(int64_t(b) * r + a) * d + c0 + j] = Ss[e];
+          Y_out[(int64_t(b) * r + a) * d + c0 + j] = Ys[e];
+        }
+      Yb = Ys;
+      ystride = dc;
+      ycol = 0;
+    }
     // per-channel power-of-two scale: max |Y_j| 2^e_j in [2^13, 2^14); one warp
     // per channel, lanes over the 2m rows (no atomics, no index division)
     if (tid < nw) ymax_bits[tid] = 0u;
     __syncthreads();
     for (int j = warp; j < dc; j += kThreads / 32) {
       float mx = 0.0f;
-      for (int a = lane; a < 2 * m; a += 32) mx = fmaxf(mx, fabsf(Yb[int64_t(a) * d + c0 + j]));
+      for (int a = lane; a < 2 * m; a += 32)
+        mx = fmaxf(mx, fabsf(Yb[int64_t(a) * ystride + ycol + j]));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       if (lane == 0) ymax_bits[j] = __float_as_uint(mx);
@@ -129,7 +188,7 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
     for (int a = warp; a < kpad; a += kThreads / 32) {
       for (int j = lane; j < nw; j += 32) {
         const float val = (a < 2 * m && j < dc)
-                              ? Yb[int64_t(a) * d + c0 + j] * __uint_as_float(ymax_bits[j])
+                              ? Yb[int64_t(a) * ystride + ycol + j] * __uint_as_float(ymax_bits[j])
                               : 0.0f;
         const __half h = __float2half_rn(val);
         const __half l = __float2half_rn(val - __half2float(h));
@@ -163,7 +222,7 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
     if (b != cur_b) {
       if (g > 0) tc::mbar_wait(&empty_bar[(g - 1) % kStages], ((g - 1) / kStages) & 1);
       __syncthreads();
-      load_y(b);
+      load_y(b, (tile % tpc) == 0);  // this CTA holds the cloud's first tile
       __syncthreads();
       cur_b = b;
     }
@@ -181,11 +240,11 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       for (int c = 0; c < nch; ++c) {
         const uint32_t gg = g + c, s = gg % kStages, u = gg / kStages;
         if (u >= 1) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
-        const uint32_t acol = tmem + lane_field + kColA + 128 * s + 16 * q;
+        const uint32_t acol = tmem + lane_field + kColA + 128 * s + (KF / 8) * q;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {  // two halves of 8 frequencies (register pressure)
+        for (int h = 0; h < KF / 64; ++h) {  // halves of 8 frequencies (register pressure)
           float v[16];
-          const int f0 = 64 * c + 16 * q + 8 * h;
+          const int f0 = kFpc * c + (kFpc / 4) * q + 8 * h;
           // Frequencies beyond m (zero omega) meet zero rows of Y^T: no masking.
           // omega . x for 2 frequencies per packed FP32 instruction, in the
           // operation order of fmaf(wz, z, fmaf(wy, y, wx * x)).
@@ -210,7 +269,7 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
 #pragma unroll
           for (int j = 0; j < 8; ++j) tc::split_f16x2(v[2 * j], v[2 * j + 1], hi[j], lo[j]);
           tc::tmem_st8(acol + 8 * h, hi);
-          tc::tmem_st8(acol + 64 + 8 * h, lo);
+          tc::tmem_st8(acol + KF / 2 + 8 * h, lo);
         }
         tc::tmem_st_wait();
         tc::tc_fence_before();
@@ -237,7 +296,7 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
             const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
             tc::mma_f16_ts(dcol, a0 + 8 * kk, bh0 + adv, idesc, acc);
             tc::mma_f16_ts(dcol, a0 + 8 * kk, bl0 + adv, idesc, 1u);
-            tc::mma_f16_ts(dcol, a0 + 64 + 8 * kk, bh0 + adv, idesc, 1u);
+            tc::mma_f16_ts(dcol, a0 + KF / 2 + 8 * kk, bh0 + adv, idesc, 1u);
           }
           tc::mma_commit(&empty_bar[s]);
           if (c == nch - 1) tc::mma_commit(&dfull_bar[buf]);
@@ -304,35 +363,44 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
 
 }  // namespace
 
-size_t pass2_tc_smem(int m, int nw) {
-  const int nch = (m + 63) / 64;
-  return size_t(2) * nw * nch * kChunkF * 2 + size_t(nch * 64) * 3 * sizeof(float);
+size_t pass2_tc_smem(int m, int nw, int fuse_dc) {
+  const int fpc = m <= 32 ? 32 : 64;  // frequencies per chunk (KF / 2)
+  const int nch = (m + fpc - 1) / fpc;
+  return size_t(2) * nw * nch * (2 * fpc) * 2 + size_t(nch * fpc) * 3 * sizeof(float) +
+         size_t(2 * m) * fuse_dc * (sizeof(double) + sizeof(float));
 }
 
 int pass2_tc_width(int m) {
   // widest column chunk (multiple of 16, <= 64) whose Y^T operand fits
   for (int nw = 64; nw > 16; nw -= 16)
-    if (pass2_tc_smem(m, nw) <= kPass2MaxSmem) return nw;
+    if (pass2_tc_smem(m, nw, 0) <= kPass2MaxSmem) return nw;
   return 16;
 }
 
 void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
                      int sms, const float* Y, const float* F, float* out, int d, int c0, int dc,
+                     const float* part, int ranges, const double* C, double* S, float* Yw,
                      cudaStream_t s) {
   LaunchScope L("rfd_pass2_tc", s);
   const int nw = (dc + 15) / 16 * 16;  // MMA N: the chunk's columns, padded to 16
-  const size_t smem = pass2_tc_smem(m, nw);
+  const size_t smem = pass2_tc_smem(m, nw, part ? dc : 0);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(pass2_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(pass2_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kPass2MaxSmem));
+    cudaFuncSetAttribute(pass2_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kPass2MaxSmem));
     configured = true;
   }
   const int64_t ntiles = ((n + kTile - 1) / kTile) * batch;
   int64_t grid = int64_t(sms);  // one CTA per SM (full TMEM)
   if (grid > ntiles) grid = ntiles;
-  pass2_tc_kernel<<<unsigned(grid), kThreads, smem, s>>>(pts, omega4, m, n, batch, Y, F, out, d,
-                                                         c0, dc, nw);
+  if (m <= 32)
+    pass2_tc_kernel<64><<<unsigned(grid), kThreads, smem, s>>>(
+        pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part, ranges, C, S, Yw);
+  else
+    pass2_tc_kernel<128><<<unsigned(grid), kThreads, smem, s>>>(
+        pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part, ranges, C, S, Yw);
 }
 
 }  // namespace rfd

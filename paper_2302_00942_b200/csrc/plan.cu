@@ -485,7 +485,16 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
     const char* e = getenv("RFD_PASS1");
     return e && strcmp(e, "simt") == 0;
   }();
+  static const bool p2_simt = [] {
+    const char* e = getenv("RFD_PASS2");
+    return e && strcmp(e, "simt") == 0;
+  }();
   const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
+  // Small r (<= 128) with d in one chunk and few partials: a7 (S reduction and
+  // Y = C^ S) runs fused in pass 2's prologue -- two launches fewer per call
+  // (every pass-2 CTA re-reduces its cloud's partials, hence the bound).
+  const bool fuse = !p1_simt && !p2_simt && p->r <= 128 && d <= 64 &&
+                    int64_t(ranges) * p->r * d <= 16384;
   // pass 1 on the tensor cores takes up to 64 columns per launch (MMA N = the
   // chunk's columns): the features are regenerated once per chunk (NEXT-2)
   const int w1 = p1_simt ? 16 : 64;
@@ -496,18 +505,14 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
                         p->s_partial, st);
       rfd::launch_reduce_S(p->s_partial, p->m, p->batch, p->pg.chunks, d, c0, dc, p->S, st);
     } else {
-      rfd::launch_pass1_tc(p->pts16, p->omega_rad4, p->m, p->n, p->batch, p->sms, ranges, F, d, c0, dc,
-                           p->s_partial, st);
-      rfd::launch_reduce_S(p->s_partial, p->m, p->batch, ranges, d, c0, dc, p->S, st);
+      rfd::launch_pass1_tc(p->pts16, p->omega_rad4, p->m, p->n, p->batch, p->sms, ranges, F, d,
+                           c0, dc, p->s_partial, st);
+      if (!fuse) rfd::launch_reduce_S(p->s_partial, p->m, p->batch, ranges, d, c0, dc, p->S, st);
     }
   }
-  rfd::launch_core_apply(p->C, p->S, p->m, p->batch, d, p->Y, st);
+  if (!fuse) rfd::launch_core_apply(p->C, p->S, p->m, p->batch, d, p->Y, st);
   // a8 on the tensor cores unless the SIMT kernel is requested (RFD_PASS2=simt,
   // A/B comparison only).
-  static const bool p2_simt = [] {
-    const char* e = getenv("RFD_PASS2");
-    return e && strcmp(e, "simt") == 0;
-  }();
   // pass 2 on the tensor cores takes up to 64 columns per launch (MMA N = the
   // chunk's columns): the features are regenerated once per chunk (NEXT-2)
   const int w2 = p2_simt ? 16 : rfd::pass2_tc_width(p->m);
@@ -517,8 +522,8 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
       rfd::launch_pass2(p->pts, p->omega4, p->m, p->n, p->batch, p->pg, p->Y, F, out, d, c0, dc,
                         st);
     else
-      rfd::launch_pass2_tc(p->pts, p->omega_rad4, p->m, p->n, p->batch, p->sms, p->Y, F, out, d, c0,
-                           dc, st);
+      rfd::launch_pass2_tc(p->pts, p->omega_rad4, p->m, p->n, p->batch, p->sms, p->Y, F, out, d,
+                           c0, dc, fuse ? p->s_partial : nullptr, ranges, p->C, p->S, p->Y, st);
   }
   RFD_CUDA(cudaGetLastError());
   p->last_d = d;

@@ -112,11 +112,14 @@ void launch_pass2(const float4* pts, const float4* omega4, int m, int64_t n,
                   float* out, int d, int c0, int dc, cudaStream_t s);
 
 // Tensor-core pass 2 (k_pass2_tc.cu): dc <= 16 columns per launch.
-size_t pass2_tc_smem(int m, int nw);
+size_t pass2_tc_smem(int m, int nw, int fuse_dc);
 // widest column chunk one pass-2 launch takes (16..64) for m frequencies
 int pass2_tc_width(int m);
+// part != nullptr: fused a7 (each CTA reduces the pass-1 partials of its
+// cloud and forms Y = C^ S; small r, d within one pass-1 chunk).
 void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
                      int sms, const float* Y, const float* F, float* out, int d, int c0, int dc,
+                     const float* part, int ranges, const double* C, double* S, float* Yw,
                      cudaStream_t s);
 
 // Tensor-core pass 1 (k_pass1_tc.cu): partial[b][range][2m][dc].

@@ -376,7 +376,16 @@ def test_launch_counter_and_profiler():
     prof = rfd.profile_read()
     rfd.profile_enable(False)
     assert rfd.launch_count() > c0
-    assert {"rfd_reduce_S", "rfd_core_apply"} <= set(prof)
+    # cfg 1 (r = 32): a7 runs fused in pass 2 (no separate reduce / apply)
+    assert not ({"rfd_reduce_S", "rfd_core_apply"} & set(prof))
     assert {"rfd_pass1", "rfd_pass1_tc"} & set(prof)
     assert {"rfd_pass2", "rfd_pass2_tc"} & set(prof)
     assert all(v[1] > 0 for v in prof.values())
+    # r = 256 (cfg 4's m): the separate a7 kernels
+    x4 = _sphere(4000, 3)
+    plan4 = rfd.Plan(torch.from_numpy(x4).cuda(), 0.05, -0.8, 128, 3)
+    rfd.profile_enable(True)
+    plan4.integrate(torch.from_numpy(np.ones((4000, 3), np.float32)).cuda())
+    prof4 = rfd.profile_read()
+    rfd.profile_enable(False)
+    assert {"rfd_reduce_S", "rfd_core_apply", "rfd_pass1_tc", "rfd_pass2_tc"} <= set(prof4)
