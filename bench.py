@@ -289,7 +289,7 @@ def run_rfd(args, rank, world, local, pg):
     # The call reads back the scaling exponent and an overflow flag, so its
     # time includes two device->host round trips.
     rts = []
-    for i in range(args.warmup + args.steps):
+    for i in range(0 if args.no_configs else args.warmup + args.steps):
         torch.cuda.synchronize()
         ev0.record(stream)
         plan.reparam(p["eps"] * (1.0 + 0.25 * (i % 2)), p["lam"])
@@ -299,7 +299,7 @@ def run_rfd(args, rank, world, local, pg):
             rts.append(ev0.elapsed_time(ev1))
     # ---- spectrum: k = 32 smallest eigenvalues of exp(lambda W~)
     sts = []
-    for i in range(2 + 3):
+    for i in range(0 if args.no_configs else 2 + 3):
         torch.cuda.synchronize()
         ev0.record(stream)
         plan.spectrum(32)
@@ -307,10 +307,10 @@ def run_rfd(args, rank, world, local, pg):
         torch.cuda.synchronize()
         if i >= 2:
             sts.append(ev0.elapsed_time(ev1))
-    spectrum = {"ms_per_call": float(np.median(sts)), "k": 32,
+    spectrum = None if not sts else {"ms_per_call": float(np.median(sts)), "k": 32,
                 "note": "rfd_plan_spectrum at cfg5 (r = 512): Householder tridiagonalisation "
                         "of D^1/2 G D^1/2 in fp64 + bisection, median of 3"}
-    reparam = {"ms_per_call": float(np.median(rts)),
+    reparam = None if not rts else {"ms_per_call": float(np.median(rts)),
                "plan_create_ms": ms_step - ims,
                "note": "rfd_plan_reparam(eps, lambda) at cfg5: nu + core on the stored Gram "
                        "(median of %d); plan_create_ms = step - integrate" % len(rts)}

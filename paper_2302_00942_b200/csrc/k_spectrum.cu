@@ -16,7 +16,8 @@
 //                       (g = 1 for r <= 128: one CTA per cloud) that meet at
 //                       a group barrier twice per column (matvec -> update).
 //   K2 bisect_kernel    all r eigenvalues of the tridiagonal matrix by
-//                       bisection on Sturm counts (one thread per index).
+//                       multisection on Sturm counts (a warp per index, 32
+//                       points per step).
 //   K3 merge_kernel     mu -> exp(lambda mu), merged with the eigenvalue 1 of
 //                       multiplicity N - r, ascending; the first k returned.
 //                       For N < r the r - N eigenvalues of smallest modulus
@@ -172,31 +173,48 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e, int
   return cnt;
 }
 
-__global__ void bisect_kernel(const double* __restrict__ diag, const double* __restrict__ off,
-                              int r, double* __restrict__ mu) {
+// The i-th smallest eigenvalue by multisection: a warp per eigenvalue; per
+// step the 32 lanes evaluate Sturm counts at 32 interior points of the
+// bracket, which shrinks 33-fold (fp64 resolution in ~11 steps).
+__global__ void __launch_bounds__(256)
+bisect_kernel(const double* __restrict__ diag, const double* __restrict__ off, int r,
+              double* __restrict__ mu) {
   const int b = blockIdx.y;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (i >= r) return;
   const double* d = diag + int64_t(b) * r;
   const double* e = off + int64_t(b) * r;
-  // Gershgorin interval
+  // Gershgorin interval (lanes split the rows, then a max/min reduction)
   double lo = 1e300, hi = -1e300;
-  for (int k = 0; k < r; ++k) {
+  for (int k = lane; k < r; k += 32) {
     const double rad = (k > 0 ? fabs(e[k - 1]) : 0.0) + (k + 1 < r ? fabs(e[k]) : 0.0);
     lo = fmin(lo, d[k] - rad);
     hi = fmax(hi, d[k] + rad);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
   const double span = fmax(fabs(lo), fabs(hi));
   lo -= 1e-12 * span + 1e-300;
   hi += 1e-12 * span + 1e-300;
-  // the i-th smallest (0-based): count(lo) <= i < count(hi)
-  for (int it = 0; it < 200; ++it) {
-    const double mid = 0.5 * (lo + hi);
-    if (mid <= lo || mid >= hi) break;  // interval at fp64 resolution
-    if (sturm_count(d, e, r, mid) > i) hi = mid;
-    else lo = mid;
+  // invariant: count(lo) <= i < count(hi)
+  for (int it = 0; it < 64; ++it) {
+    const double x = lo + (hi - lo) * double(lane + 1) / 33.0;
+    const bool above = (x > lo && x < hi) ? (sturm_count(d, e, r, x) > i) : (x >= hi);
+    const unsigned mask = __ballot_sync(0xffffffffu, above);
+    const int first = mask ? __ffs(mask) - 1 : 32;  // first point with count > i
+    const double xf = __shfl_sync(0xffffffffu, x, first < 32 ? first : 31);
+    const double xp = __shfl_sync(0xffffffffu, x, first > 0 ? first - 1 : 0);
+    const double nlo = (first == 0) ? lo : xp;
+    const double nhi = (first == 32) ? hi : xf;
+    if (nlo == lo && nhi == hi) break;  // fp64 resolution reached
+    lo = nlo;
+    hi = nhi;
   }
-  mu[int64_t(b) * r + i] = 0.5 * (lo + hi);
+  if (lane == 0) mu[int64_t(b) * r + i] = 0.5 * (lo + hi);
 }
 
 __global__ void merge_kernel(const double* __restrict__ mu, int r, int64_t n, double lambda,
@@ -266,7 +284,7 @@ cudaError_t launch_spectrum(const double* G, const double* nu, int m, int batch,
   }
   {
     LaunchScope L("rfd_spec_bisect", s);
-    bisect_kernel<<<dim3((r + 127) / 128, batch), 128, 0, s>>>(diag, off, r, mu);
+    bisect_kernel<<<dim3((r + 7) / 8, batch), 256, 0, s>>>(diag, off, r, mu);
   }
   {
     LaunchScope L("rfd_spec_merge", s);

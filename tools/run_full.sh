@@ -10,7 +10,7 @@ SMI=$!
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench rc $?
 kill $SMI
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo ref rc $?
-C="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
+C="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-configs"
 timeout 600 $C > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $C > gpurun_out/ncu_launches.log 2>&1; echo launches rc $?
 C2="python tools/profile_step.py"
 timeout 300 $C2 > gpurun_out/plain2.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"gram_pair_kernel|pass1_tc|pass2_tc" -c 3 -o gpurun_out/full $C2 > gpurun_out/ncu_full.log 2>&1; echo full rc $?
