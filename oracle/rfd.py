@@ -299,6 +299,49 @@ def spectrum(G, nu, lam, n, k):
 
 
 # --------------------------------------------------------------------------
+# NEXT-1  Wasserstein barycenter (Alg. 1)
+# --------------------------------------------------------------------------
+BARY_CLAMP = 1e-30  # denominator clamp
+
+
+def barycenter(apply_k, mus, area, alpha, max_iter, tol=0.0):
+    """Entropic Wasserstein barycenter, Appendix D Algorithm 1
+    (lines 1036-1051), with the readings of SPEC.md:559, 628-629 (DESIGN.md
+    A20): mu reset to all-ones at each outer iteration; denominators clamped
+    at 1e-30; stop after max_iter or when ||mu_new - mu_old||_1 < tol; output
+    normalised so <a, mu> = 1.
+
+    apply_k(X) applies the kernel FM_K to the columns of X (N x k).
+    mus: k x N input distributions; area: N; alpha: k.
+    Returns (mu, iterations run).
+    """
+    mus = np.asarray(mus, np.float64)
+    k, N = mus.shape
+    a = np.asarray(area, np.float64)
+    al = np.asarray(alpha, np.float64)
+    v = np.ones((N, k))
+    mu = np.ones(N)
+    it = 0
+    for it in range(1, max_iter + 1):
+        mu_old = mu
+        # 1. w^i <- mu^i / FM_K(a * v^i)
+        w = mus.T / np.maximum(apply_k(a[:, None] * v), BARY_CLAMP)
+        # 2. d^i <- v^i * FM_K(a * w^i), clamped at 1e-30 (it is the
+        #    denominator of step 4 and the base of step 3's power; the
+        #    random-feature kernel can map positive vectors to negative ones)
+        dd = np.maximum(v * apply_k(a[:, None] * w), BARY_CLAMP)
+        # 3. mu <- prod_i (d^i)^alpha_i   (mu reset to ones first)
+        mu = np.prod(dd ** al[None, :], axis=1)
+        # 4. v^i <- v^i * mu / d^i
+        v = v * mu[:, None] / dd
+        if not (np.isfinite(mu).all() and np.isfinite(v).all()):
+            raise FloatingPointError("barycenter: non-finite iterate at iteration %d" % it)
+        if tol > 0 and np.abs(mu - mu_old).sum() < tol:
+            break
+    return mu / float(a @ mu), it
+
+
+# --------------------------------------------------------------------------
 # plan + apply
 # --------------------------------------------------------------------------
 class Plan:
@@ -326,6 +369,10 @@ class Plan:
     def spectrum(self, k):
         """k smallest eigenvalues of exp(lam W~) (NEXT-3; see ``spectrum``)."""
         return spectrum(self.G, self.nu, self.lam, self.X.shape[0], k)
+
+    def barycenter(self, mus, area, alpha, max_iter, tol=0.0):
+        """Alg. 1 with FM_K = this integrator (NEXT-1; see ``barycenter``)."""
+        return barycenter(lambda X: self.apply(X)["out"], mus, area, alpha, max_iter, tol)
 
     def apply(self, F, rows=None):
         """Inference (Eq. 13, bracket order).

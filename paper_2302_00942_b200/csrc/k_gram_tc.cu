@@ -1021,6 +1021,7 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
         }
         ++epoch;
       }
+      if (kTrace && blockIdx.x == 0 && it < 4096 && tid == 160) g_trace[it][7] = clock64();
     }
     while (pend0 >= 0) {
       tc::mbar_wait(&accf_bar, uint32_t(pend0) & 1u);
@@ -1200,10 +1201,26 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, i
         gram_pair_kernel<true><<<2 * sc.G, kThreads, kPSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
         static long long h[4096][8];
         cudaMemcpyFromSymbol(h, g_trace, sizeof(h));
-        for (int i = 0; i < 40; ++i)
-          fprintf(stderr, "it %3d mma_wait %7lld go %7lld | prod top %7lld go %7lld comp %7lld probe %7lld fence %7lld\n", i,
+        for (int i = 600; i < 620; ++i)
+          fprintf(stderr, "it %4d mma_wait %8lld go %8lld | prod top %8lld go %8lld comp %8lld probe %8lld fence %8lld end %8lld\n", i,
                   h[i][0] - h[0][2], h[i][1] - h[0][2], h[i][2] - h[0][2], h[i][3] - h[0][2],
-                  h[i][4] - h[0][2], h[i][5] - h[0][2], h[i][6] - h[0][2]);
+                  h[i][4] - h[0][2], h[i][5] - h[0][2], h[i][6] - h[0][2], h[i][7] - h[0][2]);
+        // steady-state averages (cycles per step) over steps 200..1999
+        double mw = 0, pw = 0, pc = 0, pp = 0, pf = 0, pe = 0, pt = 0, st = 0;
+        const int i0 = 200, i1 = 2000;
+        for (int i = i0; i < i1; ++i) {
+          mw += double(h[i][1] - h[i][0]);
+          pw += double(h[i][3] - h[i][2]);
+          pc += double(h[i][4] - h[i][3]);
+          pp += double(h[i][5] - h[i][4]);
+          pf += double(h[i][6] - h[i][5]);
+          pe += double(h[i][7] - h[i][6]);
+          pt += double(h[i + 1][2] - h[i][7]);
+          st += double(h[i + 1][2] - h[i][2]);
+        }
+        const double k = 1.0 / (i1 - i0);
+        fprintf(stderr, "avg/step: step %.0f | mma full-wait %.0f | prod wait %.0f compute %.0f probe %.0f fence %.0f arrive %.0f top %.0f\n",
+                st * k, mw * k, pw * k, pc * k, pp * k, pf * k, pe * k, pt * k);
       } else {
         gram_pair_kernel<false><<<2 * sc.G, kThreads, kPSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
       }

@@ -152,6 +152,48 @@ def test_spectrum_special_cases():
     np.testing.assert_allclose(rfd.spectrum(G, np.array([1.0]), 0.7, 3, 3)[-1], math.exp(0.7))
 
 
+def _bumps(X, centers, sigma):
+    return np.stack([np.exp(-((X - c) ** 2).sum(1) / (2 * sigma ** 2)) for c in centers])
+
+
+def test_barycenter_identity_kernel_fixed_point():
+    # FM = identity (lambda = 0), a uniform, k = 1 -> mu = mu^1
+    # after one iteration (the iteration is w = mu1 / v, d = v w = mu1, mu = d).
+    X, rng = _cloud(200, seed=4)
+    a = np.full(200, 1.0 / 200)
+    mu1 = _bumps(X, [X[0]], 0.5)
+    mu1 /= a @ mu1[0]
+    plan = rfd.Plan(X, 0.3, 0.0, 8, seed=1, c_r=C_R)
+    mu, it = plan.barycenter(mu1, a, [1.0], 1)
+    np.testing.assert_allclose(mu, mu1[0], rtol=1e-12)
+
+
+def test_barycenter_against_dense_kernel_and_symmetry():
+    # Alg. 1 with FM = the RFD closed form equals Alg. 1 with FM = the dense
+    # exp(lam W~) (independent route); identical inputs give d^1 = d^2, i.e.
+    # the same barycenter as the single input with alpha = 1.
+    X, rng = _cloud(300, seed=6)
+    a = np.full(300, 1.0 / 300)
+    mus = _bumps(X, [X[0], X[100], X[200]], 0.6)
+    mus /= (mus @ a)[:, None]
+    lam = 0.5
+    plan = rfd.Plan(X, 0.3, lam, 12, seed=3, c_r=C_R)
+    W = _lowrank_dense(plan)
+    dense = lambda Y: dense_apply(W, lam, Y)
+    alpha = [1 / 3, 1 / 3, 1 / 3]
+    mu_rfd, _ = plan.barycenter(mus, a, alpha, 8)
+    mu_dense, _ = rfd.barycenter(dense, mus, a, alpha, 8)
+    np.testing.assert_allclose(mu_rfd, mu_dense, rtol=1e-8)
+    two, _ = plan.barycenter(np.stack([mus[1], mus[1]]), a, [0.5, 0.5], 8)
+    one, _ = plan.barycenter(mus[1:2], a, [1.0], 8)
+    np.testing.assert_allclose(two, one, rtol=1e-10)
+    assert abs(a @ mu_rfd - 1.0) < 1e-12
+
+
+def dense_apply(W, lam, Y):
+    return dense.symmetric_expm_apply(W, lam, Y)
+
+
 def test_rows_subset_matches_full():
     X, rng = _cloud(500, seed=9)
     F = rng.standard_normal((500, 4))
