@@ -153,7 +153,9 @@ def test_spectrum_special_cases():
 
 
 def _bumps(X, centers, sigma):
-    return np.stack([np.exp(-((X - c) ** 2).sum(1) / (2 * sigma ** 2)) for c in centers])
+    X = np.asarray(X, np.float64)
+    return np.stack([np.exp(-((X - np.asarray(c, np.float64)) ** 2).sum(1) / (2 * sigma ** 2))
+                     for c in centers])
 
 
 def test_barycenter_identity_kernel_fixed_point():
