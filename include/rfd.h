@@ -128,6 +128,31 @@ rfd_status rfd_plan_reparam(rfd_plan* plan, double eps, double lambda,
 rfd_status rfd_plan_spectrum(rfd_plan* plan, int32_t k, double* out, rfd_stream stream);
 
 /*
+ * rfd_barycenter -- entropic Wasserstein barycenter of k distributions on the
+ * plan's cloud (Appendix D Algorithm 1,
+ * lines 1036-1051, with FM_K = rfd_integrate):
+ *   w^i <- mu^i / FM_K(a * v^i);  d^i <- v^i * FM_K(a * w^i);
+ *   mu <- prod_i (d^i)^alpha_i (mu reset to ones each iteration);
+ *   v^i <- v^i * mu / d^i
+ * with the readings of SPEC.md:559, 628-629 (A20): denominators
+ * (FM_K(a * v^i) and d^i) clamped at 1e-30, stop after max_iter or when
+ * ||mu_new - mu_old||_1 < tol (tol = 0: run max_iter), output normalised so
+ * <a, mu> = 1.  The k distributions are the k columns of one field, so each
+ * FM_K is one multi-column rfd_integrate.  The paper runs it with lambda > 0
+ * (0.5).
+ *   mu     DEVICE k x N fp32 (row i = distribution i).   area  DEVICE N fp32.
+ *   alpha  HOST k fp64, > 0, sum 1.   1 <= k <= 16, max_iter >= 1, tol >= 0.
+ *   out    DEVICE N fp32 (the barycenter).   iters  HOST (may be NULL):
+ *          iterations run.
+ * Single-cloud plans only.  Blocks the host (convergence test / final
+ * read-back).  Errors: EINVAL, ERANGE (non-finite iterate; the message names
+ * the iteration), ENOMEM, ECUDA.
+ */
+rfd_status rfd_barycenter(rfd_plan* plan, const float* mu, const float* area, const double* alpha,
+                          int32_t k, int32_t max_iter, double tol, float* out, int32_t* iters,
+                          rfd_stream stream);
+
+/*
  * rfd_integrate -- inference, Eq. 13 in bracket order:
  *   S = Phi^T F (a6), Y = C^ S (a7), out = F + Phi Y (a8).
  *   F    DEVICE, (batch x) N x d fp32.   out  DEVICE, same shape; may alias F.

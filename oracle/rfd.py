@@ -301,7 +301,7 @@ def spectrum(G, nu, lam, n, k):
 # --------------------------------------------------------------------------
 # NEXT-1  Wasserstein barycenter (Alg. 1)
 # --------------------------------------------------------------------------
-BARY_CLAMP = 1e-30  # denominator clamp
+BARY_CLAMP = 1e-20  # denominator clamp (SPEC.md:559 uses 1e-30; A20)
 
 
 def barycenter(apply_k, mus, area, alpha, max_iter, tol=0.0):
@@ -324,6 +324,10 @@ def barycenter(apply_k, mus, area, alpha, max_iter, tol=0.0):
     it = 0
     for it in range(1, max_iter + 1):
         mu_old = mu
+        # each v^i rescaled to max 1: mu and d are invariant under per-column
+        # scaling of v (w scales inversely); keeps the iterates in fp32 range
+        # on the GPU side (A20)
+        v = v / v.max(axis=0)[None, :]
         # 1. w^i <- mu^i / FM_K(a * v^i)
         w = mus.T / np.maximum(apply_k(a[:, None] * v), BARY_CLAMP)
         # 2. d^i <- v^i * FM_K(a * w^i), clamped at 1e-30 (it is the

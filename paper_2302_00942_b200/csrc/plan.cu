@@ -530,6 +530,74 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
   return RFD_OK;
 }
 
+// NEXT-1: Alg. 1 with FM_K = rfd_integrate on the
+// N x k field of the k distributions (k_sinkhorn.cu).
+rfd_status barycenter_impl(rfd_plan* p, const float* mu_in, const float* area,
+                           const double* alpha, int k, int max_iter, double tol, float* out,
+                           int32_t* iters_out, cudaStream_t st) {
+  if (!p) return fail(RFD_EINVAL, "plan is NULL");
+  if (p->batch != 1) return fail(RFD_EINVAL, "barycenter needs a single-cloud plan");
+  if (!mu_in || !area || !alpha || !out) return fail(RFD_EINVAL, "NULL argument");
+  if (k < 1 || k > 16) return fail(RFD_EINVAL, "k must be in [1, 16]");
+  if (max_iter < 1) return fail(RFD_EINVAL, "max_iter must be >= 1");
+  if (!(tol >= 0.0)) return fail(RFD_EINVAL, "tol must be >= 0");
+  double asum = 0.0;
+  for (int i = 0; i < k; ++i) {
+    if (!(alpha[i] > 0.0) || !isfinite(alpha[i])) return fail(RFD_EINVAL, "alpha must be > 0");
+    asum += alpha[i];
+  }
+  if (fabs(asum - 1.0) > 1e-6) return fail(RFD_EINVAL, "alpha must sum to 1");
+  if (!is_device_pointer(mu_in) || !is_device_pointer(area) || !is_device_pointer(out))
+    return fail(RFD_EINVAL, "mu, area and out must be device pointers");
+  p->stream = st;
+  const int64_t n = p->n;
+  const size_t nk = size_t(n) * k;
+  TempBuffers tmp(st);
+  float *Mt = nullptr, *V = nullptr, *X = nullptr, *Y = nullptr, *mu = nullptr, *sc = nullptr,
+        *vmax = nullptr;
+  double *part = nullptr, *red = nullptr;
+  int* flag = nullptr;
+  RFD_CUDA(tmp.alloc(&Mt, nk));
+  RFD_CUDA(tmp.alloc(&V, nk));
+  RFD_CUDA(tmp.alloc(&X, nk));
+  RFD_CUDA(tmp.alloc(&Y, nk));
+  RFD_CUDA(tmp.alloc(&mu, size_t(n)));
+  RFD_CUDA(tmp.alloc(&part, size_t(rfd::bary_blocks(n))));
+  RFD_CUDA(tmp.alloc(&vmax, size_t(rfd::bary_blocks(n)) * 16));
+  RFD_CUDA(tmp.alloc(&sc, size_t(16)));
+  RFD_CUDA(tmp.alloc(&red, size_t(2)));
+  RFD_CUDA(tmp.alloc(&flag, size_t(1)));
+  RFD_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  float al[16];
+  for (int i = 0; i < k; ++i) al[i] = float(alpha[i]);
+  rfd::launch_bary_init(mu_in, area, n, k, Mt, V, X, mu, sc, st);
+  int it = 0;
+  for (it = 1; it <= max_iter; ++it) {
+    rfd_status rs = integrate_impl(p, X, k, Y, st);          // FM_K(a * v^i)
+    if (rs != RFD_OK) return rs;
+    rfd::launch_bary_step1(area, Mt, Y, sc, n, k, X, st);     // a * w^i
+    rs = integrate_impl(p, X, k, Y, st);                       // FM_K(a * w^i)
+    if (rs != RFD_OK) return rs;
+    rfd::launch_bary_step2(area, Y, al, n, k, V, mu, X, sc, part, vmax, red, flag, st);
+    if (tol > 0.0 || it == max_iter) {
+      double delta = 0.0;
+      int hflag = 0;
+      RFD_CUDA(cudaMemcpyAsync(&delta, red, sizeof(double), cudaMemcpyDeviceToHost, st));
+      RFD_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+      RFD_CUDA(cudaStreamSynchronize(st));
+      if (hflag) return fail(RFD_ERANGE, "barycenter: non-finite iterate at iteration " +
+                                             std::to_string(it));
+      if (tol > 0.0 && delta < tol) break;
+    }
+  }
+  if (it > max_iter) it = max_iter;
+  rfd::launch_bary_finish(area, mu, n, part, red + 1, out, st);
+  RFD_CUDA(cudaGetLastError());
+  RFD_CUDA(cudaStreamSynchronize(st));
+  if (iters_out) *iters_out = it;
+  return RFD_OK;
+}
+
 // interleaved feature index (2k + t) for the paper's blocked index (t m + k)
 inline int interleaved(int a, int m) { return a < m ? 2 * a : 2 * (a - m) + 1; }
 
@@ -553,6 +621,13 @@ rfd_status rfd_plan_create_batched(const float* points, int32_t batch, int64_t n
 
 rfd_status rfd_plan_reparam(rfd_plan* plan, double eps, double lambda, rfd_stream stream) {
   return reparam_impl(plan, eps, lambda, reinterpret_cast<cudaStream_t>(stream));
+}
+
+rfd_status rfd_barycenter(rfd_plan* plan, const float* mu, const float* area, const double* alpha,
+                          int32_t k, int32_t max_iter, double tol, float* out, int32_t* iters,
+                          rfd_stream stream) {
+  return barycenter_impl(plan, mu, area, alpha, k, max_iter, tol, out, iters,
+                         reinterpret_cast<cudaStream_t>(stream));
 }
 
 rfd_status rfd_plan_spectrum(rfd_plan* plan, int32_t k, double* out, rfd_stream stream) {

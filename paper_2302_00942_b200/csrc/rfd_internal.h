@@ -88,6 +88,19 @@ cudaError_t launch_spectrum(const double* G, const double* nu, int m, int batch,
                             double* off, double* mu, unsigned int* bar, double* out,
                             cudaStream_t s);
 
+// ---------------------------------------------------------------- barycenter
+// NEXT-1 (k_sinkhorn.cu): elementwise steps of Alg. 1 on N x k fields.
+int bary_blocks(int64_t n);
+void launch_bary_init(const float* mu_in, const float* area, int64_t n, int k, float* Mt, float* V,
+                      float* X, float* mu, float* sc, cudaStream_t s);
+void launch_bary_step1(const float* area, const float* Mt, const float* Y, const float* sc,
+                       int64_t n, int k, float* X, cudaStream_t s);
+void launch_bary_step2(const float* area, const float* Y, const float* alpha, int64_t n, int k,
+                       float* V, float* mu, float* X, float* sc, double* part, float* vmax_part,
+                       double* delta, int* flag, cudaStream_t s);
+void launch_bary_finish(const float* area, const float* mu, int64_t n, double* part, double* mass,
+                        float* out, cudaStream_t s);
+
 // ---------------------------------------------------------------- passes
 struct PassGeom {
   int fblocks;    // ceil(m / 32)

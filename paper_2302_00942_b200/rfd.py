@@ -24,7 +24,7 @@ FIELDS = {"omega": 0, "nu": 1, "gram": 2, "core": 3, "S": 4, "Y": 5}
 
 # Every symbol include/rfd.h declares (checked by tests/test_abi.py).
 EXPORTED = ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_reparam",
-            "rfd_plan_spectrum", "rfd_integrate",
+            "rfd_plan_spectrum", "rfd_barycenter", "rfd_integrate",
             "rfd_integrate_host", "rfd_destroy", "rfd_last_error", "rfd_plan_info",
             "rfd_plan_export", "rfd_launch_count", "rfd_profile_enable",
             "rfd_profile_read")
@@ -67,6 +67,7 @@ def load_library(path=LIB_PATH):
     lib.rfd_plan_create_batched.argtypes = [vp, i32, i64, dbl, dbl, i32, u64, vp, pp]
     lib.rfd_plan_reparam.argtypes = [vp, dbl, dbl, vp]
     lib.rfd_plan_spectrum.argtypes = [vp, i32, vp, vp]
+    lib.rfd_barycenter.argtypes = [vp, vp, vp, vp, i32, i32, dbl, vp, ctypes.POINTER(i32), vp]
     lib.rfd_integrate.argtypes = [vp, vp, i32, vp, vp]
     lib.rfd_integrate_host.argtypes = [vp, vp, i32, vp, vp]
     lib.rfd_destroy.argtypes = [vp]
@@ -79,7 +80,7 @@ def load_library(path=LIB_PATH):
     lib.rfd_profile_read.argtypes = [ctypes.POINTER(ProfileEntry), i32]
     lib.rfd_profile_read.restype = i32
     for name in ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_reparam",
-                 "rfd_plan_spectrum", "rfd_integrate",
+                 "rfd_plan_spectrum", "rfd_barycenter", "rfd_integrate",
                  "rfd_integrate_host", "rfd_plan_info", "rfd_plan_export",
                  "rfd_profile_enable"):
         getattr(lib, name).restype = ctypes.c_int
@@ -180,6 +181,22 @@ class Plan:
         _check(load_library().rfd_plan_spectrum(self._h, int(k), _ptr(out),
                                                 _stream_handle(stream)))
         return out[0] if self.batch == 1 else out
+
+    def barycenter(self, mus, area, alpha, max_iter, tol=0.0, stream=None):
+        """Wasserstein barycenter (Alg. 1, NEXT-1) of the k rows of ``mus``
+        (CUDA float32 k x N) with area weights ``area`` (CUDA float32 N).
+        Returns (mu CUDA float32 N, iterations run)."""
+        import torch
+        _check_f32(mus, "mus")
+        _check_f32(area, "area")
+        k = int(mus.shape[0])
+        al = np.ascontiguousarray(np.asarray(alpha, np.float64))
+        out = torch.empty((self.n,), dtype=torch.float32, device=mus.device)
+        its = ctypes.c_int32(0)
+        _check(load_library().rfd_barycenter(self._h, _ptr(mus), _ptr(area), _ptr(al), k,
+                                             int(max_iter), float(tol), _ptr(out),
+                                             ctypes.byref(its), _stream_handle(stream)))
+        return out, its.value
 
     # -- inference -----------------------------------------------------------
     def _field_dims(self, F):

@@ -258,6 +258,63 @@ def test_multi_column_parity(n, m, d):
     _check_against_oracle(plan, out, x, F, p)
 
 
+def _bary_inputs(n, seed=7):
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal((n, 3))
+    x = (g / np.linalg.norm(g, axis=1, keepdims=True)).astype(np.float32)
+    a = np.full(n, 1.0 / n)
+    xd = x.astype(np.float64)
+    mus = np.stack([np.exp(-((xd - xd[i]) ** 2).sum(1) / (2 * 0.5 ** 2)) for i in range(3)])
+    # (bumps of width 0.5 around three points; area weights uniform)
+    mus /= (mus @ a)[:, None]
+    return x, a, mus
+
+
+def test_barycenter_matches_oracle():
+    # NEXT-1: Alg. 1 with FM_K = rfd_integrate (k = 3 columns per integrate),
+    # lambda > 0 as in the paper's barycenter runs.  Trajectory parity for the
+    # first iterations; from about the fourth on the iterates depend on the
+    # RELATIVE accuracy of FM_K(a v) where it is tiny (the ratios mu / FM_K(a v)
+    # far from the mass), which a normwise-accurate fp32 kernel application does
+    # not have -- so after 10 iterations only validity is checked
+    # (A20).
+    n, eps, lam, m = 2000, 0.03, 0.1, 256
+    x, a, mus = _bary_inputs(n)
+    plan = rfd.Plan(torch.from_numpy(x).cuda(), eps, lam, m, 5)
+    mus_d = torch.from_numpy(mus.astype(np.float32)).cuda()
+    a_d = torch.from_numpy(a.astype(np.float32)).cuda()
+    for iters in (1, 2, 3):
+        got, its = plan.barycenter(mus_d, a_d, [1 / 3] * 3, iters)
+        ref, rits = orf.Plan(x, eps, lam, m, 5).barycenter(mus, a, [1 / 3] * 3, iters)
+        assert its == rits == iters
+        g = got.cpu().numpy().astype(np.float64)
+        err = relerr(g, ref)
+        print("barycenter iters=%d err %.2e" % (iters, err))
+        assert err <= TOL
+        assert np.isfinite(g).all() and abs(float(a @ g) - 1.0) < 1e-5
+    got, its = plan.barycenter(mus_d, a_d, [1 / 3] * 3, 10)
+    g = got.cpu().numpy().astype(np.float64)
+    assert its == 10 and np.isfinite(g).all() and (g >= 0).all()
+    assert abs(float(a @ g) - 1.0) < 1e-5
+
+
+def test_barycenter_tol_stop_and_errors():
+    n = 2000
+    x, a, mus = _bary_inputs(n)
+    plan = rfd.Plan(torch.from_numpy(x).cuda(), 0.03, 0.1, 256, 5)
+    mus_d = torch.from_numpy(mus.astype(np.float32)).cuda()
+    a_d = torch.from_numpy(a.astype(np.float32)).cuda()
+    _, its = plan.barycenter(mus_d, a_d, [1 / 3] * 3, 200, tol=1e-3)
+    _, rits = orf.Plan(x, 0.03, 0.1, 256, 5).barycenter(mus, a, [1 / 3] * 3, 200, tol=1e-3)
+    assert its < 200 and rits < 200
+    for alpha in ([0.5, 0.5, 0.5], [1.0, 0.0, 0.0], [-1.0, 1.0, 1.0]):
+        with pytest.raises(rfd.RFDError):
+            plan.barycenter(mus_d, a_d, alpha, 3)
+    batched = rfd.Plan(torch.from_numpy(np.stack([x, x])).cuda(), 0.03, 0.1, 256, 5)
+    with pytest.raises(rfd.RFDError):
+        batched.barycenter(mus_d, a_d, [1 / 3] * 3, 3)
+
+
 @pytest.mark.parametrize("n,m,seed,lam", [(1000, 40, 11, -0.8), (3001, 96, 14, -0.3),
                                           (2000, 128, 13, 0.05)])
 def test_negative_nu_nonsymmetric_route(n, m, seed, lam):
