@@ -473,24 +473,27 @@ def config_legs(args, pk):
     # NEXT-1 barycenter: k = 3 localized distributions on the cfg-5 points,
     # uniform area weights, lambda > 0 (Alg. 1 runs with lambda = 0.5 in the
     # paper); time per outer iteration (2 x 3-column integrate + 2 elementwise)
-    plan.reparam(p["eps"], 0.1)
     xs = torch.from_numpy(x[:3].astype(np.float32)).cuda()
     xg = torch.from_numpy(x).cuda()
     mus = torch.exp(-((xg[None, :, :] - xs[:, None, :]) ** 2).sum(-1) / (2 * 0.25 ** 2))
     area = torch.full((p["n"],), 1.0 / p["n"], device="cuda")
     mus = (mus / (mus @ area)[:, None]).contiguous()
-    plan.barycenter(mus, area, [1 / 3] * 3, 2)
-    bts = []
-    for iters in (2, 12):
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        plan.barycenter(mus, area, [1 / 3] * 3, iters)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        bts.append(ev0.elapsed_time(ev1))
-    out["cfg5_barycenter"] = {"ms_per_iteration": (bts[1] - bts[0]) / 10, "k": 3,
-                              "note": "rfd_barycenter, Alg. 1 on the cfg-5 points (N = 4M), "
-                                      "k = 3, lambda = 0.1; (t(12 it) - t(2 it)) / 10"}
+    try:
+        plan.reparam(p["eps"], 0.01)  # lambda > 0 small enough for exp(lambda G D) in fp32
+        plan.barycenter(mus, area, [1 / 3] * 3, 2)
+        bts = []
+        for iters in (2, 12):
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            plan.barycenter(mus, area, [1 / 3] * 3, iters)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            bts.append(ev0.elapsed_time(ev1))
+        out["cfg5_barycenter"] = {"ms_per_iteration": (bts[1] - bts[0]) / 10, "k": 3,
+                                  "note": "rfd_barycenter, Alg. 1 on the cfg-5 points (N = 4M), "
+                                          "k = 3, lambda = 0.01; (t(12 it) - t(2 it)) / 10"}
+    except rfd.RFDError as e:  # the iteration can leave fp32 range on this cloud
+        out["cfg5_barycenter"] = {"error": str(e)}
     plan.reparam(p["eps"], p["lam"])
     out["cfg5_d64"] = {"integrate_ms": t64, "value": N * 64 / (t64 * 1e-3), "unit": UNIT,
                        "ms_per_16_columns": t64 / 4, "d16_ms": t_a,
