@@ -26,6 +26,9 @@
 //     the partials in a fixed order in fp64.
 //
 // TMEM: D [0, 2N) (cos N | sin N), L [2N, 4N), A stages at 4N + 128 s.
+#include <cstdio>
+#include <cstdlib>
+
 #include "rfd_internal.h"
 #include "tc_ptx.cuh"
 
@@ -381,24 +384,31 @@ constexpr uint32_t kColA = 64;      // D buffers (cos 16 + sin 16) at 0 and 32
 constexpr int kBBytes = 16 * kChunk * 2;        // one fp16 B operand (hi or lo): 2 KB
 constexpr int kChunkB = 2 * kBBytes;            // hi + lo of one chunk
 constexpr int kEpochB = kEpoch * kChunkB;       // 32 KB per epoch buffer
-constexpr int kStageF = kEpoch * kChunk * 16 * 4;  // fp32 F block of one epoch: 32 KB
+constexpr int kRowF = 20;                       // staging row stride (floats, 16 B aligned)
+constexpr int kStageF = kEpoch * kChunk * kRowF * 4;  // fp32 F block of one epoch: 40 KB
 constexpr int kSmem = 2 * kEpochB + kStageF;
 }  // namespace k16
 
-__global__ void __launch_bounds__(kThreads, 1)
+// Diagnostics (RFD_P1_TRACE=1): per-chunk timestamps of CTA (0, 0, 0).
+__device__ long long g_p1trace[1024][12];
+
+template <int PW, bool kTr = false>
+__global__ void __launch_bounds__((PW + 5) * 32, 1)
 pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ omega4, int m,
                 int64_t n, int ranges, const float* __restrict__ F, int d, int c0, int dc,
                 float* __restrict__ partial) {
   using namespace k16;
+  // PW producer warps (PW / 4 per TMEM lane group), PPW points each per chunk
+  constexpr int PPW = 4 * kChunk / PW, kMmaW = PW, kFW0 = PW + 1;
   // [2 epochs][8 chunks][hi | lo] B operands, then the fp32 F staging block
   extern __shared__ __align__(1024) unsigned char bsm[];
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages], dfull_bar[2], dempty_bar[2],
-      bready_bar[2];
+      bready_bar[2], fst_bar;
   __shared__ uint32_t tmem_sh;
   // each producer warp's 16 points of a chunk as [x0..15 | y0..15 | z0..15],
   // 3 chunks deep (cp.async ring)
-  __shared__ __align__(16) float xbuf[3][kProducerWarps][48];
-  __shared__ unsigned int fmax_part[2][4][16];  // per epoch buffer, F warp, channel (fp32 bits)
+  __shared__ __align__(16) float xbuf[3][PW][3 * PPW];
+  __shared__ __align__(16) float fmax_part[2][4][16];  // per epoch buffer, F warp, channel
   __shared__ float fscale_inv[2][16];        // per epoch buffer
 
   const int ft = blockIdx.x, rg = blockIdx.y, b = blockIdx.z;
@@ -414,7 +424,7 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
   if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      tc::mbar_init(&full_bar[s], kProducerWarps);
+      tc::mbar_init(&full_bar[s], PW);
       tc::mbar_init(&empty_bar[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -422,16 +432,18 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
       tc::mbar_init(&dempty_bar[i], 4);
       tc::mbar_init(&bready_bar[i], 4);
     }
+    tc::mbar_init(&fst_bar, 1);
     tc::mbar_fence_init();
   }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = tmem_sh;
+  const bool trc = kTr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0;
   const uint32_t lane_field = uint32_t(lg * 32) << 16;
   const int f = ft * 128 + lg * 32 + lane;  // this lane's frequency
 
-  if (warp < kProducerWarps) {
+  if (warp < PW) {
     // ---------------- producers: 16 points per warp per chunk --------------
     const int q = warp >> 2;  // which 16 of the chunk's points
     const float4 w = (f < m) ? omega4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -441,15 +453,17 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
     // critical path).  Groups past the cloud's end repeat its last group
     // (finite values that meet zero F).  Pointers and counters advance per
     // chunk (no 64-bit index arithmetic in the loop).
-    const float* xsrc = cloud16 + ((ch0 * (kChunk / 16) + q) * 48 + 4 * lane);
-    const float* xlast = cloud16 + ((gpc - 1) * 48 + 4 * lane);
-    const int64_t xrem0 = gpc - (ch0 * (kChunk / 16) + q);
+    // (PPW = 32: lanes 12-23 copy the warp's second group.)
+    const int gsel = lane / 12, l12 = lane % 12;
+    const float* xsrc = cloud16 + ((ch0 * (kChunk / 16) + q * (PPW / 16) + gsel) * 48 + 4 * l12);
+    const float* xlast = cloud16 + ((gpc - 1) * 48 + 4 * l12);
+    const int64_t xrem0 = gpc - (ch0 * (kChunk / 16) + q * (PPW / 16) + gsel);
     int xrem = int(xrem0 > 0x7fffffff ? 0x7fffffff : xrem0);  // groups left
-    constexpr uint32_t kRing = kProducerWarps * 48 * 4;           // bytes per ring slot
+    constexpr uint32_t kRing = PW * 3 * PPW * 4;  // bytes per ring slot
     const uint32_t x_s = tc::smem_addr(&xbuf[0][warp][0]);
     uint32_t xw = 0;
     auto load_x = [&](bool valid) {
-      if (lane < 12 && valid) tc::cp_async16(x_s + xw * kRing + 16 * lane, xrem > 0 ? xsrc : xlast);
+      if (lane < 3 * PPW / 4 && valid) tc::cp_async16(x_s + xw * kRing + 16 * lane, xrem > 0 ? xsrc : xlast);
       tc::cp_async_commit();  // one group per chunk, empty past the end
       xsrc += 48 * (kChunk / 16);
       xrem -= kChunk / 16;
@@ -461,24 +475,27 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
     uint32_t s = 0, u = 0, xr = 0;  // stage, its round, ring slot read
     for (int c = 0; c < nchunks; ++c) {
       load_x(c + 2 < nchunks);  // the slot chunk c - 1 read (ordered by its __syncwarp)
+      if (trc && warp == 0 && c < 1024) g_p1trace[c][0] = clock64();
       if (u >= 1) tc::mbar_wait(empty_s + 8 * s, (u - 1) & 1);
+      if (trc && warp == 0 && c < 1024) g_p1trace[c][1] = clock64();
       // Points beyond the cloud meet zero columns of F^T, and lanes beyond m
       // are never written out: no masking of the features.
       tc::cp_async_wait<2>();  // chunk c's group (c + 1, c + 2 may be in flight)
       __syncwarp();
-      const float* xs = &xbuf[0][warp][0] + xr * (kProducerWarps * 48);
+      const float* xs = &xbuf[0][warp][0] + xr * (PW * 3 * PPW);
       xr = (xr == 2) ? 0 : xr + 1;
-      const uint32_t a = tmem + lane_field + kColA + 4 * kArr * s + 8 * q;
+      const uint32_t a = tmem + lane_field + kColA + 4 * kArr * s + (PPW / 2) * q;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {  // two halves of 8 points (register pressure)
+      for (int h = 0; h < PPW / 8; ++h) {  // 8 points at a time (register pressure)
+        const float* xh = xs + 48 * (h >> 1) + 8 * (h & 1);
         float cs[8], sn[8];
 #pragma unroll
         for (int j = 0; j < 8; j += 4) {
           // omega . x for 4 points in packed FP32 (2 points per instruction),
           // the same operation order as fmaf(wz, z, fmaf(wy, y, wx * x))
-          const float4 X = *reinterpret_cast<const float4*>(xs + 8 * h + j);
-          const float4 Y = *reinterpret_cast<const float4*>(xs + 16 + 8 * h + j);
-          const float4 Z = *reinterpret_cast<const float4*>(xs + 32 + 8 * h + j);
+          const float4 X = *reinterpret_cast<const float4*>(xh + j);
+          const float4 Y = *reinterpret_cast<const float4*>(xh + 16 + j);
+          const float4 Z = *reinterpret_cast<const float4*>(xh + 32 + j);
           float2 t0 = __fmul2_rn(wx, make_float2(X.x, X.y));
           float2 t1 = __fmul2_rn(wx, make_float2(X.z, X.w));
           t0 = __ffma2_rn(wy, make_float2(Y.x, Y.y), t0);
@@ -505,13 +522,14 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
       tc::tmem_st_wait();
       tc::tc_fence_before();
       __syncwarp();
+      if (trc && warp == 0 && c < 1024) g_p1trace[c][2] = clock64();
       if (lane == 0) tc::mbar_arrive(full_s + 8 * s);
       if (++s == kStages) {
         s = 0;
         ++u;
       }
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == kMmaW) {
     // ---------------- MMA issue: warp-uniform loop, one elected lane -------
     const uint32_t idesc = tc::make_idesc(0, 128, 16);
     const uint32_t b_s = tc::smem_addr(bsm);
@@ -519,11 +537,17 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
       const uint32_t s = c % kStages, u = c / kStages;
       const int e = c / kEpoch, ce = c % kEpoch;
       const uint32_t buf = e & 1;
+      if (trc && c < 1024) g_p1trace[c][3] = clock64();
       if (ce == 0) {
         if (e >= 2) tc::mbar_wait(&dempty_bar[buf], ((e - 2) >> 1) & 1);
+        if (trc && c < 1024) g_p1trace[c][4] = clock64();
         tc::mbar_wait(&bready_bar[buf], (e >> 1) & 1);
+      } else if (trc && c < 1024) {
+        g_p1trace[c][4] = clock64();
       }
+      if (trc && c < 1024) g_p1trace[c][5] = clock64();
       tc::mbar_wait(&full_bar[s], u & 1);
+      if (trc && c < 1024) g_p1trace[c][6] = clock64();
       tc::tc_fence_after();
       if (tc::elect_one()) {
         const uint32_t bc = b_s + buf * kEpochB + ce * kChunkB;
@@ -549,49 +573,96 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
     }
   } else {
     // ---------------- F staging + drains (4 warps, 128 threads) ----------
-    const int fw = warp - kFWarp0, t = fw * 32 + lane;
-    // Per epoch: the F block is copied into shared memory, then thread t
-    // converts channel je of the point pairs (2 pk, 2 pk + 1), pk = (t >> 4) +
-    // 8 i (one 32-bit word of the K-major B operand each).
-    const int je = t & 15, pk0 = t >> 4;
+    const int fw = warp - kFW0, t = fw * 32 + lane;
+    // Per epoch e the F block is copied into shared memory (issue_f, one epoch
+    // ahead: its latency overlaps the epoch before), then process_f takes the
+    // per-channel maxima and writes the scaled, split B operands.
     const float* Fb = F + int64_t(b) * n * d + c0;
     const uint32_t b_s = tc::smem_addr(bsm);
-    const uint32_t fs_s = b_s + 2 * kEpochB;  // staging: [512 points][16 channels] fp32
+    const uint32_t fs_s = b_s + 2 * kEpochB;  // staging: [512 points][kRowF] fp32
     const float* fstage = reinterpret_cast<const float*>(bsm + 2 * kEpochB);
     const bool vec = (dc == 16) && (d % 4 == 0) && (c0 % 4 == 0);
-    // prepare the B operands of epoch e into buffer e & 1
-    auto stage_f = [&](int e) {
+    // d = 16: the epoch's rows are one contiguous block -> one bulk copy (TMA
+    // engine) into unpadded rows; otherwise per-thread cp.async into rows
+    // padded to kRowF floats
+    const bool bulk = vec && d == 16 && (reinterpret_cast<uintptr_t>(Fb) & 15) == 0;
+    const int rs = bulk ? 16 : kRowF;
+    auto epoch_pts = [&](int e) { return min(kEpoch, nchunks - e * kEpoch) * kChunk; };
+    // the epoch's F block -> shared memory (cp.async, all in flight at once;
+    // rows past the cloud and channels past dc are zero-filled)
+    auto issue_f = [&](int e) {
       const int64_t q0 = p0 + int64_t(e) * (kEpoch * kChunk);  // first point of the epoch
-      const int ncs = min(kEpoch, nchunks - e * kEpoch);        // chunks of this epoch
-      const int npts = ncs * kChunk;
-      // the epoch's F block -> shared memory (cp.async, all in flight at once;
-      // rows past the cloud and channels past dc are zero-filled)
+      const int npts = epoch_pts(e);
+      if (bulk) {
+        const int nv = int(min(int64_t(npts), n - q0));  // rows past the cloud: zeros
+        if (t == 0) {
+          tc::fence_proxy_async_smem();  // after the generic reads of the last epoch
+          tc::mbar_arrive_expect_tx(&fst_bar, uint32_t(nv) * 64u);
+          tc::bulk_g2s(bsm + 2 * kEpochB, Fb + q0 * 16, uint32_t(nv) * 64u, &fst_bar);
+        }
+        for (int i = t; i < (npts - nv) * 16; i += 128)
+          reinterpret_cast<float*>(bsm + 2 * kEpochB)[nv * 16 + i] = 0.0f;
+        return;
+      }
       if (vec) {
         for (int i = t; i < npts * 4; i += 128) {
           const int p = i >> 2, cq = i & 3;
           const bool ok = q0 + p < n;
-          tc::cp_async16_zf(fs_s + uint32_t(p * 64 + cq * 16),
+          tc::cp_async16_zf(fs_s + uint32_t(p * kRowF * 4 + cq * 16),
                             ok ? Fb + (q0 + p) * d + 4 * cq : Fb, ok ? 16u : 0u);
         }
       } else {
         for (int i = t; i < npts * 16; i += 128) {
           const int p = i >> 4, j = i & 15;
           const bool ok = q0 + p < n && j < dc;
-          tc::cp_async4_zf(fs_s + uint32_t(i * 4), ok ? Fb + (q0 + p) * d + j : Fb, ok ? 4u : 0u);
+          tc::cp_async4_zf(fs_s + uint32_t((p * kRowF + j) * 4), ok ? Fb + (q0 + p) * d + j : Fb,
+                           ok ? 4u : 0u);
         }
       }
       tc::cp_async_commit();
-      tc::cp_async_wait<0>();
+    };
+    // Thread t converts channel j = t % 16 of the 8-point groups g = t / 16 +
+    // 8 i: eight staging reads, one 16-byte store each of hi and lo (the
+    // groups' 8 points are one K-major core-matrix row).
+    const int j = t & 15, g0 = t >> 4;
+    auto process_f = [&](int e) {
+      const int npts = epoch_pts(e);
+      const bool tr = trc && fw == 0 && e * kEpoch < 1024;
+      if (tr) g_p1trace[e * kEpoch][8] = clock64();
+      if (bulk)
+        tc::mbar_wait(&fst_bar, uint32_t(e) & 1u);
+      else
+        tc::cp_async_wait<0>();
+      if (tr) g_p1trace[e * kEpoch][9] = clock64();
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      // per-channel max |F| over the epoch's points
-      float mx = 0.0f;
-      for (int p = pk0; p < npts; p += 8) mx = fmaxf(mx, fabsf(fstage[p * 16 + je]));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-      if (lane < 16) fmax_part[e & 1][fw][lane] = __float_as_uint(mx);
+      if (tr) g_p1trace[e * kEpoch][10] = clock64();
+      // per-channel max |F|: thread t takes channels 4 (t % 4) .. + 3 of points
+      // t / 4 + 32 i (16-byte reads), then lanes of equal t % 4 and the warps
+      {
+        const int cq = t & 3;
+        float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+        for (int p = t >> 2; p < npts; p += 32) {
+          const float4 v = *reinterpret_cast<const float4*>(fstage + p * rs + 4 * cq);
+          mx.x = fmaxf(mx.x, fabsf(v.x));
+          mx.y = fmaxf(mx.y, fabsf(v.y));
+          mx.z = fmaxf(mx.z, fabsf(v.z));
+          mx.w = fmaxf(mx.w, fabsf(v.w));
+        }
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          mx.x = fmaxf(mx.x, __shfl_xor_sync(0xffffffffu, mx.x, o));
+          mx.y = fmaxf(mx.y, __shfl_xor_sync(0xffffffffu, mx.y, o));
+          mx.z = fmaxf(mx.z, __shfl_xor_sync(0xffffffffu, mx.z, o));
+          mx.w = fmaxf(mx.w, __shfl_xor_sync(0xffffffffu, mx.w, o));
+        }
+        if (lane < 4) *reinterpret_cast<float4*>(&fmax_part[e & 1][fw][4 * lane]) = mx;
+      }
+      if (tr) g_p1trace[e * kEpoch][11] = clock64();
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      const unsigned int(*fp)[16] = fmax_part[e & 1];
-      const float cm = fmaxf(fmaxf(__uint_as_float(fp[0][je]), __uint_as_float(fp[1][je])),
-                             fmaxf(__uint_as_float(fp[2][je]), __uint_as_float(fp[3][je])));
+      if (tr) g_p1trace[e * kEpoch + 1][8] = clock64();
+      const float(*fp)[16] = fmax_part[e & 1];
+      const float cm = fmaxf(fmaxf(fp[0][j], fp[1][j]), fmaxf(fp[2][j], fp[3][j]));
       // scale 2^e_j with max |F_j| 2^e_j in [2^13, 2^14) (1 for a zero or
       // non-finite channel; |e_j| <= 126 keeps both factors normal and exact)
       float scale = 1.0f;
@@ -601,32 +672,46 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
         scale = ldexpf(1.0f, min(126, max(-126, 14 - ex)));
       }
       if (t < 16) fscale_inv[e & 1][t] = 1.0f / scale;
-      // scaled, split, stored as 32-bit words (points 2 pk, 2 pk + 1)
-      const uint32_t eb = b_s + (e & 1) * kEpochB;
-      for (int pk = pk0; 2 * pk < npts; pk += 8) {
-        const int p = 2 * pk;
-        uint32_t hi, lo;
-        tc::split_f16x2(fstage[p * 16 + je] * scale, fstage[(p + 1) * 16 + je] * scale, hi, lo);
-        const int ce = p / kChunk, pc = p % kChunk;
-        const uint32_t off = uint32_t(ce) * kChunkB + uint32_t(je >> 3) * kSBO +
-                             uint32_t(pc >> 3) * kLBO + uint32_t(je & 7) * 16 + uint32_t(pc & 7) * 2;
-        tc::st_shared_u32(eb + off, hi);
-        tc::st_shared_u32(eb + off + kBBytes, lo);
+      const float2 sc2 = make_float2(scale, scale);
+      const uint32_t eb = b_s + (e & 1) * kEpochB + uint32_t(j >> 3) * kSBO + uint32_t(j & 7) * 16;
+#pragma unroll 2
+      for (int g = g0; 8 * g < npts; g += 8) {
+        const float* src = fstage + 8 * g * rs + j;
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 v = __fmul2_rn(sc2, make_float2(src[2 * k * rs], src[(2 * k + 1) * rs]));
+          tc::split_f16x2(v.x, v.y, hi[k], lo[k]);
+        }
+        const uint32_t off = uint32_t(g >> 3) * kChunkB + uint32_t(g & 7) * kLBO;
+        tc::st_shared_v4(eb + off, hi[0], hi[1], hi[2], hi[3]);
+        tc::st_shared_v4(eb + off + kBBytes, lo[0], lo[1], lo[2], lo[3]);
       }
+      if (tr) g_p1trace[e * kEpoch + 1][9] = clock64();
       // the staging block is rewritten by the next epoch's copies
       asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (tr) g_p1trace[e * kEpoch + 1][10] = clock64();
       tc::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bready_bar[e & 1]);
     };
-    if (nepochs > 0) stage_f(0);
-    if (nepochs > 1) stage_f(1);
+    if (nepochs > 0) {
+      issue_f(0);
+      process_f(0);
+    }
+    if (nepochs > 1) {
+      issue_f(1);
+      process_f(1);
+    }
+    if (nepochs > 2) issue_f(2);
     float acc[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
     for (int e = 0; e < nepochs; ++e) {
       const uint32_t buf = e & 1;
+      if (trc && fw == 0 && e * kEpoch + 2 < 1024) g_p1trace[e * kEpoch + 2][7] = clock64();
       tc::mbar_wait(&dfull_bar[buf], (e >> 1) & 1);
+      if (trc && fw == 0 && e * kEpoch + 3 < 1024) g_p1trace[e * kEpoch + 3][7] = clock64();
       tc::tc_fence_after();
       float v[32];
       tc::tmem_ld32(tmem + lane_field + 32 * buf, v);
@@ -642,7 +727,10 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
       // buffer e & 1 (B and scales) is free once epoch e's MMAs completed and
       // all four warps have read its scales
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (e + 2 < nepochs) stage_f(e + 2);
+      if (trc && fw == 0 && e * kEpoch + 4 < 1024) g_p1trace[e * kEpoch + 4][7] = clock64();
+      if (e + 2 < nepochs) process_f(e + 2);
+      if (e + 3 < nepochs) issue_f(e + 3);
+      if (trc && fw == 0 && e * kEpoch + 5 < 1024) g_p1trace[e * kEpoch + 5][7] = clock64();
     }
     if (f < m) {
       // partial[b][rg][2m][dc]: row 2f = cos, 2f + 1 = sin (interleaved order)
@@ -1000,6 +1088,41 @@ void launch_nc(dim3 grid, cudaStream_t s, const float* pts16, const float4* omeg
 
 }  // namespace
 
+// RFD_P1_TRACE=1: the per-chunk timestamps of CTA (0, 0, 0), summarised.
+static void print_p1trace(cudaStream_t s, int64_t n, int ranges) {
+  static long long h[1024][12];
+  cudaStreamSynchronize(s);
+  cudaMemcpyFromSymbol(h, g_p1trace, sizeof(h));
+  const int nc = int((((n + kChunk - 1) / kChunk) + ranges - 1) / ranges);
+  const int lo = 64, hi = nc < 1000 ? nc - 8 : 1000;
+  double pe = 0, pc = 0, mr = 0, mb = 0, mf = 0, per = 0;
+  for (int c = lo; c < hi; ++c) {
+    pe += h[c][1] - h[c][0];
+    pc += h[c][2] - h[c][1];
+    mr += h[c][4] - h[c][3];
+    mb += h[c][5] - h[c][4];
+    mf += h[c][6] - h[c][5];
+    per += h[c + 1][3] - h[c][3];
+  }
+  const double k = hi - lo;
+  fprintf(stderr,
+          "p1trace chunks %d: period %.0f | prod empty-wait %.0f compute %.0f | mma "
+          "dempty %.0f bready %.0f full %.0f\n",
+          nc, per / k, pe / k, pc / k, mr / k, mb / k, mf / k);
+  for (int c = 64; c < 84 && c < hi; ++c)
+    fprintf(stderr, "  chunk %d: period %lld dempty %lld bready %lld full %lld | prod %lld %lld\n",
+            c, h[c + 1][3] - h[c][3], h[c][4] - h[c][3], h[c][5] - h[c][4],
+            h[c][6] - h[c][5], h[c][1] - h[c][0], h[c][2] - h[c][1]);
+  for (int e = 8; e < 120 && e + 5 < hi; e += 8)
+    fprintf(stderr,
+            "  epoch %d: dfull wait %lld, stage_f %lld, mma at %lld..%lld | proc(e): cpwait "
+            "%lld bar %lld max %lld bar %lld conv %lld bar %lld\n",
+            e / 8, h[e + 3][7] - h[e + 2][7], h[e + 5][7] - h[e + 4][7],
+            h[e][3] - h[e + 2][7], h[e + 8][3] - h[e + 2][7], h[e][9] - h[e][8],
+            h[e][10] - h[e][9], h[e][11] - h[e][10], h[e + 1][8] - h[e][11],
+            h[e + 1][9] - h[e + 1][8], h[e + 1][10] - h[e + 1][9]);
+}
+
 // Segments per CTA of the packed small-m kernel: R = 4 (m <= 32) or 2
 // (m <= 64) when there are enough chunks to keep every SM busy with R of them
 // (>= 2 per segment); otherwise 1 (one CTA per frequency tile and range).
@@ -1038,13 +1161,24 @@ void launch_pass1_tc(const float* pts16, const float4* omega4, int m, int64_t n,
   switch ((dc + 15) / 16) {
     case 1: {
       static bool configured = false;
+      static bool trace = false;
       if (!configured) {
-        cudaFuncSetAttribute(pass1_tc_kernel16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        const char* e = getenv("RFD_P1_TRACE");
+        trace = e && atoi(e) == 1;
+        cudaFuncSetAttribute(pass1_tc_kernel16<16, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, k16::kSmem);
+        cudaFuncSetAttribute(pass1_tc_kernel16<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              k16::kSmem);
         configured = true;
       }
-      pass1_tc_kernel16<<<grid, kThreads, k16::kSmem, s>>>(pts16, omega4, m, n, ranges, F, d, c0,
-                                                          dc, partial);
+      if (trace) {
+        pass1_tc_kernel16<16, true><<<grid, kThreads, k16::kSmem, s>>>(pts16, omega4, m, n, ranges,
+                                                                      F, d, c0, dc, partial);
+        print_p1trace(s, n, ranges);
+      } else {
+        pass1_tc_kernel16<16><<<grid, kThreads, k16::kSmem, s>>>(pts16, omega4, m, n, ranges, F,
+                                                                d, c0, dc, partial);
+      }
       break;
     }
     case 2: launch_nc<2>(grid, s, pts16, omega4, m, n, ranges, F, d, c0, dc, partial); break;
