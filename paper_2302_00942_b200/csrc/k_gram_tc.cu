@@ -739,7 +739,7 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
       tc::mbar_init(&pts_empty[c], kProducerWarps);
     }
     tc::mbar_init(&accf_bar, 1);
-    tc::mbar_init(&acce_bar, kProducerWarps + (rank == 0 ? 1 : 0));
+    tc::mbar_init(&acce_bar, kProducerWarps * (rank == 0 ? 2 : 1));
     tc::mbar_fence_init();
   }
   {  // omega table (rows of padding frequencies >= m are zero)
@@ -787,31 +787,16 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
   } else if (warp == kMmaWarp) {
     // ============================================ MMA issue (leader) / relay (follower)
     if (rank == 1) {
-      // Relay: the follower's producers and drains arrive on its local full /
-      // acce barriers (release at CTA scope: cheap); one thread forwards each
-      // completed phase to the leader with ONE release at cluster scope (that
-      // arrive compiles to MEMBAR.GPU + L1 invalidate: too costly per warp).
+      // Relay: the follower's producers arrive on its local full barriers
+      // (release at CTA scope: cheap); one thread forwards each completed
+      // phase to the leader with ONE release at cluster scope (that arrive
+      // compiles to MEMBAR.GPU + L1 invalidate: too costly per warp and step).
+      // The drains (once per epoch) arrive on the leader's acce directly.
       if (lane == 0) {
-        int n_epochs = 0;  // the epochs of this CTA's step range: ceil(len / E) per segment
-        for (int lo = 0, hi = hi0; lo < nsteps; lo = hi, hi = min(nsteps, hi + Si))
-          n_epochs += (hi - lo + kPEpoch - 1) / kPEpoch;
         const uint32_t full_lead0 = tc::mapa(&full_bar[0], 0);
-        const uint32_t acce_lead = tc::mapa(&acce_bar, 0);
-        int fi = 0, ei = 0;
-        while (fi < nsteps || ei < n_epochs) {
-          bool moved = false;
-          if (fi < nsteps &&
-              tc::mbar_test_wait(&full_bar[fi % kPStages], uint32_t(fi / kPStages) & 1u)) {
-            tc::mbar_arrive_cluster(full_lead0 + 8u * uint32_t(fi % kPStages));
-            ++fi;
-            moved = true;
-          }
-          if (ei < n_epochs && tc::mbar_test_wait(&acce_bar, uint32_t(ei) & 1u)) {
-            tc::mbar_arrive_cluster(acce_lead);
-            ++ei;
-            moved = true;
-          }
-          if (!moved) __nanosleep(32);
+        for (int fi = 0; fi < nsteps; ++fi) {
+          tc::mbar_wait(&full_bar[fi % kPStages], uint32_t(fi / kPStages) & 1u);
+          tc::mbar_arrive_cluster(full_lead0 + 8u * uint32_t(fi % kPStages));
         }
       }
       __syncwarp();
@@ -888,11 +873,15 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
       diag = I == J;
     };
     int pend0 = -1, pend1 = -1, info0 = 0, info1 = 0, last0 = 0, last1 = 0;
+    const uint32_t acce_lead = tc::mapa(&acce_bar, 0);
     auto drain0 = [&]() {
       drain_epoch(tmem + lane_field, qd, lane, 2, (info0 >> 29) & 1, (info0 >> 30) & 1,
                   partial + (int64_t(info0 & 0x0FFFFFFF) * 256 + 128 * rank + rho) * 256,
                   nullptr, false);
-      if (lane == 0) tc::mbar_arrive(&acce_bar);  // leader: counted; follower: relayed
+      if (lane == 0) {  // D is free again (the follower's drains: on the leader's barrier)
+        if (rank == 0) tc::mbar_arrive(&acce_bar);
+        else tc::mbar_arrive_cluster(acce_lead);
+      }
       pend0 = pend1;
       info0 = info1;
       last0 = last1;
