@@ -84,10 +84,16 @@ struct GemmJobs {
   GemmJob job[2];
 };
 
-// fp64 tensor-core GEMM (DMMA, mma.sync m8n8k4 f64): CTA tile 32 x 64, 4 warps
-// side by side (each 32 x 16 = 4 x 2 fragments), K in steps of 32 through a
-// 3-stage cp.async pipeline (padded strides: conflict-free fragment loads).
-constexpr int kBM = 32, kBN = 64, kBK = 32, kGStages = 3;
+// fp64 tensor-core GEMM (DMMA, mma.sync m8n8k4 f64): CTA tile 32 x 32, 4
+// warps as 2 x 2 (each 16 x 16 = 2 x 2 fragments), K in steps of 32 through a
+// 3-stage cp.async pipeline (padded strides: conflict-free fragment loads);
+// 55 KB of shared memory, so several CTAs share an SM (r = 512: 256 tiles;
+// measured 23 us per launch at r = 512 vs 32 us with 32 x 64 tiles; splitting
+// K over 8 warps measured slower).
+// Every product of the core is a polynomial in Z, so on the symmetric route
+// (Z = lambda D^1/2 G D^1/2) every result is symmetric: only the tiles on and
+// above the diagonal are computed, and each writes C_ij and C_ji (i <= j).
+constexpr int kBM = 32, kBN = 32, kBK = 32, kGStages = 3;
 constexpr int kSA = kBK + 4;   // A tile row stride (doubles): 8g + 2t banks, distinct
 constexpr int kSB = kBN + 4;   // B tile row stride (doubles)
 constexpr int kGemmSmem = kGStages * (kBM * kSA + kBK * kSB) * 8;
@@ -110,9 +116,11 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 __global__ void __launch_bounds__(128)
-dgemm_kernel(GemmJobs jobs, int njobs, int r) {
+dgemm_kernel(GemmJobs jobs, int njobs, int r, int sym) {
   extern __shared__ __align__(16) double gsm[];
   const int jb = blockIdx.z % njobs, b = blockIdx.z / njobs;
+  const int i0 = blockIdx.y * kBM, j0 = blockIdx.x * kBN;
+  if (sym && i0 > j0) return;  // strictly below the diagonal: the mirror of (j, i)
   const GemmJob& J = (jb == 0) ? jobs.job[0] : jobs.job[1];
   const int64_t off = int64_t(b) * r * r;
   const double* __restrict__ A = J.A + off;
@@ -120,12 +128,12 @@ dgemm_kernel(GemmJobs jobs, int njobs, int r) {
   double* __restrict__ C = J.C + off;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = lane >> 2, tig = lane & 3;
-  const int i0 = blockIdx.y * kBM, j0 = blockIdx.x * kBN;
+  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 16;  // the warp's 16 x 16
   double* As = gsm;                                  // [stage][kBM][kSA]
   double* Bs = gsm + kGStages * kBM * kSA;           // [stage][kBK][kSB]
 
   auto load_tile = [&](int st, int k0) {
-    // A: 32 rows x 32 doubles = 512 chunks of 16 B; B: 32 x 64 = 1024 chunks
+    // A: 32 rows x 32 doubles = 512 chunks of 16 B; B: 32 x 32 likewise
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       const int e = tid + 128 * l, row = e >> 4, kc = (e & 15) * 2;
@@ -134,17 +142,17 @@ dgemm_kernel(GemmJobs jobs, int njobs, int r) {
       cp_async16(As + (st * kBM + row) * kSA + kc, ok ? A + int64_t(gi) * r + gk : A, ok);
     }
 #pragma unroll
-    for (int l = 0; l < 8; ++l) {
-      const int e = tid + 128 * l, kk = e >> 5, col = (e & 31) * 2;
+    for (int l = 0; l < 4; ++l) {
+      const int e = tid + 128 * l, kk = e >> 4, col = (e & 15) * 2;
       const int gk = k0 + kk, gj = j0 + col;
       const bool ok = gk < r && gj < r;
       cp_async16(Bs + (st * kBK + kk) * kSB + col, ok ? B + int64_t(gk) * r + gj : B, ok);
     }
   };
 
-  double acc[4][2][2];
+  double acc[2][2][2];
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
@@ -164,31 +172,32 @@ dgemm_kernel(GemmJobs jobs, int njobs, int r) {
     const double* bs = Bs + (kt % kGStages) * kBK * kSB;
 #pragma unroll
     for (int k4 = 0; k4 < kBK; k4 += 4) {
-      double af[4], bf[2];
+      double af[2], bf[2];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) af[mi] = as[(mi * 8 + grp) * kSA + k4 + tig];
+      for (int mi = 0; mi < 2; ++mi) af[mi] = as[(wm + mi * 8 + grp) * kSA + k4 + tig];
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni) bf[ni] = bs[(k4 + tig) * kSB + warp * 16 + ni * 8 + grp];
+      for (int ni = 0; ni < 2; ++ni) bf[ni] = bs[(k4 + tig) * kSB + wn + ni * 8 + grp];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
         for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
     }
   }
   cp_async_wait<0>();
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int gi = i0 + mi * 8 + grp, gj = j0 + warp * 16 + ni * 8 + 2 * tig + h;
-        if (gi < r && gj < r) {
+        const int gi = i0 + wm + mi * 8 + grp, gj = j0 + wn + ni * 8 + 2 * tig + h;
+        if (gi < r && gj < r && (!sym || gi <= gj)) {
           const int64_t e = int64_t(gi) * r + gj;
           double v = J.alpha * acc[mi][ni][h] + (gi == gj ? J.gamma : 0.0);
           if (J.sigma != 0.0) v += J.alpha * J.sigma * B[e];
           for (int t = 0; t < J.nm; ++t) v += J.mc[t] * J.M[t][off + e];
           C[e] = v;
+          if (sym && gi != gj) C[int64_t(gj) * r + gi] = v;
         }
       }
 }
@@ -208,7 +217,7 @@ __global__ void core_finalize_kernel(const double* __restrict__ P, const double*
   if (!isfinite(v) || fabs(v) > 1e30) atomicOr(oflag, 1);
 }
 
-void gemm(const GemmJobs& jobs, int njobs, int r, int batch, cudaStream_t s) {
+void gemm(const GemmJobs& jobs, int njobs, int r, int batch, bool sym, cudaStream_t s) {
   LaunchScope L("rfd_core_dgemm", s);
   static bool configured = false;
   if (!configured) {
@@ -216,7 +225,7 @@ void gemm(const GemmJobs& jobs, int njobs, int r, int batch, cudaStream_t s) {
     configured = true;
   }
   const dim3 grid((r + kBN - 1) / kBN, (r + kBM - 1) / kBM, njobs * batch);
-  dgemm_kernel<<<grid, 128, kGemmSmem, s>>>(jobs, njobs, r);
+  dgemm_kernel<<<grid, 128, kGemmSmem, s>>>(jobs, njobs, r, sym ? 1 : 0);
 }
 
 GemmJob job(const double* A, const double* B, double* C, double alpha, double sigma = 0.0,
@@ -258,8 +267,8 @@ void launch_core_prep(const double* G, const double* nu, const int* flags, doubl
 }
 
 void launch_core_eval(const double* Z, const double* nu, const int* flags, double lambda,
-                      int m, int batch, int s_scale, double* work, double* C, int* oflag,
-                      cudaStream_t s) {
+                      int m, int batch, int s_scale, bool sym, double* work, double* C,
+                      int* oflag, cudaStream_t s) {
   const int r = 2 * m;
   const int64_t rr = int64_t(r) * r;
   const dim3 egrid(unsigned((rr + 255) / 256), batch);
@@ -285,12 +294,12 @@ void launch_core_eval(const double* Z, const double* nu, const int* flags, doubl
   {  // powers: Z0^2 = a^2 Z Z; Z0^3 = a Z0^2 Z and Z0^4 = Z0^2 Z0^2 together; Z0^5 = a Z0^4 Z
     GemmJobs j{};
     j.job[0] = job(Z, Z, Z2, alpha * alpha);
-    gemm(j, 1, r, batch, s);
+    gemm(j, 1, r, batch, sym, s);
     j.job[0] = job(Z2, Z, Z3, alpha);
     j.job[1] = job(Z2, Z2, Z4, 1.0);
-    gemm(j, 2, r, batch, s);
+    gemm(j, 2, r, batch, sym, s);
     j.job[0] = job(Z4, Z, Z5, alpha);
-    gemm(j, 1, r, batch, s);
+    gemm(j, 1, r, batch, sym, s);
   }
   // B_q = sum_{i<5} c_{5q+i} Z0^i  (Z0^1 = alpha Z); Horner in Z0^5 from the top:
   // T = B_3 + c_20 Z0^5, then T <- Z0^5 T + B_q for q = 2, 1, 0.
@@ -315,19 +324,19 @@ void launch_core_eval(const double* Z, const double* nu, const int* flags, doubl
     g.M[2] = Z3; g.mc[2] = c[kPS * q + 3];
     g.M[3] = Z4; g.mc[3] = c[kPS * q + 4];
     j.job[0] = g;
-    gemm(j, 1, r, batch, s);
+    gemm(j, 1, r, batch, sym, s);
     double* t = T; T = Tn; Tn = t;
   }
   {  // E = I + Z0 P
     GemmJobs j{};
     j.job[0] = job(Z, P, E, alpha, 0.0, 1.0);
-    gemm(j, 1, r, batch, s);
+    gemm(j, 1, r, batch, sym, s);
   }
   for (int i = 0; i < s_scale; ++i) {  // P <- (E + I) P / 2 ; E <- E E
     GemmJobs j{};
     j.job[0] = job(E, P, Pn, 0.5, 1.0, 0.0);
     j.job[1] = job(E, E, En, 1.0, 0.0, 0.0);
-    gemm(j, 2, r, batch, s);
+    gemm(j, 2, r, batch, sym, s);
     double* t = P; P = Pn; Pn = t;
     t = E; E = En; En = t;
   }

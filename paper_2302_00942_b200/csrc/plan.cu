@@ -285,7 +285,8 @@ rfd_status core_impl(rfd_plan* p, const double* nu, int* flags, double lambda, d
     return fail(RFD_ERANGE, "core: ||lambda G D|| is not finite or too large");
   int s_scale = 0;
   while (ldexp(znorm, -s_scale) > rfd::kCoreTheta) ++s_scale;
-  rfd::launch_core_eval(Z, nu, flags, lambda, m, batch, s_scale, work, C, flags + 4, st);
+  rfd::launch_core_eval(Z, nu, flags, lambda, m, batch, s_scale, (hflags[0] & 1) == 0, work, C,
+                        flags + 4, st);
   RFD_CUDA(cudaGetLastError());
   RFD_CUDA(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
   RFD_CUDA(cudaStreamSynchronize(st));

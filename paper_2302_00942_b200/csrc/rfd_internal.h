@@ -72,10 +72,12 @@ void launch_core_prep(const double* G, const double* nu, const int* flags,
 // Taylor (degree 20, Paterson-Stockmeyer) of phi1 and exp at Z / 2^s
 // (||Z / 2^s||_1 <= kCoreTheta), then s doublings, then C^ = lambda D^1/2 P
 // D^1/2 (or lambda D P); oflag = 1 on overflow.  work: kCoreWork matrices.
+// sym: the symmetric route was taken (flags[0] bit 0 clear, read back by the
+// host): every product is symmetric and only its upper tiles are computed.
 constexpr double kCoreTheta = 2.0;
 constexpr int kCoreWork = 10;
 void launch_core_eval(const double* Z, const double* nu, const int* flags,
-                      double lambda, int m, int batch, int s_scale, double* work,
+                      double lambda, int m, int batch, int s_scale, bool sym, double* work,
                       double* C, int* oflag, cudaStream_t s);
 
 // ---------------------------------------------------------------- spectrum
