@@ -88,6 +88,18 @@ def peaks_of(pk):
             "hbm": pk["hbm_gbs"] * 1e9, "f16": bf16, "tf32": bf16 / 2}
 
 
+def ncu_traffic(name):
+    """DRAM bytes per launch of kernel `name` from the committed `ncu --set full`
+    capture of this workload (profiles/traffic.json, written by
+    tools/save_profiles.sh via tools/ncu_traffic.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            e = json.load(f).get(name)
+        return None if e is None else float(e["bytes_per_launch"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def roofline_of(name, N, m, d, ms_per_launch, pk):
     """Roofline of one kernel: the slowest of its algorithmic HBM bytes, tensor
     flops (tensor-core kernels: the contraction runs there) or FP32 FMA (SIMT
@@ -105,7 +117,9 @@ def roofline_of(name, N, m, d, ms_per_launch, pk):
         terms["alu"] = w["fma"] / P["fma"]
     bound = max(terms, key=terms.get)
     t_roof = terms[bound]
-    out = {"bound": bound, "frac": t_roof / t, "traffic": None,
+    out = {"bound": bound, "frac": t_roof / t, "traffic": ncu_traffic(name),
+           "traffic_note": "DRAM read+write bytes per launch, ncu --set full of tools/profile_step.py "
+                           "(cfg 5; profiles/traffic.json); algorithmic bytes per launch: %.4g" % w["bytes"],
            "terms_ms": {k: v * 1e3 for k, v in terms.items()}}
     if bound == "hbm":
         out.update(achieved=w["bytes"] / t / 1e9, peak=P["hbm"] / 1e9, unit="GB/s")

@@ -8,3 +8,5 @@ cp gpurun_out/smoke.log profiles/${T}_smoke.txt
 cp gpurun_out/launches.csv profiles/${T}_launches.csv
 python tools/ncu_launches.py gpurun_out/launches.csv > profiles/${T}_launches.txt
 { echo "# ncu --set full --clock-control none, tools/profile_step.py (cfg5 plan + integrate), tag $T"; python tools/ncu_summary.py gpurun_out/full.ncu-rep; [ -f gpurun_out/full2.ncu-rep ] && python tools/ncu_summary.py gpurun_out/full2.ncu-rep; } > profiles/${T}_ncu_full.txt
+python tools/ncu_traffic.py gpurun_out/full.ncu-rep $( [ -f gpurun_out/full2.ncu-rep ] && echo gpurun_out/full2.ncu-rep ) > profiles/traffic.json
+cp profiles/traffic.json profiles/${T}_traffic.json
