@@ -18,6 +18,9 @@
 // overlaps the MMAs.  The epilogue (TMEM -> registers, + F, store) of tile t
 // runs after the first chunk of tile t+1 has been produced.  Persistent CTAs
 // over contiguous tile ranges; d is handled in column chunks of <= 16.
+#include <cstdio>
+#include <cstdlib>
+
 #include "rfd_internal.h"
 #include "tc_ptx.cuh"
 
@@ -38,7 +41,14 @@ constexpr size_t kPass2MaxSmem = 200 * 1024;
 
 // KF = features per K-chunk: 128 (64 frequencies) or, for m <= 32, 64 (32
 // frequencies: no chunk half filled with padding frequencies).
-template <int KF>
+// Diagnostics (RFD_P2_TRACE=1): per-chunk / per-tile timestamps of CTA 0.
+__device__ long long g_p2trace[1024][5];
+__device__ long long g_p2tile[256][6];
+
+// kFuse (part != nullptr) is a separate instantiation: the fused a7 prologue
+// is most of the kernel's code, and compiled into the plain kernel it cost
+// 6 % (0.73 -> 0.78 ms at cfg 5).
+template <int KF, bool kFuse, bool kTr = false>
 __global__ void __launch_bounds__(kThreads, 1)
 pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4, int m, int64_t n,
                 int batch, const float* __restrict__ Y, const float* F, float* out, int d, int c0,
@@ -70,7 +80,6 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   // fused a7: S_b (fp64 [2m][dc]) and Y_b (fp32 [2m][dc]) after the omegas
   double* Ss = reinterpret_cast<double*>(oz + nch * kFpc);
   float* Ys = reinterpret_cast<float*>(Ss + 2 * m * dc);
-  const bool fuse = part != nullptr;
   __shared__ unsigned int ymax_bits[64];
   __shared__ float yscale_inv[64];
   const uint32_t kColA = 2 * nw;
@@ -101,6 +110,8 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   const uint32_t tmem = tmem_sh;
   const uint32_t lane_field = uint32_t(lg * 32) << 16;
   const uint32_t idesc = tc::make_idesc(0, 128, nw);
+  const bool trc = kTr && blockIdx.x == 0 && lane == 0;
+  __shared__ long long trs[kTr ? 128 : 1][5], trt[kTr ? 32 : 1][6];
 
   const int64_t tpc = (n + kTile - 1) / kTile;
   const int64_t ntiles = tpc * batch;
@@ -114,7 +125,7 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
     const int r = 2 * m;
     const float* Yb = Y + int64_t(b) * 2 * m * d;
     int ystride = d, ycol = c0;  // Y element (a, j) at Yb[a * ystride + ycol + j]
-    if (fuse) {
+    if constexpr (kFuse) {
       // S = sum over the ranges' partials, in range order (fp64)
       const float* pb = part + int64_t(b) * ranges * r * dc;
       for (int e = tid; e < r * dc; e += kThreads) {
@@ -208,21 +219,29 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   // Each producer lane's point, copied one tile ahead into a private 2-slot
   // shared-memory ring (cp.async: no register scoreboard on the global load).
   __shared__ __align__(16) float4 xring[2][kProducerWarps][32];
-  auto copy_x = [&](int64_t t, int slot) {
-    const int bt = int(t / tpc);
-    const int64_t i = (t % tpc) * kTile + lg * 32 + lane;
+  auto copy_x = [&](int bt, int64_t tin, int slot) {
+    const int64_t i = tin * kTile + lg * 32 + lane;
     // points past the cloud's end read its first point (finite; their rows
     // of the output are never stored)
     tc::cp_async16(tc::smem_addr(&xring[slot][warp][lane]), pts + int64_t(bt) * n + (i < n ? i : 0));
     tc::cp_async_commit();
   };
+  // (cloud, tile within the cloud) advance incrementally: no 64-bit division
+  // per tile (measured: ~1500 cycles of producer bubble at every tile change)
+  int b = int(t_begin / tpc);
+  int64_t tin = t_begin - int64_t(b) * tpc;
   for (int64_t tile = t_begin; tile < t_end; ++tile, ++it) {
-    const int b = int(tile / tpc);
-    const int64_t base = (tile % tpc) * kTile;
+    const int64_t base = tin * kTile;
+    int nb = b;  // the next tile's cloud and index
+    int64_t ntin = tin + 1;
+    if (ntin == tpc) {
+      ntin = 0;
+      ++nb;
+    }
     if (b != cur_b) {
       if (g > 0) tc::mbar_wait(&empty_bar[(g - 1) % kStages], ((g - 1) / kStages) & 1);
       __syncthreads();
-      load_y(b, (tile % tpc) == 0);  // this CTA holds the cloud's first tile
+      load_y(b, tin == 0);  // this CTA holds the cloud's first tile
       __syncthreads();
       cur_b = b;
     }
@@ -231,15 +250,18 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       // ---------------- producers: 16 frequencies per thread per chunk -----
       const int q = warp >> 2;  // which 16 of the chunk's 64 frequencies
       // This tile's point (prefetched during the previous tile) and the next's.
-      if (tile == t_begin) copy_x(tile, 0);
-      if (tile + 1 < t_end) copy_x(tile + 1, int(it + 1) & 1);
+      if (trc && warp == 0 && it < 32) trt[it][5] = clock64();
+      if (tile == t_begin) copy_x(b, tin, 0);
+      if (tile + 1 < t_end) copy_x(nb, ntin, int(it + 1) & 1);
       else tc::cp_async_commit();
       tc::cp_async_wait<1>();  // this tile's copy
       const float4 x = xring[it & 1][warp][lane];
       const float2 xx = make_float2(x.x, x.x), xy = make_float2(x.y, x.y), xz = make_float2(x.z, x.z);
       for (int c = 0; c < nch; ++c) {
         const uint32_t gg = g + c, s = gg % kStages, u = gg / kStages;
+        if (trc && warp == 0 && gg < 128) trs[gg][0] = clock64();
         if (u >= 1) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
+        if (trc && warp == 0 && gg < 128) trs[gg][1] = clock64();
         const uint32_t acol = tmem + lane_field + kColA + 128 * s + (KF / 8) * q;
 #pragma unroll
         for (int h = 0; h < KF / 64; ++h) {  // halves of 8 frequencies (register pressure)
@@ -274,17 +296,22 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
         tc::tmem_st_wait();
         tc::tc_fence_before();
         __syncwarp();
+        if (trc && warp == 0 && gg < 128) trs[gg][2] = clock64();
         if (lane == 0) tc::mbar_arrive(&full_bar[s]);
       }
     } else if (warp == kMmaWarp) {
       // ---------------- MMA issue: warp-uniform loop, one elected lane -----
+      if (trc && it < 32) trt[it][0] = clock64();
       if (it >= 2) tc::mbar_wait(&dempty_bar[buf], ((it - 2) >> 1) & 1);
+      if (trc && it < 32) trt[it][1] = clock64();
       const uint32_t dcol = tmem + nw * buf;
       const uint64_t bh0 = tc::make_sdesc(yb_s, kLBO, sbo);
       const uint64_t bl0 = tc::make_sdesc(yl_s, kLBO, sbo);
       for (int c = 0; c < nch; ++c) {
         const uint32_t gg = g + c, s = gg % kStages, u = gg / kStages;
+        if (trc && gg < 128) trs[gg][3] = clock64();
         tc::mbar_wait(&full_bar[s], u & 1);
+        if (trc && gg < 128) trs[gg][4] = clock64();
         tc::tc_fence_after();
         if (tc::elect_one()) {
           const uint32_t a0 = tmem + kColA + 128 * s;
@@ -308,7 +335,10 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       // (16-column groups; D is released once every group has been read)
       const int64_t i = base + lg * 32 + lane;
       const int64_t idx = int64_t(b) * n + i;
+      const bool tre = trc && warp == kEpiWarp0 && it < 32;
+      if (tre) trt[it][2] = clock64();
       tc::mbar_wait(&dfull_bar[buf], (it >> 1) & 1);
+      if (tre) trt[it][3] = clock64();
       tc::tc_fence_after();
       for (int g16 = 0; g16 < nw; g16 += 16) {
         const int dcg = min(16, dc - g16);
@@ -352,16 +382,76 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       }
       tc::tc_fence_before();
       __syncwarp();
+      if (tre) trt[it][4] = clock64();
       if (lane == 0) tc::mbar_arrive(&dempty_bar[buf]);
     }
     g += nch;
+    b = nb;
+    tin = ntin;
   }
   tc::tc_fence_before();
   __syncthreads();
+  if (kTr && blockIdx.x == 0) {
+    for (int i = tid; i < 128 * 5; i += kThreads) g_p2trace[i / 5][i % 5] = trs[i / 5][i % 5];
+    for (int i = tid; i < 32 * 6; i += kThreads) g_p2tile[i / 6][i % 6] = trt[i / 6][i % 6];
+  }
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
 }  // namespace
+
+template <int KF, bool kFuse, bool kTr = false>
+void launch_p2(int64_t grid, size_t smem, cudaStream_t s, const float4* pts, const float4* omega4,
+               int m, int64_t n, int batch, const float* Y, const float* F, float* out, int d,
+               int c0, int dc, int nw, const float* part, int ranges, const double* C, double* S,
+               float* Yw) {
+  static bool configured = false;
+  if (!configured) {  // (the trace variant's static trace buffers take 6 KB)
+    cudaFuncSetAttribute(pass2_tc_kernel<KF, kFuse, kTr>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kPass2MaxSmem) - (kTr ? 8192 : 0));
+    configured = true;
+  }
+  pass2_tc_kernel<KF, kFuse, kTr><<<unsigned(grid), kThreads, smem, s>>>(
+      pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part, ranges, C, S, Yw);
+}
+
+static void print_p2trace(cudaStream_t s, int nch) {
+  static long long h[1024][5], t[256][6];
+  cudaStreamSynchronize(s);
+  cudaMemcpyFromSymbol(h, g_p2trace, sizeof(h));
+  cudaMemcpyFromSymbol(t, g_p2tile, sizeof(t));
+  double pe = 0, pc = 0, pr = 0, mf = 0, per = 0;
+  const int lo = 20, hi = 120;
+  for (int c = lo; c < hi; ++c) {
+    pe += h[c][1] - h[c][0];
+    pc += h[c][2] - h[c][1];
+    pr += h[c + 1][0] - h[c][2];
+    mf += h[c][4] - h[c][3];
+    per += h[c + 1][3] - h[c][3];
+  }
+  const double k = hi - lo;
+  fprintf(stderr, "p2trace chunk: period %.0f | prod empty-wait %.0f compute %.0f rest %.0f | mma full-wait %.0f\n",
+          per / k, pe / k, pc / k, pr / k, mf / k);
+  double md = 0, ew = 0, ep = 0, tp = 0;
+  const int tl = 5, th = 30;
+  for (int i = tl; i < th; ++i) {
+    md += t[i][1] - t[i][0];
+    ew += t[i][3] - t[i][2];
+    ep += t[i][4] - t[i][3];
+    tp += t[i + 1][0] - t[i][0];
+  }
+  const double kt = th - tl;
+  for (int i = 15; i < 19; ++i)
+    fprintf(stderr, "  tile %d: prod tile-top at +%lld after the last arrive, first chunk wait at +%lld\n", i,
+            t[i][5] - h[4 * i - 1][2], h[4 * i][0] - t[i][5]);
+  for (int c = 60; c < 76; ++c)
+    fprintf(stderr, "  chunk %d: mma period %lld full-wait %lld | prod empty-wait %lld compute %lld rest %lld\n",
+            c, h[c + 1][3] - h[c][3], h[c][4] - h[c][3], h[c][1] - h[c][0], h[c][2] - h[c][1],
+            h[c + 1][0] - h[c][2]);
+  fprintf(stderr, "p2trace tile (%d chunks): period %.0f | mma dempty-wait %.0f | epi dfull-wait %.0f work %.0f\n",
+          nch, tp / kt, md / kt, ew / kt, ep / kt);
+}
 
 size_t pass2_tc_smem(int m, int nw, int fuse_dc) {
   const int fpc = m <= 32 ? 32 : 64;  // frequencies per chunk (KF / 2)
@@ -384,23 +474,33 @@ void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, 
   LaunchScope L("rfd_pass2_tc", s);
   const int nw = (dc + 15) / 16 * 16;  // MMA N: the chunk's columns, padded to 16
   const size_t smem = pass2_tc_smem(m, nw, part ? dc : 0);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(pass2_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(kPass2MaxSmem));
-    cudaFuncSetAttribute(pass2_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(kPass2MaxSmem));
-    configured = true;
-  }
   const int64_t ntiles = ((n + kTile - 1) / kTile) * batch;
   int64_t grid = int64_t(sms);  // one CTA per SM (full TMEM)
   if (grid > ntiles) grid = ntiles;
-  if (m <= 32)
-    pass2_tc_kernel<64><<<unsigned(grid), kThreads, smem, s>>>(
-        pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part, ranges, C, S, Yw);
-  else
-    pass2_tc_kernel<128><<<unsigned(grid), kThreads, smem, s>>>(
-        pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part, ranges, C, S, Yw);
+  static const bool trace = [] {
+    const char* e = getenv("RFD_P2_TRACE");
+    return e && atoi(e) == 1;
+  }();
+  const bool fuse = part != nullptr;
+  if (trace && m > 32 && !fuse) {
+    launch_p2<128, false, true>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw,
+                                part, ranges, C, S, Yw);
+    print_p2trace(s, (m + 63) / 64);
+  } else if (m <= 32) {
+    if (fuse)
+      launch_p2<64, true>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part,
+                          ranges, C, S, Yw);
+    else
+      launch_p2<64, false>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part,
+                           ranges, C, S, Yw);
+  } else {
+    if (fuse)
+      launch_p2<128, true>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part,
+                           ranges, C, S, Yw);
+    else
+      launch_p2<128, false>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw,
+                            part, ranges, C, S, Yw);
+  }
 }
 
 }  // namespace rfd
