@@ -600,11 +600,13 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
           tc::mbar_arrive_expect_tx(&fst_bar, uint32_t(nv) * 64u);
           tc::bulk_g2s(bsm + 2 * kEpochB, Fb + q0 * 16, uint32_t(nv) * 64u, &fst_bar);
         }
+#pragma unroll 1
         for (int i = t; i < (npts - nv) * 16; i += 128)
           reinterpret_cast<float*>(bsm + 2 * kEpochB)[nv * 16 + i] = 0.0f;
         return;
       }
       if (vec) {
+#pragma unroll 1
         for (int i = t; i < npts * 4; i += 128) {
           const int p = i >> 2, cq = i & 3;
           const bool ok = q0 + p < n;
@@ -612,6 +614,7 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
                             ok ? Fb + (q0 + p) * d + 4 * cq : Fb, ok ? 16u : 0u);
         }
       } else {
+#pragma unroll 1
         for (int i = t; i < npts * 16; i += 128) {
           const int p = i >> 4, j = i & 15;
           const bool ok = q0 + p < n && j < dc;
@@ -695,13 +698,10 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bready_bar[e & 1]);
     };
-    if (nepochs > 0) {
-      issue_f(0);
-      process_f(0);
-    }
-    if (nepochs > 1) {
-      issue_f(1);
-      process_f(1);
+#pragma unroll 1
+    for (int e = 0; e < min(2, nepochs); ++e) {
+      issue_f(e);
+      process_f(e);
     }
     if (nepochs > 2) issue_f(2);
     float acc[32];
