@@ -440,6 +440,7 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
   tc::tc_fence_after();
   const uint32_t tmem = tmem_sh;
   const bool trc = kTr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0;
+  __shared__ long long tr1[kTr ? 128 : 1][12];  // trace in shared memory (cheap stores)
   const uint32_t lane_field = uint32_t(lg * 32) << 16;
   const int f = ft * 128 + lg * 32 + lane;  // this lane's frequency
 
@@ -475,9 +476,9 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
     uint32_t s = 0, u = 0, xr = 0;  // stage, its round, ring slot read
     for (int c = 0; c < nchunks; ++c) {
       load_x(c + 2 < nchunks);  // the slot chunk c - 1 read (ordered by its __syncwarp)
-      if (trc && warp == 0 && c < 1024) g_p1trace[c][0] = clock64();
+      if (trc && warp == 0 && c < 128) tr1[c][0] = clock64();
       if (u >= 1) tc::mbar_wait(empty_s + 8 * s, (u - 1) & 1);
-      if (trc && warp == 0 && c < 1024) g_p1trace[c][1] = clock64();
+      if (trc && warp == 0 && c < 128) tr1[c][1] = clock64();
       // Points beyond the cloud meet zero columns of F^T, and lanes beyond m
       // are never written out: no masking of the features.
       tc::cp_async_wait<2>();  // chunk c's group (c + 1, c + 2 may be in flight)
@@ -522,7 +523,7 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
       tc::tmem_st_wait();
       tc::tc_fence_before();
       __syncwarp();
-      if (trc && warp == 0 && c < 1024) g_p1trace[c][2] = clock64();
+      if (trc && warp == 0 && c < 128) tr1[c][2] = clock64();
       if (lane == 0) tc::mbar_arrive(full_s + 8 * s);
       if (++s == kStages) {
         s = 0;
@@ -537,17 +538,17 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
       const uint32_t s = c % kStages, u = c / kStages;
       const int e = c / kEpoch, ce = c % kEpoch;
       const uint32_t buf = e & 1;
-      if (trc && c < 1024) g_p1trace[c][3] = clock64();
+      if (trc && c < 128) tr1[c][3] = clock64();
       if (ce == 0) {
         if (e >= 2) tc::mbar_wait(&dempty_bar[buf], ((e - 2) >> 1) & 1);
-        if (trc && c < 1024) g_p1trace[c][4] = clock64();
+        if (trc && c < 128) tr1[c][4] = clock64();
         tc::mbar_wait(&bready_bar[buf], (e >> 1) & 1);
-      } else if (trc && c < 1024) {
-        g_p1trace[c][4] = clock64();
+      } else if (trc && c < 128) {
+        tr1[c][4] = clock64();
       }
-      if (trc && c < 1024) g_p1trace[c][5] = clock64();
+      if (trc && c < 128) tr1[c][5] = clock64();
       tc::mbar_wait(&full_bar[s], u & 1);
-      if (trc && c < 1024) g_p1trace[c][6] = clock64();
+      if (trc && c < 128) tr1[c][6] = clock64();
       tc::tc_fence_after();
       if (tc::elect_one()) {
         const uint32_t bc = b_s + buf * kEpochB + ce * kChunkB;
@@ -630,15 +631,15 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
     const int j = t & 15, g0 = t >> 4;
     auto process_f = [&](int e) {
       const int npts = epoch_pts(e);
-      const bool tr = trc && fw == 0 && e * kEpoch < 1024;
-      if (tr) g_p1trace[e * kEpoch][8] = clock64();
+      const bool tr = trc && fw == 0 && e * kEpoch < 128;
+      if (tr) tr1[e * kEpoch][8] = clock64();
       if (bulk)
         tc::mbar_wait(&fst_bar, uint32_t(e) & 1u);
       else
         tc::cp_async_wait<0>();
-      if (tr) g_p1trace[e * kEpoch][9] = clock64();
+      if (tr) tr1[e * kEpoch][9] = clock64();
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (tr) g_p1trace[e * kEpoch][10] = clock64();
+      if (tr) tr1[e * kEpoch][10] = clock64();
       // per-channel max |F|: thread t takes channels 4 (t % 4) .. + 3 of points
       // t / 4 + 32 i (16-byte reads), then lanes of equal t % 4 and the warps
       {
@@ -661,9 +662,9 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
         }
         if (lane < 4) *reinterpret_cast<float4*>(&fmax_part[e & 1][fw][4 * lane]) = mx;
       }
-      if (tr) g_p1trace[e * kEpoch][11] = clock64();
+      if (tr) tr1[e * kEpoch][11] = clock64();
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (tr) g_p1trace[e * kEpoch + 1][8] = clock64();
+      if (tr) tr1[e * kEpoch + 1][8] = clock64();
       const float(*fp)[16] = fmax_part[e & 1];
       const float cm = fmaxf(fmaxf(fp[0][j], fp[1][j]), fmaxf(fp[2][j], fp[3][j]));
       // scale 2^e_j with max |F_j| 2^e_j in [2^13, 2^14) (1 for a zero or
@@ -690,10 +691,10 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
         tc::st_shared_v4(eb + off, hi[0], hi[1], hi[2], hi[3]);
         tc::st_shared_v4(eb + off + kBBytes, lo[0], lo[1], lo[2], lo[3]);
       }
-      if (tr) g_p1trace[e * kEpoch + 1][9] = clock64();
+      if (tr) tr1[e * kEpoch + 1][9] = clock64();
       // the staging block is rewritten by the next epoch's copies
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (tr) g_p1trace[e * kEpoch + 1][10] = clock64();
+      if (tr) tr1[e * kEpoch + 1][10] = clock64();
       tc::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bready_bar[e & 1]);
@@ -709,9 +710,9 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
     for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
     for (int e = 0; e < nepochs; ++e) {
       const uint32_t buf = e & 1;
-      if (trc && fw == 0 && e * kEpoch + 2 < 1024) g_p1trace[e * kEpoch + 2][7] = clock64();
+      if (trc && fw == 0 && e * kEpoch + 2 < 128) tr1[e * kEpoch + 2][7] = clock64();
       tc::mbar_wait(&dfull_bar[buf], (e >> 1) & 1);
-      if (trc && fw == 0 && e * kEpoch + 3 < 1024) g_p1trace[e * kEpoch + 3][7] = clock64();
+      if (trc && fw == 0 && e * kEpoch + 3 < 128) tr1[e * kEpoch + 3][7] = clock64();
       tc::tc_fence_after();
       float v[32];
       tc::tmem_ld32(tmem + lane_field + 32 * buf, v);
@@ -727,10 +728,10 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
       // buffer e & 1 (B and scales) is free once epoch e's MMAs completed and
       // all four warps have read its scales
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (trc && fw == 0 && e * kEpoch + 4 < 1024) g_p1trace[e * kEpoch + 4][7] = clock64();
+      if (trc && fw == 0 && e * kEpoch + 4 < 128) tr1[e * kEpoch + 4][7] = clock64();
       if (e + 2 < nepochs) process_f(e + 2);
       if (e + 3 < nepochs) issue_f(e + 3);
-      if (trc && fw == 0 && e * kEpoch + 5 < 1024) g_p1trace[e * kEpoch + 5][7] = clock64();
+      if (trc && fw == 0 && e * kEpoch + 5 < 128) tr1[e * kEpoch + 5][7] = clock64();
     }
     if (f < m) {
       // partial[b][rg][2m][dc]: row 2f = cos, 2f + 1 = sin (interleaved order)
@@ -746,6 +747,8 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
   }
   tc::tc_fence_before();
   __syncthreads();
+  if (kTr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+    for (int i = tid; i < 128 * 12; i += (PW + 5) * 32) g_p1trace[i / 12][i % 12] = tr1[i / 12][i % 12];
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
@@ -1094,7 +1097,7 @@ static void print_p1trace(cudaStream_t s, int64_t n, int ranges) {
   cudaStreamSynchronize(s);
   cudaMemcpyFromSymbol(h, g_p1trace, sizeof(h));
   const int nc = int((((n + kChunk - 1) / kChunk) + ranges - 1) / ranges);
-  const int lo = 64, hi = nc < 1000 ? nc - 8 : 1000;
+  const int lo = 16, hi = nc < 120 ? nc - 8 : 120;
   double pe = 0, pc = 0, mr = 0, mb = 0, mf = 0, per = 0;
   for (int c = lo; c < hi; ++c) {
     pe += h[c][1] - h[c][0];
