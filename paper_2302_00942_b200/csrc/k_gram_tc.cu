@@ -207,6 +207,7 @@ __device__ __forceinline__ void drain_epoch(uint32_t tm_lane, int q, int lane, i
 
 // Diagnostics: per-step timestamps of CTA 0 (mode 3).
 __device__ long long g_trace[4096][8];
+__device__ int g_trace_cta;  // mode 6: the traced CTA
 
 // kMode (diagnostics only, RFD_GRAM_MODE): 0 = normal, 1 = no MMAs issued,
 // 2 = no feature generation (the pipeline still runs; results are wrong).
@@ -727,6 +728,11 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
   const int Si = int(sc.S);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t sbase = tc::smem_addr(smem);
+  // diagnostics (RFD_GRAM_MODE=6): steps kTr0 .. kTr0 + 127 of CTA g_trace_cta,
+  // timestamps in shared memory (cheap), copied out at the end
+  __shared__ long long gtr[kTrace ? 128 : 1][8];
+  constexpr int kTr0 = 400;
+  const bool trc = kTrace && int(blockIdx.x) == g_trace_cta;
 
   if (tid == 0) {
     // full / acce: the CTA's 16 warps, plus (leader) the follower's relay
@@ -815,9 +821,9 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
         const bool efirst = (k & (kPEpoch - 1)) == 0;
         const bool elast = ((k + 1) & (kPEpoch - 1)) == 0 || it + 1 == m_hi;
         if (efirst && epoch > 0) tc::mbar_wait_cluster(&acce_bar, uint32_t(epoch - 1) & 1u);
-        if (kTrace && blockIdx.x == 0 && it < 4096 && lane == 0) g_trace[it][0] = clock64();
+        if (kTrace && trc && (lane == 0) && unsigned(it - kTr0) < 128u) gtr[it - kTr0][0] = clock64();
         tc::mbar_wait_cluster(&full_bar[s], uint32_t(it / kPStages) & 1u);
-        if (kTrace && blockIdx.x == 0 && it < 4096 && lane == 0) g_trace[it][1] = clock64();
+        if (kTrace && trc && (lane == 0) && unsigned(it - kTr0) < 128u) gtr[it - kTr0][1] = clock64();
         tc::tc_fence_after();
         __syncwarp();
         const uint32_t stage = sbase + uint32_t(s) * kPStageBytes;
@@ -914,12 +920,12 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
         __syncwarp();
         drain0();
       }
-      if (kTrace && blockIdx.x == 0 && it < 4096 && tid == 160) g_trace[it][2] = clock64();
+      if (kTrace && trc && (tid == 160) && unsigned(it - kTr0) < 128u) gtr[it - kTr0][2] = clock64();
       if (it >= kPStages) tc::mbar_wait(&empty_bar[s], ph ^ 1u);
       if (it % kChunkSteps == 0 || it == 0)
         tc::mbar_wait(&pts_bar[ch % kChunks], uint32_t(ch / kChunks) & 1u);
       __syncwarp();
-      if (kTrace && blockIdx.x == 0 && it < 4096 && tid == 160) g_trace[it][3] = clock64();
+      if (kTrace && trc && (tid == 160) && unsigned(it - kTr0) < 128u) gtr[it - kTr0][3] = clock64();
       const int cnt = (it == tail_it) ? tail : kStep;
       const float* grp = reinterpret_cast<const float*>(
           ring + (ch % kChunks) * kChunkBytes + (it % kChunkSteps) * kStepBytes + q * kGroupBytes);
@@ -976,16 +982,16 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
         tc::st_shared_v4(loR + off_c, cl[0], cl[1], cl[2], cl[3]);
         tc::st_shared_v4(loR + off_s, sl[0], sl[1], sl[2], sl[3]);
       }
-      if (kTrace && blockIdx.x == 0 && it < 4096 && tid == 160) g_trace[it][4] = clock64();
+      if (kTrace && trc && (tid == 160) && unsigned(it - kTr0) < 128u) gtr[it - kTr0][4] = clock64();
       // a second, mid-step probe: the MMA warp idles until the drain is done
       if (pend0 >= 0 && __any_sync(0xffffffffu, tc::mbar_test_wait(&accf_bar, uint32_t(pend0) & 1u))) {
         __syncwarp();
         drain0();
       }
-      if (kTrace && blockIdx.x == 0 && it < 4096 && tid == 160) g_trace[it][5] = clock64();
+      if (kTrace && trc && (tid == 160) && unsigned(it - kTr0) < 128u) gtr[it - kTr0][5] = clock64();
       tc::fence_proxy_async_smem();
       __syncwarp();
-      if (kTrace && blockIdx.x == 0 && it < 4096 && tid == 160) g_trace[it][6] = clock64();
+      if (kTrace && trc && (tid == 160) && unsigned(it - kTr0) < 128u) gtr[it - kTr0][6] = clock64();
       if (lane == 0) {
         tc::mbar_arrive(&full_bar[s]);  // leader: counted; follower: relayed
         if (it % kChunkSteps == kChunkSteps - 1 || it == nsteps - 1)
@@ -1010,7 +1016,7 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
         }
         ++epoch;
       }
-      if (kTrace && blockIdx.x == 0 && it < 4096 && tid == 160) g_trace[it][7] = clock64();
+      if (kTrace && trc && (tid == 160) && unsigned(it - kTr0) < 128u) gtr[it - kTr0][7] = clock64();
     }
     while (pend0 >= 0) {
       tc::mbar_wait(&accf_bar, uint32_t(pend0) & 1u);
@@ -1020,6 +1026,8 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
   }
   tc::tc_fence_before();
   __syncthreads();
+  if (kTrace && trc)
+    for (int i = tid; i < 128 * 8; i += kThreads) g_trace[i / 8][i % 8] = gtr[i / 8][i % 8];
   tc::cluster_sync();
   if (warp == 0) tc::tmem_dealloc_pair<512>(tmem);
 }
@@ -1187,16 +1195,15 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, i
     {
       LaunchScope L("rfd_gram_tc", s);
       if (mode == 6) {
+        const char* tc_env = getenv("RFD_GRAM_TRACE_CTA");
+        const int tcta = tc_env ? atoi(tc_env) : 0;
+        cudaMemcpyToSymbol(g_trace_cta, &tcta, sizeof(int));
         gram_pair_kernel<true><<<2 * sc.G, kThreads, kPSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
         static long long h[4096][8];
         cudaMemcpyFromSymbol(h, g_trace, sizeof(h));
-        for (int i = 600; i < 620; ++i)
-          fprintf(stderr, "it %4d mma_wait %8lld go %8lld | prod top %8lld go %8lld comp %8lld probe %8lld fence %8lld end %8lld\n", i,
-                  h[i][0] - h[0][2], h[i][1] - h[0][2], h[i][2] - h[0][2], h[i][3] - h[0][2],
-                  h[i][4] - h[0][2], h[i][5] - h[0][2], h[i][6] - h[0][2], h[i][7] - h[0][2]);
-        // steady-state averages (cycles per step) over steps 200..1999
+        // averages (cycles per step) over the 127 traced steps
         double mw = 0, pw = 0, pc = 0, pp = 0, pf = 0, pe = 0, pt = 0, st = 0;
-        const int i0 = 200, i1 = 2000;
+        const int i0 = 0, i1 = 127;
         for (int i = i0; i < i1; ++i) {
           mw += double(h[i][1] - h[i][0]);
           pw += double(h[i][3] - h[i][2]);
@@ -1208,8 +1215,8 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, i
           st += double(h[i + 1][2] - h[i][2]);
         }
         const double k = 1.0 / (i1 - i0);
-        fprintf(stderr, "avg/step: step %.0f | mma full-wait %.0f | prod wait %.0f compute %.0f probe %.0f fence %.0f arrive %.0f top %.0f\n",
-                st * k, mw * k, pw * k, pc * k, pp * k, pf * k, pe * k, pt * k);
+        fprintf(stderr, "cta %d avg/step: step %.0f | mma full-wait %.0f | prod wait %.0f compute %.0f probe %.0f fence %.0f arrive %.0f top %.0f\n",
+                tcta, st * k, mw * k, pw * k, pc * k, pp * k, pf * k, pe * k, pt * k);
       } else {
         gram_pair_kernel<false><<<2 * sc.G, kThreads, kPSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
       }
