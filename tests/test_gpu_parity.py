@@ -165,6 +165,28 @@ def test_field_column_scales_parity():
         assert e_out <= TOL and e_del <= TOL, (c, e_out, e_del)
 
 
+def test_misaligned_field_rejected():
+    # include/rfd.h: F and out must be 16-byte aligned (pass 1 bulk-copies
+    # F blocks, pass 2 uses 16-byte loads and stores): EINVAL otherwise, and
+    # the plan stays usable.
+    n, d = 3001, 16
+    x = _sphere(n, 17)
+    F = np.random.default_rng(3).standard_normal((n, d)).astype(np.float32)
+    plan = rfd.Plan(torch.from_numpy(x).cuda(), 0.05, -0.8, 128, 9)
+    Fd = torch.from_numpy(F).cuda()
+    buf = torch.empty(n * d + 1, device="cuda")
+    Fu = buf[1:].view(n, d)
+    assert Fu.data_ptr() % 16 == 4
+    Fu.copy_(Fd)
+    with pytest.raises(rfd.RFDError, match="aligned"):
+        plan.integrate(Fu)
+    with pytest.raises(rfd.RFDError, match="aligned"):
+        plan.integrate(Fd, out=torch.empty(n * d + 1, device="cuda")[1:].view(n, d))
+    out = plan.integrate(Fd).cpu().numpy()
+    oref = orf.Plan(x, 0.05, -0.8, 128, 9).apply(F.astype(np.float64))["out"]
+    assert relerr(out, oref) <= TOL
+
+
 @pytest.mark.parametrize("cfg", [2, 4])
 def test_reparam_bitwise_equals_fresh_plan_and_oracle(cfg):
     # NEXT-4: rfd_plan_reparam keeps G and recomputes nu and C^; the result is
