@@ -368,6 +368,16 @@ def run_rfd(args, rank, world, local, pg):
     dom = max(prof.items(), key=lambda kv: kv[1][1])[0]
     roof = roofline_of(dom, N, m, d, prof[dom][1] / prof[dom][0], pk) or {}
     roof = dict(roof, kernel=dom, peak_src=pk["src"])
+    if dom == "rfd_gram_tc" and 2 * m >= 256 and roof.get("unit") == "TFLOP/s":
+        # What the kernel executes: per 256 x 256 pair tile and point, 2 (diagonal)
+        # or 3 (off-diagonal) fp16 products of the hi/lo split (Gram):
+        # even at a fully busy tensor pipe frac cannot exceed algorithmic/executed.
+        T2 = (2 * m + 255) // 256
+        ex = 2.0 * 256 * 256 * N * (2 * T2 + 3 * T2 * (T2 - 1) // 2)
+        alg = kernel_work(dom, N, m, d)["tensor_flop"]
+        t = prof[dom][1] / prof[dom][0] * 1e-3
+        roof.update(executed_tflop_per_s=ex / t / 1e12, split_ceiling_frac=alg / ex,
+                    executed_frac=ex / t / 1e12 / roof["peak"])
 
     ikern = {}
     itotal = sum(v[1] for v in iprof.values()) or 1.0
