@@ -38,12 +38,14 @@ constexpr int kStages = 3;
 // fp16), lo at +64.
 constexpr uint32_t kLBO = 128;
 constexpr size_t kPass2MaxSmem = 200 * 1024;
+constexpr size_t kCStage = 32 * 1024;  // fused a7: C^ row-block staging
 
 // KF = features per K-chunk: 128 (64 frequencies) or, for m <= 32, 64 (32
 // frequencies: no chunk half filled with padding frequencies).
 // Diagnostics (RFD_P2_TRACE=1): per-chunk / per-tile timestamps of CTA 0.
 __device__ long long g_p2trace[1024][5];
 __device__ long long g_p2tile[256][6];
+__device__ long long g_p2load[4][8];
 
 // kFuse (part != nullptr) is a separate instantiation: the fused a7 prologue
 // is most of the kernel's code, and compiled into the plain kernel it cost
@@ -80,6 +82,9 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   // fused a7: S_b (fp64 [2m][dc]) and Y_b (fp32 [2m][dc]) after the omegas
   double* Ss = reinterpret_cast<double*>(oz + nch * kFpc);
   float* Ys = reinterpret_cast<float*>(Ss + 2 * m * dc);
+  // fused a7: row blocks of C^_b staged in shared memory (kCStage bytes)
+  double* Cs = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(Ys + 2 * m * dc) + 15) & ~uintptr_t(15));
   __shared__ unsigned int ymax_bits[64];
   __shared__ float yscale_inv[64];
   const uint32_t kColA = 2 * nw;
@@ -111,7 +116,8 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   const uint32_t lane_field = uint32_t(lg * 32) << 16;
   const uint32_t idesc = tc::make_idesc(0, 128, nw);
   const bool trc = kTr && blockIdx.x == 0 && lane == 0;
-  __shared__ long long trs[kTr ? 128 : 1][5], trt[kTr ? 32 : 1][6];
+  __shared__ long long trs[kTr ? 128 : 1][5], trt[kTr ? 32 : 1][6], trl[kTr ? 4 : 1][8];
+  int ncc = 0;  // trace: cloud changes so far
 
   const int64_t tpc = (n + kTile - 1) / kTile;
   const int64_t ntiles = tpc * batch;
@@ -128,37 +134,54 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
     if constexpr (kFuse) {
       // S = sum over the ranges' partials, in range order (fp64)
       const float* pb = part + int64_t(b) * ranges * r * dc;
+#pragma unroll 1
       for (int e = tid; e < r * dc; e += kThreads) {
         double acc = 0.0;
+#pragma unroll 4
         for (int rg = 0; rg < ranges; ++rg) acc += double(__ldg(pb + int64_t(rg) * r * dc + e));
         Ss[e] = acc;
       }
       __syncthreads();
-      // Y = C^ S: a warp per row a, lanes over k, butterfly per column
-      for (int a = warp; a < r; a += kThreads / 32) {
-        const double* Ca = C + (int64_t(b) * r + a) * r;
-        for (int j0 = 0; j0 < dc; j0 += 16) {  // column groups of 16
-          double acc[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) acc[j] = 0.0;
-          for (int k = lane; k < r; k += 32) {
-            const double cv = __ldg(Ca + k);
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j0 + j < dc) acc[j] = fma(cv, Ss[k * dc + j0 + j], acc[j]);
-          }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (j0 + j < dc) {
-              double x = acc[j];
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-              if (lane == 0) Ys[a * dc + j0 + j] = float(x);
-            }
-          }
+      if (kTr && blockIdx.x == 0 && tid == 0 && ncc < 4) trl[ncc][5] = clock64();
+      // Y = C^ S by blocks of rows: the block of C^_b is copied into shared
+      // memory (row stride r + 1: conflict-free column walks), then one thread
+      // per output (a, j) runs its dot product over k.  Compact on purpose:
+      // this runs once per cloud from a cold instruction cache (the earlier
+      // warp-per-row form, unrolled over 16 columns, took ~13k cycles at r = 64).
+      const int cs = r + 1;
+      const int rb = min(r, int(kCStage / (8 * cs)));
+      for (int a0 = 0; a0 < r; a0 += rb) {
+        const int nr = min(rb, r - a0);
+        const double* src = C + (int64_t(b) * r + a0) * r;
+        const double2* src2 = reinterpret_cast<const double2*>(src);  // r even: 16-byte rows
+#pragma unroll 4
+        for (int e = tid; e < nr * r / 2; e += kThreads) {  // loads in flight together
+          const double2 v = __ldg(src2 + e);
+          const int ar = (2 * e) / r, k = 2 * e - ar * r;
+          Cs[ar * cs + k] = v.x;
+          Cs[ar * cs + k + 1] = v.y;
         }
+        __syncthreads();
+        // 8 lanes per output (k = ks, ks + 8, ...; fixed-order butterfly)
+        const int ks = lane & 7;
+#pragma unroll 1
+        for (int e0 = 0; e0 < nr * dc; e0 += kThreads / 8) {
+          const int e = e0 + (tid >> 3);
+          const bool ok = e < nr * dc;
+          const int ar = ok ? e / dc : 0, j = ok ? e - ar * dc : 0;
+          const double* Ca = Cs + ar * cs;
+          double acc = 0.0;
+#pragma unroll 4
+          for (int k = ks; k < r; k += 8) acc = fma(Ca[k], Ss[k * dc + j], acc);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+          if (ok && ks == 0) Ys[(a0 + ar) * dc + j] = float(acc);
+        }
+        __syncthreads();  // the block buffer is rewritten next
       }
       __syncthreads();
+      if (kTr && blockIdx.x == 0 && tid == 0 && ncc < 4) trl[ncc][6] = clock64();
       if (owner)
         for (int e = tid; e < r * dc; e += kThreads) {
           const int a = e / dc, j = e - (e / dc) * dc;
@@ -239,11 +262,18 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       ++nb;
     }
     if (b != cur_b) {
+      const bool trl_on = kTr && blockIdx.x == 0 && tid == 0 && ncc < 4;
+      if (trl_on) trl[ncc][0] = clock64();
       if (g > 0) tc::mbar_wait(&empty_bar[(g - 1) % kStages], ((g - 1) / kStages) & 1);
+      if (trl_on) trl[ncc][1] = clock64();
       __syncthreads();
+      if (trl_on) trl[ncc][2] = clock64();
       load_y(b, tin == 0);  // this CTA holds the cloud's first tile
+      if (trl_on) trl[ncc][3] = clock64();
       __syncthreads();
+      if (trl_on) trl[ncc][4] = clock64();
       cur_b = b;
+      ++ncc;
     }
     const uint32_t buf = it & 1;
     if (warp < kProducerWarps) {
@@ -394,6 +424,7 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   if (kTr && blockIdx.x == 0) {
     for (int i = tid; i < 128 * 5; i += kThreads) g_p2trace[i / 5][i % 5] = trs[i / 5][i % 5];
     for (int i = tid; i < 32 * 6; i += kThreads) g_p2tile[i / 6][i % 6] = trt[i / 6][i % 6];
+    for (int i = tid; i < 4 * 8; i += kThreads) g_p2load[i / 8][i % 8] = trl[i / 8][i % 8];
   }
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
@@ -417,8 +448,13 @@ void launch_p2(int64_t grid, size_t smem, cudaStream_t s, const float4* pts, con
 }
 
 static void print_p2trace(cudaStream_t s, int nch) {
-  static long long h[1024][5], t[256][6];
+  static long long h[1024][5], t[256][6], L[4][8];
   cudaStreamSynchronize(s);
+  cudaMemcpyFromSymbol(L, g_p2load, sizeof(L));
+  for (int i = 0; i < 4; ++i)
+    fprintf(stderr, "  cloud change %d: drain %lld, sync %lld, S-sum %lld, Y=CS %lld, max+convert %lld, sync %lld\n",
+            i, L[i][1] - L[i][0], L[i][2] - L[i][1], L[i][5] - L[i][2], L[i][6] - L[i][5],
+            L[i][3] - L[i][6], L[i][4] - L[i][3]);
   cudaMemcpyFromSymbol(h, g_p2trace, sizeof(h));
   cudaMemcpyFromSymbol(t, g_p2tile, sizeof(t));
   double pe = 0, pc = 0, pr = 0, mf = 0, per = 0;
@@ -457,7 +493,8 @@ size_t pass2_tc_smem(int m, int nw, int fuse_dc) {
   const int fpc = m <= 32 ? 32 : 64;  // frequencies per chunk (KF / 2)
   const int nch = (m + fpc - 1) / fpc;
   return size_t(2) * nw * nch * (2 * fpc) * 2 + size_t(nch * fpc) * 3 * sizeof(float) +
-         size_t(2 * m) * fuse_dc * (sizeof(double) + sizeof(float));
+         size_t(2 * m) * fuse_dc * (sizeof(double) + sizeof(float)) +
+         (fuse_dc > 0 ? kCStage + 16 : 0);
 }
 
 int pass2_tc_width(int m) {
@@ -486,6 +523,10 @@ void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, 
     launch_p2<128, false, true>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw,
                                 part, ranges, C, S, Yw);
     print_p2trace(s, (m + 63) / 64);
+  } else if (trace && m <= 32 && fuse) {
+    launch_p2<64, true, true>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw,
+                              part, ranges, C, S, Yw);
+    print_p2trace(s, (m + 31) / 32);
   } else if (m <= 32) {
     if (fuse)
       launch_p2<64, true>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part,
