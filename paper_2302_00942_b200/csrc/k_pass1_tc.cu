@@ -615,16 +615,23 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
                             ok ? Fb + (q0 + p) * d + 4 * cq : Fb, ok ? 16u : 0u);
         }
       } else {
+        // only the dc real channels (columns dc..15 were zeroed once, below)
 #pragma unroll 1
-        for (int i = t; i < npts * 16; i += 128) {
-          const int p = i >> 4, j = i & 15;
-          const bool ok = q0 + p < n && j < dc;
-          tc::cp_async4_zf(fs_s + uint32_t((p * kRowF + j) * 4), ok ? Fb + (q0 + p) * d + j : Fb,
-                           ok ? 4u : 0u);
+        for (int p = t; p < npts; p += 128) {
+          const bool ok = q0 + p < n;
+          const float* src = ok ? Fb + (q0 + p) * d : Fb;
+          for (int j = 0; j < dc; ++j)
+            tc::cp_async4_zf(fs_s + uint32_t((p * kRowF + j) * 4), src + (ok ? j : 0), ok ? 4u : 0u);
         }
       }
       tc::cp_async_commit();
     };
+    if (!bulk && !vec) {  // staging columns dc..15 stay zero for the whole kernel
+      float* fz = reinterpret_cast<float*>(bsm + 2 * kEpochB);
+#pragma unroll 1
+      for (int i = t; i < kEpoch * kChunk * 16; i += 128)
+        if ((i & 15) >= dc) fz[(i >> 4) * kRowF + (i & 15)] = 0.0f;
+    }
     // Thread t converts channel j = t % 16 of the 8-point groups g = t / 16 +
     // 8 i: eight staging reads, one 16-byte store each of hi and lo (the
     // groups' 8 points are one K-major core-matrix row).
