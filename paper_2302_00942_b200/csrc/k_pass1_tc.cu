@@ -70,12 +70,14 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
   constexpr int N = C::N, kStages = C::kStages, kEpoch = C::kEpoch;
   // [2 epochs][E chunks][hi | lo] B operands, then the fp32 F staging block
   extern __shared__ __align__(1024) unsigned char bsm[];
-  __shared__ uint64_t full_bar[kStages], empty_bar[kStages], dfull_bar, dempty_bar, bready_bar[2];
+  __shared__ uint64_t full_bar[kStages], empty_bar[kStages], dfull_bar, dempty_bar, bready_bar[2],
+      fst_bar;
   __shared__ uint32_t tmem_sh;
   // each producer warp's 16 points of a chunk as [x0..15 | y0..15 | z0..15],
   // 3 chunks deep (cp.async ring)
   __shared__ __align__(16) float xbuf[3][kProducerWarps][48];
   __shared__ float fmax_part[128];
+  __shared__ float4 fmax4[128];
   __shared__ float fscale_inv[2][N];  // per epoch buffer
 
   const int ft = blockIdx.x, rg = blockIdx.y, b = blockIdx.z;
@@ -97,6 +99,7 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
     tc::mbar_init(&dfull_bar, 1);
     tc::mbar_init(&dempty_bar, 4);
     for (int i = 0; i < 2; ++i) tc::mbar_init(&bready_bar[i], 4);
+    tc::mbar_init(&fst_bar, 1);
     tc::mbar_fence_init();
   }
   tc::tc_fence_before();
@@ -232,13 +235,31 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
     // Per epoch: the F block is copied into shared memory, the per-channel
     // maxima taken, and thread t converts channel (t % N) of point pairs
     // (one 32-bit word of the K-major B operand each).
-    auto stage_f = [&](int e) {
+    // d = N (32 or 64): the epoch's rows are one contiguous block -> one bulk
+    // copy (TMA engine) into unpadded rows; otherwise per-thread cp.async into
+    // rows padded to kRowF floats.  Either is issued one epoch ahead.
+    constexpr bool kPow2 = (N & (N - 1)) == 0;
+    const bool bulk = kPow2 && vec && d == N && (reinterpret_cast<uintptr_t>(Fb) & 15) == 0;
+    auto issue_f = [&](int e) {
       const int64_t q0 = p0 + int64_t(e) * (kEpoch * kChunk);  // first point of the epoch
       const int ncs = min(kEpoch, nchunks - e * kEpoch);        // chunks of this epoch
       const int npts = ncs * kChunk;
+      if (bulk) {
+        const int nv = int(min(int64_t(npts), n - q0));  // rows past the cloud: zeros
+        if (t == 0) {
+          tc::fence_proxy_async_smem();  // after the generic reads of the last epoch
+          tc::mbar_arrive_expect_tx(&fst_bar, uint32_t(nv) * (N * 4u));
+          tc::bulk_g2s(bsm + 2 * C::kEpochB, Fb + q0 * N, uint32_t(nv) * (N * 4u), &fst_bar);
+        }
+#pragma unroll 1
+        for (int i = t; i < (npts - nv) * N; i += 128)
+          reinterpret_cast<float*>(bsm + 2 * C::kEpochB)[nv * N + i] = 0.0f;
+        return;
+      }
       // the epoch's F block -> shared memory (cp.async, all in flight at once;
       // rows past the cloud and channels past dc are zero-filled)
       if (vec) {
+#pragma unroll 1
         for (int i = t; i < npts * (N / 4); i += 128) {
           const int p = i / (N / 4), cq = i % (N / 4);
           const bool ok = q0 + p < n;
@@ -246,6 +267,7 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
                             ok ? Fb + (q0 + p) * d + 4 * cq : Fb, ok ? 16u : 0u);
         }
       } else {
+#pragma unroll 1
         for (int i = t; i < npts * N; i += 128) {
           const int p = i / N, j = i % N;
           const bool ok = q0 + p < n && j < dc;
@@ -254,10 +276,74 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
         }
       }
       tc::cp_async_commit();
-      tc::cp_async_wait<0>();
+    };
+    auto process_f = [&](int e) {
+      const int ncs = min(kEpoch, nchunks - e * kEpoch);
+      const int npts = ncs * kChunk;
+      if (bulk)
+        tc::mbar_wait(&fst_bar, uint32_t(e) & 1u);
+      else
+        tc::cp_async_wait<0>();
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      // per-channel max |F| over the epoch: thread t takes channel t % N, points
-      // t / N, t / N + 128 / N, ...; then the 128 / N partial maxima per channel
+
+      // per-channel max |F| over the epoch.  Bulk (unpadded rows, N a power of
+      // two): thread t takes channels 4 (t % (N/4)) .. + 3 of points t / (N/4) +
+      // (512 / N) i with 16-byte reads; partial maxima via fmax4.
+      if (bulk) {
+        constexpr int Q = kPow2 ? N / 4 : 1, PS = 128 / Q;
+        const int cq = t % Q;
+        float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+        for (int p = t / Q; p < npts; p += PS) {
+          const float4 v = *reinterpret_cast<const float4*>(fstage + p * N + 4 * cq);
+          mx.x = fmaxf(mx.x, fabsf(v.x));
+          mx.y = fmaxf(mx.y, fabsf(v.y));
+          mx.z = fmaxf(mx.z, fabsf(v.z));
+          mx.w = fmaxf(mx.w, fabsf(v.w));
+        }
+        fmax4[t] = mx;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (t < N) {
+          const float* f4 = reinterpret_cast<const float*>(fmax4);
+          float cm = 0.0f;
+          for (int i = 0; i < PS; ++i) cm = fmaxf(cm, f4[4 * (t / 4 + Q * i) + (t % 4)]);
+          fmax_part[t] = cm;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (t < N) {
+          const float cm = fmax_part[t];
+          float scale = 1.0f;
+          if (cm > 0.0f && isfinite(cm)) {
+            int ex = 0;
+            frexpf(cm, &ex);
+            scale = ldexpf(1.0f, min(126, max(-126, 14 - ex)));
+          }
+          fmax_part[t] = scale;
+          fscale_inv[e & 1][t] = 1.0f / scale;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        // thread t converts channel j = t % N of the 8-point groups g = t / N +
+        // (128 / N) i: one 16-byte hi and lo store per group (one K-major
+        // core-matrix row); lanes walk consecutive channels (no bank conflicts)
+        const int j = t % N;
+        const float sc = fmax_part[j];
+        const float2 sc2 = make_float2(sc, sc);
+        const uint32_t eb = b_s + (e & 1) * C::kEpochB + uint32_t(j >> 3) * kSBO +
+                            uint32_t(j & 7) * 16;
+#pragma unroll 2
+        for (int g = t / N; 8 * g < npts; g += 128 / N) {
+          const float* src = fstage + 8 * g * N + j;
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 v = __fmul2_rn(sc2, make_float2(src[2 * k * N], src[(2 * k + 1) * N]));
+            tc::split_f16x2(v.x, v.y, hi[k], lo[k]);
+          }
+          const uint32_t off = uint32_t(g >> 3) * C::kChunkB + uint32_t(g & 7) * kLBO;
+          tc::st_shared_v4(eb + off, hi[0], hi[1], hi[2], hi[3]);
+          tc::st_shared_v4(eb + off + C::kBBytes, lo[0], lo[1], lo[2], lo[3]);
+        }
+      } else {
       {
         const int j = t % N, st = 128 / N;
         float m0 = 0.0f, m1 = 0.0f, m2 = 0.0f, m3 = 0.0f;  // 4 loads in flight
@@ -311,14 +397,19 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
           tc::st_shared_u32(eb + off + C::kBBytes, lo);
         }
       }
+      }  // (non-bulk)
       // the staging block and fmax_part are rewritten by the next epoch
       asm volatile("bar.sync 1, 128;" ::: "memory");
       tc::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bready_bar[e & 1]);
     };
-    if (nepochs > 0) stage_f(0);
-    if (nepochs > 1) stage_f(1);
+#pragma unroll 1
+    for (int e = 0; e < min(2, nepochs); ++e) {
+      issue_f(e);
+      process_f(e);
+    }
+    if (nepochs > 2) issue_f(2);
     const uint32_t tl = tmem + lane_field;
     float* out = partial + (int64_t(b) * ranges + rg) * int64_t(2 * m) * dc;
     for (int e = 0; e < nepochs; ++e) {
@@ -347,7 +438,8 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
       // buffer e & 1 (B and scales) is free once epoch e's MMAs completed
       // and all four warps have read its scales
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (e + 2 < nepochs) stage_f(e + 2);
+      if (e + 2 < nepochs) process_f(e + 2);
+      if (e + 3 < nepochs) issue_f(e + 3);
     }
     // L -> partial[b][rg][2m][dc]: row 2f = cos, 2f + 1 = sin (interleaved)
 #pragma unroll 1
