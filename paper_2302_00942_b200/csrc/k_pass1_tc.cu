@@ -1060,8 +1060,11 @@ pass1_tc_packed(const float* __restrict__ pts16, const float4* __restrict__ omeg
     const uint32_t fs_s = b_s + 2 * C::kEpochB;  // staging [E*64 points][N] fp32
     const float* fstage = reinterpret_cast<const float*>(bsm + 2 * C::kEpochB);
     const int ncol = R * dc;                     // real columns: 16 g + j, j < dc
-    auto stage_f = [&](int e) {
+    // the epoch's F block is copied one epoch ahead (issue_f), then maxima,
+    // scales and B operands (process_f)
+    auto issue_f = [&](int e) {
       const int npts = min(kEpoch, nchunks - e * kEpoch) * kChunk;
+#pragma unroll 1
       for (int i = t; i < npts * ncol; i += 128) {
         const int p = i / ncol, cc = i % ncol, g = cc / dc, j = cc % dc;
         const int64_t cl = int64_t(e) * kEpoch * kChunk + p;  // point of segment g
@@ -1071,6 +1074,9 @@ pass1_tc_packed(const float* __restrict__ pts16, const float4* __restrict__ omeg
         tc::cp_async4_zf(fs_s + uint32_t((p * N + 16 * g + j) * 4), src, ok ? 4u : 0u);
       }
       tc::cp_async_commit();
+    };
+    auto process_f = [&](int e) {
+      const int npts = min(kEpoch, nchunks - e * kEpoch) * kChunk;
       tc::cp_async_wait<0>();
       asm volatile("bar.sync 1, 128;" ::: "memory");
       // per-column max |F| over the epoch (real columns; the rest keep scale 1)
@@ -1117,8 +1123,12 @@ pass1_tc_packed(const float* __restrict__ pts16, const float4* __restrict__ omeg
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bready_bar[e & 1]);
     };
-    if (nepochs > 0) stage_f(0);
-    if (nepochs > 1) stage_f(1);
+#pragma unroll 1
+    for (int e = 0; e < min(2, nepochs); ++e) {
+      issue_f(e);
+      process_f(e);
+    }
+    if (nepochs > 2) issue_f(2);
     // drains: lane group lg reads its segment's blocks (cos 16 g, sin N + 16 g)
     float acc[32];
 #pragma unroll
@@ -1141,7 +1151,8 @@ pass1_tc_packed(const float* __restrict__ pts16, const float4* __restrict__ omeg
         acc[16 + j] = fmaf(vs[j], inv, acc[16 + j]);
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (e + 2 < nepochs) stage_f(e + 2);
+      if (e + 2 < nepochs) process_f(e + 2);
+      if (e + 3 < nepochs) issue_f(e + 3);
     }
     const int64_t sg = int64_t(blockIdx.x) * R + g_me;
     if (f < m && sg < nseg) {
