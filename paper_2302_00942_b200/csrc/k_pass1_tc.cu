@@ -90,6 +90,7 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
   const int nepochs = (nchunks + kEpoch - 1) / kEpoch;
   const float* cloud16 = pts16 + int64_t(b) * gpc * 48;
 
+  asm volatile("griddepcontrol.launch_dependents;");  // pass 2 may start its setup
   if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -513,6 +514,7 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
   const int nepochs = (nchunks + kEpoch - 1) / kEpoch;
   const float* cloud16 = pts16 + int64_t(b) * gpc * 48;
 
+  asm volatile("griddepcontrol.launch_dependents;");  // pass 2 may start its setup
   if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -917,6 +919,7 @@ pass1_tc_packed(const float* __restrict__ pts16, const float4* __restrict__ omeg
   }
   const int nepochs = (nchunks + kEpoch - 1) / kEpoch;
 
+  asm volatile("griddepcontrol.launch_dependents;");  // pass 2 may start its setup
   if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {

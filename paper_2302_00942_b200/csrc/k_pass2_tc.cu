@@ -112,6 +112,10 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
+  // Programmatic dependent launch: the setup above (TMEM, barriers, omegas:
+  // plan data) may overlap the previous kernel's tail; everything below reads
+  // its results (partials / Y) or the field.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem = tmem_sh;
   const uint32_t lane_field = uint32_t(lg * 32) << 16;
   const uint32_t idesc = tc::make_idesc(0, 128, nw);
@@ -443,8 +447,18 @@ void launch_p2(int64_t grid, size_t smem, cudaStream_t s, const float4* pts, con
                          int(kPass2MaxSmem) - (kTr ? 8192 : 0));
     configured = true;
   }
-  pass2_tc_kernel<KF, kFuse, kTr><<<unsigned(grid), kThreads, smem, s>>>(
-      pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part, ranges, C, S, Yw);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, pass2_tc_kernel<KF, kFuse, kTr>, pts, omega4, m, n, batch, Y, F, out,
+                     d, c0, dc, nw, part, ranges, C, S, Yw);
 }
 
 static void print_p2trace(cudaStream_t s, int nch) {

@@ -145,6 +145,7 @@ reduce_S_kernel(const float* __restrict__ partial, int r, int chunks, int d, int
 __global__ void __launch_bounds__(256)
 core_apply_kernel(const double* __restrict__ C, const double* __restrict__ S, int r, int d,
                   int rpw, float* __restrict__ Y) {
+  asm volatile("griddepcontrol.launch_dependents;");  // pass 2 may start its setup
   extern __shared__ double St[];  // [dc][r]
   const int b = blockIdx.y, c0 = blockIdx.z * 16;
   const int dc = min(16, d - c0);
