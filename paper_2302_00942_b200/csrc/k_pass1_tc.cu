@@ -106,6 +106,9 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
+  // Programmatic dependent launch: the setup above may overlap the previous
+  // kernel (pass 2 of an earlier integrate); F and the partials only after it.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem = tmem_sh;
   const uint32_t lane_field = uint32_t(lg * 32) << 16;
   const int f = ft * 128 + lg * 32 + lane;  // this lane's frequency
@@ -532,6 +535,9 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
+  // Programmatic dependent launch: the setup above may overlap the previous
+  // kernel (pass 2 of an earlier integrate); F and the partials only after it.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem = tmem_sh;
   const bool trc = kTr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0;
   __shared__ long long tr1[kTr ? 128 : 1][12];  // trace in shared memory (cheap stores)
@@ -941,6 +947,9 @@ pass1_tc_packed(const float* __restrict__ pts16, const float4* __restrict__ omeg
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
+  // Programmatic dependent launch: the setup above may overlap the previous
+  // kernel (pass 2 of an earlier integrate); F and the partials only after it.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem = tmem_sh;
   const uint32_t lane_field = uint32_t(lg * 32) << 16;
   const int g_me = lg / kGroupsPerSeg;                          // this lane group's segment
@@ -1185,8 +1194,8 @@ void launch_packed(cudaStream_t s, const float* pts16, const float4* omega4, int
     configured = true;
   }
   const int64_t ctas = (int64_t(batch) * ranges + R - 1) / R;
-  pass1_tc_packed<R><<<unsigned(ctas), kThreads, PK<R>::kSmem, s>>>(pts16, omega4, m, n, batch,
-                                                                   ranges, F, d, c0, dc, partial);
+  launch_pdl(pass1_tc_packed<R>, dim3(unsigned(ctas)), dim3(kThreads), PK<R>::kSmem, s, pts16,
+             omega4, m, n, batch, ranges, F, d, c0, dc, partial);
 }
 
 template <int NC>
@@ -1198,8 +1207,8 @@ void launch_nc(dim3 grid, cudaStream_t s, const float* pts16, const float4* omeg
                          P1<NC>::kSmem);
     configured = true;
   }
-  pass1_tc_kernel<NC><<<grid, kThreads, P1<NC>::kSmem, s>>>(pts16, omega4, m, n, ranges, F, d, c0,
-                                                           dc, partial);
+  launch_pdl(pass1_tc_kernel<NC>, grid, dim3(kThreads), P1<NC>::kSmem, s, pts16, omega4, m, n,
+             ranges, F, d, c0, dc, partial);
 }
 
 }  // namespace
@@ -1292,8 +1301,8 @@ void launch_pass1_tc(const float* pts16, const float4* omega4, int m, int64_t n,
                                                                       F, d, c0, dc, partial);
         print_p1trace(s, n, ranges);
       } else {
-        pass1_tc_kernel16<16><<<grid, kThreads, k16::kSmem, s>>>(pts16, omega4, m, n, ranges, F,
-                                                                d, c0, dc, partial);
+        launch_pdl(pass1_tc_kernel16<16>, grid, dim3(kThreads), k16::kSmem, s, pts16, omega4, m, n,
+                   ranges, F, d, c0, dc, partial);
       }
       break;
     }

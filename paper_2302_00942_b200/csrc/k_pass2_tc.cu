@@ -90,6 +90,7 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   const uint32_t kColA = 2 * nw;
   const uint32_t yb_s = tc::smem_addr(yb), yl_s = tc::smem_addr(yl);
 
+  asm volatile("griddepcontrol.launch_dependents;");  // the next pass 1 may start its setup
   if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -447,18 +448,8 @@ void launch_p2(int64_t grid, size_t smem, cudaStream_t s, const float4* pts, con
                          int(kPass2MaxSmem) - (kTr ? 8192 : 0));
     configured = true;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(grid));
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, pass2_tc_kernel<KF, kFuse, kTr>, pts, omega4, m, n, batch, Y, F, out,
-                     d, c0, dc, nw, part, ranges, C, S, Yw);
+  launch_pdl(pass2_tc_kernel<KF, kFuse, kTr>, dim3(unsigned(grid)), dim3(kThreads), smem, s, pts,
+             omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part, ranges, C, S, Yw);
 }
 
 static void print_p2trace(cudaStream_t s, int nch) {

@@ -9,6 +9,30 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
+namespace rfd {
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// once the previous kernel in the stream has executed
+// griddepcontrol.launch_dependents; it must execute griddepcontrol.wait
+// before touching that kernel's results.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+}  // namespace rfd
+
 namespace rfd {
 
 constexpr uint32_t kFreqTag = 0x52464421u;  // counter word 2 (A14)
