@@ -108,6 +108,7 @@ pass1_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4, 
 __global__ void __launch_bounds__(256)
 reduce_S_kernel(const float* __restrict__ partial, int r, int chunks, int d, int c0, int dc,
                 double* __restrict__ S) {
+  asm volatile("griddepcontrol.launch_dependents;");  // core_apply may launch
   __shared__ double red[8][33];
   const int b = blockIdx.y;
   const int el = threadIdx.x & 31, sl = threadIdx.x >> 5;
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(256)
 core_apply_kernel(const double* __restrict__ C, const double* __restrict__ S, int r, int d,
                   int rpw, float* __restrict__ Y) {
   asm volatile("griddepcontrol.launch_dependents;");  // pass 2 may start its setup
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // S from reduce_S
   extern __shared__ double St[];  // [dc][r]
   const int b = blockIdx.y, c0 = blockIdx.z * 16;
   const int dc = min(16, d - c0);
@@ -355,6 +357,7 @@ void launch_reduce_S(const float* partial, int m, int batch, int chunks, int d, 
                      double* S, cudaStream_t s) {
   LaunchScope L("rfd_reduce_S", s);
   const int r = 2 * m;
+  // (a normal launch: launched early, its waiting CTAs would sit beside pass 1's)
   reduce_S_kernel<<<dim3((r * dc + 31) / 32, batch), 256, 0, s>>>(partial, r, chunks, d, c0, dc,
                                                                    S);
 }
@@ -375,8 +378,8 @@ void launch_core_apply(const double* C, const double* S, int m, int batch, int d
   int64_t rpw64 = (int64_t(r) * batch) / (8 * 148 * 2);
   if (rpw64 > (r + 7) / 8) rpw64 = (r + 7) / 8;
   const int rpw = rpw64 < 1 ? 1 : int(rpw64);
-  core_apply_kernel<<<dim3((r + 8 * rpw - 1) / (8 * rpw), batch, (d + 15) / 16), 256, smem, s>>>(
-      C, S, r, d, rpw, Y);
+  launch_pdl(core_apply_kernel, dim3((r + 8 * rpw - 1) / (8 * rpw), batch, (d + 15) / 16),
+             dim3(256), smem, s, C, S, r, d, rpw, Y);
 }
 
 void launch_pass2(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
