@@ -408,6 +408,46 @@ def test_properties_determinism_inplace_linearity_symmetry_semigroup():
     assert relerr(two.cpu().numpy(), a.cpu().numpy()) < 1e-4
 
 
+@pytest.mark.parametrize("cfg", [1, 3, 4, 5])
+def test_back_to_back_integrates_equal_synchronised(cfg):
+    # Consecutive integrates overlap (programmatic dependent launch: pass 1's
+    # setup runs during the previous pass 2, pass 2's during pass 1 /
+    # core_apply).  Chains of in-place integrates, each output feeding the
+    # next call, with no host synchronisation must equal the same chain run
+    # with a device synchronisation after every call, bit for bit (fused a7
+    # for cfgs 1 and 3; reduce_S + core_apply for cfgs 4 and 5).
+    p, x, F = make_config(cfg)
+    if cfg == 3:
+        F = F[0]
+    if cfg == 5:
+        x, F = x[: 1 << 19], F[: 1 << 19]
+    xd = torch.from_numpy(x).cuda()
+    plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
+    F0 = torch.from_numpy(np.ascontiguousarray(F)).cuda()
+    ref = F0.clone()
+    outs_ref = []
+    for _ in range(6):
+        plan.integrate(ref, out=ref)
+        torch.cuda.synchronize()
+        outs_ref.append(ref.clone())
+    # (separate buffers: no other kernel between one call's pass 2 and the
+    # next call's pass 1)
+    bufs = [F0] + [torch.empty_like(F0) for _ in range(6)]
+    torch.cuda.synchronize()
+    for k in range(6):
+        plan.integrate(bufs[k], out=bufs[k + 1])
+    torch.cuda.synchronize()
+    for a, b in zip(bufs[1:], outs_ref):
+        assert torch.equal(a, b)
+    # the same chain in place, back to back
+    cur = F0.clone()
+    torch.cuda.synchronize()
+    for _ in range(6):
+        plan.integrate(cur, out=cur)
+    torch.cuda.synchronize()
+    assert torch.equal(cur, outs_ref[-1])
+
+
 def test_host_buffers_match_device():
     p, x, F = make_config(4)
     plan = rfd.Plan(x, p["eps"], p["lam"], p["m"], p["seed"])  # host points
