@@ -152,9 +152,10 @@ core_apply_kernel(const double* __restrict__ C, const double* __restrict__ S, in
   const int b = blockIdx.y, c0 = blockIdx.z * 16;
   const int dc = min(16, d - c0);
   const double* Sb = S + int64_t(b) * r * d + c0;
-  for (int i = threadIdx.x; i < dc * r; i += 256) {
+#pragma unroll 8
+  for (int i = threadIdx.x; i < dc * r; i += 256) {  // loads in flight together
     const int k = i / dc, j = i - k * dc;
-    St[j * r + k] = Sb[int64_t(k) * d + j];
+    St[j * r + k] = __ldg(Sb + int64_t(k) * d + j);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
