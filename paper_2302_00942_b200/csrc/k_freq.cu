@@ -98,15 +98,16 @@ __global__ void nu_kernel(const float4* __restrict__ omega4, double* __restrict_
 // as [x0..x15 | y0..y15 | z0..z15] (pass 1 reads a group with 12 16-byte
 // copies and pairs neighbouring points in packed FP32 math); the tail group is
 // zero-padded (the buffer is cleared first when n % 16 != 0).
+// I: index type (32-bit when the batch's points fit: no 64-bit division per point)
+template <typename I>
 __global__ void pack_kernel(const float* __restrict__ xyz, float4* __restrict__ pts,
-                            float* __restrict__ pts16, int64_t n, int64_t total) {
-  const int64_t gpc = (n + 15) / 16;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const float x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+                            float* __restrict__ pts16, I n, I total) {
+  const I gpc = (n + 15) / 16;
+  for (I i = blockIdx.x * I(blockDim.x) + threadIdx.x; i < total; i += I(gridDim.x) * blockDim.x) {
+    const float x = xyz[int64_t(3) * i], y = xyz[int64_t(3) * i + 1], z = xyz[int64_t(3) * i + 2];
     pts[i] = make_float4(x, y, z, 0.0f);
-    const int64_t b = i / n, k = i - b * n;
-    float* g = pts16 + (b * gpc + k / 16) * 48 + (k & 15);
+    const I b = i / n, k = i - b * n;
+    float* g = pts16 + (int64_t(b) * gpc + k / 16) * 48 + (k & 15);
     g[0] = x;
     g[16] = y;
     g[32] = z;
@@ -135,7 +136,10 @@ void launch_pack_points(const float* xyz, float4* pts, float* pts16, int64_t n, 
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  pack_kernel<<<int(blocks), 256, 0, s>>>(xyz, pts, pts16, n, total);
+  if (total < (int64_t(1) << 30))  // (i + grid stride stays below 2^31)
+    pack_kernel<int><<<int(blocks), 256, 0, s>>>(xyz, pts, pts16, int(n), int(total));
+  else
+    pack_kernel<int64_t><<<int(blocks), 256, 0, s>>>(xyz, pts, pts16, n, total);
 }
 
 }  // namespace rfd

@@ -550,13 +550,15 @@ gram_tc_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict_
 
 // Points -> Gram layout (groups of 8: x[8] y[8] z[8] 0[8]), clouds padded
 // with zero groups to S K-steps.  One thread per (padded) point.
-__global__ void gram_pack_kernel(const float4* __restrict__ pts, int64_t n, int64_t per_cloud,
-                                 int64_t total, float* __restrict__ out) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t b = i / per_cloud, p = i - b * per_cloud;
-    const float4 v = (p < n) ? __ldg(pts + b * n + p) : make_float4(0.f, 0.f, 0.f, 0.f);
-    float* g = out + (i >> 3) * 32 + (i & 7);
+// I: index type (32-bit when the batch's points fit: no 64-bit division per point)
+template <typename I>
+__global__ void gram_pack_kernel(const float4* __restrict__ pts, I n, I per_cloud, I total,
+                                 float* __restrict__ out) {
+  for (I i = blockIdx.x * I(blockDim.x) + threadIdx.x; i < total; i += I(gridDim.x) * blockDim.x) {
+    const I b = i / per_cloud, p = i - b * per_cloud;
+    const float4 v =
+        (p < n) ? __ldg(pts + int64_t(b) * n + p) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float* g = out + int64_t(i >> 3) * 32 + (i & 7);
     g[0] = v.x;
     g[8] = v.y;
     g[16] = v.z;
@@ -1188,7 +1190,11 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, i
     const int64_t per_cloud = int64_t(g.chunk) * kStep, total = per_cloud * batch;
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    gram_pack_kernel<<<int(blocks), 256, 0, s>>>(pts, n, per_cloud, total, gpts);
+    if (total < (int64_t(1) << 30))  // (i + grid stride stays below 2^31)
+      gram_pack_kernel<int><<<int(blocks), 256, 0, s>>>(pts, int(n), int(per_cloud), int(total),
+                                                         gpts);
+    else
+      gram_pack_kernel<int64_t><<<int(blocks), 256, 0, s>>>(pts, n, per_cloud, total, gpts);
   }
   const unsigned char* gp = reinterpret_cast<const unsigned char*>(gpts);
   if (pairs) {
