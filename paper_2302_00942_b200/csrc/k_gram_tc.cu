@@ -205,13 +205,11 @@ __device__ __forceinline__ void drain_epoch(uint32_t tm_lane, int q, int lane, i
   if (lane == 0 && acce_bar) tc::mbar_arrive(acce_bar);  // D is free again
 }
 
-// Diagnostics: per-step timestamps of CTA 0 (mode 3).
+// Instrumentation (RFD_GRAM_TRACE=1, pair kernel): per-step timestamps of one
+// CTA (RFD_GRAM_TRACE_CTA); results are unchanged.
 __device__ long long g_trace[4096][8];
-__device__ int g_trace_cta;  // mode 6: the traced CTA
+__device__ int g_trace_cta;
 
-// kMode (diagnostics only, RFD_GRAM_MODE): 0 = normal, 1 = no MMAs issued,
-// 2 = no feature generation (the pipeline still runs; results are wrong).
-template <int kMode>
 __global__ void __launch_bounds__(kThreads, 1)
 gram_tc_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict__ omega4, int m,
                int64_t n, const __grid_constant__ Sched sc, float* __restrict__ partial) {
@@ -311,11 +309,8 @@ gram_tc_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict_
       const int k = it - m_lo;
       const bool efirst = (k & (kEpoch - 1)) == 0;
       const bool elast = ((k + 1) & (kEpoch - 1)) == 0 || it + 1 == m_hi;
-      if (kMode == 4 && cta == 0 && it < 4096 && lane == 0) g_trace[it][0] = clock64();
       if (efirst && epoch > 0) RFD_WAIT(&acce_bar, uint32_t(epoch - 1) & 1u, 2, it);
-      if (kMode == 4 && cta == 0 && it < 4096 && lane == 0) g_trace[it][1] = clock64();
       RFD_WAIT(&full_bar[s], uint32_t(it / kStages) & 1u, 3, it);
-      if (kMode == 4 && cta == 0 && it < 4096 && lane == 0) g_trace[it][2] = clock64();
       tc::tc_fence_after();
       __syncwarp();
       const uint32_t stage = sbase + uint32_t(s) * kStageBytes;
@@ -335,7 +330,7 @@ gram_tc_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict_
           const uint64_t bhi = tc::make_sdesc(stage + kBHi + ko, kLBO, kSBO);
           const uint64_t blo = tc::make_sdesc(stage + kBLo + ko, kLBO, kSBO);
           const uint32_t acc0 = (efirst && kk == 0) ? 0u : 1u;
-          if (kMode != 1 && kMode != 3) {
+          {
             tc::mma_f16(tmem, ahi, bhi, idesc_n, acc0);
             tc::mma_f16(tmem, ahi, blo, idesc_n, 1u);
             if (!d0 && !d1) {
@@ -352,7 +347,6 @@ gram_tc_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict_
         if (elast) tc::mma_commit(&accf_bar);
       }
       __syncwarp();
-      if (kMode == 4 && cta == 0 && it < 4096 && lane == 0) g_trace[it][3] = clock64();
       if (elast) ++epoch;
       if (it + 1 == m_hi && it + 1 < nsteps) {
         ++m_bu;
@@ -400,7 +394,7 @@ gram_tc_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict_
       drain_epoch(tmem + lane_field, qd, lane, ((info0 >> 28) & 1) + 1, (info0 >> 29) & 1,
                   (info0 >> 30) & 1,
                   partial + (int64_t(info0 & 0x0FFFFFFF) * 128 + rho) * 256, &acce_bar,
-                  kMode == 5);
+                  false);
       pend0 = pend1;
       info0 = info1;
       last0 = last1;
@@ -433,12 +427,10 @@ gram_tc_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict_
         __syncwarp();
         drain0();
       }
-      if (kMode == 3 && cta == 0 && it < 4096 && lane == 0 && warp == 5) g_trace[it][0] = clock64();
       if (it >= kStages) RFD_WAIT(&empty_bar[s], ph ^ 1u, 5, it);
       if (it % kChunkSteps == 0 || it == 0)  // a chunk's points arrive together
         RFD_WAIT(&pts_bar[ch % kChunks], uint32_t(ch / kChunks) & 1u, 6, it);
       __syncwarp();
-      if (kMode == 3 && cta == 0 && it < 4096 && lane == 0 && warp == 5) g_trace[it][1] = clock64();
       const int cnt = (it == tail_it) ? tail : kStep;
       const float* grp = reinterpret_cast<const float*>(
           ring + (ch % kChunks) * kChunkBytes + (it % kChunkSteps) * kStepBytes + q * kGroupBytes);
@@ -454,7 +446,7 @@ gram_tc_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict_
       RFD_CHECK((const unsigned char*)grp >= ring && (const unsigned char*)grp + 128 <= ring + kChunks * kChunkBytes, "ring", ch, it);
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        if (i >= nloc || kMode == 2 || kMode == 4) break;
+        if (i >= nloc) break;
         RFD_CHECK((locs >> (8 * i) & 15) < sc.T, "block", locs, i);
         const int li = locs >> (8 * i);
         const float4 wi = om_s[(li & 15) * kFreqs + f];
@@ -508,7 +500,6 @@ gram_tc_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict_
           tc::st_shared_v4(stage + kALo + off_s, sl[0], sl[1], sl[2], sl[3]);
         }
       }
-      if (kMode == 3 && cta == 0 && it < 4096 && lane == 0 && warp == 5) g_trace[it][2] = clock64();
       tc::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -516,7 +507,6 @@ gram_tc_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict_
         if (it % kChunkSteps == kChunkSteps - 1 || it == nsteps - 1)
           tc::mbar_arrive(&pts_empty[ch % kChunks]);  // done with this chunk's points
       }
-      if (kMode == 3 && cta == 0 && it < 4096 && lane == 0 && warp == 5) g_trace[it][3] = clock64();
       if (elast) {
         if (pend1 >= 0) {  // queue full: the oldest epoch's MMAs are all issued
           RFD_WAIT(&accf_bar, uint32_t(pend0) & 1u, 7, it);
@@ -1126,10 +1116,8 @@ Sched make_pair_sched(int m, int64_t n, int batch, int sms) {
   return sc;
 }
 
-bool use_pairs(int m) {
-  const char* e = getenv("RFD_GRAM_PAIRS");  // "0": the 1-SM kernel (A/B comparison)
-  return (m + kFreqs - 1) / kFreqs >= 2 && !(e && e[0] == '0');
-}
+// CTA pairs from two 64-frequency blocks on (one pair-tile = 256 features).
+bool use_pairs(int m) { return (m + kFreqs - 1) / kFreqs >= 2; }
 
 }  // namespace
 
@@ -1162,26 +1150,15 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, i
   const Sched sc = pairs ? make_pair_sched(m, n, batch, 2 * g.chunks)
                          : make_sched(m, n, batch, g.chunks);
   static bool configured = false;
-  static int mode = 0;
+  static bool trace = false;
   if (!configured) {
-    cudaFuncSetAttribute(gram_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemBytes);
-    cudaFuncSetAttribute(gram_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemBytes);
-    cudaFuncSetAttribute(gram_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemBytes);
-    cudaFuncSetAttribute(gram_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemBytes);
-    cudaFuncSetAttribute(gram_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemBytes);
-    cudaFuncSetAttribute(gram_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemBytes);
+    cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     cudaFuncSetAttribute(gram_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kPSmemBytes);
     cudaFuncSetAttribute(gram_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kPSmemBytes);
-    const char* e = getenv("RFD_GRAM_MODE");  // diagnostics only
-    mode = e ? atoi(e) : 0;
+    const char* e = getenv("RFD_GRAM_TRACE");  // instrumentation only
+    trace = e && e[0] == '1';
     configured = true;
   }
   float* gpts = partial + gram_tc_partial_only(g, batch);
@@ -1200,7 +1177,7 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, i
   if (pairs) {
     {
       LaunchScope L("rfd_gram_tc", s);
-      if (mode == 6) {
+      if (trace) {
         const char* tc_env = getenv("RFD_GRAM_TRACE_CTA");
         const int tcta = tc_env ? atoi(tc_env) : 0;
         cudaMemcpyToSymbol(g_trace_cta, &tcta, sizeof(int));
@@ -1236,24 +1213,7 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, i
   }
   {
     LaunchScope L("rfd_gram_tc", s);
-    if (mode == 1)
-      gram_tc_kernel<1><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
-    else if (mode == 2)
-      gram_tc_kernel<2><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
-    else if (mode == 5)
-      gram_tc_kernel<5><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
-    else if (mode == 3 || mode == 4) {
-      if (mode == 3)
-        gram_tc_kernel<3><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
-      else
-        gram_tc_kernel<4><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
-      static long long h[4096][8];
-      cudaMemcpyFromSymbol(h, g_trace, sizeof(h));
-      for (int i = 0; i < 64; ++i)
-        fprintf(stderr, "it %3d t0 %7lld t1 %7lld t2 %7lld t3 %7lld\n", i,
-                h[i][0] - h[0][0], h[i][1] - h[0][0], h[i][2] - h[0][0], h[i][3] - h[0][0]);
-    } else
-      gram_tc_kernel<0><<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
+    gram_tc_kernel<<<sc.G, kThreads, kSmemBytes, s>>>(gp, omega4, m, n, sc, partial);
   }
   {
     LaunchScope L("rfd_gram_reduce", s);

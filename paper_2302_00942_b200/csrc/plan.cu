@@ -105,7 +105,6 @@ struct rfd_plan {
   uint64_t seed = 0;
   int scaling = 0;
   int symmetric = 1;
-  rfd::PassGeom pg{};
   // owned device state
   float4* pts = nullptr;      // batch*n
   float* pts16 = nullptr;     // batch*ceil(n/16)*48: SoA groups of 16 points (pass 1)
@@ -355,16 +354,8 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   rfd::launch_pack_points(dev_xyz, p->pts, p->pts16, n, batch, st);
   rfd::launch_freq(p->omega4, p->omega_rad4, p->nu, p->flags, m, seed, eps, RFD_TRUNCATION_R, cached_c_r(), st);
 
-  // a4: Gram -- tensor cores (tcgen05, fp16 hi/lo split) unless the SIMT
-  // kernel is requested for A/B comparison (RFD_GRAM=simt).
-  const char* gram_env = getenv("RFD_GRAM");
-  const bool gram_simt = gram_env && strcmp(gram_env, "simt") == 0;
-  if (gram_simt) {
-    const rfd::GramGeom gg = rfd::gram_geometry(m, n, batch, p->sms);
-    float* gpart = nullptr;
-    RFD_CUDA(tmp.alloc(&gpart, rfd::gram_partial_elems(gg, batch)));
-    rfd::launch_gram(p->pts, p->omega4, m, n, batch, gg, gpart, p->G, st);
-  } else {
+  // a4: Gram on the tensor cores (tcgen05, fp16 hi/lo split)
+  {
     const rfd::GramGeom gg = rfd::gram_tc_geometry(m, n, batch, p->sms);
     float* gpart = nullptr;
     RFD_CUDA(tmp.alloc(&gpart, rfd::gram_tc_partial_elems(gg, batch)));
@@ -380,7 +371,6 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
     p->symmetric = sym;
   }
 
-  p->pg = rfd::pass_geometry(m, n, batch, p->sms);
   guard.keep = true;
   *plan_out = p;
   return RFD_OK;
@@ -461,9 +451,8 @@ rfd_status ensure_workspace(rfd_plan* p, int d, cudaStream_t st) {
   dfree(p->Y, st);
   p->ws_d = 0;
   const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
-  // pass-1 partials: (chunks or ranges) x r x (column chunk <= 64)
-  const size_t part = size_t(p->batch) * (p->pg.chunks > ranges ? p->pg.chunks : ranges) * p->r *
-                      size_t(d < 64 ? d : 64);
+  // pass-1 partials: ranges x r x (column chunk <= 64)
+  const size_t part = size_t(p->batch) * ranges * p->r * size_t(d < 64 ? d : 64);
   RFD_CUDA(dalloc(&p->s_partial, part, st));
   RFD_CUDA(dalloc(&p->S, size_t(p->batch) * p->r * d, st));
   RFD_CUDA(dalloc(&p->Y, size_t(p->batch) * p->r * d, st));
@@ -480,51 +469,29 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
   p->stream = st;
   rfd_status rs = ensure_workspace(p, d, st);
   if (rs != RFD_OK) return rs;
-  // a6 on the tensor cores unless the SIMT kernel is requested (RFD_PASS1=simt,
-  // A/B comparison only).
-  static const bool p1_simt = [] {
-    const char* e = getenv("RFD_PASS1");
-    return e && strcmp(e, "simt") == 0;
-  }();
-  static const bool p2_simt = [] {
-    const char* e = getenv("RFD_PASS2");
-    return e && strcmp(e, "simt") == 0;
-  }();
   const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
   // Small r (<= 128) with d in one chunk and few partials: a7 (S reduction and
   // Y = C^ S) runs fused in pass 2's prologue -- two launches fewer per call
   // (every pass-2 CTA re-reduces its cloud's partials, hence the bound).
-  const bool fuse = !p1_simt && !p2_simt && p->r <= 128 && d <= 64 &&
+  const bool fuse = p->r <= 128 && d <= 64 &&
                     int64_t(ranges) * p->r * d <= 16384;
   // pass 1 on the tensor cores takes up to 64 columns per launch (MMA N = the
   // chunk's columns): the features are regenerated once per chunk (NEXT-2)
-  const int w1 = p1_simt ? 16 : 64;
+  const int w1 = 64;
   for (int c0 = 0; c0 < d; c0 += w1) {
     const int dc = (d - c0 < w1) ? d - c0 : w1;
-    if (p1_simt) {
-      rfd::launch_pass1(p->pts, p->omega4, p->m, p->n, p->batch, p->pg, F, d, c0, dc,
-                        p->s_partial, st);
-      rfd::launch_reduce_S(p->s_partial, p->m, p->batch, p->pg.chunks, d, c0, dc, p->S, st);
-    } else {
-      rfd::launch_pass1_tc(p->pts16, p->omega_rad4, p->m, p->n, p->batch, p->sms, ranges, F, d,
-                           c0, dc, p->s_partial, st);
-      if (!fuse) rfd::launch_reduce_S(p->s_partial, p->m, p->batch, ranges, d, c0, dc, p->S, st);
-    }
+    rfd::launch_pass1_tc(p->pts16, p->omega_rad4, p->m, p->n, p->batch, p->sms, ranges, F, d, c0,
+                         dc, p->s_partial, st);
+    if (!fuse) rfd::launch_reduce_S(p->s_partial, p->m, p->batch, ranges, d, c0, dc, p->S, st);
   }
   if (!fuse) rfd::launch_core_apply(p->C, p->S, p->m, p->batch, d, p->Y, st);
-  // a8 on the tensor cores unless the SIMT kernel is requested (RFD_PASS2=simt,
-  // A/B comparison only).
-  // pass 2 on the tensor cores takes up to 64 columns per launch (MMA N = the
-  // chunk's columns): the features are regenerated once per chunk (NEXT-2)
-  const int w2 = p2_simt ? 16 : rfd::pass2_tc_width(p->m);
+  // a8: pass 2 on the tensor cores takes up to 64 columns per launch (MMA N =
+  // the chunk's columns): the features are regenerated once per chunk (NEXT-2)
+  const int w2 = rfd::pass2_tc_width(p->m);
   for (int c0 = 0; c0 < d; c0 += w2) {
     const int dc = (d - c0 < w2) ? d - c0 : w2;
-    if (p2_simt)
-      rfd::launch_pass2(p->pts, p->omega4, p->m, p->n, p->batch, p->pg, p->Y, F, out, d, c0, dc,
-                        st);
-    else
-      rfd::launch_pass2_tc(p->pts, p->omega_rad4, p->m, p->n, p->batch, p->sms, p->Y, F, out, d,
-                           c0, dc, fuse ? p->s_partial : nullptr, ranges, p->C, p->S, p->Y, st);
+    rfd::launch_pass2_tc(p->pts, p->omega_rad4, p->m, p->n, p->batch, p->sms, p->Y, F, out, d, c0,
+                         dc, fuse ? p->s_partial : nullptr, ranges, p->C, p->S, p->Y, st);
   }
   RFD_CUDA(cudaGetLastError());
   p->last_d = d;

@@ -75,11 +75,6 @@ struct GramGeom {
   int chunks;     // point chunks per cloud
   int64_t chunk;  // points per chunk (multiple of 16)
 };
-GramGeom gram_geometry(int m, int64_t n, int batch, int sms);
-size_t gram_partial_elems(const GramGeom& g, int batch);
-void launch_gram(const float4* pts, const float4* omega4, int m, int64_t n,
-                 int batch, const GramGeom& g, float* partial, double* G,
-                 cudaStream_t s);
 // Tensor-core Gram (k_gram_tc.cu): GramGeom.ntiles holds the number of units.
 GramGeom gram_tc_geometry(int m, int64_t n, int batch, int sms);
 size_t gram_tc_partial_elems(const GramGeom& g, int batch);
@@ -128,28 +123,12 @@ void launch_bary_finish(const float* area, const float* mu, int64_t n, double* p
                         float* out, cudaStream_t s);
 
 // ---------------------------------------------------------------- passes
-struct PassGeom {
-  int fblocks;    // ceil(m / 32)
-  int chunks;     // pass-1 point chunks per cloud
-  int64_t chunk;  // points per pass-1 chunk
-  int p2_blocks;  // pass-2 persistent grid size
-};
-PassGeom pass_geometry(int m, int64_t n, int batch, int sms);
-// Partial S for columns [c0, c0 + dc) of F (row stride d):
-// partial[b][chunk][2m][dc] fp32 (interleaved features).
-void launch_pass1(const float4* pts, const float4* omega4, int m, int64_t n,
-                  int batch, const PassGeom& g, const float* F, int d, int c0,
-                  int dc, float* partial, cudaStream_t s);
-// S[b][2m][d] fp64 += fixed-order sum of the chunk partials of columns
-// [c0, c0+dc); then (after all chunks) Y = C^ S in fp32.
+// S[b][2m][d] fp64 = fixed-order sum of the `chunks` range partials of
+// columns [c0, c0+dc) (partial[b][chunk][2m][dc] fp32, interleaved features).
 void launch_reduce_S(const float* partial, int m, int batch, int chunks,
                      int d, int c0, int dc, double* S, cudaStream_t s);
 void launch_core_apply(const double* C, const double* S, int m, int batch,
                        int d, float* Y, cudaStream_t s);
-void launch_pass2(const float4* pts, const float4* omega4, int m, int64_t n,
-                  int batch, const PassGeom& g, const float* Y, const float* F,
-                  float* out, int d, int c0, int dc, cudaStream_t s);
-
 // Tensor-core pass 2 (k_pass2_tc.cu): dc <= 16 columns per launch.
 size_t pass2_tc_smem(int m, int nw, int fuse_dc);
 // widest column chunk one pass-2 launch takes (16..64) for m frequencies
