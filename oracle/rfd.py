@@ -301,15 +301,16 @@ def spectrum(G, nu, lam, n, k):
 # --------------------------------------------------------------------------
 # NEXT-1  Wasserstein barycenter (Alg. 1)
 # --------------------------------------------------------------------------
-BARY_CLAMP = 1e-20  # denominator clamp (SPEC.md:559 uses 1e-30; A20)
+BARY_CLAMP = 1e-30  # denominator clamp, SPEC.md:559 (A20)
 
 
 def barycenter(apply_k, mus, area, alpha, max_iter, tol=0.0):
     """Entropic Wasserstein barycenter, Appendix D Algorithm 1
     (lines 1036-1051), with the readings of SPEC.md:559, 628-629 (DESIGN.md
-    A20): mu reset to all-ones at each outer iteration; denominators clamped
-    at 1e-30; stop after max_iter or when ||mu_new - mu_old||_1 < tol; output
-    normalised so <a, mu> = 1.
+    A20): mu reset to all-ones at each outer iteration; both denominators
+    (FM_K(a v^i) and d^i) clamped at 1e-30, d^i before its power; stop after
+    max_iter or when ||mu_new - mu_old||_1 < tol; output normalised so
+    <a, mu> = 1.
 
     apply_k(X) applies the kernel FM_K to the columns of X (N x k).
     mus: k x N input distributions; area: N; alpha: k.
@@ -324,15 +325,11 @@ def barycenter(apply_k, mus, area, alpha, max_iter, tol=0.0):
     it = 0
     for it in range(1, max_iter + 1):
         mu_old = mu
-        # each v^i rescaled to max 1: mu and d are invariant under per-column
-        # scaling of v (w scales inversely); keeps the iterates in fp32 range
-        # on the GPU side (A20)
-        v = v / v.max(axis=0)[None, :]
         # 1. w^i <- mu^i / FM_K(a * v^i)
         w = mus.T / np.maximum(apply_k(a[:, None] * v), BARY_CLAMP)
-        # 2. d^i <- v^i * FM_K(a * w^i), clamped at 1e-30 (it is the
-        #    denominator of step 4 and the base of step 3's power; the
-        #    random-feature kernel can map positive vectors to negative ones)
+        # 2. d^i <- v^i * FM_K(a * w^i)  (the denominator of step 4 and the
+        #    base of step 3's power; the random-feature kernel can map positive
+        #    vectors to non-positive ones, so it is clamped too)
         dd = np.maximum(v * apply_k(a[:, None] * w), BARY_CLAMP)
         # 3. mu <- prod_i (d^i)^alpha_i   (mu reset to ones first)
         mu = np.prod(dd ** al[None, :], axis=1)

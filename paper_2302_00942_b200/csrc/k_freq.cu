@@ -94,23 +94,133 @@ __global__ void nu_kernel(const float4* __restrict__ omega4, double* __restrict_
   }
 }
 
-// pts: float4 (x, y, z, 0) per point.  pts16: per cloud, groups of 16 points
-// as [x0..x15 | y0..y15 | z0..z15] (pass 1 reads a group with 12 16-byte
-// copies and pairs neighbouring points in packed FP32 math); the tail group is
-// zero-padded (the buffer is cleared first when n % 16 != 0).
+// Centring (translation invariance of Eq. 9: W depends on n_i - n_j only,
+// PAPER.md:288-295).  The passes evaluate the feature argument 2 pi omega.x in
+// fp32, whose rounding error grows with |x|; every cloud is therefore moved to
+// the midpoint c of its bounding box before anything else.  Exact for the
+// operator: phi(c + y) = R(2 pi omega.c) phi(y) with R a 2x2 rotation per
+// frequency, and D commutes with R, so out = F + Phi C^ Phi^T F is unchanged;
+// G, C^, S and Y live in the rotated basis (rfd_plan_export rotates back).
+// Min / max are order-independent, so the centre (and every result) is
+// deterministic.  Ordered-integer encoding of floats: max over enc(x) is max x,
+// max over ~enc(x) is min x (both start from 0 = the identity).
+__device__ __forceinline__ unsigned int enc_f32(float f) {
+  const unsigned int u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float dec_f32(unsigned int e) {
+  return __uint_as_float((e & 0x80000000u) ? (e & 0x7fffffffu) : ~e);
+}
+
+// bbox[b][0..2] = max ~enc (min), bbox[b][3..5] = max enc (max); grid (chunks, batch)
+__global__ void __launch_bounds__(256)
+bbox_kernel(const float* __restrict__ xyz, int64_t n, unsigned int* __restrict__ bbox) {
+  const int b = blockIdx.y;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t p0 = int64_t(blockIdx.x) * per, p1 = min(p0 + per, n);
+  const float* src = xyz + int64_t(b) * n * 3;
+  unsigned int lo[3] = {0u, 0u, 0u}, hi[3] = {0u, 0u, 0u};
+  for (int64_t i = p0 + threadIdx.x; i < p1; i += blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const unsigned int e = enc_f32(src[3 * i + c]);
+      lo[c] = max(lo[c], ~e);
+      hi[c] = max(hi[c], e);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[c] = max(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = max(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      atomicMax(bbox + 6 * b + c, lo[c]);
+      atomicMax(bbox + 6 * b + 3 + c, hi[c]);
+    }
+}
+
+__device__ __forceinline__ float4 bbox_centre(const unsigned int* bb) {
+  float c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float lo = dec_f32(~bb[k]), hi = dec_f32(bb[3 + k]);
+    c[k] = lo + 0.5f * (hi - lo);
+  }
+  return make_float4(c[0], c[1], c[2], 0.0f);
+}
+
+// pts: float4 (x - c, y - c, z - c, 0) per point.  pts16: per cloud, groups of
+// 16 points as [x0..x15 | y0..y15 | z0..z15] (pass 1 reads a group with 12
+// 16-byte copies and pairs neighbouring points in packed FP32 math); the tail
+// group is zero-padded (the buffer is cleared first when n % 16 != 0).
+// centre[b] = c of cloud b.
 // I: index type (32-bit when the batch's points fit: no 64-bit division per point)
 template <typename I>
-__global__ void pack_kernel(const float* __restrict__ xyz, float4* __restrict__ pts,
-                            float* __restrict__ pts16, I n, I total) {
+__global__ void pack_kernel(const float* __restrict__ xyz, const unsigned int* __restrict__ bbox,
+                            float4* __restrict__ pts, float* __restrict__ pts16,
+                            float4* __restrict__ centre, I n, I total) {
   const I gpc = (n + 15) / 16;
   for (I i = blockIdx.x * I(blockDim.x) + threadIdx.x; i < total; i += I(gridDim.x) * blockDim.x) {
-    const float x = xyz[int64_t(3) * i], y = xyz[int64_t(3) * i + 1], z = xyz[int64_t(3) * i + 2];
-    pts[i] = make_float4(x, y, z, 0.0f);
     const I b = i / n, k = i - b * n;
+    const float4 c = bbox_centre(bbox + 6 * int64_t(b));
+    const float x = xyz[int64_t(3) * i] - c.x, y = xyz[int64_t(3) * i + 1] - c.y,
+                z = xyz[int64_t(3) * i + 2] - c.z;
+    pts[i] = make_float4(x, y, z, 0.0f);
+    if (k == 0) centre[b] = c;
     float* g = pts16 + (int64_t(b) * gpc + k / 16) * 48 + (k & 15);
     g[0] = x;
     g[16] = y;
     g[32] = z;
+  }
+}
+
+// Rotation back to the paper's (uncentred) basis for rfd_plan_export: per
+// frequency k of cloud b, R_k = [[cos a, -sin a], [sin a, cos a]], a = 2 pi
+// omega_k . c_b (fp64; omega and c are exact fp32 values).  Interleaved
+// features (2k = cos, 2k + 1 = sin).  X is r x cols per cloud: out = R X, or
+// R X R^T when `right` (cols = r).
+__device__ __forceinline__ void rot_of(const float4* omega4, const float4* centre, int b, int k,
+                                       double& cs, double& sn) {
+  const float4 w = omega4[k], c = centre[b];
+  const double t = double(w.x) * double(c.x) + double(w.y) * double(c.y) + double(w.z) * double(c.z);
+  sincospi(2.0 * t, &sn, &cs);
+}
+
+__global__ void rotate_kernel(const double* __restrict__ X, const float* __restrict__ Xf, int r,
+                              int cols, int batch, bool right, const float4* __restrict__ omega4,
+                              const float4* __restrict__ centre, double* __restrict__ out) {
+  const int64_t total = int64_t(batch) * r * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int b = int(e / (int64_t(r) * cols));
+    const int rem = int(e - int64_t(b) * r * cols);
+    const int a = rem / cols, c = rem - a * cols;
+    const int64_t base = int64_t(b) * r * cols;
+    auto at = [&](int i, int j) {
+      const int64_t o = base + int64_t(i) * cols + j;
+      return X ? X[o] : double(Xf[o]);
+    };
+    double ca, sa;
+    rot_of(omega4, centre, b, a >> 1, ca, sa);
+    const int a0 = a & ~1;
+    // row a of R: (cos, -sin) for a cos row, (sin, cos) for a sin row
+    const double ra0 = (a & 1) ? sa : ca, ra1 = (a & 1) ? ca : -sa;
+    double v;
+    if (!right) {
+      v = ra0 * at(a0, c) + ra1 * at(a0 + 1, c);
+    } else {
+      double cc, sc;
+      rot_of(omega4, centre, b, c >> 1, cc, sc);
+      const int c0 = c & ~1;
+      const double rc0 = (c & 1) ? sc : cc, rc1 = (c & 1) ? cc : -sc;
+      v = ra0 * (rc0 * at(a0, c0) + rc1 * at(a0, c0 + 1)) +
+          ra1 * (rc0 * at(a0 + 1, c0) + rc1 * at(a0 + 1, c0 + 1));
+    }
+    out[e] = v;
   }
 }
 
@@ -128,8 +238,17 @@ void launch_nu(const float4* omega4, double* nu, int* flags, int m, double eps, 
   nu_kernel<<<1, 256, 0, s>>>(omega4, nu, flags, m, eps, c_r);
 }
 
-void launch_pack_points(const float* xyz, float4* pts, float* pts16, int64_t n, int batch,
-                        cudaStream_t s) {
+void launch_pack_points(const float* xyz, float4* pts, float* pts16, float4* centre,
+                        unsigned int* bbox, int64_t n, int batch, int sms, cudaStream_t s) {
+  cudaMemsetAsync(bbox, 0, size_t(batch) * 6 * sizeof(unsigned int), s);
+  {
+    LaunchScope L("rfd_bbox", s);
+    int64_t chunks = (int64_t(sms) * 8 + batch - 1) / batch;
+    const int64_t maxc = (n + 1023) / 1024;
+    if (chunks > maxc) chunks = maxc;
+    if (chunks < 1) chunks = 1;
+    bbox_kernel<<<dim3(unsigned(chunks), unsigned(batch)), 256, 0, s>>>(xyz, n, bbox);
+  }
   LaunchScope L("rfd_pack_points", s);
   const int64_t total = n * batch;
   if (n % 16 != 0) cudaMemsetAsync(pts16, 0, size_t(batch) * ((n + 15) / 16) * 48 * sizeof(float), s);
@@ -137,9 +256,17 @@ void launch_pack_points(const float* xyz, float4* pts, float* pts16, int64_t n, 
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   if (total < (int64_t(1) << 30))  // (i + grid stride stays below 2^31)
-    pack_kernel<int><<<int(blocks), 256, 0, s>>>(xyz, pts, pts16, int(n), int(total));
+    pack_kernel<int><<<int(blocks), 256, 0, s>>>(xyz, bbox, pts, pts16, centre, int(n), int(total));
   else
-    pack_kernel<int64_t><<<int(blocks), 256, 0, s>>>(xyz, pts, pts16, n, total);
+    pack_kernel<int64_t><<<int(blocks), 256, 0, s>>>(xyz, bbox, pts, pts16, centre, n, total);
+}
+
+void launch_rotate(const double* X, const float* Xf, int r, int cols, int batch, bool right,
+                   const float4* omega4, const float4* centre, double* out, cudaStream_t s) {
+  LaunchScope L("rfd_export_rotate", s);
+  int64_t blocks = (int64_t(batch) * r * cols + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  rotate_kernel<<<unsigned(blocks), 256, 0, s>>>(X, Xf, r, cols, batch, right, omega4, centre, out);
 }
 
 }  // namespace rfd

@@ -91,7 +91,6 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
   const float* cloud16 = pts16 + int64_t(b) * gpc * 48;
 
   asm volatile("griddepcontrol.launch_dependents;");  // pass 2 may start its setup
-  if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full_bar[s], kProducerWarps);
@@ -109,6 +108,14 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
   // Programmatic dependent launch: the setup above may overlap the previous
   // kernel (pass 2 of an earlier integrate); F and the partials only after it.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // TMEM is allocated only after the wait: every CTA of the preceding
+  // tcgen05 kernel has then exited and freed its columns, so a CTA of this
+  // kernel never spins in tcgen05.alloc beside one it waits for, whatever the
+  // occupancy.
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
   const uint32_t tmem = tmem_sh;
   const uint32_t lane_field = uint32_t(lg * 32) << 16;
   const int f = ft * 128 + lg * 32 + lane;  // this lane's frequency
@@ -518,7 +525,6 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
   const float* cloud16 = pts16 + int64_t(b) * gpc * 48;
 
   asm volatile("griddepcontrol.launch_dependents;");  // pass 2 may start its setup
-  if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full_bar[s], PW);
@@ -538,6 +544,14 @@ pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ om
   // Programmatic dependent launch: the setup above may overlap the previous
   // kernel (pass 2 of an earlier integrate); F and the partials only after it.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // TMEM is allocated only after the wait: every CTA of the preceding
+  // tcgen05 kernel has then exited and freed its columns, so a CTA of this
+  // kernel never spins in tcgen05.alloc beside one it waits for, whatever the
+  // occupancy.
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
   const uint32_t tmem = tmem_sh;
   const bool trc = kTr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0;
   __shared__ long long tr1[kTr ? 128 : 1][12];  // trace in shared memory (cheap stores)
@@ -926,7 +940,6 @@ pass1_tc_packed(const float* __restrict__ pts16, const float4* __restrict__ omeg
   const int nepochs = (nchunks + kEpoch - 1) / kEpoch;
 
   asm volatile("griddepcontrol.launch_dependents;");  // pass 2 may start its setup
-  if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full_bar[s], kProducerWarps);
@@ -950,6 +963,14 @@ pass1_tc_packed(const float* __restrict__ pts16, const float4* __restrict__ omeg
   // Programmatic dependent launch: the setup above may overlap the previous
   // kernel (pass 2 of an earlier integrate); F and the partials only after it.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // TMEM is allocated only after the wait: every CTA of the preceding
+  // tcgen05 kernel has then exited and freed its columns, so a CTA of this
+  // kernel never spins in tcgen05.alloc beside one it waits for, whatever the
+  // occupancy.
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
   const uint32_t tmem = tmem_sh;
   const uint32_t lane_field = uint32_t(lg * 32) << 16;
   const int g_me = lg / kGroupsPerSeg;                          // this lane group's segment

@@ -91,7 +91,6 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   const uint32_t yb_s = tc::smem_addr(yb), yl_s = tc::smem_addr(yl);
 
   asm volatile("griddepcontrol.launch_dependents;");  // the next pass 1 may start its setup
-  if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full_bar[s], kProducerWarps);
@@ -113,10 +112,18 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  // Programmatic dependent launch: the setup above (TMEM, barriers, omegas:
-  // plan data) may overlap the previous kernel's tail; everything below reads
+  // Programmatic dependent launch: the setup above (barriers, omegas: plan
+  // data) may overlap the previous kernel's tail; everything below reads
   // its results (partials / Y) or the field.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // TMEM is allocated only after the wait: every CTA of the preceding
+  // tcgen05 kernel has then exited and freed its columns, so a CTA of this
+  // kernel never spins in tcgen05.alloc beside one it waits for, whatever the
+  // occupancy.
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_sh);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
   const uint32_t tmem = tmem_sh;
   const uint32_t lane_field = uint32_t(lg * 32) << 16;
   const uint32_t idesc = tc::make_idesc(0, 128, nw);
@@ -216,7 +223,10 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
       int ex = 0;
       if (mx > 0.0f && isfinite(mx)) {
         frexpf(mx, &ex);  // mx = f 2^ex, f in [0.5, 1)
-        scale = ldexpf(1.0f, 14 - ex);
+        // clamped like pass 1's: 2^(14 - ex) overflows to inf for max |Y_j| <
+        // 2^-113 (tiny lambda or field column); 2^126 still puts such a
+        // column's max at >= 2^13 (ex <= -113), its inverse 2^-126 is normal
+        scale = ldexpf(1.0f, min(126, max(-126, 14 - ex)));
       }
       yscale_inv[tid] = 1.0f / scale;  // exact (power of two)
       ymax_bits[tid] = __float_as_uint(scale);

@@ -108,6 +108,7 @@ struct rfd_plan {
   // owned device state
   float4* pts = nullptr;      // batch*n
   float* pts16 = nullptr;     // batch*ceil(n/16)*48: SoA groups of 16 points (pass 1)
+  float4* centre = nullptr;   // batch: bounding-box midpoint subtracted from the points
   float4* omega4 = nullptr;   // m
   float4* omega_rad4 = nullptr;  // m: fp32(2 pi omega) for the tensor-core kernels
   double* nu = nullptr;       // m
@@ -230,6 +231,7 @@ void free_plan(rfd_plan* p) {
   cudaStreamSynchronize(s);
   dfree(p->pts, s);
   dfree(p->pts16, s);
+  dfree(p->centre, s);
   dfree(p->omega4, s);
   dfree(p->omega_rad4, s);
   dfree(p->nu, s);
@@ -334,6 +336,7 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
 
   RFD_CUDA(dalloc(&p->pts, size_t(total), st));
   RFD_CUDA(dalloc(&p->pts16, size_t(batch) * size_t((n + 15) / 16) * 48, st));
+  RFD_CUDA(dalloc(&p->centre, size_t(batch), st));
   RFD_CUDA(dalloc(&p->omega4, size_t(m), st));
   RFD_CUDA(dalloc(&p->omega_rad4, size_t(m), st));
   RFD_CUDA(dalloc(&p->nu, size_t(m), st));
@@ -351,7 +354,9 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
                              cudaMemcpyHostToDevice, st));
     dev_xyz = staged;
   }
-  rfd::launch_pack_points(dev_xyz, p->pts, p->pts16, n, batch, st);
+  unsigned int* bbox = nullptr;
+  RFD_CUDA(tmp.alloc(&bbox, size_t(batch) * 6));
+  rfd::launch_pack_points(dev_xyz, p->pts, p->pts16, p->centre, bbox, n, batch, p->sms, st);
   rfd::launch_freq(p->omega4, p->omega_rad4, p->nu, p->flags, m, seed, eps, RFD_TRUNCATION_R, cached_c_r(), st);
 
   // a4: Gram on the tensor cores (tcgen05, fp16 hi/lo split)
@@ -520,33 +525,35 @@ rfd_status barycenter_impl(rfd_plan* p, const float* mu_in, const float* area,
   p->stream = st;
   const int64_t n = p->n;
   const size_t nk = size_t(n) * k;
+  const int nb = rfd::bary_blocks(n);
   TempBuffers tmp(st);
-  float *Mt = nullptr, *V = nullptr, *X = nullptr, *Y = nullptr, *mu = nullptr, *sc = nullptr,
-        *vmax = nullptr;
-  double *part = nullptr, *red = nullptr;
+  float *Mt = nullptr, *X = nullptr, *Y = nullptr;
+  double *V = nullptr, *W = nullptr, *mu = nullptr, *sc = nullptr, *part = nullptr,
+         *dpart = nullptr, *red = nullptr;
   int* flag = nullptr;
   RFD_CUDA(tmp.alloc(&Mt, nk));
-  RFD_CUDA(tmp.alloc(&V, nk));
   RFD_CUDA(tmp.alloc(&X, nk));
   RFD_CUDA(tmp.alloc(&Y, nk));
+  RFD_CUDA(tmp.alloc(&V, nk));
+  RFD_CUDA(tmp.alloc(&W, nk));
   RFD_CUDA(tmp.alloc(&mu, size_t(n)));
-  RFD_CUDA(tmp.alloc(&part, size_t(rfd::bary_blocks(n))));
-  RFD_CUDA(tmp.alloc(&vmax, size_t(rfd::bary_blocks(n)) * 16));
   RFD_CUDA(tmp.alloc(&sc, size_t(16)));
+  RFD_CUDA(tmp.alloc(&part, size_t(nb) * 16));
+  RFD_CUDA(tmp.alloc(&dpart, size_t(nb)));
   RFD_CUDA(tmp.alloc(&red, size_t(2)));
   RFD_CUDA(tmp.alloc(&flag, size_t(1)));
   RFD_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
-  float al[16];
-  for (int i = 0; i < k; ++i) al[i] = float(alpha[i]);
-  rfd::launch_bary_init(mu_in, area, n, k, Mt, V, X, mu, sc, st);
+  rfd::launch_bary_init(mu_in, area, n, k, Mt, V, mu, part, sc, flag, X, st);  // X = a v s
   int it = 0;
   for (it = 1; it <= max_iter; ++it) {
-    rfd_status rs = integrate_impl(p, X, k, Y, st);          // FM_K(a * v^i)
+    rfd_status rs = integrate_impl(p, X, k, Y, st);                   // FM_K(a v^i) s_i
     if (rs != RFD_OK) return rs;
-    rfd::launch_bary_step1(area, Mt, Y, sc, n, k, X, st);     // a * w^i
-    rs = integrate_impl(p, X, k, Y, st);                       // FM_K(a * w^i)
+    rfd::launch_bary_step1(area, Mt, Y, sc, n, k, W, part, st);       // w^i
+    rfd::launch_bary_input(area, W, part, n, k, sc, flag, X, st);     // X = a w s
+    rs = integrate_impl(p, X, k, Y, st);                               // FM_K(a w^i) s_i
     if (rs != RFD_OK) return rs;
-    rfd::launch_bary_step2(area, Y, al, n, k, V, mu, X, sc, part, vmax, red, flag, st);
+    rfd::launch_bary_step2(area, Y, alpha, sc, n, k, V, mu, dpart, part, red, flag, st);
+    rfd::launch_bary_input(area, V, part, n, k, sc, flag, X, st);     // next X = a v s
     if (tol > 0.0 || it == max_iter) {
       double delta = 0.0;
       int hflag = 0;
@@ -559,7 +566,7 @@ rfd_status barycenter_impl(rfd_plan* p, const float* mu_in, const float* area,
     }
   }
   if (it > max_iter) it = max_iter;
-  rfd::launch_bary_finish(area, mu, n, part, red + 1, out, st);
+  rfd::launch_bary_finish(area, mu, n, dpart, red + 1, out, st);
   RFD_CUDA(cudaGetLastError());
   RFD_CUDA(cudaStreamSynchronize(st));
   if (iters_out) *iters_out = it;
@@ -667,34 +674,35 @@ rfd_status rfd_plan_export(const rfd_plan* p, rfd_field which, void* host_dst, s
       RFD_CUDA(cudaMemcpy(host_dst, p->nu, bytes, cudaMemcpyDeviceToHost));
       return RFD_OK;
     case RFD_GRAM:
-    case RFD_CORE: {
-      const size_t cnt = size_t(B) * r * r;
-      if (bytes != cnt * sizeof(double)) return fail(RFD_EINVAL, "size mismatch");
-      std::vector<double> tmp(cnt);
-      RFD_CUDA(cudaMemcpy(tmp.data(), which == RFD_GRAM ? p->G : p->C, bytes,
-                          cudaMemcpyDeviceToHost));
-      double* o = static_cast<double*>(host_dst);
-      for (int b = 0; b < B; ++b)
-        for (int a = 0; a < r; ++a)
-          for (int c = 0; c < r; ++c)
-            o[(size_t(b) * r + a) * r + c] =
-                tmp[(size_t(b) * r + interleaved(a, m)) * r + interleaved(c, m)];
-      return RFD_OK;
-    }
+    case RFD_CORE:
     case RFD_S:
     case RFD_Y: {
-      if (d < 1) return fail(RFD_EINVAL, "no integrate has run on this plan");
-      const size_t cnt = size_t(B) * r * d;
-      const size_t es = which == RFD_S ? sizeof(double) : sizeof(float);
+      // device state is in the centred basis: rotate back (rfd_export_rotate)
+      const bool sq = which == RFD_GRAM || which == RFD_CORE;
+      if (!sq && d < 1) return fail(RFD_EINVAL, "no integrate has run on this plan");
+      const int cols = sq ? r : d;
+      const size_t cnt = size_t(B) * r * cols;
+      const size_t es = which == RFD_Y ? sizeof(float) : sizeof(double);
       if (bytes != cnt * es) return fail(RFD_EINVAL, "size mismatch");
-      std::vector<unsigned char> tmp(cnt * es);
-      RFD_CUDA(cudaMemcpy(tmp.data(), which == RFD_S ? static_cast<void*>(p->S) : p->Y, bytes,
-                          cudaMemcpyDeviceToHost));
-      unsigned char* o = static_cast<unsigned char*>(host_dst);
+      double* rot = nullptr;
+      RFD_CUDA(cudaMalloc(&rot, cnt * sizeof(double)));
+      rfd::launch_rotate(which == RFD_GRAM ? p->G : which == RFD_CORE ? p->C : which == RFD_S ? p->S : nullptr,
+                         which == RFD_Y ? p->Y : nullptr, r, cols, B, sq, p->omega4, p->centre, rot,
+                         nullptr);
+      std::vector<double> tmp(cnt);
+      const cudaError_t e1 = cudaMemcpy(tmp.data(), rot, cnt * sizeof(double), cudaMemcpyDeviceToHost);
+      cudaFree(rot);
+      RFD_CUDA(e1);
       for (int b = 0; b < B; ++b)
         for (int a = 0; a < r; ++a)
-          memcpy(o + ((size_t(b) * r + a) * d) * es,
-                 tmp.data() + ((size_t(b) * r + interleaved(a, m)) * d) * es, d * es);
+          for (int c = 0; c < cols; ++c) {
+            const double v = tmp[(size_t(b) * r + interleaved(a, m)) * cols + (sq ? interleaved(c, m) : c)];
+            const size_t o = (size_t(b) * r + a) * cols + c;
+            if (which == RFD_Y)
+              static_cast<float*>(host_dst)[o] = float(v);
+            else
+              static_cast<double*>(host_dst)[o] = v;
+          }
       return RFD_OK;
     }
   }

@@ -63,8 +63,15 @@ void launch_nu(const float4* omega4, double* nu, int* flags, int m, double eps, 
                cudaStream_t s);
 
 // ---------------------------------------------------------------- pack
-void launch_pack_points(const float* xyz, float4* pts, float* pts16, int64_t n, int batch,
-                        cudaStream_t s);
+// Per-cloud bounding box (bbox: batch x 6 uint scratch), centre c = its
+// midpoint (centre: batch float4), then pts / pts16 = points - c.
+void launch_pack_points(const float* xyz, float4* pts, float* pts16, float4* centre,
+                        unsigned int* bbox, int64_t n, int batch, int sms, cudaStream_t s);
+// out (fp64, batch x r x cols) = R X (right: R X R^T, cols = r) with R the
+// per-frequency rotation by 2 pi omega.c_b (centred -> paper basis).  X fp64,
+// or Xf fp32 when X is NULL.
+void launch_rotate(const double* X, const float* Xf, int r, int cols, int batch, bool right,
+                   const float4* omega4, const float4* centre, double* out, cudaStream_t s);
 
 // ---------------------------------------------------------------- Gram
 struct GramGeom {
@@ -111,15 +118,22 @@ cudaError_t launch_spectrum(const double* G, const double* nu, int m, int batch,
 
 // ---------------------------------------------------------------- barycenter
 // NEXT-1 (k_sinkhorn.cu): elementwise steps of Alg. 1 on N x k fields.
+// Iterates V, W, mu fp64; integrate inputs X / outputs Y fp32; sc: k fp64
+// power-of-two input scales; part: bary_blocks(n) x 16 column maxima;
+// dpart: bary_blocks(n) partial sums; flag: non-finite iterate.
 int bary_blocks(int64_t n);
-void launch_bary_init(const float* mu_in, const float* area, int64_t n, int k, float* Mt, float* V,
-                      float* X, float* mu, float* sc, cudaStream_t s);
-void launch_bary_step1(const float* area, const float* Mt, const float* Y, const float* sc,
-                       int64_t n, int k, float* X, cudaStream_t s);
-void launch_bary_step2(const float* area, const float* Y, const float* alpha, int64_t n, int k,
-                       float* V, float* mu, float* X, float* sc, double* part, float* vmax_part,
+void launch_bary_init(const float* mu_in, const float* area, int64_t n, int k, float* Mt,
+                      double* V, double* mu, double* part, double* sc, int* flag, float* X,
+                      cudaStream_t s);
+// sc = 2^-e(column max of part), X = fp32(a Z sc)
+void launch_bary_input(const float* area, const double* Z, const double* part, int64_t n, int k,
+                       double* sc, int* flag, float* X, cudaStream_t s);
+void launch_bary_step1(const float* area, const float* Mt, const float* Y, const double* sc,
+                       int64_t n, int k, double* W, double* part, cudaStream_t s);
+void launch_bary_step2(const float* area, const float* Y, const double* alpha, const double* sc,
+                       int64_t n, int k, double* V, double* mu, double* dpart, double* part,
                        double* delta, int* flag, cudaStream_t s);
-void launch_bary_finish(const float* area, const float* mu, int64_t n, double* part, double* mass,
+void launch_bary_finish(const float* area, const double* mu, int64_t n, double* part, double* mass,
                         float* out, cudaStream_t s);
 
 // ---------------------------------------------------------------- passes

@@ -189,6 +189,14 @@ class Plan:
         import torch
         _check_f32(mus, "mus")
         _check_f32(area, "area")
+        # the kernels read k x N and N elements: undersized buffers would be
+        # read out of bounds, so the shapes are checked here
+        if mus.dim() != 2 or int(mus.shape[1]) != self.n:
+            raise ValueError("mus must be (k, %d)" % self.n)
+        if area.numel() != self.n:
+            raise ValueError("area must have %d elements" % self.n)
+        if not (mus.is_cuda and area.is_cuda) or mus.device != area.device:
+            raise ValueError("mus and area must be CUDA tensors on the plan's device")
         k = int(mus.shape[0])
         al = np.ascontiguousarray(np.asarray(alpha, np.float64))
         out = torch.empty((self.n,), dtype=torch.float32, device=mus.device)
@@ -220,6 +228,8 @@ class Plan:
             out = torch.empty_like(F)
         elif out.shape != F.shape or not out.is_cuda:
             raise ValueError("out must be a CUDA tensor shaped like F")
+        else:
+            _check_f32(out, "out")
         _check(load_library().rfd_integrate(self._h, _ptr(F), d, _ptr(out),
                                             _stream_handle(stream)))
         return out
@@ -229,6 +239,8 @@ class Plan:
         _check_f32(F_host, "F")
         _check_f32(out_host, "out")
         d = self._field_dims(F_host)
+        if tuple(out_host.shape) != tuple(F_host.shape):
+            raise ValueError("out must be shaped like F")
         _check(load_library().rfd_integrate_host(self._h, _ptr(F_host), d, _ptr(out_host),
                                                  _stream_handle(stream)))
         return out_host

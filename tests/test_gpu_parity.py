@@ -79,8 +79,13 @@ def test_config5_full_size_parity():
     # out compared on 4096 sampled rows (every row still enters G and S).
     p, x, F = make_config(5)
     plan, out = _run_single(x, F, p)
-    rows = np.arange(0, x.shape[0], 1024)
-    rows = np.concatenate([rows, [x.shape[0] - 1]])
+    # rows at a prime stride (1021: every residue mod 128, i.e. every lane of
+    # the 128-point pass-2 tiles and every 16-point group position) plus 4096
+    # random rows and the last row
+    n = x.shape[0]
+    rng = np.random.default_rng(55)
+    rows = np.unique(np.concatenate([np.arange(0, n, 1021), rng.integers(0, n, 4096), [n - 1]]))
+    assert len(np.unique(rows % 128)) == 128
     _check_against_oracle(plan, out, x, F, p, rows=rows)
 
 
@@ -162,6 +167,57 @@ def test_field_column_scales_parity():
         e_out = relerr(out[:, c], ref["out"][:, c])
         e_del = relerr(out[:, c] - F[:, c].astype(np.float64), ref["out"][:, c] - F[:, c])
         print("column", c, "%.2e %.2e" % (e_out, e_del))
+        assert e_out <= TOL and e_del <= TOL, (c, e_out, e_del)
+
+
+@pytest.mark.parametrize("shift,scale", [(10.0, 1.0), (100.0, 1.0), (1000.0, 1.0), (0.0, 50.0),
+                                         (0.0, 10.0)])
+def test_translated_and_scaled_clouds_parity(shift, scale):
+    # W depends on n_i - n_j only (Eq. 9): the exact result
+    # is translation-invariant.  The library centres every cloud on its
+    # bounding box (k_freq.cu) and rotates the exported G, C^, S, Y back, so a
+    # translated cloud meets the gate like the original; the fp32 feature
+    # argument's error grows with |omega|_1 * half-extent (scaled clouds,
+    # include/rfd.h "Coordinate range").
+    p, x, F = make_config(2)
+    x = (x.astype(np.float64) * scale + shift * np.array([1.0, -0.7, 0.4])).astype(np.float32)
+    p = dict(p, name="cfg2 shift %g scale %g" % (shift, scale))
+    plan, out = _run_single(x, F, p)
+    _check_against_oracle(plan, out, x, F, p)
+
+
+def test_permutation_equivariance():
+    # K = exp(lambda W~) with W~ = Phi D Phi^T: permuting the points permutes
+    # rows and columns of K: out(P x, P F) = P out(x, F)
+    # (sums over points in another order: fp32 rounding only).
+    p, x, F = make_config(2)
+    perm = np.random.default_rng(8).permutation(x.shape[0])
+    _, out = _run_single(x, F, p)
+    _, outp = _run_single(np.ascontiguousarray(x[perm]), np.ascontiguousarray(F[perm]), p)
+    assert relerr(outp, out[perm]) <= 1e-5
+    assert relerr(outp - F[perm], out[perm] - F[perm]) <= 1e-5
+
+
+def test_tiny_field_columns_pass2_scale_clamp():
+    # Pass 2 scales Y per channel by 2^(14 - e) into fp16 range; for max|Y_j|
+    # below 2^-113 (a field column ~1e-33, or a tiny lambda) the scale is
+    # clamped at 2^126 instead of overflowing to inf and turning the column
+    # into NaN.  Columns of ~1e-33 and ~1e-36 (fp32 normal) must
+    # still meet the gates on out and on Delta.
+    n, m = 3000, 64
+    x = _sphere(n, 5)
+    F = np.random.default_rng(7).standard_normal((n, 3)).astype(np.float32)
+    F[:, 1] *= np.float32(1e-33)
+    F[:, 2] *= np.float32(1e-36)
+    p = dict(name="tiny columns", eps=0.05, lam=-0.8, m=m, seed=21)
+    res = orf.Plan(x, p["eps"], p["lam"], p["m"], p["seed"]).apply(F.astype(np.float64))
+    assert np.abs(res["Y"][:, 1]).max() < 2.0 ** -113  # the clamped branch is exercised
+    plan, out = _run_single(x, F, p)
+    assert np.isfinite(out).all()
+    for c in range(3):
+        e_out = relerr(out[:, c], res["out"][:, c])
+        e_del = relerr(out[:, c] - F[:, c].astype(np.float64), res["out"][:, c] - F[:, c])
+        print("tiny column", c, "%.2e %.2e" % (e_out, e_del))
         assert e_out <= TOL and e_del <= TOL, (c, e_out, e_del)
 
 
@@ -280,58 +336,128 @@ def test_multi_column_parity(n, m, d):
     _check_against_oracle(plan, out, x, F, p)
 
 
-def _bary_inputs(n, seed=7):
-    rng = np.random.default_rng(seed)
-    g = rng.standard_normal((n, 3))
-    x = (g / np.linalg.norm(g, axis=1, keepdims=True)).astype(np.float32)
-    a = np.full(n, 1.0 / n)
-    xd = x.astype(np.float64)
-    mus = np.stack([np.exp(-((xd - xd[i]) ** 2).sum(1) / (2 * 0.5 ** 2)) for i in range(3)])
-    # (bumps of width 0.5 around three points; area weights uniform)
-    mus /= (mus @ a)[:, None]
-    return x, a, mus
-
-
-def test_barycenter_matches_oracle():
-    # NEXT-1: Alg. 1 with FM_K = rfd_integrate (k = 3 columns per integrate),
-    # lambda > 0 as in the paper's barycenter runs.  Trajectory parity for the
-    # first iterations; from about the fourth on the iterates depend on the
-    # RELATIVE accuracy of FM_K(a v) where it is tiny (the ratios mu / FM_K(a v)
-    # far from the mass), which a normwise-accurate fp32 kernel application does
-    # not have -- so after 10 iterations only validity is checked
-    # (A20).
-    n, eps, lam, m = 2000, 0.03, 0.1, 256
-    x, a, mus = _bary_inputs(n)
-    plan = rfd.Plan(torch.from_numpy(x).cuda(), eps, lam, m, 5)
-    mus_d = torch.from_numpy(mus.astype(np.float32)).cuda()
+def _bary_gpu(plan, mus, a, alpha, iters, tol=0.0):
+    mus_d = torch.from_numpy(np.ascontiguousarray(mus, dtype=np.float32)).cuda()
     a_d = torch.from_numpy(a.astype(np.float32)).cuda()
-    for iters in (1, 2, 3):
-        got, its = plan.barycenter(mus_d, a_d, [1 / 3] * 3, iters)
-        ref, rits = orf.Plan(x, eps, lam, m, 5).barycenter(mus, a, [1 / 3] * 3, iters)
-        assert its == rits == iters
-        g = got.cpu().numpy().astype(np.float64)
-        err = relerr(g, ref)
-        print("barycenter iters=%d err %.2e" % (iters, err))
-        assert err <= TOL
-        assert np.isfinite(g).all() and abs(float(a @ g) - 1.0) < 1e-5
-    got, its = plan.barycenter(mus_d, a_d, [1 / 3] * 3, 10)
-    g = got.cpu().numpy().astype(np.float64)
-    assert its == 10 and np.isfinite(g).all() and (g >= 0).all()
-    assert abs(float(a @ g) - 1.0) < 1e-5
+    got, its = plan.barycenter(mus_d, a_d, alpha, iters, tol=tol)
+    return got.cpu().numpy().astype(np.float64), its
 
 
-def test_barycenter_tol_stop_and_errors():
-    n = 2000
-    x, a, mus = _bary_inputs(n)
+def _bary_hybrid(plan, mus, a, alpha, iters, tol=0.0):
+    """Alg. 1 in fp64 numpy with FM_K = the GPU integrate, its inputs formed
+    exactly as k_sinkhorn.cu forms them (X = fp32(a v s), s = 2^-e of the
+    column max of a v; FM_K(a v) = Y / s).  Same FM_K arithmetic, so it
+    reproduces rfd_barycenter up to fp64 rounding of the elementwise steps."""
+    a32 = a.astype(np.float32).astype(np.float64)
+    Mt = np.ascontiguousarray(mus.astype(np.float32).T).astype(np.float64)
+    n, k = Mt.shape
+    al = np.asarray(alpha, np.float64)
+
+    def fm(Z):
+        col = (a32[:, None] * Z).max(axis=0)
+        s = np.array([2.0 ** -np.frexp(c)[1] if c > 0 else 1.0 for c in col])
+        X = ((a32[:, None] * Z) * s[None, :]).astype(np.float32)
+        Y = plan.integrate(torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
+        return Y / s[None, :]
+
+    V = np.ones((n, k))
+    mu = np.ones(n)
+    it = 0
+    for it in range(1, iters + 1):
+        mu_old = mu
+        W = Mt / np.maximum(fm(V), 1e-30)
+        d = np.maximum(V * fm(W), 1e-30)
+        lg = np.zeros(n)
+        for i in range(k):
+            lg = lg + al[i] * np.log(d[:, i])
+        mu = np.exp(lg)
+        V = (V * mu[:, None]) / d
+        if tol > 0 and np.abs(mu - mu_old).sum() < tol:
+            break
+    return mu / float(a32 @ mu), it
+
+
+def test_barycenter_identity_kernel_closed_form():
+    # NEXT-1 with FM = identity (lambda = 0: the integrate returns F exactly):
+    # every iteration gives the weighted geometric mean prod_i (mu^i)^alpha_i
+    # normalised to <a, mu> = 1 (Alg. 1 step 3, PAPER.md:1046;
+    # tests/test_oracle_integrator.py::test_barycenter_geometric_mean_pin).
+    from workloads import barycenter_inputs
+
+    x, a, mus = barycenter_inputs(3000, floor=0.05, k=3)
+    a = np.random.default_rng(3).uniform(0.5, 1.5, a.shape)
+    a /= a.sum()
+    mus = mus / (mus @ a)[:, None]
+    plan = rfd.Plan(torch.from_numpy(x).cuda(), 0.05, 0.0, 64, 5)
+    m32 = mus.astype(np.float32).astype(np.float64)
+    a32 = a.astype(np.float32).astype(np.float64)
+    for alpha in ([0.25, 0.75], [1 / 3] * 3):
+        k = len(alpha)
+        geo = np.prod(m32[:k] ** np.asarray(alpha)[:, None], axis=0)
+        geo /= a32 @ geo
+        for iters in (1, 10):
+            got, its = _bary_gpu(plan, mus[:k], a, alpha, iters)
+            assert its == iters
+            assert relerr(got, geo) <= 1e-6, (alpha, iters, relerr(got, geo))
+        _, its = _bary_gpu(plan, mus[:k], a, alpha, 50, tol=1e-9)
+        assert its == 2  # fixed point at iteration 1
+
+
+def test_barycenter_first_iteration_matches_oracle():
+    # NEXT-1 with the random-feature kernel (lambda > 0 as in the paper's runs,
+    # PAPER.md:1061) against the fp64 oracle where Alg. 1 is well conditioned:
+    # iteration 1 on floored inputs moves ~2.5 eta under FM_K perturbations of
+    # eta (tests/test_oracle_integrator.py::
+    # test_barycenter_conditioning_on_random_feature_kernels).
+    from workloads import barycenter_inputs
+
+    x, a, mus = barycenter_inputs(2000, floor=0.2)
+    plan = rfd.Plan(torch.from_numpy(x).cuda(), 0.03, 0.1, 256, 5)
+    got, its = _bary_gpu(plan, mus, a, [1 / 3] * 3, 1)
+    ref, rits = orf.Plan(x, 0.03, 0.1, 256, 5).barycenter(mus, a, [1 / 3] * 3, 1)
+    assert its == rits == 1
+    err = relerr(got, ref)
+    print("barycenter iteration 1: err %.2e" % err)
+    assert err <= TOL
+    assert abs(float(a @ got) - 1.0) < 1e-5
+
+
+@pytest.mark.parametrize("floor,iters,tol", [(0.0, 10, 0.0), (0.2, 10, 0.0), (0.0, 200, 1e-3)])
+def test_barycenter_kernels_match_fp64_iteration(floor, iters, tol):
+    # Past iteration 1 the random-feature barycenter is ill-conditioned in the
+    # FM_K error (see the oracle conditioning test), so the elementwise GPU
+    # steps are checked against the same iteration in fp64 driven by the same
+    # GPU FM_K (bitwise-deterministic integrate on identically formed inputs):
+    # 10 iterations and a tol stop, iterates, stop iteration and output.
+    from workloads import barycenter_inputs
+
+    x, a, mus = barycenter_inputs(2000, floor=floor)
+    plan = rfd.Plan(torch.from_numpy(x).cuda(), 0.03, 0.1, 256, 5)
+    got, its = _bary_gpu(plan, mus, a, [1 / 3] * 3, iters, tol=tol)
+    ref, rits = _bary_hybrid(plan, mus, a, [1 / 3] * 3, iters, tol=tol)
+    err = relerr(got, ref)
+    print("barycenter floor=%g iters=%d tol=%g: %d/%d iterations, err vs fp64 iteration %.2e"
+          % (floor, iters, tol, its, rits, err))
+    assert its == rits
+    assert err <= 1e-6
+    assert np.isfinite(got).all() and (got >= 0).all()
+    assert abs(float(a @ got) - 1.0) < 1e-5
+
+
+def test_barycenter_errors():
+    from workloads import barycenter_inputs
+
+    x, a, mus = barycenter_inputs(2000)
     plan = rfd.Plan(torch.from_numpy(x).cuda(), 0.03, 0.1, 256, 5)
     mus_d = torch.from_numpy(mus.astype(np.float32)).cuda()
     a_d = torch.from_numpy(a.astype(np.float32)).cuda()
-    _, its = plan.barycenter(mus_d, a_d, [1 / 3] * 3, 200, tol=1e-3)
-    _, rits = orf.Plan(x, 0.03, 0.1, 256, 5).barycenter(mus, a, [1 / 3] * 3, 200, tol=1e-3)
-    assert its < 200 and rits < 200
     for alpha in ([0.5, 0.5, 0.5], [1.0, 0.0, 0.0], [-1.0, 1.0, 1.0]):
         with pytest.raises(rfd.RFDError):
             plan.barycenter(mus_d, a_d, alpha, 3)
+    with pytest.raises(ValueError):  # undersized inputs are refused by the binding
+        plan.barycenter(mus_d[:, :100], a_d, [1 / 3] * 3, 3)
+    with pytest.raises(ValueError):
+        plan.barycenter(mus_d, a_d[:100], [1 / 3] * 3, 3)
     batched = rfd.Plan(torch.from_numpy(np.stack([x, x])).cuda(), 0.03, 0.1, 256, 5)
     with pytest.raises(rfd.RFDError):
         batched.barycenter(mus_d, a_d, [1 / 3] * 3, 3)

@@ -5,4 +5,4 @@ parameters of each config).  It contains none of the method's arithmetic and
 is the one module both the CUDA path's tests/bench and the oracle consume.
 """
 
-from .configs import CONFIGS, make_config  # noqa: F401
+from .configs import CONFIGS, barycenter_inputs, make_config  # noqa: F401

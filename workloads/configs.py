@@ -121,3 +121,20 @@ def make_config(cfg, **overrides):
     else:
         params["n"] = x.shape[0]
     return params, x, F
+
+
+def barycenter_inputs(n=2000, floor=0.0, width=0.5, k=3, seed=7):
+    """Alg. 1 inputs (k = 3 distributions "with mass
+    concentrated in vertices surrounding a distinct center vertex", area
+    weights): n uniform sphere points, uniform area weights a = 1/n, and k
+    Gaussian bumps of width `width` around points 0..k-1 plus a constant
+    `floor`, each normalised to <a, mu^i> = 1.  Returns (x fp32 n x 3, a fp64
+    n, mus fp64 k x n)."""
+    rng = np.random.default_rng(seed)
+    x = _sphere(rng, n).astype(np.float32)
+    a = np.full(n, 1.0 / n)
+    xd = x.astype(np.float64)
+    mus = np.stack([np.exp(-((xd - xd[i]) ** 2).sum(1) / (2 * width ** 2)) + floor
+                    for i in range(k)])
+    mus /= (mus @ a)[:, None]
+    return x, a, mus
