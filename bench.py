@@ -7,8 +7,11 @@ the BASELINE.json scoring config (cfg 5: N = 4,194,304 points in the unit
 cube, m = 256, d = 16, eps = 0.01, lambda = -0.3): rfd_plan_create
 (frequencies, Gram, core) + rfd_integrate (pass 1, Y, pass 2), inputs
 resident in HBM.  value = N * d * steps * ranks / max-over-ranks time
-(points x dims / s).  Multi-GPU: each rank integrates its own independent
-cloud (weak scaling, no data-path collective).
+(points x dims / s).  Multi-GPU: ONE
+cloud of ranks x 4M points sharded over the ranks (rfd_plan_create_sharded);
+the Gram and S partials are all-gathered over NCCL (torch.distributed) and
+summed in rank order by the library -- weak scaling (4M points per GPU).
+``--gpus N`` without torchrun re-launches itself under torch.distributed.run.
 
 Extra keys: ``integrate`` (inference only, plan reused: the paper's
 "inference"), ``roofline`` for the dominant kernel (timed with
@@ -203,6 +206,17 @@ class ClockSampler:
 def dist_setup(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world:
+        if world == 1 and "RANK" not in os.environ:  # spawn the N ranks ourselves
+            import socket
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                       "--nproc-per-node=%d" % args.gpus, "--master-addr",
+                                       "127.0.0.1", "--master-port", str(port),
+                                       os.path.abspath(__file__)] + sys.argv[1:])
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     pg = None
@@ -237,20 +251,25 @@ def run_rfd(args, rank, world, local, pg):
     from paper_2302_00942_b200 import rfd
 
     p, x, F = make_config(5)
-    if rank > 0:  # each rank: its own independent cloud (weak scaling)
+    if rank > 0:  # rank r's shard of the one cloud: 4M more uniform cube points
         rng = np.random.default_rng(4 + 1000 * rank)
         x = rng.random(x.shape, dtype=np.float32)
         F = rng.standard_normal(F.shape, dtype=np.float32)
     N, m, d = p["n"], p["m"], p["d"]
-    seed = p["seed"] + 1000 * rank
+    seed = p["seed"]
     stream = torch.cuda.current_stream()
+
+    def make_plan(points):
+        if world > 1:
+            return rfd.Plan.sharded(points, p["eps"], p["lam"], m, seed)
+        return rfd.Plan(points, p["eps"], p["lam"], m, seed)
     xd = torch.from_numpy(x).cuda()
     Fd = torch.from_numpy(F).cuda()
     outd = torch.empty_like(Fd)
     pk = peaks()
 
     def step():
-        plan = rfd.Plan(xd, p["eps"], p["lam"], m, seed)
+        plan = make_plan(xd)
         plan.integrate(Fd, out=outd)
         plan.close()
 
@@ -281,7 +300,7 @@ def run_rfd(args, rank, world, local, pg):
     ms_step = ms_max / args.steps
 
     # ---- inference only (plan reused), same protocol
-    plan = rfd.Plan(xd, p["eps"], p["lam"], m, seed)
+    plan = make_plan(xd)
     for _ in range(args.warmup):
         plan.integrate(Fd, out=outd)
     torch.cuda.synchronize()
@@ -343,7 +362,7 @@ def run_rfd(args, rank, world, local, pg):
         oh = torch.empty_like(Fh).pin_memory()
 
         def e2e_step():
-            pl = rfd.Plan(xh, p["eps"], p["lam"], m, seed)  # H2D of the points inside
+            pl = make_plan(xh)                                # H2D of the points inside
             pl.integrate_host(Fh, oh)                        # H2D F, integrate, D2H out
             pl.close()
         for _ in range(max(1, args.warmup)):
@@ -447,17 +466,21 @@ def config_legs(args, pk):
         p, x, F = make_config(cfg)
         xd, Fd = torch.from_numpy(x).cuda(), torch.from_numpy(F).cuda()
         od = torch.empty_like(Fd)
+        mk = lambda: rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"]).close()  # noqa: E731
+        pmed = timed(mk, 5)[0]
         plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
         med, p10, p90 = timed(lambda: plan.integrate(Fd, out=od), 200)
         N, m, d = p["n"], p["m"], p["d"]
         rl = roof(N, m, d)
         out["cfg%d" % cfg] = {"integrate_us": med * 1e3, "p10_us": p10 * 1e3, "p90_us": p90 * 1e3,
                               "value": N * d / (med * 1e-3), "unit": UNIT,
-                              "strict_roofline_us": rl * 1e3, "strict_roofline_frac": rl / med}
+                              "strict_roofline_us": rl * 1e3, "strict_roofline_frac": rl / med,
+                              "plan_create_ms": pmed}
         plan.close()
     # cfg 3: 50 applications back to back on device-resident vectors
     p, x, V = make_config(3)
     xd = torch.from_numpy(x).cuda()
+    pmed3 = timed(lambda: rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"]).close(), 5)[0]
     plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
     Vd = torch.from_numpy(V).cuda()
     outs = torch.empty_like(Vd)
@@ -482,7 +505,8 @@ def config_legs(args, pk):
     out["cfg3_reuse_loop"] = {"applications": A, "clouds": p["clouds"], "plain_ms": med,
                               "graph_ms": gmed, "graph_p10_ms": gp10, "graph_p90_ms": gp90,
                               "us_per_application_graph": gmed * 1e3 / A,
-                              "strict_roofline_ms": rl, "strict_roofline_frac_graph": rl / gmed}
+                              "strict_roofline_ms": rl, "strict_roofline_frac_graph": rl / gmed,
+                              "plan_create_ms": pmed3}
     plan.close()
     del Vd, outs, g
     # eps-independence at cfg 5 (same plan re-parameterised: identical G)
@@ -534,6 +558,69 @@ def config_legs(args, pk):
     return out
 
 
+def relerr(got, ref):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.abs(got - ref).max() / np.abs(ref).max())
+
+
+def parity_leg():
+    """Max relative error (normwise, A13) of the timed workload's
+    GPU result against the fp64 oracle: cfg 5 at full size, G and S over all
+    4M points, out and Delta = out - F on rows at stride 1021 (every
+    128-point tile lane) plus 4096 random rows and the last row."""
+    import torch
+    from oracle import rfd as orf
+    from paper_2302_00942_b200 import rfd
+    p, x, F = make_config(5)
+    plan = rfd.Plan(torch.from_numpy(x).cuda(), p["eps"], p["lam"], p["m"], p["seed"])
+    out = plan.integrate(torch.from_numpy(F).cuda()).cpu().numpy()
+    n = x.shape[0]
+    rows = np.unique(np.concatenate([np.arange(0, n, 1021),
+                                     np.random.default_rng(55).integers(0, n, 4096), [n - 1]]))
+    t0 = time.perf_counter()
+    ref = orf.Plan(x, p["eps"], p["lam"], p["m"], p["seed"])
+    res = ref.apply(F, rows=rows)
+    dt = time.perf_counter() - t0
+    F64 = F[rows].astype(np.float64)
+    errs = {"out": relerr(out[rows], res["out"]), "delta": relerr(out[rows] - F64, res["out"] - F64),
+            "G": relerr(plan.export("gram"), ref.G), "C": relerr(plan.export("core"), ref.C),
+            "S": relerr(plan.export("S", d=p["d"]), res["S"]),
+            "Y": relerr(plan.export("Y", d=p["d"]), res["Y"])}
+    plan.close()
+    return {"max_rel_err_out": errs["out"], "max_rel_err_delta": errs["delta"],
+            "intermediates": {k: errs[k] for k in ("G", "C", "S", "Y")}, "tolerance": 1e-4,
+            "rows_compared": int(rows.size), "oracle_s": dt,
+            "note": "normwise max|gpu-oracle|/max|oracle| (DESIGN.md A13) at cfg5 full size; "
+                    "G and S over all N points; out / Delta on the sampled rows"}
+
+
+def eps_graph_leg():
+    """SURVEY 8(c) step 7 (a diagnostic, never a gate): the relative error of
+    RFD (the GPU output) against the exact epsilon-graph diffusion exp(lambda A) F
+    on the L-infinity (primary, reading A2) and L1 (the norm the paper names)
+    graphs, cfgs 1 and 2."""
+    import torch
+    from oracle import dense
+    from paper_2302_00942_b200 import rfd
+    out = {}
+    for cfg in (1, 2):
+        p, x, F = make_config(cfg)
+        plan = rfd.Plan(torch.from_numpy(x).cuda(), p["eps"], p["lam"], p["m"], p["seed"])
+        got = plan.integrate(torch.from_numpy(F).cuda()).cpu().numpy().astype(np.float64)
+        plan.close()
+        row = {}
+        for norm, key in (("inf", "Linf"), (1, "L1")):
+            ex = dense.exact_diffusion_sparse(x, F, p["eps"], p["lam"], norm)
+            row["rel_err_vs_" + key] = relerr(got, ex)
+            row["rel_err_delta_vs_" + key] = relerr(got - F, ex - F)
+        row["m"] = p["m"]
+        out["cfg%d" % cfg] = row
+    out["note"] = ("approximation quality of the random-feature surrogate (m frequencies) vs the exact "
+                   "graph; not a parity gate (parity is against the oracle's RF result)")
+    return out
+
+
 def oracle_sample(n_sample, steps=1):
     """The oracle as it stands on a bounded sample of cfg 5 (first n_sample
     points of the same generator recipe): plan + apply, all rows."""
@@ -564,6 +651,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 20)
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config legs")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -604,6 +692,10 @@ def main():
     legs = None
     if world == 1 and not args.no_configs:
         legs = config_legs(args, peaks())
+    parity = eps_graph = None
+    if world == 1 and not args.no_parity:
+        parity = parity_leg()
+        eps_graph = eps_graph_leg()
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         _, cval, cdt = oracle_sample(args.cpu_sample)
@@ -614,9 +706,13 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic", "config": dict(cfg_desc, parallelism="dp%d (independent clouds)" % world),
+            "dtype": "f32", "data": "synthetic",
+            "config": dict(cfg_desc, parallelism=(
+                "sharded%d: one cloud of %d x 4M points, G and S partials all-gathered over NCCL "
+                "and summed in rank order (SURVEY 8(e))" % (world, world)) if world > 1 else "single GPU"),
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
             "gpu_launches": res["launches"], "clocks": res["clocks"],
+            "parity": parity, "eps_graph_diagnostic": eps_graph,
             "integrate": res["integrate"], "reparam": res["reparam"], "spectrum": res["spectrum"], "configs": legs,
             "kernels": res["kernels"]}
     print(json.dumps(line))

@@ -91,6 +91,50 @@ rfd_status rfd_plan_create_batched(const float* points, int32_t batch,
                                    rfd_plan** plan_out);
 
 /*
+ * Multi-GPU: one cloud sharded across the ranks of a process group (SURVEY
+ * Sec. 8(e)), one GPU per rank, each rank holding a contiguous part of the
+ * points (and the same rows of every field).  The two sums over points -- G =
+ * Phi^T Phi (B^T A) at plan creation and S = Phi^T F
+ * (Eq. 13's first bracket) in every rfd_integrate -- are linear in the points
+ * (PAPER.md:359), so each rank computes its shard's partial and the ranks
+ * exchange partials once per sum (plus the shards' bounding boxes once at
+ * creation, so that every rank centres the cloud on the same point).  The
+ * exchange is an ALL-GATHER performed by the caller's collective library
+ * through `allgather` (the Python binding uses torch.distributed over NCCL):
+ *   allgather(ctx, send, recv, count, stream)  send: `count` fp64 on the
+ *     plan's device; recv: world x count fp64 on the device, rank-major (recv
+ *     + q count = rank q's send).  Ordered on `stream` (enqueued on it, or
+ *     complete on return).  Returns 0 on success (non-zero -> RFD_ECUDA).
+ * The library adds the gathered partials in rank order, so every rank holds
+ * bitwise the same G, C^, S and Y; each rank's out rows are its own points'.
+ * Every rank must make the same sequence of calls (collective semantics).
+ */
+typedef int (*rfd_allgather_fn)(void* ctx, const double* send, double* recv, size_t count,
+                                rfd_stream stream);
+typedef struct {
+  int32_t rank;               /* 0 <= rank < world                            */
+  int32_t world;              /* ranks in the group (>= 1)                    */
+  rfd_allgather_fn allgather; /* the exchange (see above); NULL iff world == 1 */
+  void* ctx;                  /* passed through to allgather                  */
+} rfd_shard;
+
+/*
+ * rfd_plan_create_sharded -- rfd_plan_create for this rank's shard of one
+ * cloud.  points: n_local x 3 (host or device), n_local >= 1; eps, lambda, m,
+ * seed as rfd_plan_create and equal on every rank.  The plan records N = the
+ * sum of the shards' n_local (rfd_plan_info_t.n_total).  rfd_integrate and
+ * rfd_integrate_host on the plan take this rank's n_local x d rows and
+ * exchange S; rfd_plan_reparam / rfd_plan_spectrum / rfd_plan_export work on
+ * the merged (global) G.  rfd_barycenter refuses sharded plans (EINVAL).
+ * Errors: as rfd_plan_create, EINVAL for a bad `shard`, ECUDA if the
+ * exchange fails.
+ */
+rfd_status rfd_plan_create_sharded(const float* points, int64_t n_local, double eps,
+                                   double lambda, int32_t m, uint64_t seed,
+                                   const rfd_shard* shard, rfd_stream stream,
+                                   rfd_plan** plan_out);
+
+/*
  * rfd_plan_reparam -- re-parameterise a plan to a new (eps, lambda) without
  * recomputing the Gram matrix: G = Phi^T Phi
  * depends only on the points and omega, so only nu
@@ -190,6 +234,9 @@ typedef struct {
   int32_t symmetric;/* 1: core via D^1/2 G D^1/2 (all nu > 0) */
   double eps, lambda;
   uint64_t seed;
+  int64_t n_total;  /* points of the whole cloud (= n unless sharded) */
+  int32_t rank;     /* shard of this plan (0 unless sharded)          */
+  int32_t world;    /* shards (1 unless sharded)                      */
 } rfd_plan_info_t;
 rfd_status rfd_plan_info(const rfd_plan* plan, rfd_plan_info_t* info);
 

@@ -112,35 +112,40 @@ __device__ __forceinline__ float dec_f32(unsigned int e) {
   return __uint_as_float((e & 0x80000000u) ? (e & 0x7fffffffu) : ~e);
 }
 
-// bbox[b][0..2] = max ~enc (min), bbox[b][3..5] = max enc (max); grid (chunks, batch)
+// bbox[b][0..2] = max ~enc (min), bbox[b][3..5] = max enc (max); grid
+// (chunks, batch).  Block-level reduction first: one atomic per block and
+// component (per-warp atomics on the same 6 words serialised at L2: 54 us at
+// cfg 5).
 __global__ void __launch_bounds__(256)
 bbox_kernel(const float* __restrict__ xyz, int64_t n, unsigned int* __restrict__ bbox) {
+  __shared__ unsigned int red[8][6];
   const int b = blockIdx.y;
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t p0 = int64_t(blockIdx.x) * per, p1 = min(p0 + per, n);
   const float* src = xyz + int64_t(b) * n * 3;
-  unsigned int lo[3] = {0u, 0u, 0u}, hi[3] = {0u, 0u, 0u};
+  unsigned int v[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+#pragma unroll 4
   for (int64_t i = p0 + threadIdx.x; i < p1; i += blockDim.x) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const unsigned int e = enc_f32(src[3 * i + c]);
-      lo[c] = max(lo[c], ~e);
-      hi[c] = max(hi[c], e);
+      const unsigned int e = enc_f32(__ldg(src + 3 * i + c));
+      v[c] = max(v[c], ~e);
+      v[3 + c] = max(v[3 + c], e);
     }
   }
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
+  for (int c = 0; c < 6; ++c)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      lo[c] = max(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
-      hi[c] = max(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
-    }
+    for (int o = 16; o > 0; o >>= 1) v[c] = max(v[c], __shfl_xor_sync(0xffffffffu, v[c], o));
   if ((threadIdx.x & 31) == 0)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      atomicMax(bbox + 6 * b + c, lo[c]);
-      atomicMax(bbox + 6 * b + 3 + c, hi[c]);
-    }
+    for (int c = 0; c < 6; ++c) red[threadIdx.x >> 5][c] = v[c];
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    unsigned int mx = 0u;
+    for (int w = 0; w < 8; ++w) mx = max(mx, red[w][threadIdx.x]);
+    atomicMax(bbox + 6 * b + threadIdx.x, mx);
+  }
 }
 
 __device__ __forceinline__ float4 bbox_centre(const unsigned int* bb) {
@@ -153,16 +158,21 @@ __device__ __forceinline__ float4 bbox_centre(const unsigned int* bb) {
   return make_float4(c[0], c[1], c[2], 0.0f);
 }
 
-// pts: float4 (x - c, y - c, z - c, 0) per point.  pts16: per cloud, groups of
-// 16 points as [x0..x15 | y0..y15 | z0..z15] (pass 1 reads a group with 12
-// 16-byte copies and pairs neighbouring points in packed FP32 math); the tail
-// group is zero-padded (the buffer is cleared first when n % 16 != 0).
+// Writes the centred points in all three layouts the kernels read:
+//   pts    float4 (x - c, y - c, z - c, 0) per point (pass 2);
+//   pts16  per cloud, groups of 16 points as [x0..x15 | y0..y15 | z0..z15]
+//          (pass 1 reads a group with 12 16-byte copies and pairs neighbouring
+//          points in packed FP32 math); the tail group is zero-padded (the
+//          buffer is cleared first when n % 16 != 0);
+//   gpts   the Gram's layout: per cloud, gper points (whole 64-point K-steps)
+//          in groups of 8 as x[8] y[8] z[8] 0[8] (cleared first when padded).
 // centre[b] = c of cloud b.
 // I: index type (32-bit when the batch's points fit: no 64-bit division per point)
 template <typename I>
 __global__ void pack_kernel(const float* __restrict__ xyz, const unsigned int* __restrict__ bbox,
                             float4* __restrict__ pts, float* __restrict__ pts16,
-                            float4* __restrict__ centre, I n, I total) {
+                            float* __restrict__ gpts, I gper, float4* __restrict__ centre, I n,
+                            I total) {
   const I gpc = (n + 15) / 16;
   for (I i = blockIdx.x * I(blockDim.x) + threadIdx.x; i < total; i += I(gridDim.x) * blockDim.x) {
     const I b = i / n, k = i - b * n;
@@ -175,6 +185,12 @@ __global__ void pack_kernel(const float* __restrict__ xyz, const unsigned int* _
     g[0] = x;
     g[16] = y;
     g[32] = z;
+    const int64_t gi = int64_t(b) * gper + k;
+    float* h = gpts + (gi >> 3) * 32 + (gi & 7);
+    h[0] = x;
+    h[8] = y;
+    h[16] = z;
+    h[24] = 0.0f;
   }
 }
 
@@ -238,27 +254,33 @@ void launch_nu(const float4* omega4, double* nu, int* flags, int m, double eps, 
   nu_kernel<<<1, 256, 0, s>>>(omega4, nu, flags, m, eps, c_r);
 }
 
-void launch_pack_points(const float* xyz, float4* pts, float* pts16, float4* centre,
-                        unsigned int* bbox, int64_t n, int batch, int sms, cudaStream_t s) {
+void launch_bbox(const float* xyz, unsigned int* bbox, int64_t n, int batch, int sms,
+                 cudaStream_t s) {
   cudaMemsetAsync(bbox, 0, size_t(batch) * 6 * sizeof(unsigned int), s);
-  {
-    LaunchScope L("rfd_bbox", s);
-    int64_t chunks = (int64_t(sms) * 8 + batch - 1) / batch;
-    const int64_t maxc = (n + 1023) / 1024;
-    if (chunks > maxc) chunks = maxc;
-    if (chunks < 1) chunks = 1;
-    bbox_kernel<<<dim3(unsigned(chunks), unsigned(batch)), 256, 0, s>>>(xyz, n, bbox);
-  }
+  LaunchScope L("rfd_bbox", s);
+  int64_t chunks = (int64_t(sms) * 2 + batch - 1) / batch;
+  const int64_t maxc = (n + 4095) / 4096;
+  if (chunks > maxc) chunks = maxc;
+  if (chunks < 1) chunks = 1;
+  bbox_kernel<<<dim3(unsigned(chunks), unsigned(batch)), 256, 0, s>>>(xyz, n, bbox);
+}
+
+void launch_pack_points(const float* xyz, const unsigned int* bbox, float4* pts, float* pts16,
+                        float* gpts, int64_t gper, float4* centre, int64_t n, int batch,
+                        cudaStream_t s) {
   LaunchScope L("rfd_pack_points", s);
   const int64_t total = n * batch;
   if (n % 16 != 0) cudaMemsetAsync(pts16, 0, size_t(batch) * ((n + 15) / 16) * 48 * sizeof(float), s);
+  if (gper != n) cudaMemsetAsync(gpts, 0, size_t(batch) * gper * 4 * sizeof(float), s);
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  if (total < (int64_t(1) << 30))  // (i + grid stride stays below 2^31)
-    pack_kernel<int><<<int(blocks), 256, 0, s>>>(xyz, bbox, pts, pts16, centre, int(n), int(total));
+  if (total < (int64_t(1) << 30) && gper * batch < (int64_t(1) << 30))  // (i + grid stride < 2^31)
+    pack_kernel<int><<<int(blocks), 256, 0, s>>>(xyz, bbox, pts, pts16, gpts, int(gper), centre,
+                                                  int(n), int(total));
   else
-    pack_kernel<int64_t><<<int(blocks), 256, 0, s>>>(xyz, bbox, pts, pts16, centre, n, total);
+    pack_kernel<int64_t><<<int(blocks), 256, 0, s>>>(xyz, bbox, pts, pts16, gpts, gper, centre, n,
+                                                      total);
 }
 
 void launch_rotate(const double* X, const float* Xf, int r, int cols, int batch, bool right,

@@ -538,24 +538,6 @@ gram_tc_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict_
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
-// Points -> Gram layout (groups of 8: x[8] y[8] z[8] 0[8]), clouds padded
-// with zero groups to S K-steps.  One thread per (padded) point.
-// I: index type (32-bit when the batch's points fit: no 64-bit division per point)
-template <typename I>
-__global__ void gram_pack_kernel(const float4* __restrict__ pts, I n, I per_cloud, I total,
-                                 float* __restrict__ out) {
-  for (I i = blockIdx.x * I(blockDim.x) + threadIdx.x; i < total; i += I(gridDim.x) * blockDim.x) {
-    const I b = i / per_cloud, p = i - b * per_cloud;
-    const float4 v =
-        (p < n) ? __ldg(pts + int64_t(b) * n + p) : make_float4(0.f, 0.f, 0.f, 0.f);
-    float* g = out + int64_t(i >> 3) * 32 + (i & 7);
-    g[0] = v.x;
-    g[8] = v.y;
-    g[16] = v.z;
-    g[24] = 0.0f;
-  }
-}
-
 // K2: G[b] (interleaved r x r, fp64) from the segment partials, fixed order.
 // grid: (16 chunks x upper tiles, batch); tile (bi <= bj) of the block grid.
 __global__ void __launch_bounds__(256)
@@ -1142,8 +1124,12 @@ static size_t gram_tc_partial_only(const GramGeom& g, int batch) {
 size_t gram_tc_partial_elems(const GramGeom& g, int batch) {
   return gram_tc_partial_only(g, batch) + size_t(batch) * size_t(g.chunk) * (kStepBytes / 4);
 }
+float* gram_points(const GramGeom& g, int batch, float* partial, int64_t* per_cloud) {
+  *per_cloud = int64_t(g.chunk) * kStep;
+  return partial + gram_tc_partial_only(g, batch);
+}
 
-void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, int batch,
+void launch_gram_tc(const float4* omega4, int m, int64_t n, int batch,
                     const GramGeom& g, float* partial, double* G, cudaStream_t s) {
   const bool pairs = g.tile == 2 * kBlk;
   // same partition as gram_tc_geometry (G = g.chunks CTAs or CTA pairs)
@@ -1161,18 +1147,8 @@ void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n, i
     trace = e && e[0] == '1';
     configured = true;
   }
-  float* gpts = partial + gram_tc_partial_only(g, batch);
-  {
-    LaunchScope L("rfd_gram_pack", s);
-    const int64_t per_cloud = int64_t(g.chunk) * kStep, total = per_cloud * batch;
-    int64_t blocks = (total + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    if (total < (int64_t(1) << 30))  // (i + grid stride stays below 2^31)
-      gram_pack_kernel<int><<<int(blocks), 256, 0, s>>>(pts, int(n), int(per_cloud), int(total),
-                                                         gpts);
-    else
-      gram_pack_kernel<int64_t><<<int(blocks), 256, 0, s>>>(pts, n, per_cloud, total, gpts);
-  }
+  // the points in the Gram layout were written by the pack kernel (gram_points)
+  const float* gpts = partial + gram_tc_partial_only(g, batch);
   const unsigned char* gp = reinterpret_cast<const unsigned char*>(gpts);
   if (pairs) {
     {

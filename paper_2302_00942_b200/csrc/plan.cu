@@ -105,6 +105,11 @@ struct rfd_plan {
   uint64_t seed = 0;
   int scaling = 0;
   int symmetric = 1;
+  // sharded cloud: this rank's shard of n_total points
+  int rank = 0, world = 1;
+  rfd_allgather_fn allgather = nullptr;
+  void* ctx = nullptr;
+  int64_t n_total = 0;
   // owned device state
   float4* pts = nullptr;      // batch*n
   float* pts16 = nullptr;     // batch*ceil(n/16)*48: SoA groups of 16 points (pass 1)
@@ -119,6 +124,7 @@ struct rfd_plan {
   int ws_d = 0;
   float* s_partial = nullptr; // batch*chunks*r*16
   double* S = nullptr;        // batch*r*d
+  double* S_parts = nullptr;  // world*r*d (sharded plans: the gathered partials)
   float* Y = nullptr;         // batch*r*d
   int last_d = 0;
   // host-buffer staging
@@ -240,6 +246,7 @@ void free_plan(rfd_plan* p) {
   dfree(p->flags, s);
   dfree(p->s_partial, s);
   dfree(p->S, s);
+  dfree(p->S_parts, s);
   dfree(p->Y, s);
   dfree(p->stage, s);
   delete p;
@@ -298,8 +305,18 @@ rfd_status core_impl(rfd_plan* p, const double* nu, int* flags, double lambda, d
   return RFD_OK;
 }
 
+// all-gather of `count` fp64 through the caller's collective (sharded plans)
+rfd_status exchange(const rfd_plan* p, const double* send, double* recv, size_t count,
+                    cudaStream_t st) {
+  if (p->allgather(p->ctx, send, recv, count, reinterpret_cast<rfd_stream>(st)) != 0)
+    return fail(RFD_ECUDA, "sharded plan: the allgather callback failed");
+  RFD_CUDA(cudaGetLastError());
+  return RFD_OK;
+}
+
 rfd_status create_impl(const float* points, int batch, int64_t n, double eps, double lambda,
-                       int m, uint64_t seed, cudaStream_t st, rfd_plan** plan_out) {
+                       int m, uint64_t seed, const rfd_shard* shard, cudaStream_t st,
+                       rfd_plan** plan_out) {
   if (!plan_out) return fail(RFD_EINVAL, "plan_out is NULL");
   *plan_out = nullptr;
   if (!points) return fail(RFD_EINVAL, "points is NULL");
@@ -310,6 +327,11 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   if (!isfinite(lambda)) return fail(RFD_EINVAL, "lambda must be finite");
   if (reinterpret_cast<uintptr_t>(points) % 4 != 0)
     return fail(RFD_EINVAL, "points must be 4-byte aligned");
+  const int world = shard ? shard->world : 1;
+  if (shard && (shard->world < 1 || shard->rank < 0 || shard->rank >= shard->world ||
+                (shard->world > 1 && !shard->allgather)))
+    return fail(RFD_EINVAL, "shard: need 0 <= rank < world and an allgather for world > 1");
+  if (world > 1 && batch != 1) return fail(RFD_EINVAL, "sharded plans hold one cloud");
 
   int dev = 0;
   RFD_CUDA(cudaGetDevice(&dev));
@@ -331,6 +353,13 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   p->eps = eps;
   p->lambda = lambda;
   p->seed = seed;
+  p->n_total = n;
+  if (shard) {
+    p->rank = shard->rank;
+    p->world = shard->world;
+    p->allgather = shard->allgather;
+    p->ctx = shard->ctx;
+  }
   const int64_t total = n * batch;
   const size_t rr = size_t(p->r) * p->r;
 
@@ -354,17 +383,43 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
                              cudaMemcpyHostToDevice, st));
     dev_xyz = staged;
   }
+  // a4's workspace first: the pack kernel writes the Gram's point layout into it
+  const rfd::GramGeom gg = rfd::gram_tc_geometry(m, n, batch, p->sms);
+  float* gpart = nullptr;
+  RFD_CUDA(tmp.alloc(&gpart, rfd::gram_tc_partial_elems(gg, batch)));
+  int64_t gper = 0;
+  float* gpts = rfd::gram_points(gg, batch, gpart, &gper);
   unsigned int* bbox = nullptr;
   RFD_CUDA(tmp.alloc(&bbox, size_t(batch) * 6));
-  rfd::launch_pack_points(dev_xyz, p->pts, p->pts16, p->centre, bbox, n, batch, p->sms, st);
+  rfd::launch_bbox(dev_xyz, bbox, n, batch, p->sms, st);
+  if (world > 1) {  // one centre for the whole cloud: merge the shards' boxes
+    double *send = nullptr, *recv = nullptr;
+    RFD_CUDA(tmp.alloc(&send, size_t(7)));
+    RFD_CUDA(tmp.alloc(&recv, size_t(7) * world));
+    rfd::launch_bbox_export(bbox, n, send, st);
+    rfd_status xs = exchange(p, send, recv, 7, st);
+    if (xs != RFD_OK) return xs;
+    rfd::launch_bbox_merge(recv, world, bbox, st);
+    std::vector<double> h(size_t(7) * world);
+    RFD_CUDA(cudaMemcpyAsync(h.data(), recv, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RFD_CUDA(cudaStreamSynchronize(st));
+    p->n_total = 0;
+    for (int q = 0; q < world; ++q) p->n_total += int64_t(h[size_t(q) * 7 + 6]);
+  }
+  rfd::launch_pack_points(dev_xyz, bbox, p->pts, p->pts16, gpts, gper, p->centre, n, batch, st);
   rfd::launch_freq(p->omega4, p->omega_rad4, p->nu, p->flags, m, seed, eps, RFD_TRUNCATION_R, cached_c_r(), st);
 
   // a4: Gram on the tensor cores (tcgen05, fp16 hi/lo split)
-  {
-    const rfd::GramGeom gg = rfd::gram_tc_geometry(m, n, batch, p->sms);
-    float* gpart = nullptr;
-    RFD_CUDA(tmp.alloc(&gpart, rfd::gram_tc_partial_elems(gg, batch)));
-    rfd::launch_gram_tc(p->pts, p->omega_rad4, m, n, batch, gg, gpart, p->G, st);
+  if (world > 1) {  // this shard's partial, all-gathered, summed in rank order
+    double *Gl = nullptr, *parts = nullptr;
+    RFD_CUDA(tmp.alloc(&Gl, rr));
+    RFD_CUDA(tmp.alloc(&parts, rr * world));
+    rfd::launch_gram_tc(p->omega_rad4, m, n, batch, gg, gpart, Gl, st);
+    rfd_status xs = exchange(p, Gl, parts, rr, st);
+    if (xs != RFD_OK) return xs;
+    rfd::launch_sum_parts(parts, world, int64_t(rr), p->G, st);
+  } else {
+    rfd::launch_gram_tc(p->omega_rad4, m, n, batch, gg, gpart, p->G, st);
   }
 
   // a5: core
@@ -427,7 +482,7 @@ rfd_status reparam_impl(rfd_plan* p, double eps, double lambda, cudaStream_t st)
 rfd_status spectrum_impl(rfd_plan* p, int k, double* out, cudaStream_t st) {
   if (!p) return fail(RFD_EINVAL, "plan is NULL");
   if (!out) return fail(RFD_EINVAL, "out is NULL");
-  if (k < 1 || int64_t(k) > p->n) return fail(RFD_EINVAL, "k must be in [1, n]");
+  if (k < 1 || int64_t(k) > p->n_total) return fail(RFD_EINVAL, "k must be in [1, n]");
   if (!p->symmetric)
     return fail(RFD_EINVAL, "spectrum needs all nu > 0 (symmetric route D^1/2 G D^1/2)");
   p->stream = st;
@@ -442,7 +497,7 @@ rfd_status spectrum_impl(rfd_plan* p, int k, double* out, cudaStream_t st) {
   RFD_CUDA(tmp.alloc(&mu, size_t(B) * r));
   RFD_CUDA(tmp.alloc(&o, size_t(B) * k));
   RFD_CUDA(tmp.alloc(&bar, size_t(2)));
-  RFD_CUDA(rfd::launch_spectrum(p->G, p->nu, p->m, B, p->n, p->lambda, k, W, P, dg, of, mu, bar,
+  RFD_CUDA(rfd::launch_spectrum(p->G, p->nu, p->m, B, p->n_total, p->lambda, k, W, P, dg, of, mu, bar,
                                 o, st));
   RFD_CUDA(cudaMemcpyAsync(out, o, size_t(B) * k * sizeof(double), cudaMemcpyDefault, st));
   RFD_CUDA(cudaStreamSynchronize(st));
@@ -453,6 +508,7 @@ rfd_status ensure_workspace(rfd_plan* p, int d, cudaStream_t st) {
   if (p->ws_d >= d) return RFD_OK;
   dfree(p->s_partial, st);
   dfree(p->S, st);
+  dfree(p->S_parts, st);
   dfree(p->Y, st);
   p->ws_d = 0;
   const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
@@ -461,6 +517,7 @@ rfd_status ensure_workspace(rfd_plan* p, int d, cudaStream_t st) {
   RFD_CUDA(dalloc(&p->s_partial, part, st));
   RFD_CUDA(dalloc(&p->S, size_t(p->batch) * p->r * d, st));
   RFD_CUDA(dalloc(&p->Y, size_t(p->batch) * p->r * d, st));
+  if (p->world > 1) RFD_CUDA(dalloc(&p->S_parts, size_t(p->world) * p->r * d, st));
   p->ws_d = d;
   return RFD_OK;
 }
@@ -478,7 +535,7 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
   // Small r (<= 128) with d in one chunk and few partials: a7 (S reduction and
   // Y = C^ S) runs fused in pass 2's prologue -- two launches fewer per call
   // (every pass-2 CTA re-reduces its cloud's partials, hence the bound).
-  const bool fuse = p->r <= 128 && d <= 64 &&
+  const bool fuse = p->world == 1 && p->r <= 128 && d <= 64 &&
                     int64_t(ranges) * p->r * d <= 16384;
   // pass 1 on the tensor cores takes up to 64 columns per launch (MMA N = the
   // chunk's columns): the features are regenerated once per chunk (NEXT-2)
@@ -488,6 +545,11 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
     rfd::launch_pass1_tc(p->pts16, p->omega_rad4, p->m, p->n, p->batch, p->sms, ranges, F, d, c0,
                          dc, p->s_partial, st);
     if (!fuse) rfd::launch_reduce_S(p->s_partial, p->m, p->batch, ranges, d, c0, dc, p->S, st);
+  }
+  if (p->world > 1) {  // S = sum over the shards' partials, rank order
+    rfd_status xs = exchange(p, p->S, p->S_parts, size_t(p->r) * d, st);
+    if (xs != RFD_OK) return xs;
+    rfd::launch_sum_parts(p->S_parts, p->world, int64_t(p->r) * d, p->S, st);
   }
   if (!fuse) rfd::launch_core_apply(p->C, p->S, p->m, p->batch, d, p->Y, st);
   // a8: pass 2 on the tensor cores takes up to 64 columns per launch (MMA N =
@@ -510,6 +572,7 @@ rfd_status barycenter_impl(rfd_plan* p, const float* mu_in, const float* area,
                            int32_t* iters_out, cudaStream_t st) {
   if (!p) return fail(RFD_EINVAL, "plan is NULL");
   if (p->batch != 1) return fail(RFD_EINVAL, "barycenter needs a single-cloud plan");
+  if (p->world != 1) return fail(RFD_EINVAL, "barycenter: sharded plans are not supported");
   if (!mu_in || !area || !alpha || !out) return fail(RFD_EINVAL, "NULL argument");
   if (k < 1 || k > 16) return fail(RFD_EINVAL, "k must be in [1, 16]");
   if (max_iter < 1) return fail(RFD_EINVAL, "max_iter must be >= 1");
@@ -583,14 +646,22 @@ extern "C" {
 
 rfd_status rfd_plan_create(const float* points, int64_t n, double eps, double lambda, int32_t m,
                            uint64_t seed, rfd_stream stream, rfd_plan** plan_out) {
-  return create_impl(points, 1, n, eps, lambda, m, seed, reinterpret_cast<cudaStream_t>(stream),
-                     plan_out);
+  return create_impl(points, 1, n, eps, lambda, m, seed, nullptr,
+                     reinterpret_cast<cudaStream_t>(stream), plan_out);
+}
+
+rfd_status rfd_plan_create_sharded(const float* points, int64_t n_local, double eps, double lambda,
+                                   int32_t m, uint64_t seed, const rfd_shard* shard,
+                                   rfd_stream stream, rfd_plan** plan_out) {
+  if (!shard) return fail(RFD_EINVAL, "shard is NULL");
+  return create_impl(points, 1, n_local, eps, lambda, m, seed, shard,
+                     reinterpret_cast<cudaStream_t>(stream), plan_out);
 }
 
 rfd_status rfd_plan_create_batched(const float* points, int32_t batch, int64_t n, double eps,
                                    double lambda, int32_t m, uint64_t seed, rfd_stream stream,
                                    rfd_plan** plan_out) {
-  return create_impl(points, batch, n, eps, lambda, m, seed,
+  return create_impl(points, batch, n, eps, lambda, m, seed, nullptr,
                      reinterpret_cast<cudaStream_t>(stream), plan_out);
 }
 
@@ -649,6 +720,9 @@ rfd_status rfd_plan_info(const rfd_plan* p, rfd_plan_info_t* info) {
   info->eps = p->eps;
   info->lambda = p->lambda;
   info->seed = p->seed;
+  info->n_total = p->n_total;
+  info->rank = p->rank;
+  info->world = p->world;
   return RFD_OK;
 }
 

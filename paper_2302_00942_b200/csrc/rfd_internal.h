@@ -63,15 +63,28 @@ void launch_nu(const float4* omega4, double* nu, int* flags, int m, double eps, 
                cudaStream_t s);
 
 // ---------------------------------------------------------------- pack
-// Per-cloud bounding box (bbox: batch x 6 uint scratch), centre c = its
-// midpoint (centre: batch float4), then pts / pts16 = points - c.
-void launch_pack_points(const float* xyz, float4* pts, float* pts16, float4* centre,
-                        unsigned int* bbox, int64_t n, int batch, int sms, cudaStream_t s);
+// Per-cloud bounding box of the points (bbox: batch x 6 uint, ordered
+// encoding: [0..2] = max ~enc(x) (the minima), [3..5] = max enc(x)).
+void launch_bbox(const float* xyz, unsigned int* bbox, int64_t n, int batch, int sms,
+                 cudaStream_t s);
+// centre c = the bbox midpoint (centre: batch float4); pts / pts16 / gpts (the
+// Gram layout, gper points per cloud) = points - c.
+void launch_pack_points(const float* xyz, const unsigned int* bbox, float4* pts, float* pts16,
+                        float* gpts, int64_t gper, float4* centre, int64_t n, int batch,
+                        cudaStream_t s);
 // out (fp64, batch x r x cols) = R X (right: R X R^T, cols = r) with R the
 // per-frequency rotation by 2 pi omega.c_b (centred -> paper basis).  X fp64,
 // or Xf fp32 when X is NULL.
 void launch_rotate(const double* X, const float* Xf, int r, int cols, int batch, bool right,
                    const float4* omega4, const float4* centre, double* out, cudaStream_t s);
+
+// ---------------------------------------------------------------- shards
+// SURVEY Sec. 8(e) (k_shard.cu): send = the shard's bbox as 6 fp64 + its
+// point count; bbox = union of the world x 7 gathered values; out = the
+// rank-ordered sum of world x count gathered partials.
+void launch_bbox_export(const unsigned int* bbox, int64_t n_local, double* send, cudaStream_t s);
+void launch_bbox_merge(const double* recv, int world, unsigned int* bbox, cudaStream_t s);
+void launch_sum_parts(const double* parts, int world, int64_t count, double* out, cudaStream_t s);
 
 // ---------------------------------------------------------------- Gram
 struct GramGeom {
@@ -85,9 +98,11 @@ struct GramGeom {
 // Tensor-core Gram (k_gram_tc.cu): GramGeom.ntiles holds the number of units.
 GramGeom gram_tc_geometry(int m, int64_t n, int batch, int sms);
 size_t gram_tc_partial_elems(const GramGeom& g, int batch);
-void launch_gram_tc(const float4* pts, const float4* omega4, int m, int64_t n,
-                    int batch, const GramGeom& g, float* partial, double* G,
-                    cudaStream_t s);
+// where launch_pack_points writes the points in the Gram's layout inside the
+// `partial` workspace (per_cloud: padded points per cloud)
+float* gram_points(const GramGeom& g, int batch, float* partial, int64_t* per_cloud);
+void launch_gram_tc(const float4* omega4, int m, int64_t n, int batch, const GramGeom& g,
+                    float* partial, double* G, cudaStream_t s);
 
 // ---------------------------------------------------------------- core
 // Z_b = lambda D^1/2 G D^1/2 (symmetric route) or lambda G D; atomicMax of

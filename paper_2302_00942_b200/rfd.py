@@ -6,8 +6,11 @@ sizes, and status codes into exceptions.  There is no fallback: if the
 library is missing, importing the binding's entry points raises.
 
 Names follow the ABI: ``Plan`` wraps ``rfd_plan_create`` /
-``rfd_plan_create_batched`` / ``rfd_destroy``; ``Plan.integrate`` wraps
-``rfd_integrate``; ``Plan.integrate_host`` wraps ``rfd_integrate_host``.
+``rfd_plan_create_batched`` / ``rfd_destroy``; ``Plan.sharded`` wraps
+``rfd_plan_create_sharded`` (the all-gather callback is torch.distributed's
+``all_gather_into_tensor``: plumbing only, the partial sums are added by the
+library's kernels); ``Plan.integrate`` wraps ``rfd_integrate``;
+``Plan.integrate_host`` wraps ``rfd_integrate_host``.
 """
 
 import ctypes
@@ -23,7 +26,8 @@ RFD_MAX_M = 512
 FIELDS = {"omega": 0, "nu": 1, "gram": 2, "core": 3, "S": 4, "Y": 5}
 
 # Every symbol include/rfd.h declares (checked by tests/test_abi.py).
-EXPORTED = ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_reparam",
+EXPORTED = ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_create_sharded",
+            "rfd_plan_reparam",
             "rfd_plan_spectrum", "rfd_barycenter", "rfd_integrate",
             "rfd_integrate_host", "rfd_destroy", "rfd_last_error", "rfd_plan_info",
             "rfd_plan_export", "rfd_launch_count", "rfd_profile_enable",
@@ -40,7 +44,68 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("batch", ctypes.c_int32), ("m", ctypes.c_int32),
                 ("r", ctypes.c_int32), ("scaling", ctypes.c_int32),
                 ("symmetric", ctypes.c_int32), ("eps", ctypes.c_double),
-                ("lam", ctypes.c_double), ("seed", ctypes.c_uint64)]
+                ("lam", ctypes.c_double), ("seed", ctypes.c_uint64),
+                ("n_total", ctypes.c_int64), ("rank", ctypes.c_int32),
+                ("world", ctypes.c_int32)]
+
+
+# int allgather(void* ctx, const double* send, double* recv, size_t count, stream)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_size_t, ctypes.c_void_p)
+
+
+class Shard(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("allgather", ALLGATHER_FN), ("ctx", ctypes.c_void_p)]
+
+
+def shard_rows(n, rank, world):
+    """Contiguous partition of n points over `world` ranks: rank q owns rows
+    [n q / world, n (q + 1) / world) (sizes differ by at most one)."""
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+class _DeviceArray:
+    """A raw fp64 buffer as a tensor view (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, count):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 3}
+
+
+def _view(ptr, count, device):
+    import torch
+    if device.type == "cuda":
+        return torch.as_tensor(_DeviceArray(ptr, count), device=device)
+    buf = (ctypes.c_double * int(count)).from_address(int(ptr))
+    return torch.frombuffer(buf, dtype=torch.float64)
+
+
+def make_allgather(group=None, device=None):
+    """The rfd_allgather_fn for a torch.distributed process group: wraps the
+    library's send / recv buffers (device pointers; host pointers when
+    ``device`` is the CPU -- gloo, tests) and all-gathers rank-major, ordered
+    on the library's stream.  Returns the ctypes callback (keep a reference)."""
+    import torch
+    import torch.distributed as dist
+    dev = torch.device(device if device is not None else "cuda")
+    world = dist.get_world_size(group)
+
+    def cb(_ctx, send, recv, count, stream):
+        try:
+            src = _view(send, count, dev)
+            dst = _view(recv, count * world, dev)
+            if dev.type == "cuda":
+                with torch.cuda.stream(torch.cuda.ExternalStream(int(stream or 0), device=dev)):
+                    dist.all_gather_into_tensor(dst, src, group=group)
+            else:
+                dist.all_gather(list(dst.view(world, int(count)).unbind(0)), src, group=group)
+            return 0
+        except Exception as e:  # no exception may cross the C ABI
+            import sys
+            print("rfd allgather failed: %r" % (e,), file=sys.stderr)
+            return 1
+    return ALLGATHER_FN(cb)
 
 
 class ProfileEntry(ctypes.Structure):
@@ -65,6 +130,8 @@ def load_library(path=LIB_PATH):
     pp = ctypes.POINTER(ctypes.c_void_p)
     lib.rfd_plan_create.argtypes = [vp, i64, dbl, dbl, i32, u64, vp, pp]
     lib.rfd_plan_create_batched.argtypes = [vp, i32, i64, dbl, dbl, i32, u64, vp, pp]
+    lib.rfd_plan_create_sharded.argtypes = [vp, i64, dbl, dbl, i32, u64, ctypes.POINTER(Shard),
+                                            vp, pp]
     lib.rfd_plan_reparam.argtypes = [vp, dbl, dbl, vp]
     lib.rfd_plan_spectrum.argtypes = [vp, i32, vp, vp]
     lib.rfd_barycenter.argtypes = [vp, vp, vp, vp, i32, i32, dbl, vp, ctypes.POINTER(i32), vp]
@@ -79,7 +146,8 @@ def load_library(path=LIB_PATH):
     lib.rfd_profile_enable.argtypes = [ctypes.c_int]
     lib.rfd_profile_read.argtypes = [ctypes.POINTER(ProfileEntry), i32]
     lib.rfd_profile_read.restype = i32
-    for name in ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_reparam",
+    for name in ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_create_sharded",
+                 "rfd_plan_reparam",
                  "rfd_plan_spectrum", "rfd_barycenter", "rfd_integrate",
                  "rfd_integrate_host", "rfd_plan_info", "rfd_plan_export",
                  "rfd_profile_enable"):
@@ -125,14 +193,22 @@ class Plan:
     host tensor / numpy array (the library copies it).
     """
 
-    def __init__(self, points, eps, lam, m, seed, stream=None):
+    def __init__(self, points, eps, lam, m, seed, stream=None, _shard=None):
         lib = load_library()
         _check_f32(points, "points")
         shape = tuple(points.shape)
         self._keep = points
+        self._shard = _shard  # (keeps the allgather callback alive)
         handle = ctypes.c_void_p()
         s = _stream_handle(stream)
-        if len(shape) == 2 and shape[1] == 3:
+        if _shard is not None:
+            if len(shape) != 2 or shape[1] != 3:
+                raise ValueError("a shard's points must be (n_local, 3)")
+            self.batch, self.n = 1, shape[0]
+            st = lib.rfd_plan_create_sharded(_ptr(points), self.n, float(eps), float(lam), int(m),
+                                             int(seed), ctypes.byref(_shard), s,
+                                             ctypes.byref(handle))
+        elif len(shape) == 2 and shape[1] == 3:
             self.batch, self.n = 1, shape[0]
             st = lib.rfd_plan_create(_ptr(points), self.n, float(eps), float(lam), int(m),
                                      int(seed), s, ctypes.byref(handle))
@@ -148,6 +224,22 @@ class Plan:
         self.m, self.r = int(m), 2 * int(m)
         self.eps, self.lam, self.seed = float(eps), float(lam), int(seed)
         self._keep = None
+
+    @classmethod
+    def sharded(cls, points_local, eps, lam, m, seed, group=None, stream=None):
+        """This rank's shard (n_local x 3 CUDA points) of one cloud split over
+        the ranks of a torch.distributed process group: the
+        Gram and S partials are all-gathered and summed in rank order by the
+        library; every rank gets the same C^ and its own rows of out."""
+        import torch.distributed as dist
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        import torch
+        # the library's send / recv buffers are device memory (points may be host)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        cb = make_allgather(group, dev) if world > 1 else ALLGATHER_FN()
+        shard = Shard(rank, world, cb, None)
+        return cls(points_local, eps, lam, m, seed, stream=stream, _shard=shard)
 
     # -- lifecycle ---------------------------------------------------------
     def close(self):

@@ -399,27 +399,36 @@ def test_barycenter_identity_kernel_closed_form():
             got, its = _bary_gpu(plan, mus[:k], a, alpha, iters)
             assert its == iters
             assert relerr(got, geo) <= 1e-6, (alpha, iters, relerr(got, geo))
-        _, its = _bary_gpu(plan, mus[:k], a, alpha, 50, tol=1e-9)
-        assert its == 2  # fixed point at iteration 1
+        # fixed point at iteration 1 (up to the fp32 rounding of FM_K's input,
+        # ~1e-7 of each mu_n: sum |mu_2 - mu_1| ~ 3e-4)
+        _, its = _bary_gpu(plan, mus[:k], a, alpha, 50, tol=1e-3)
+        assert its == 2
 
 
-def test_barycenter_first_iteration_matches_oracle():
+@pytest.mark.parametrize("floor", [0.0, 0.2])
+def test_barycenter_matches_oracle(floor):
     # NEXT-1 with the random-feature kernel (lambda > 0 as in the paper's runs,
-    # PAPER.md:1061) against the fp64 oracle where Alg. 1 is well conditioned:
-    # iteration 1 on floored inputs moves ~2.5 eta under FM_K perturbations of
-    # eta (tests/test_oracle_integrator.py::
-    # test_barycenter_conditioning_on_random_feature_kernels).
+    # PAPER.md:1061) against the fp64 oracle (Alg. 1, readings A20) after 1, 3
+    # and 10 iterations and at the tol stop (same iteration count).  The
+    # iteration amplifies FM_K errors (tests/test_oracle_integrator.py::
+    # test_barycenter_conditioning_on_random_feature_kernels); the GPU keeps
+    # v, w, d, mu in fp64 and FM_K's normwise error is ~1e-7
+    # (tools/bary_trace.py, profiles/r02_bary_trace*.txt).
     from workloads import barycenter_inputs
 
-    x, a, mus = barycenter_inputs(2000, floor=0.2)
+    x, a, mus = barycenter_inputs(2000, floor=floor)
     plan = rfd.Plan(torch.from_numpy(x).cuda(), 0.03, 0.1, 256, 5)
-    got, its = _bary_gpu(plan, mus, a, [1 / 3] * 3, 1)
-    ref, rits = orf.Plan(x, 0.03, 0.1, 256, 5).barycenter(mus, a, [1 / 3] * 3, 1)
-    assert its == rits == 1
-    err = relerr(got, ref)
-    print("barycenter iteration 1: err %.2e" % err)
-    assert err <= TOL
-    assert abs(float(a @ got) - 1.0) < 1e-5
+    ref_plan = orf.Plan(x, 0.03, 0.1, 256, 5)
+    for iters, tol in ((1, 0.0), (3, 0.0), (10, 0.0), (300, 1e-3)):
+        got, its = _bary_gpu(plan, mus, a, [1 / 3] * 3, iters, tol=tol)
+        ref, rits = ref_plan.barycenter(mus, a, [1 / 3] * 3, iters, tol=tol)
+        err = relerr(got, ref)
+        print("barycenter floor=%g iters=%d tol=%g: %d/%d iterations, err %.2e"
+              % (floor, iters, tol, its, rits, err))
+        assert its == rits
+        assert err <= TOL
+        assert np.isfinite(got).all() and (got >= 0).all()
+        assert abs(float(a @ got) - 1.0) < 1e-5
 
 
 @pytest.mark.parametrize("floor,iters,tol", [(0.0, 10, 0.0), (0.2, 10, 0.0), (0.0, 200, 1e-3)])

@@ -229,29 +229,6 @@ def test_adjacency_error_falls_with_m_and_is_cube_graph():
     assert inf16 < _median_mse(16, 1)
 
 
-def test_dense_spec_examples():
-    # SPEC.md:199-201.
-    X = np.eye(3)
-    np.testing.assert_allclose(dense.symmetric_expm_apply(np.eye(3), 1.0, X), math.e * X, rtol=1e-14)
-    np.testing.assert_allclose(
-        dense.symmetric_expm_apply(np.diag([0.0, math.log(2.0)]), 1.0, np.ones(2))[:, 0],
-        [1.0, 2.0], rtol=1e-14)
-    rng = np.random.default_rng(0)
-    A = rng.standard_normal((30, 30))
-    W = A + A.T
-    np.testing.assert_allclose(dense.symmetric_expm_apply(W, 0.1, np.eye(30)),
-                               scipy.linalg.expm(0.1 * W), rtol=1e-10, atol=1e-12)
-
-
-def test_dense_graph_two_points():
-    X = np.array([[0.0, 0.0, 0.0], [0.1, 0.1, 0.0]])
-    # L-inf distance 0.1 <= 0.15 but L1 distance 0.2 > 0.15.
-    assert dense.epsilon_graph(X, 0.15, "inf")[0, 1] == 1.0
-    assert dense.epsilon_graph(X, 0.15, 1)[0, 1] == 0.0
-    np.testing.assert_allclose(dense.exact_diffusion(X, np.eye(2), 0.15, 1.0, 1), np.eye(2) * math.e,
-                               rtol=1e-14)
-
-
 def test_barycenter_geometric_mean_pin():
     # Alg. 1 step 3 is a weighted GEOMETRIC mean of the d^i.
     # With FM = identity, d^i = v^i (a w^i) = v^i a mu^i / (a v^i) = mu^i for
@@ -296,14 +273,16 @@ def test_barycenter_clamp_and_error():
 
 
 def test_barycenter_conditioning_on_random_feature_kernels():
-    # DESIGN.md A20 (numerics): Alg. 1 divides by FM_K outputs.  A normwise
-    # error of FM_K (relative to each column's max, as fp32 arithmetic gives)
-    # is a large RELATIVE error where an output is small, and the clamp can flip.
-    # On the GPU test's inputs (workloads.barycenter_inputs) the oracle itself
-    # moves by up to O(1e-2) after 10 iterations when each FM_K output is
-    # perturbed by 3e-6 of its column max -- no fp32 kernel can be gated at 1e-4
-    # there -- while iteration 1 on the floored inputs moves linearly (~2.5x
-    # eta): the regime the GPU is gated in against the oracle.
+    # DESIGN.md A20 (numerics): Alg. 1 divides by FM_K outputs, so it amplifies
+    # FM_K errors; how much is heavy-tailed (an entry near the clamp can flip).
+    # On the GPU test's inputs (workloads.barycenter_inputs), with every FM_K
+    # output perturbed uniformly by eta of its column max:
+    #   * iteration 1 on the floored inputs moves linearly, ~2.5 eta;
+    #   * 10 iterations stay within 2e-5 at eta = 1e-7 (GPU FM_K errors are
+    #     1e-8 .. 6e-7, tools/bary_trace.py), but eta = 1e-6 can move the
+    #     floored inputs' result by O(1).
+    # So a 1e-4 gate after 10 iterations holds only for an FM_K accurate to
+    # ~1e-7 -- fp32 iterates (the round-1 design) could not meet it.
     from workloads import barycenter_inputs
 
     x, a, mus = barycenter_inputs(2000)
@@ -320,6 +299,7 @@ def test_barycenter_conditioning_on_random_feature_kernels():
         return [np.abs(rfd.barycenter(noisy, m, a, [1 / 3] * 3, iters)[0] - ref).max()
                 / np.abs(ref).max() for _ in range(reps)]
 
-    assert max(moved(mus, 10, 3e-6)) > 1e-2
     well = moved(mus_f, 1, 1e-5)
     assert max(well) < 5e-5 and min(well) > 1e-6
+    assert max(moved(mus, 10, 1e-7)) < 2e-5
+    assert max(moved(mus_f, 10, 1e-6)) > 0.5

@@ -100,6 +100,38 @@ def test_frequency_anchor_seed0():
     assert att[0] == 1
 
 
+def test_frequencies_every_config_seed():
+    # SURVEY.md [S12] (tests/golden/pins.json "config_seed_frequencies"): for
+    # each config seed, the nu range and max|omega_c| over all m frequencies
+    # and no rejections.  Covers every frequency of every seed (a swapped
+    # (k, attempt) counter word or key word would change them).
+    pin = PINS["config_seed_frequencies"]
+    for row in pin["rows"]:
+        om, att = rfd.frequencies(row["seed"], row["m"])
+        nu = rfd.importance_weights(om, row["eps"], C_R)
+        assert att.max() == 1, row
+        assert nu.min() == pytest.approx(row["nu_min"], rel=pin["rel_tol"]), row
+        assert nu.max() == pytest.approx(row["nu_max"], rel=pin["rel_tol"]), row
+        assert float(np.abs(om).max()) == pytest.approx(row["max_abs_omega"], abs=pin["abs_tol_omega"])
+
+
+def test_estimator_unbiased_at_coincident_and_far_points():
+    # SPEC.md:390-398 (build_decomposition examples, DERIVED by Monte Carlo):
+    # over 50 seeds the RF estimate W~(v, w) = (1/m) sum cos(2 pi omega.z)
+    # tau/p has mean within 3 standard errors of f(z):
+    # 1 for coincident points, 0 at distance 2 eps.  At z = (eps, eps, 0) --
+    # L1 distance 2 eps, but a corner of the L-infinity cube -- the Fourier
+    # inversion of the product-sinc converges to the corner value 1/2 * 1/2 =
+    # 1/4, not 0: the estimator targets the cube graph (A2).
+    eps, m = 0.15, 256
+    for z, want in (([0.0, 0.0, 0.0], 1.0), ([2 * eps, 0.0, 0.0], 0.0),
+                    ([eps, eps, 0.0], 0.25)):
+        vals = np.array([rfd.estimator(np.array([z]), rfd.frequencies(5000 + s, m)[0], eps, C_R)[0]
+                         for s in range(50)])
+        se = vals.std(ddof=1) / math.sqrt(vals.size)
+        assert abs(vals.mean() - want) < 3 * se, (z, vals.mean(), se)
+
+
 def test_frequencies_truncated_and_gaussian():
     om, att = rfd.frequencies(99, 4096)
     assert np.all(np.abs(om.astype(np.float64)).sum(axis=1) <= rfd.DEFAULT_R + 1e-5)
