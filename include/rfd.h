@@ -32,6 +32,18 @@
  *   - There is no CPU fallback: every arithmetic step runs in the library's
  *     CUDA kernels (sm_100a).  Without a usable GPU the calls return
  *     RFD_ECUDA.
+ *
+ * Coordinate range.  W depends on the points only through n_i - n_j
+ * (Eq. 9), so the library first moves each cloud to the
+ * midpoint c of its bounding box (exact: phi(c + y) = R phi(y) with a 2x2
+ * rotation R per frequency that commutes with D; exported G, C^, S, Y are
+ * rotated back).  Results are therefore translation-invariant.  The feature
+ * argument 2 pi omega.(x - c) is evaluated in fp32, so the error grows with
+ * T = max_k sum_c |omega_kc| h_c (turns; h = the box's half-extents):
+ * measured normwise Delta error ~1.6e-7 T (1.1e-6 at T = 5.9, 7.2e-6 at
+ * T = 59, 4.8e-5 at T = 295; tests/test_gpu_parity.py::
+ * test_translated_and_scaled_clouds_parity).  The 1e-4 parity gate holds for
+ * T up to ~500 turns; unit-scale clouds (all five configs) have T = 3 .. 6.
  */
 #ifndef RFD_H_
 #define RFD_H_
@@ -178,12 +190,14 @@ rfd_status rfd_plan_spectrum(rfd_plan* plan, int32_t k, double* out, rfd_stream 
  *   w^i <- mu^i / FM_K(a * v^i);  d^i <- v^i * FM_K(a * w^i);
  *   mu <- prod_i (d^i)^alpha_i (mu reset to ones each iteration);
  *   v^i <- v^i * mu / d^i
- * with the readings of SPEC.md:559, 628-629 (A20): denominators
- * (FM_K(a * v^i) and d^i) clamped at 1e-30, stop after max_iter or when
+ * with the readings of SPEC.md:559, 628-629 (A20): mu reset to ones
+ * each outer iteration, both denominators (FM_K(a * v^i) and d^i) clamped at
+ * 1e-30 (d^i before its power), stop after max_iter or when
  * ||mu_new - mu_old||_1 < tol (tol = 0: run max_iter), output normalised so
- * <a, mu> = 1.  The k distributions are the k columns of one field, so each
- * FM_K is one multi-column rfd_integrate.  The paper runs it with lambda > 0
- * (0.5).
+ * <a, mu> = 1.  The iterates v, w, d, mu are fp64; the k distributions are
+ * the k columns of one field, so each FM_K is one multi-column rfd_integrate
+ * on fp32(a v s) with s a per-column power of two (exact by linearity; keeps
+ * fp32 in range).  The paper runs it with lambda > 0 (0.5).
  *   mu     DEVICE k x N fp32 (row i = distribution i).   area  DEVICE N fp32.
  *   alpha  HOST k fp64, > 0, sum 1.   1 <= k <= 16, max_iter >= 1, tol >= 0.
  *   out    DEVICE N fp32 (the barycenter).   iters  HOST (may be NULL):
@@ -242,7 +256,9 @@ rfd_status rfd_plan_info(const rfd_plan* plan, rfd_plan_info_t* info);
 
 /*
  * rfd_plan_export -- copy plan state to HOST memory (tests / introspection).
- * Feature index order is the paper's: columns 0..m-1 cosines, m..2m-1 sines.
+ * Feature index order is the paper's: columns 0..m-1 cosines, m..2m-1 sines;
+ * G, C^, S, Y in the paper's basis of the UNcentred points (rotated back from
+ * the device's centred basis in fp64; Y rounded to fp32 after the rotation).
  *   RFD_OMEGA  m x 3 fp32          RFD_NU    m fp64
  *   RFD_GRAM   batch x r x r fp64  RFD_CORE  batch x r x r fp64
  *   RFD_S      batch x r x d fp64  RFD_Y     batch x r x d fp32
