@@ -225,12 +225,36 @@ rfd_status rfd_integrate(rfd_plan* plan, const float* F, int32_t d, float* out,
 
 /*
  * rfd_integrate_host -- the same with HOST buffers: copies F host->device,
- * integrates, copies out device->host, all enqueued on `stream`.  With
+ * integrates, copies out device->host, ordered on `stream`.  Single clouds
+ * with d <= 64 and n >= 16384 are pipelined: F travels in 8 point-range
+ * chunks on an internal copy stream and pass 1 runs per chunk as it lands;
+ * pass 2 runs per chunk with each chunk's D2H copy right behind it (pass-1
+ * partials of all chunks summed in a fixed order: deterministic).  With
  * pinned host memory the call is asynchronous (synchronize `stream` before
  * reading out); with pageable memory the copies block the host.
  */
 rfd_status rfd_integrate_host(rfd_plan* plan, const float* F_host, int32_t d,
                               float* out_host, rfd_stream stream);
+
+/*
+ * rfd_gfi_host -- the whole graph-field integration i = exp(lambda W~) F
+ * (Eq. 1 with Sec. 2.4's kernel: pre-processing + inference) from
+ * HOST buffers in one call, overlapping the transfers with the computation:
+ * the points go up first, the field's H2D copies (in point-range chunks, on
+ * an internal copy stream) run while the plan's frequencies, Gram and core
+ * compute, pass 1 consumes each chunk as it lands, and the D2H copies of out
+ * follow pass 2 chunk by chunk.  Same arithmetic as rfd_plan_create +
+ * rfd_integrate_host (bitwise).
+ *   points  n x 3 HOST fp32;  F_host / out_host  n x d HOST fp32 (pinned for
+ *           asynchrony; out may alias F); other arguments as rfd_plan_create.
+ *   plan_out  NULL (the plan is destroyed) or receives the plan for reuse.
+ * Blocks the host while the plan's core is formed (as rfd_plan_create);
+ * synchronize `stream` before reading out_host.  Errors: as rfd_plan_create
+ * and rfd_integrate_host.
+ */
+rfd_status rfd_gfi_host(const float* points, int64_t n, double eps, double lambda, int32_t m,
+                        uint64_t seed, const float* F_host, int32_t d, float* out_host,
+                        rfd_stream stream, rfd_plan** plan_out);
 
 /* rfd_destroy -- frees the plan and its device memory.  NULL-safe. */
 void rfd_destroy(rfd_plan* plan);

@@ -9,6 +9,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -127,9 +128,13 @@ struct rfd_plan {
   double* S_parts = nullptr;  // world*r*d (sharded plans: the gathered partials)
   float* Y = nullptr;         // batch*r*d
   int last_d = 0;
-  // host-buffer staging
+  // host-buffer staging (rfd_integrate_host / rfd_gfi_host)
   float* stage = nullptr;
   size_t stage_elems = 0;
+  float* pipe_partial = nullptr;  // pass-1 partials of the chunked (pipelined) host path
+  size_t pipe_partial_elems = 0;
+  cudaStream_t cs_h2d = nullptr, cs_d2h = nullptr;  // copy streams of the host path
+  cudaEvent_t ev[2 * 16 + 2] = {};
   cudaStream_t stream = nullptr;  // stream of the last call (frees are ordered on it)
 };
 
@@ -249,6 +254,11 @@ void free_plan(rfd_plan* p) {
   dfree(p->S_parts, s);
   dfree(p->Y, s);
   dfree(p->stage, s);
+  dfree(p->pipe_partial, s);
+  if (p->cs_h2d) cudaStreamDestroy(p->cs_h2d);
+  if (p->cs_d2h) cudaStreamDestroy(p->cs_d2h);
+  for (cudaEvent_t e : p->ev)
+    if (e) cudaEventDestroy(e);
   delete p;
 }
 
@@ -565,6 +575,121 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
   return RFD_OK;
 }
 
+// Host buffers, pipelined: the field travels in K point-range chunks.  The
+// H2D copy of chunk c (copy stream) overlaps pass 1 of the chunks before it
+// (each chunk's pass 1 is its own launch writing its own partial slots; S =
+// the fixed-order sum of all slots, chunk-major); pass 2 runs per chunk too
+// and the D2H copy of chunk c (second copy stream) overlaps pass 2 of the
+// chunks after it.  `h2d_issued`: the caller has already enqueued the H2D
+// copies into p->stage on cs_h2d with events ev[0..K) (rfd_gfi_host starts
+// them before the plan exists).  Single-cloud plans, d <= 64 (one pass-1
+// column chunk); otherwise the serial path.
+constexpr int kPipeChunks = 8;
+
+int64_t pipe_chunk_begin(int64_t n, int c) {
+  // boundaries at multiples of 2048 points (whole pass-1 groups and pass-2
+  // tiles; F blocks stay 16-byte aligned for any d)
+  return std::min<int64_t>(n, ((n * c / kPipeChunks) + 2047) / 2048 * 2048);
+}
+
+rfd_status pipe_streams(rfd_plan* p) {
+  if (!p->cs_h2d) RFD_CUDA(cudaStreamCreateWithFlags(&p->cs_h2d, cudaStreamNonBlocking));
+  if (!p->cs_d2h) RFD_CUDA(cudaStreamCreateWithFlags(&p->cs_d2h, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : p->ev)
+    if (!e) RFD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return RFD_OK;
+}
+
+rfd_status ensure_stage(rfd_plan* p, size_t elems, cudaStream_t st) {
+  if (p->stage_elems >= elems) return RFD_OK;
+  dfree(p->stage, st);
+  p->stage_elems = 0;
+  RFD_CUDA(dalloc(&p->stage, elems, st));
+  p->stage_elems = elems;
+  return RFD_OK;
+}
+
+// enqueue the H2D copies of F's chunks on cs_h2d (after `st`'s prior work)
+rfd_status pipe_h2d(rfd_plan* p, const float* F_host, int d, cudaStream_t st) {
+  RFD_CUDA(cudaEventRecord(p->ev[2 * kPipeChunks], st));
+  RFD_CUDA(cudaStreamWaitEvent(p->cs_h2d, p->ev[2 * kPipeChunks], 0));
+  for (int c = 0; c < kPipeChunks; ++c) {
+    const int64_t a = pipe_chunk_begin(p->n, c), b = pipe_chunk_begin(p->n, c + 1);
+    if (b > a)
+      RFD_CUDA(cudaMemcpyAsync(p->stage + a * d, F_host + a * d, size_t(b - a) * d * sizeof(float),
+                               cudaMemcpyHostToDevice, p->cs_h2d));
+    RFD_CUDA(cudaEventRecord(p->ev[c], p->cs_h2d));
+  }
+  return RFD_OK;
+}
+
+rfd_status integrate_host_pipelined(rfd_plan* p, const float* F_host, int d, float* out_host,
+                                    bool h2d_issued, cudaStream_t st) {
+  p->stream = st;
+  rfd_status rs = ensure_workspace(p, d, st);
+  if (rs != RFD_OK) return rs;
+  const int r = p->r;
+  // partial slots of every chunk's pass 1
+  int rg[kPipeChunks];
+  int64_t slots = 0;
+  for (int c = 0; c < kPipeChunks; ++c) {
+    const int64_t nc = pipe_chunk_begin(p->n, c + 1) - pipe_chunk_begin(p->n, c);
+    rg[c] = nc > 0 ? rfd::pass1_tc_ranges(p->m, nc, 1, p->sms) : 0;
+    slots += rg[c];
+  }
+  const size_t need = size_t(slots) * r * d;
+  if (p->pipe_partial_elems < need) {
+    dfree(p->pipe_partial, st);
+    p->pipe_partial_elems = 0;
+    RFD_CUDA(dalloc(&p->pipe_partial, need, st));
+    p->pipe_partial_elems = need;
+  }
+  if (!h2d_issued) {
+    rs = pipe_h2d(p, F_host, d, st);
+    if (rs != RFD_OK) return rs;
+  }
+  // a6 per chunk, each as soon as its field has arrived
+  int64_t slot = 0;
+  for (int c = 0; c < kPipeChunks; ++c) {
+    const int64_t a = pipe_chunk_begin(p->n, c), nc = pipe_chunk_begin(p->n, c + 1) - a;
+    if (nc <= 0) continue;
+    RFD_CUDA(cudaStreamWaitEvent(st, p->ev[c], 0));
+    rfd::launch_pass1_tc(p->pts16 + (a / 16) * 48, p->omega_rad4, p->m, nc, 1, p->sms, rg[c],
+                         p->stage + a * d, d, 0, d, p->pipe_partial + size_t(slot) * r * d, st);
+    slot += rg[c];
+  }
+  // a7
+  rfd::launch_reduce_S(p->pipe_partial, p->m, 1, int(slots), d, 0, d, p->S, st);
+  if (p->world > 1) {
+    rs = exchange(p, p->S, p->S_parts, size_t(r) * d, st);
+    if (rs != RFD_OK) return rs;
+    rfd::launch_sum_parts(p->S_parts, p->world, int64_t(r) * d, p->S, st);
+  }
+  rfd::launch_core_apply(p->C, p->S, p->m, 1, d, p->Y, st);
+  // a8 per chunk (in place in the stage), each chunk's D2H right behind it
+  const int w2 = rfd::pass2_tc_width(p->m);
+  for (int c = 0; c < kPipeChunks; ++c) {
+    const int64_t a = pipe_chunk_begin(p->n, c), nc = pipe_chunk_begin(p->n, c + 1) - a;
+    if (nc <= 0) continue;
+    float* f = p->stage + a * d;
+    for (int c0 = 0; c0 < d; c0 += w2) {
+      const int dc = (d - c0 < w2) ? d - c0 : w2;
+      rfd::launch_pass2_tc(p->pts + a, p->omega_rad4, p->m, nc, 1, p->sms, p->Y, f, f, d, c0, dc,
+                           nullptr, 0, p->C, p->S, p->Y, st);
+    }
+    RFD_CUDA(cudaEventRecord(p->ev[kPipeChunks + c], st));
+    RFD_CUDA(cudaStreamWaitEvent(p->cs_d2h, p->ev[kPipeChunks + c], 0));
+    RFD_CUDA(cudaMemcpyAsync(out_host + a * d, f, size_t(nc) * d * sizeof(float),
+                             cudaMemcpyDeviceToHost, p->cs_d2h));
+  }
+  // the caller's stream resumes after the last copy (stream semantics)
+  RFD_CUDA(cudaEventRecord(p->ev[2 * kPipeChunks + 1], p->cs_d2h));
+  RFD_CUDA(cudaStreamWaitEvent(st, p->ev[2 * kPipeChunks + 1], 0));
+  RFD_CUDA(cudaGetLastError());
+  p->last_d = d;
+  return RFD_OK;
+}
+
 // NEXT-1: Alg. 1 with FM_K = rfd_integrate on the
 // N x k field of the k distributions (k_sinkhorn.cu).
 rfd_status barycenter_impl(rfd_plan* p, const float* mu_in, const float* area,
@@ -692,17 +817,86 @@ rfd_status rfd_integrate_host(rfd_plan* plan, const float* F_host, int32_t d, fl
   if (d < 1) return fail(RFD_EINVAL, "d must be >= 1");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t elems = size_t(plan->batch) * plan->n * d;
-  if (plan->stage_elems < elems) {
-    dfree(plan->stage, st);
-    plan->stage_elems = 0;
-    RFD_CUDA(dalloc(&plan->stage, elems, st));
-    plan->stage_elems = elems;
+  RFD_CUDA(ensure_stage(plan, elems, st) == RFD_OK ? cudaSuccess : cudaErrorMemoryAllocation);
+  if (plan->batch == 1 && d <= 64 && plan->n >= 2048 * kPipeChunks) {
+    const rfd_status ps = pipe_streams(plan);
+    if (ps != RFD_OK) return ps;
+    return integrate_host_pipelined(plan, F_host, d, out_host, false, st);
   }
   RFD_CUDA(cudaMemcpyAsync(plan->stage, F_host, elems * sizeof(float), cudaMemcpyHostToDevice, st));
   rfd_status rs = integrate_impl(plan, plan->stage, d, plan->stage, st);
   if (rs != RFD_OK) return rs;
   RFD_CUDA(cudaMemcpyAsync(out_host, plan->stage, elems * sizeof(float), cudaMemcpyDeviceToHost, st));
   return RFD_OK;
+}
+
+rfd_status rfd_gfi_host(const float* points, int64_t n, double eps, double lambda, int32_t m,
+                        uint64_t seed, const float* F_host, int32_t d, float* out_host,
+                        rfd_stream stream, rfd_plan** plan_out) {
+  if (plan_out) *plan_out = nullptr;
+  if (!points || !F_host || !out_host) return fail(RFD_EINVAL, "NULL argument");
+  if (d < 1) return fail(RFD_EINVAL, "d must be >= 1");
+  if (n < 1) return fail(RFD_EINVAL, "n must be >= 1");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (d > 64 || n < 2048 * kPipeChunks || is_device_pointer(points)) {  // nothing to overlap
+    rfd_plan* p = nullptr;
+    rfd_status rs = create_impl(points, 1, n, eps, lambda, m, seed, nullptr, st, &p);
+    if (rs != RFD_OK) return rs;
+    rs = rfd_integrate_host(p, F_host, d, out_host, stream);
+    if (rs != RFD_OK || !plan_out) rfd_destroy(p);
+    else *plan_out = p;
+    return rs;
+  }
+  // The field's H2D copies start right behind the points' and run while the
+  // plan (Gram, core) computes; pass 1 consumes each chunk as it lands.
+  rfd_plan* stub = new rfd_plan();  // holds the streams, events and stage until the plan exists
+  struct StubGuard {
+    rfd_plan* s;
+    ~StubGuard() {
+      if (s) free_plan(s);
+    }
+  } sg{stub};
+  stub->stream = st;
+  stub->n = n;
+  rfd_status rs = pipe_streams(stub);
+  if (rs != RFD_OK) return rs;
+  rs = ensure_stage(stub, size_t(n) * d, st);
+  if (rs != RFD_OK) return rs;
+  float* pts_dev = nullptr;
+  RFD_CUDA(dalloc(&pts_dev, size_t(n) * 3, st));
+  struct PtsGuard {
+    float* p;
+    cudaStream_t s;
+    ~PtsGuard() { dfree(p, s); }
+  } pg{pts_dev, st};
+  RFD_CUDA(cudaEventRecord(stub->ev[2 * kPipeChunks], st));
+  RFD_CUDA(cudaStreamWaitEvent(stub->cs_h2d, stub->ev[2 * kPipeChunks], 0));
+  RFD_CUDA(cudaMemcpyAsync(pts_dev, points, size_t(n) * 3 * sizeof(float), cudaMemcpyHostToDevice,
+                           stub->cs_h2d));
+  RFD_CUDA(cudaEventRecord(stub->ev[2 * kPipeChunks + 1], stub->cs_h2d));
+  rs = pipe_h2d(stub, F_host, d, stub->cs_h2d);
+  if (rs != RFD_OK) return rs;
+  RFD_CUDA(cudaStreamWaitEvent(st, stub->ev[2 * kPipeChunks + 1], 0));
+  rfd_plan* p = nullptr;
+  rs = create_impl(pts_dev, 1, n, eps, lambda, m, seed, nullptr, st, &p);
+  if (rs != RFD_OK) {
+    cudaStreamSynchronize(stub->cs_h2d);
+    return rs;
+  }
+  // hand the streams, events and staged field over to the plan
+  std::swap(p->stage, stub->stage);
+  std::swap(p->stage_elems, stub->stage_elems);
+  std::swap(p->cs_h2d, stub->cs_h2d);
+  std::swap(p->cs_d2h, stub->cs_d2h);
+  for (int i = 0; i < 2 * kPipeChunks + 2; ++i) std::swap(p->ev[i], stub->ev[i]);
+  rs = integrate_host_pipelined(p, F_host, d, out_host, true, st);
+  if (rs != RFD_OK || !plan_out) {
+    cudaStreamSynchronize(st);
+    rfd_destroy(p);
+  } else {
+    *plan_out = p;
+  }
+  return rs;
 }
 
 void rfd_destroy(rfd_plan* plan) { free_plan(plan); }

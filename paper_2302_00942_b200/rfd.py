@@ -29,7 +29,8 @@ FIELDS = {"omega": 0, "nu": 1, "gram": 2, "core": 3, "S": 4, "Y": 5}
 EXPORTED = ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_create_sharded",
             "rfd_plan_reparam",
             "rfd_plan_spectrum", "rfd_barycenter", "rfd_integrate",
-            "rfd_integrate_host", "rfd_destroy", "rfd_last_error", "rfd_plan_info",
+            "rfd_integrate_host", "rfd_gfi_host", "rfd_destroy", "rfd_last_error",
+            "rfd_plan_info",
             "rfd_plan_export", "rfd_launch_count", "rfd_profile_enable",
             "rfd_profile_read")
 
@@ -137,6 +138,7 @@ def load_library(path=LIB_PATH):
     lib.rfd_barycenter.argtypes = [vp, vp, vp, vp, i32, i32, dbl, vp, ctypes.POINTER(i32), vp]
     lib.rfd_integrate.argtypes = [vp, vp, i32, vp, vp]
     lib.rfd_integrate_host.argtypes = [vp, vp, i32, vp, vp]
+    lib.rfd_gfi_host.argtypes = [vp, i64, dbl, dbl, i32, u64, vp, i32, vp, vp, pp]
     lib.rfd_destroy.argtypes = [vp]
     lib.rfd_destroy.restype = None
     lib.rfd_last_error.restype = ctypes.c_char_p
@@ -149,7 +151,7 @@ def load_library(path=LIB_PATH):
     for name in ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_create_sharded",
                  "rfd_plan_reparam",
                  "rfd_plan_spectrum", "rfd_barycenter", "rfd_integrate",
-                 "rfd_integrate_host", "rfd_plan_info", "rfd_plan_export",
+                 "rfd_integrate_host", "rfd_gfi_host", "rfd_plan_info", "rfd_plan_export",
                  "rfd_profile_enable"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -362,6 +364,32 @@ class Plan:
         if field in ("gram", "core", "S", "Y") and B == 1:
             arr = arr[0]
         return arr
+
+
+def gfi_host(points, eps, lam, m, seed, F_host, out_host, keep_plan=False, stream=None):
+    """rfd_gfi_host: plan + integrate from HOST buffers in one call, the
+    transfers overlapped with the computation.  points (N, 3), F_host and
+    out_host (N[, d]) host float32 (pinned for asynchrony).  Returns the Plan
+    when keep_plan, else None; synchronize the stream before reading out_host."""
+    lib = load_library()
+    for a, nm in ((points, "points"), (F_host, "F"), (out_host, "out")):
+        _check_f32(a, nm)
+    n = int(points.shape[0])
+    if tuple(points.shape) != (n, 3) or int(F_host.shape[0]) != n or \
+            tuple(out_host.shape) != tuple(F_host.shape):
+        raise ValueError("points (N, 3), F and out (N[, d]) expected")
+    d = 1 if len(F_host.shape) == 1 else int(F_host.shape[1])
+    handle = ctypes.c_void_p()
+    _check(lib.rfd_gfi_host(_ptr(points), n, float(eps), float(lam), int(m), int(seed),
+                            _ptr(F_host), d, _ptr(out_host), _stream_handle(stream),
+                            ctypes.byref(handle) if keep_plan else None))
+    if not keep_plan:
+        return None
+    plan = Plan.__new__(Plan)
+    plan._h, plan._keep, plan._shard = handle, None, None
+    plan.batch, plan.n, plan.m, plan.r = 1, n, int(m), 2 * int(m)
+    plan.eps, plan.lam, plan.seed = float(eps), float(lam), int(seed)
+    return plan
 
 
 def launch_count():
