@@ -112,27 +112,42 @@ __device__ __forceinline__ float dec_f32(unsigned int e) {
   return __uint_as_float((e & 0x80000000u) ? (e & 0x7fffffffu) : ~e);
 }
 
-// bbox[b][0..2] = max ~enc (min), bbox[b][3..5] = max enc (max); grid
-// (chunks, batch).  Block-level reduction first: one atomic per block and
-// component (per-warp atomics on the same 6 words serialised at L2: 54 us at
-// cfg 5).
+// Two levels, no atomics: bbox_part_kernel writes each block's 6 encoded
+// extrema (grid (chunks, batch), 16-byte loads of the interleaved xyz), then
+// bbox_final_kernel folds a cloud's chunks: bbox[b][0..2] = max ~enc (the
+// minima), bbox[b][3..5] = max enc (the maxima).  (Per-warp atomics on the
+// same 6 words serialised at L2: 54 us at cfg 5.)
 __global__ void __launch_bounds__(256)
-bbox_kernel(const float* __restrict__ xyz, int64_t n, unsigned int* __restrict__ bbox) {
+bbox_part_kernel(const float* __restrict__ xyz, int64_t n, unsigned int* __restrict__ part) {
   __shared__ unsigned int red[8][6];
   const int b = blockIdx.y;
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t p0 = int64_t(blockIdx.x) * per, p1 = min(p0 + per, n);
+  // the cloud's 3n floats as float4s where aligned: a float4 at flat index q
+  // holds coordinates q*4 .. q*4+3, i.e. components (4q + j) % 3
   const float* src = xyz + int64_t(b) * n * 3;
+  const int64_t nf = 3 * n;
   unsigned int v[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+  auto take = [&](float x, int comp) {
+    const unsigned int e = enc_f32(x);
+    v[comp] = max(v[comp], ~e);
+    v[3 + comp] = max(v[3 + comp], e);
+  };
+  const bool al = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  const int64_t n4 = al ? nf / 4 : 0;
+  const int64_t per = (n4 + gridDim.x - 1) / gridDim.x;
+  const int64_t q0 = int64_t(blockIdx.x) * per, q1 = min(q0 + per, n4);
+  const float4* s4 = reinterpret_cast<const float4*>(src);
 #pragma unroll 4
-  for (int64_t i = p0 + threadIdx.x; i < p1; i += blockDim.x) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const unsigned int e = enc_f32(__ldg(src + 3 * i + c));
-      v[c] = max(v[c], ~e);
-      v[3 + c] = max(v[3 + c], e);
-    }
+  for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+    const float4 w = __ldg(s4 + q);
+    const int c = int((4 * q) % 3);
+    take(w.x, c);
+    take(w.y, c == 2 ? 0 : c + 1);
+    take(w.z, c == 0 ? 2 : c - 1);
+    take(w.w, c);
   }
+  // the unaligned remainder (tail floats, or everything when not 16-byte aligned)
+  if (blockIdx.x == 0)
+    for (int64_t i = 4 * n4 + threadIdx.x; i < nf; i += blockDim.x) take(__ldg(src + i), int(i % 3));
 #pragma unroll
   for (int c = 0; c < 6; ++c)
 #pragma unroll
@@ -144,8 +159,17 @@ bbox_kernel(const float* __restrict__ xyz, int64_t n, unsigned int* __restrict__
   if (threadIdx.x < 6) {
     unsigned int mx = 0u;
     for (int w = 0; w < 8; ++w) mx = max(mx, red[w][threadIdx.x]);
-    atomicMax(bbox + 6 * b + threadIdx.x, mx);
+    part[(int64_t(b) * gridDim.x + blockIdx.x) * 6 + threadIdx.x] = mx;
   }
+}
+
+__global__ void bbox_final_kernel(const unsigned int* __restrict__ part, int chunks,
+                                  unsigned int* __restrict__ bbox) {
+  const int b = blockIdx.x, c = threadIdx.x;
+  if (c >= 6) return;
+  unsigned int mx = 0u;
+  for (int k = 0; k < chunks; ++k) mx = max(mx, part[(int64_t(b) * chunks + k) * 6 + c]);
+  bbox[6 * b + c] = mx;
 }
 
 __device__ __forceinline__ float4 bbox_centre(const unsigned int* bb) {
@@ -254,15 +278,19 @@ void launch_nu(const float4* omega4, double* nu, int* flags, int m, double eps, 
   nu_kernel<<<1, 256, 0, s>>>(omega4, nu, flags, m, eps, c_r);
 }
 
-void launch_bbox(const float* xyz, unsigned int* bbox, int64_t n, int batch, int sms,
-                 cudaStream_t s) {
-  cudaMemsetAsync(bbox, 0, size_t(batch) * 6 * sizeof(unsigned int), s);
-  LaunchScope L("rfd_bbox", s);
-  int64_t chunks = (int64_t(sms) * 2 + batch - 1) / batch;
-  const int64_t maxc = (n + 4095) / 4096;
+int bbox_chunks(int64_t n, int batch, int sms) {
+  int64_t chunks = (int64_t(sms) * 8 + batch - 1) / batch;
+  const int64_t maxc = (n + 2047) / 2048;
   if (chunks > maxc) chunks = maxc;
-  if (chunks < 1) chunks = 1;
-  bbox_kernel<<<dim3(unsigned(chunks), unsigned(batch)), 256, 0, s>>>(xyz, n, bbox);
+  return chunks < 1 ? 1 : int(chunks);
+}
+
+void launch_bbox(const float* xyz, unsigned int* bbox, unsigned int* part, int64_t n, int batch,
+                 int sms, cudaStream_t s) {
+  LaunchScope L("rfd_bbox", s);
+  const int chunks = bbox_chunks(n, batch, sms);
+  bbox_part_kernel<<<dim3(unsigned(chunks), unsigned(batch)), 256, 0, s>>>(xyz, n, part);
+  bbox_final_kernel<<<batch, 32, 0, s>>>(part, chunks, bbox);
 }
 
 void launch_pack_points(const float* xyz, const unsigned int* bbox, float4* pts, float* pts16,

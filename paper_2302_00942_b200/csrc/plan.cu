@@ -401,7 +401,9 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   float* gpts = rfd::gram_points(gg, batch, gpart, &gper);
   unsigned int* bbox = nullptr;
   RFD_CUDA(tmp.alloc(&bbox, size_t(batch) * 6));
-  rfd::launch_bbox(dev_xyz, bbox, n, batch, p->sms, st);
+  unsigned int* bpart = nullptr;
+  RFD_CUDA(tmp.alloc(&bpart, size_t(rfd::bbox_chunks(n, batch, p->sms)) * batch * 6));
+  rfd::launch_bbox(dev_xyz, bbox, bpart, n, batch, p->sms, st);
   if (world > 1) {  // one centre for the whole cloud: merge the shards' boxes
     double *send = nullptr, *recv = nullptr;
     RFD_CUDA(tmp.alloc(&send, size_t(7)));

@@ -65,8 +65,10 @@ void launch_nu(const float4* omega4, double* nu, int* flags, int m, double eps, 
 // ---------------------------------------------------------------- pack
 // Per-cloud bounding box of the points (bbox: batch x 6 uint, ordered
 // encoding: [0..2] = max ~enc(x) (the minima), [3..5] = max enc(x)).
-void launch_bbox(const float* xyz, unsigned int* bbox, int64_t n, int batch, int sms,
-                 cudaStream_t s);
+// part: scratch of bbox_chunks(n, batch, sms) x batch x 6 uint.
+int bbox_chunks(int64_t n, int batch, int sms);
+void launch_bbox(const float* xyz, unsigned int* bbox, unsigned int* part, int64_t n, int batch,
+                 int sms, cudaStream_t s);
 // centre c = the bbox midpoint (centre: batch float4); pts / pts16 / gpts (the
 // Gram layout, gper points per cloud) = points - c.
 void launch_pack_points(const float* xyz, const unsigned int* bbox, float4* pts, float* pts16,
