@@ -139,7 +139,7 @@ bbox_part_kernel(const float* __restrict__ xyz, int64_t n, unsigned int* __restr
 #pragma unroll 4
   for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
     const float4 w = __ldg(s4 + q);
-    const int c = int((4 * q) % 3);
+    const int c = int(q % 3);  // (4 q) mod 3 = q mod 3
     take(w.x, c);
     take(w.y, c == 2 ? 0 : c + 1);
     take(w.z, c == 0 ? 2 : c - 1);
@@ -163,13 +163,27 @@ bbox_part_kernel(const float* __restrict__ xyz, int64_t n, unsigned int* __restr
   }
 }
 
-__global__ void bbox_final_kernel(const unsigned int* __restrict__ part, int chunks,
-                                  unsigned int* __restrict__ bbox) {
-  const int b = blockIdx.x, c = threadIdx.x;
-  if (c >= 6) return;
-  unsigned int mx = 0u;
-  for (int k = 0; k < chunks; ++k) mx = max(mx, part[(int64_t(b) * chunks + k) * 6 + c]);
-  bbox[6 * b + c] = mx;
+__global__ void __launch_bounds__(256)
+bbox_final_kernel(const unsigned int* __restrict__ part, int chunks, unsigned int* __restrict__ bbox) {
+  __shared__ unsigned int red[8][6];
+  const int b = blockIdx.x;
+  unsigned int v[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+  for (int k = threadIdx.x; k < chunks; k += blockDim.x)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) v[c] = max(v[c], part[(int64_t(b) * chunks + k) * 6 + c]);
+#pragma unroll
+  for (int c = 0; c < 6; ++c)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[c] = max(v[c], __shfl_xor_sync(0xffffffffu, v[c], o));
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) red[threadIdx.x >> 5][c] = v[c];
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    unsigned int mx = 0u;
+    for (int w = 0; w < 8; ++w) mx = max(mx, red[w][threadIdx.x]);
+    bbox[6 * b + threadIdx.x] = mx;
+  }
 }
 
 __device__ __forceinline__ float4 bbox_centre(const unsigned int* bb) {
@@ -290,7 +304,7 @@ void launch_bbox(const float* xyz, unsigned int* bbox, unsigned int* part, int64
   LaunchScope L("rfd_bbox", s);
   const int chunks = bbox_chunks(n, batch, sms);
   bbox_part_kernel<<<dim3(unsigned(chunks), unsigned(batch)), 256, 0, s>>>(xyz, n, part);
-  bbox_final_kernel<<<batch, 32, 0, s>>>(part, chunks, bbox);
+  bbox_final_kernel<<<batch, 256, 0, s>>>(part, chunks, bbox);
 }
 
 void launch_pack_points(const float* xyz, const unsigned int* bbox, float4* pts, float* pts16,

@@ -27,10 +27,15 @@
 namespace rfd {
 namespace {
 
-constexpr int kProducerWarps = 16;            // 4 per TMEM lane group
-constexpr int kMmaWarp = 16;
-constexpr int kEpiWarp0 = 17;                 // warps 17..20: epilogue
-constexpr int kThreads = 21 * 32;
+// Warp roles: PW producer warps (PW / 4 per TMEM lane group), one MMA warp,
+// four epilogue warps (one per lane group).
+template <int PW>
+struct Roles {
+  static constexpr int kProducerWarps = PW;
+  static constexpr int kMmaWarp = PW;
+  static constexpr int kEpiWarp0 = PW + 1;
+  static constexpr int kThreads = (PW + 5) * 32;
+};
 constexpr int kTile = 128;      // points per tile (= TMEM lanes)
 constexpr int kStages = 3;
 // TMEM columns: accumulators [0, nw) and [nw, 2 nw) (nw = the launch's column
@@ -50,8 +55,8 @@ __device__ long long g_p2load[4][8];
 // kFuse (part != nullptr) is a separate instantiation: the fused a7 prologue
 // is most of the kernel's code, and compiled into the plain kernel it cost
 // 6 % (0.73 -> 0.78 ms at cfg 5).
-template <int KF, bool kFuse, bool kTr = false>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int KF, bool kFuse, bool kTr = false, int PW = 16>
+__global__ void __launch_bounds__(Roles<PW>::kThreads, 1)
 pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega4, int m, int64_t n,
                 int batch, const float* __restrict__ Y, const float* F, float* out, int d, int c0,
                 int dc, int nw, const float* __restrict__ part, int ranges,
@@ -62,6 +67,9 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
   // writes S and Y to the plan (export).
   // F and out may alias (in place): each epilogue thread reads F_i before
   // writing out_i.
+  constexpr int kProducerWarps = Roles<PW>::kProducerWarps, kMmaWarp = Roles<PW>::kMmaWarp,
+                kEpiWarp0 = Roles<PW>::kEpiWarp0, kThreads = Roles<PW>::kThreads;
+  constexpr int QW = PW / 4;  // producer warps per lane group
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages], dfull_bar[2], dempty_bar[2];
   __shared__ uint64_t yready_bar;
@@ -293,7 +301,7 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
     const uint32_t buf = it & 1;
     if (warp < kProducerWarps) {
       // ---------------- producers: 16 frequencies per thread per chunk -----
-      const int q = warp >> 2;  // which 16 of the chunk's 64 frequencies
+      const int q = warp >> 2;  // which 1/QW of the chunk's frequencies
       // This tile's point (prefetched during the previous tile) and the next's.
       if (trc && warp == 0 && it < 32) trt[it][5] = clock64();
       if (tile == t_begin) copy_x(b, tin, 0);
@@ -307,11 +315,11 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
         if (trc && warp == 0 && gg < 128) trs[gg][0] = clock64();
         if (u >= 1) tc::mbar_wait(&empty_bar[s], (u - 1) & 1);
         if (trc && warp == 0 && gg < 128) trs[gg][1] = clock64();
-        const uint32_t acol = tmem + lane_field + kColA + 128 * s + (KF / 8) * q;
+        const uint32_t acol = tmem + lane_field + kColA + 128 * s + (KF / (2 * QW)) * q;
 #pragma unroll
-        for (int h = 0; h < KF / 64; ++h) {  // halves of 8 frequencies (register pressure)
+        for (int h = 0; h < KF / (16 * QW); ++h) {  // groups of 8 frequencies (register pressure)
           float v[16];
-          const int f0 = kFpc * c + (kFpc / 4) * q + 8 * h;
+          const int f0 = kFpc * c + (kFpc / QW) * q + 8 * h;
           // Frequencies beyond m (zero omega) meet zero rows of Y^T: no masking.
           // omega . x for 2 frequencies per packed FP32 instruction, in the
           // operation order of fmaf(wz, z, fmaf(wy, y, wx * x)).
@@ -446,19 +454,20 @@ pass2_tc_kernel(const float4* __restrict__ pts, const float4* __restrict__ omega
 
 }  // namespace
 
-template <int KF, bool kFuse, bool kTr = false>
+template <int KF, bool kFuse, bool kTr = false, int PW = 16>
 void launch_p2(int64_t grid, size_t smem, cudaStream_t s, const float4* pts, const float4* omega4,
                int m, int64_t n, int batch, const float* Y, const float* F, float* out, int d,
                int c0, int dc, int nw, const float* part, int ranges, const double* C, double* S,
                float* Yw) {
   static bool configured = false;
   if (!configured) {  // (the trace variant's static trace buffers take 6 KB)
-    cudaFuncSetAttribute(pass2_tc_kernel<KF, kFuse, kTr>,
+    cudaFuncSetAttribute(pass2_tc_kernel<KF, kFuse, kTr, PW>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kPass2MaxSmem) - (kTr ? 8192 : 0));
     configured = true;
   }
-  launch_pdl(pass2_tc_kernel<KF, kFuse, kTr>, dim3(unsigned(grid)), dim3(kThreads), smem, s, pts,
+  launch_pdl(pass2_tc_kernel<KF, kFuse, kTr, PW>, dim3(unsigned(grid)), dim3(Roles<PW>::kThreads),
+             smem, s, pts,
              omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part, ranges, C, S, Yw);
 }
 
@@ -534,6 +543,10 @@ void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, 
     return e && atoi(e) == 1;
   }();
   const bool fuse = part != nullptr;
+  static const int pw = [] {
+    const char* e = getenv("RFD_P2_PW");
+    return e ? atoi(e) : 16;
+  }();
   if (trace && m > 32 && !fuse) {
     launch_p2<128, false, true>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw,
                                 part, ranges, C, S, Yw);
@@ -542,6 +555,22 @@ void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, 
     launch_p2<64, true, true>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw,
                               part, ranges, C, S, Yw);
     print_p2trace(s, (m + 31) / 32);
+  } else if (pw == 8) {  // (A/B: RFD_P2_PW=8)
+    if (m <= 32) {
+      if (fuse)
+        launch_p2<64, true, false, 8>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0, dc,
+                                      nw, part, ranges, C, S, Yw);
+      else
+        launch_p2<64, false, false, 8>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0,
+                                       dc, nw, part, ranges, C, S, Yw);
+    } else {
+      if (fuse)
+        launch_p2<128, true, false, 8>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0,
+                                       dc, nw, part, ranges, C, S, Yw);
+      else
+        launch_p2<128, false, false, 8>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0,
+                                        dc, nw, part, ranges, C, S, Yw);
+    }
   } else if (m <= 32) {
     if (fuse)
       launch_p2<64, true>(grid, smem, s, pts, omega4, m, n, batch, Y, F, out, d, c0, dc, nw, part,
