@@ -126,10 +126,12 @@ bbox_part_kernel(const float* __restrict__ xyz, int64_t n, unsigned int* __restr
   const float* src = xyz + int64_t(b) * n * 3;
   const int64_t nf = 3 * n;
   unsigned int v[6] = {0u, 0u, 0u, 0u, 0u, 0u};
-  auto take = [&](float x, int comp) {
+  // (components are selected with compile-time indices only: a runtime index
+  // into v[] would put it in local memory)
+  auto take = [&](int k, float x) {
     const unsigned int e = enc_f32(x);
-    v[comp] = max(v[comp], ~e);
-    v[3 + comp] = max(v[3 + comp], e);
+    v[k] = max(v[k], ~e);
+    v[3 + k] = max(v[3 + k], e);
   };
   const bool al = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
   const int64_t n4 = al ? nf / 4 : 0;
@@ -139,15 +141,25 @@ bbox_part_kernel(const float* __restrict__ xyz, int64_t n, unsigned int* __restr
 #pragma unroll 4
   for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
     const float4 w = __ldg(s4 + q);
-    const int c = int(q % 3);  // (4 q) mod 3 = q mod 3
-    take(w.x, c);
-    take(w.y, c == 2 ? 0 : c + 1);
-    take(w.z, c == 0 ? 2 : c - 1);
-    take(w.w, c);
+    // flat float 4q + j is component (4q + j) mod 3 = (c + j) mod 3, c = q mod 3:
+    // component k holds element (k - c) mod 3, and element 3 too when k == c
+    const int c = int(q % 3);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int j0 = (k - c + 3) % 3;
+      take(k, j0 == 0 ? w.x : (j0 == 1 ? w.y : w.z));
+      if (k == c) take(k, w.w);
+    }
   }
   // the unaligned remainder (tail floats, or everything when not 16-byte aligned)
   if (blockIdx.x == 0)
-    for (int64_t i = 4 * n4 + threadIdx.x; i < nf; i += blockDim.x) take(__ldg(src + i), int(i % 3));
+    for (int64_t i = 4 * n4 + threadIdx.x; i < nf; i += blockDim.x) {
+      const int k = int(i % 3);
+      const float x = __ldg(src + i);
+      if (k == 0) take(0, x);
+      else if (k == 1) take(1, x);
+      else take(2, x);
+    }
 #pragma unroll
   for (int c = 0; c < 6; ++c)
 #pragma unroll

@@ -843,16 +843,13 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
     const uint32_t lane_field = uint32_t(32 * lg) << 16;
     const int rho = 32 * lg + lane;
     // blocks of this CTA: A = 2I + rank, B = 2J + rank (diag: the same block)
-    // (the lane's frequency of each block: loaded once per unit, not per step
-    // -- a 16-byte load per lane per step and block was the kernel's
-    // shared-memory conflict count in ncu)
+    int blkA = 0, blkB = 0;
     bool diag = true;
-    float4 wA = make_float4(0.f, 0.f, 0.f, 0.f), wB = wA;
     auto setup_unit = [&](int u) {
       int I, J;
       pair_tile(sc.T, u, I, J);
-      wA = om_s[(2 * I + int(rank)) * kFreqs + f];
-      wB = om_s[(2 * J + int(rank)) * kFreqs + f];
+      blkA = 2 * I + int(rank);
+      blkB = 2 * J + int(rank);
       diag = I == J;
     };
     int pend0 = -1, pend1 = -1, info0 = 0, info1 = 0, last0 = 0, last1 = 0;
@@ -917,7 +914,8 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         if (i == 1 && diag) break;
-        const float4 wi = (i == 0) ? wA : wB;
+        const int blk = (i == 0) ? blkA : blkB;
+        const float4 wi = om_s[blk * kFreqs + f];
         const float2 wx = make_float2(wi.x, wi.x), wy = make_float2(wi.y, wi.y),
                      wz = make_float2(wi.z, wi.z);
         float c[8], sn[8];
