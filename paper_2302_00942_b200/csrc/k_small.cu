@@ -1,0 +1,381 @@
+// Narrow fields (d <= 4): the whole inference of Eq. 13 (PAPER.md:351-358,
+// SURVEY Sec. 8(a) rows a3, a6-a8) in ONE persistent cooperative launch:
+//
+//   phase 1  S partials = Phi^T F per (cloud, point segment)      [a6]
+//   barrier
+//   phase 2  S = fixed-order sum of the segment partials (fp64)    [a7]
+//   barrier
+//   phase 3  Y = C^ S (fp64 -> fp32)                               [a7]
+//   barrier
+//   phase 4  out = F + Phi Y                                       [a8]
+//
+// With d <= 4 the contraction is 2d FMA per (point, frequency) -- a handful
+// of FP32 instructions next to the sin/cos pair -- so the tensor-core passes'
+// per-feature overheads (fp16 hi/lo splits, TMEM stores, MMA pipeline) cost
+// more than the contraction they move; here every (point, frequency) is
+// ~5.5 + d SIMT instructions and the pass is MUFU-bound.  One launch instead
+// of 2-4 also takes the launch and pipeline-fill latency of small clouds
+// (cfgs 1-3) off the critical path.
+//
+// Phase 1 is frequency-stationary: thread = (frequency k, point group g);
+// the segment's points and field rows are staged in shared memory (SoA) and
+// read as broadcasts, 4 consecutive points per 16-byte load, 2 per packed
+// FP32 instruction; the 2 x d accumulators (cos, sin per channel) stay in
+// registers, then the point groups are added in a fixed order.  Phase 4 is
+// point-stationary: 2 points per thread, omega and Y broadcast from shared
+// memory.  Features (a3) are regenerated in registers in both phases, as in
+// the tensor-core passes: fp32(2 pi omega) . x (centred), MUFU sin/cos.
+// Deterministic: fixed partition and reduction order, no floating-point
+// atomics.  Interleaved feature order (2k cos, 2k + 1 sin) as everywhere.
+#include <math.h>
+
+#include "rfd_internal.h"
+
+namespace rfd {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kBatchPts = 512;  // points staged per phase-1 batch
+constexpr int kTilePts = 512;   // points per phase-4 tile (2 per thread)
+
+// Generation barrier over the whole (co-resident) grid: a CTA reads the
+// generation before arriving; the last arrival resets the count and advances
+// the generation (self-resetting: the next launch starts from count 0).
+__device__ __forceinline__ void grid_sync(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = bar + 1;
+    const unsigned int my = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == my) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+struct SmallArgs {
+  const float4* pts;     // batch x n, centred (x, y, z, 0)
+  const float4* omega4;  // m: fp32(2 pi omega)
+  int m, fb, nfb;        // frequencies; frequency block (32..256, power of two); blocks
+  int64_t n;
+  int batch, d;
+  int segs;              // point segments per cloud (phase 1)
+  int64_t seg_len;       // points per segment (multiple of 4)
+  const float* F;        // (batch x) n x d
+  float* out;            // same shape (may alias F)
+  const double* C;       // batch x r x r
+  float* part;           // batch x segs x r x d
+  double* S;             // batch x r x d
+  float* Y;              // batch x r x d
+  unsigned int* bar;     // 2 words, zero before the first launch
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+integrate_small_kernel(const SmallArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = 2 * a.m;
+  const int d = a.d;
+
+  // ------------------------------------------------ phase 1: S partials
+  {
+    const int G = kThreads / a.fb;  // point groups
+    const int g = tid / a.fb;
+    float* xs = sm;                         // [kBatchPts] x, y, z, then F[D][kBatchPts]
+    float* ys = xs + kBatchPts;
+    float* zs = ys + kBatchPts;
+    float* fs = zs + kBatchPts;
+    float* red = fs + D * kBatchPts;        // [G][fb][2D]
+    const int64_t items = int64_t(a.batch) * a.segs * a.nfb;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      const int fbk = int(it % a.nfb);
+      const int64_t bs = it / a.nfb;
+      const int b = int(bs / a.segs), seg = int(bs % a.segs);
+      const int k = fbk * a.fb + (tid % a.fb);
+      const float4 w = (k < a.m) ? a.omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float2 wx = make_float2(w.x, w.x), wy = make_float2(w.y, w.y), wz = make_float2(w.z, w.z);
+      float2 acc[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc[j] = make_float2(0.f, 0.f);
+      const int64_t p0 = int64_t(seg) * a.seg_len, p1 = min(p0 + a.seg_len, a.n);
+      const float4* cloud = a.pts + int64_t(b) * a.n;
+      const float* Fb = a.F + int64_t(b) * a.n * d;
+      for (int64_t base = p0; base < p1; base += kBatchPts) {
+        const int np = int(p1 - base < kBatchPts ? p1 - base : kBatchPts);
+        const int np4 = (np + 3) & ~3;
+        __syncthreads();  // the previous batch has been read
+        for (int i = tid; i < np4; i += kThreads) {
+          const float4 x = (i < np) ? __ldg(cloud + base + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+          xs[i] = x.x;
+          ys[i] = x.y;
+          zs[i] = x.z;
+        }
+        for (int i = tid; i < np4 * D; i += kThreads) {
+          const int p = i / D, j = i - p * D;
+          fs[j * kBatchPts + p] = (p < np && j < d) ? __ldg(Fb + (base + p) * d + j) : 0.0f;
+        }
+        __syncthreads();
+        // group g takes 4-point quads g, g + G, ... of the batch
+        for (int q = 4 * g; q < np4; q += 4 * G) {
+          const float4 X = *reinterpret_cast<const float4*>(xs + q);
+          const float4 Yv = *reinterpret_cast<const float4*>(ys + q);
+          const float4 Z = *reinterpret_cast<const float4*>(zs + q);
+          float2 t0 = __fmul2_rn(make_float2(X.x, X.y), wx);
+          float2 t1 = __fmul2_rn(make_float2(X.z, X.w), wx);
+          t0 = __ffma2_rn(make_float2(Yv.x, Yv.y), wy, t0);
+          t1 = __ffma2_rn(make_float2(Yv.z, Yv.w), wy, t1);
+          t0 = __ffma2_rn(make_float2(Z.x, Z.y), wz, t0);
+          t1 = __ffma2_rn(make_float2(Z.z, Z.w), wz, t1);
+          float2 cs[4];
+          __sincosf(t0.x, &cs[0].y, &cs[0].x);
+          __sincosf(t0.y, &cs[1].y, &cs[1].x);
+          __sincosf(t1.x, &cs[2].y, &cs[2].x);
+          __sincosf(t1.y, &cs[3].y, &cs[3].x);
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const float4 f = *reinterpret_cast<const float4*>(fs + j * kBatchPts + q);
+            acc[j] = __ffma2_rn(cs[0], make_float2(f.x, f.x), acc[j]);
+            acc[j] = __ffma2_rn(cs[1], make_float2(f.y, f.y), acc[j]);
+            acc[j] = __ffma2_rn(cs[2], make_float2(f.z, f.z), acc[j]);
+            acc[j] = __ffma2_rn(cs[3], make_float2(f.w, f.w), acc[j]);
+          }
+        }
+      }
+      // the G point groups, added in group order
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        red[(g * a.fb + tid % a.fb) * 2 * D + 2 * j] = acc[j].x;
+        red[(g * a.fb + tid % a.fb) * 2 * D + 2 * j + 1] = acc[j].y;
+      }
+      __syncthreads();
+      for (int e = tid; e < a.fb * 2 * d; e += kThreads) {
+        const int kk = e / (2 * d), rem = e - kk * 2 * d, t = rem / d, j = rem - t * d;
+        const int kg = fbk * a.fb + kk;
+        if (kg >= a.m) continue;
+        float s = 0.0f;
+        for (int gg = 0; gg < G; ++gg) s += red[(gg * a.fb + kk) * 2 * D + 2 * j + t];
+        a.part[((int64_t(b) * a.segs + seg) * r + 2 * kg + t) * d + j] = s;
+      }
+    }
+  }
+  grid_sync(a.bar);
+
+  // ------------------------------------------------ phase 2: S (fp64, fixed order)
+  {
+    // element e of (batch x r x d): 8 lanes per element, lane l sums segments
+    // l, l + 8, ... in order; then the 8 slice sums in order
+    const int64_t E = int64_t(a.batch) * r * d;
+    const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
+    for (int64_t w0 = (int64_t(blockIdx.x) * (kThreads / 32) + warp) * 4; w0 < E; w0 += warps * 4) {
+      const int64_t e0 = w0 + (lane >> 3);  // 4 elements per warp (uniform trip count)
+      const bool ok = e0 < E;
+      const int sl = lane & 7;
+      double acc = 0.0;
+      if (ok) {
+        const int64_t b = e0 / (int64_t(r) * d), rem = e0 - b * r * d;
+        const float* src = a.part + b * a.segs * r * d + rem;
+        for (int sg = sl; sg < a.segs; sg += 8) acc += double(__ldg(src + int64_t(sg) * r * d));
+      }
+      // fixed-order combine of the 8 slices (lanes 8i .. 8i + 7)
+      const int base = lane & ~7;
+      double tot = 0.0;
+#pragma unroll
+      for (int l = 0; l < 8; ++l) tot += __shfl_sync(0xffffffffu, acc, base + l);
+      if (ok && sl == 0) a.S[e0] = tot;
+    }
+  }
+  grid_sync(a.bar);
+
+  // ------------------------------------------------ phase 3: Y = C^ S
+  {
+    // one warp per (cloud, row a): lanes split the r columns, fixed-order butterfly
+    const int64_t rows = int64_t(a.batch) * r;
+    for (int64_t row = int64_t(blockIdx.x) * (kThreads / 32) + warp; row < rows;
+         row += int64_t(gridDim.x) * (kThreads / 32)) {
+      const int64_t b = row / r;
+      const double* Crow = a.C + row * r;
+      const double* Sb = a.S + b * r * d;
+      double acc[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc[j] = 0.0;
+      for (int c = lane; c < r; c += 32) {
+        const double cv = __ldg(Crow + c);
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+          if (j < d) acc[j] = fma(cv, __ldg(Sb + int64_t(c) * d + j), acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+        if (lane == 0 && j < d) a.Y[row * d + j] = float(acc[j]);
+      }
+    }
+  }
+  grid_sync(a.bar);
+
+  // ------------------------------------------------ phase 4: out = F + Phi Y
+  {
+    const int mp = (a.m + 3) & ~3;
+    float* ox = sm;             // [mp] omega x, y, z (zero-padded)
+    float* oy = ox + mp;
+    float* oz = oy + mp;
+    float* yc = oz + mp;        // [mp][2D]: Yc[k][0..D), Ys[k][0..D) (zero-padded)
+    for (int k = tid; k < mp; k += kThreads) {
+      const float4 w = (k < a.m) ? a.omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+      ox[k] = w.x;
+      oy[k] = w.y;
+      oz[k] = w.z;
+    }
+    const int64_t tpc = (a.n + kTilePts - 1) / kTilePts;
+    const int64_t tiles = tpc * a.batch;
+    int cur_b = -1;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int b = int(t / tpc);
+      const int64_t base = (t - int64_t(b) * tpc) * kTilePts;
+      if (b != cur_b) {
+        __syncthreads();
+        const float* Yb = a.Y + int64_t(b) * r * d;
+        for (int e = tid; e < mp * 2 * D; e += kThreads) {
+          const int k = e / (2 * D), rem = e - k * 2 * D, tt = rem / D, j = rem - tt * D;
+          yc[e] = (k < a.m && j < d) ? Yb[(2 * k + tt) * d + j] : 0.0f;
+        }
+        cur_b = b;
+        __syncthreads();
+      }
+      const int64_t i0 = base + tid, i1 = base + tid + kThreads;
+      const float4* cloud = a.pts + int64_t(b) * a.n;
+      const float4 p0 = (i0 < a.n) ? __ldg(cloud + i0) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 p1 = (i1 < a.n) ? __ldg(cloud + i1) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float2 X = make_float2(p0.x, p1.x), Yp = make_float2(p0.y, p1.y),
+                   Z = make_float2(p0.z, p1.z);
+      float2 acc[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc[j] = make_float2(0.f, 0.f);
+#pragma unroll 2
+      for (int k = 0; k < mp; k += 4) {
+        const float4 WX = *reinterpret_cast<const float4*>(ox + k);
+        const float4 WY = *reinterpret_cast<const float4*>(oy + k);
+        const float4 WZ = *reinterpret_cast<const float4*>(oz + k);
+        const float wxs[4] = {WX.x, WX.y, WX.z, WX.w}, wys[4] = {WY.x, WY.y, WY.z, WY.w},
+                    wzs[4] = {WZ.x, WZ.y, WZ.z, WZ.w};
+        // Y of the 4 frequencies: 8D floats = 2D 16-byte loads
+        float yv[8 * D];
+#pragma unroll
+        for (int v4 = 0; v4 < 2 * D; ++v4)
+          *reinterpret_cast<float4*>(yv + 4 * v4) =
+              *reinterpret_cast<const float4*>(yc + k * 2 * D + 4 * v4);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float2 th = __fmul2_rn(X, make_float2(wxs[u], wxs[u]));
+          th = __ffma2_rn(Yp, make_float2(wys[u], wys[u]), th);
+          th = __ffma2_rn(Z, make_float2(wzs[u], wzs[u]), th);
+          float2 c, s;
+          __sincosf(th.x, &s.x, &c.x);
+          __sincosf(th.y, &s.y, &c.y);
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            acc[j] = __ffma2_rn(c, make_float2(yv[u * 2 * D + j], yv[u * 2 * D + j]), acc[j]);
+            acc[j] = __ffma2_rn(s, make_float2(yv[u * 2 * D + D + j], yv[u * 2 * D + D + j]), acc[j]);
+          }
+        }
+      }
+      const float* Fb = a.F + int64_t(b) * a.n * d;
+      float* Ob = a.out + int64_t(b) * a.n * d;
+      // (F and out may alias: each row is read before it is written, by this thread)
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        if (j < d) {
+          if (i0 < a.n) Ob[i0 * d + j] = Fb[i0 * d + j] + acc[j].x;
+          if (i1 < a.n) Ob[i1 * d + j] = Fb[i1 * d + j] + acc[j].y;
+        }
+      }
+    }
+  }
+}
+
+template <int D>
+cudaError_t launch_d(const SmallArgs& a, size_t smem, int sms, cudaStream_t s) {
+  static int occ = -1;
+  static size_t occ_smem = 0;
+  if (occ < 0 || occ_smem != smem) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(integrate_small_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, integrate_small_kernel<D>, kThreads, smem);
+    if (occ < 1) occ = 1;
+    if (occ > 4) occ = 4;
+    occ_smem = smem;
+  }
+  // cooperative (all CTAs co-resident: the grid barriers), via cudaLaunchKernelEx
+  // so that the launch can be captured in a CUDA graph
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms * occ);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, integrate_small_kernel<D>, a);
+}
+
+}  // namespace
+
+int small_segments(int m, int64_t n, int batch, int sms) {
+  // about 2 items per CTA slot (4 CTAs per SM), whole 4-point quads
+  const int fb = m <= 32 ? 32 : (m <= 64 ? 64 : (m <= 128 ? 128 : 256));
+  const int nfb = (m + fb - 1) / fb;
+  int64_t segs = (int64_t(sms) * 8 + int64_t(batch) * nfb - 1) / (int64_t(batch) * nfb);
+  const int64_t maxs = (n + 255) / 256;
+  if (segs > maxs) segs = maxs;
+  return segs < 1 ? 1 : int(segs);
+}
+
+cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int m, int64_t n,
+                                   int batch, int sms, const float* F, int d, float* out,
+                                   const double* C, float* part, double* S, float* Y,
+                                   unsigned int* bar, cudaStream_t s) {
+  LaunchScope L("rfd_integrate_small", s);
+  SmallArgs a{};
+  a.pts = pts;
+  a.omega4 = omega4;
+  a.m = m;
+  a.fb = m <= 32 ? 32 : (m <= 64 ? 64 : (m <= 128 ? 128 : 256));
+  a.nfb = (m + a.fb - 1) / a.fb;
+  a.n = n;
+  a.batch = batch;
+  a.d = d;
+  a.segs = small_segments(m, n, batch, sms);
+  a.seg_len = ((n + a.segs - 1) / a.segs + 3) & ~int64_t(3);
+  a.segs = int((n + a.seg_len - 1) / a.seg_len);
+  a.F = F;
+  a.out = out;
+  a.C = C;
+  a.part = part;
+  a.S = S;
+  a.Y = Y;
+  a.bar = bar;
+  const int D = d <= 1 ? 1 : (d <= 2 ? 2 : (d <= 3 ? 3 : 4));
+  const int mp = (m + 3) & ~3;
+  const size_t s1 = (size_t(3 + D) * kBatchPts + size_t(kThreads) * 2 * D) * sizeof(float);
+  const size_t s4 = (size_t(3) * mp + size_t(mp) * 2 * D) * sizeof(float);
+  const size_t smem = s1 > s4 ? s1 : s4;
+  switch (D) {
+    case 1: return launch_d<1>(a, smem, sms, s);
+    case 2: return launch_d<2>(a, smem, sms, s);
+    case 3: return launch_d<3>(a, smem, sms, s);
+    default: return launch_d<4>(a, smem, sms, s);
+  }
+}
+
+}  // namespace rfd

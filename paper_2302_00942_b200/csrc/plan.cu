@@ -126,6 +126,8 @@ struct rfd_plan {
   float* s_partial = nullptr; // batch*chunks*r*16
   double* S = nullptr;        // batch*r*d
   double* S_parts = nullptr;  // world*r*d (sharded plans: the gathered partials)
+  float* small_part = nullptr;  // d <= 4 path: batch*segments*r*4 segment partials
+  unsigned int* bar = nullptr;  // d <= 4 path: grid barrier (2 words, self-resetting)
   float* Y = nullptr;         // batch*r*d
   int last_d = 0;
   // host-buffer staging (rfd_integrate_host / rfd_gfi_host)
@@ -252,6 +254,8 @@ void free_plan(rfd_plan* p) {
   dfree(p->s_partial, s);
   dfree(p->S, s);
   dfree(p->S_parts, s);
+  dfree(p->small_part, s);
+  dfree(p->bar, s);
   dfree(p->Y, s);
   dfree(p->stage, s);
   dfree(p->pipe_partial, s);
@@ -383,6 +387,8 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   RFD_CUDA(dalloc(&p->C, rr * batch, st));
   RFD_CUDA(dalloc(&p->flags, size_t(8), st));
   RFD_CUDA(cudaMemsetAsync(p->flags, 0, 8 * sizeof(int), st));
+  RFD_CUDA(dalloc(&p->bar, size_t(2), st));
+  RFD_CUDA(cudaMemsetAsync(p->bar, 0, 2 * sizeof(unsigned int), st));
 
   TempBuffers tmp(st);
   const float* dev_xyz = points;
@@ -543,6 +549,17 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
   p->stream = st;
   rfd_status rs = ensure_workspace(p, d, st);
   if (rs != RFD_OK) return rs;
+  if (d <= 4 && p->world == 1) {
+    // narrow fields: the whole inference in one cooperative SIMT launch (k_small.cu)
+    if (!p->small_part) {
+      const size_t segs = size_t(rfd::small_segments(p->m, p->n, p->batch, p->sms));
+      RFD_CUDA(dalloc(&p->small_part, size_t(p->batch) * segs * p->r * 4, st));
+    }
+    RFD_CUDA(rfd::launch_integrate_small(p->pts, p->omega_rad4, p->m, p->n, p->batch, p->sms, F, d,
+                                         out, p->C, p->small_part, p->S, p->Y, p->bar, st));
+    p->last_d = d;
+    return RFD_OK;
+  }
   const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
   // Small r (<= 128) with d in one chunk and few partials: a7 (S reduction and
   // Y = C^ S) runs fused in pass 2's prologue -- two launches fewer per call
@@ -820,7 +837,7 @@ rfd_status rfd_integrate_host(rfd_plan* plan, const float* F_host, int32_t d, fl
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t elems = size_t(plan->batch) * plan->n * d;
   RFD_CUDA(ensure_stage(plan, elems, st) == RFD_OK ? cudaSuccess : cudaErrorMemoryAllocation);
-  if (plan->batch == 1 && d <= 64 && plan->n >= 2048 * kPipeChunks) {
+  if (plan->batch == 1 && d > 4 && d <= 64 && plan->n >= 2048 * kPipeChunks) {
     const rfd_status ps = pipe_streams(plan);
     if (ps != RFD_OK) return ps;
     return integrate_host_pipelined(plan, F_host, d, out_host, false, st);
@@ -840,7 +857,7 @@ rfd_status rfd_gfi_host(const float* points, int64_t n, double eps, double lambd
   if (d < 1) return fail(RFD_EINVAL, "d must be >= 1");
   if (n < 1) return fail(RFD_EINVAL, "n must be >= 1");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (d > 64 || n < 2048 * kPipeChunks || is_device_pointer(points)) {  // nothing to overlap
+  if (d <= 4 || d > 64 || n < 2048 * kPipeChunks || is_device_pointer(points)) {  // nothing to overlap
     rfd_plan* p = nullptr;
     rfd_status rs = create_impl(points, 1, n, eps, lambda, m, seed, nullptr, st, &p);
     if (rs != RFD_OK) return rs;

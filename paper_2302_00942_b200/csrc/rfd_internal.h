@@ -171,6 +171,16 @@ void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, 
                      const float* part, int ranges, const double* C, double* S, float* Yw,
                      cudaStream_t s);
 
+// Narrow fields, d <= 4 (k_small.cu): the whole inference (S partials,
+// fixed-order S, Y = C^ S, out = F + Phi Y) in one cooperative launch.
+// part: batch x small_segments(...) x r x d fp32; S, Y: batch x r x d (plan
+// export); bar: 2 words zeroed once (self-resetting grid barrier).
+int small_segments(int m, int64_t n, int batch, int sms);
+cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int m, int64_t n,
+                                   int batch, int sms, const float* F, int d, float* out,
+                                   const double* C, float* part, double* S, float* Y,
+                                   unsigned int* bar, cudaStream_t s);
+
 // Tensor-core pass 1 (k_pass1_tc.cu): partial[b][range][2m][dc].
 int pass1_tc_ranges(int m, int64_t n, int batch, int sms);
 void launch_pass1_tc(const float* pts16, const float4* omega4, int m, int64_t n, int batch,

@@ -206,7 +206,8 @@ def test_tiny_field_columns_pass2_scale_clamp():
     # still meet the gates on out and on Delta.
     n, m = 3000, 64
     x = _sphere(n, 5)
-    F = np.random.default_rng(7).standard_normal((n, 3)).astype(np.float32)
+    # (d = 5: the tensor-core passes; d <= 4 runs the one-launch SIMT path)
+    F = np.random.default_rng(7).standard_normal((n, 5)).astype(np.float32)
     F[:, 1] *= np.float32(1e-33)
     F[:, 2] *= np.float32(1e-36)
     p = dict(name="tiny columns", eps=0.05, lam=-0.8, m=m, seed=21)
@@ -214,7 +215,7 @@ def test_tiny_field_columns_pass2_scale_clamp():
     assert np.abs(res["Y"][:, 1]).max() < 2.0 ** -113  # the clamped branch is exercised
     plan, out = _run_single(x, F, p)
     assert np.isfinite(out).all()
-    for c in range(3):
+    for c in range(5):
         e_out = relerr(out[:, c], res["out"][:, c])
         e_del = relerr(out[:, c] - F[:, c].astype(np.float64), res["out"][:, c] - F[:, c])
         print("tiny column", c, "%.2e %.2e" % (e_out, e_del))
@@ -591,9 +592,7 @@ def test_host_buffers_match_device():
     plan.integrate_host(Fh, oh)
     torch.cuda.synchronize()
     od = plan.integrate(Fh.cuda()).cpu()
-    # (the host path is pipelined in point-range chunks: S is summed in another
-    # grouping, so equal up to fp32 rounding)
-    assert relerr(oh.numpy(), od.numpy()) <= 1e-6
+    assert torch.equal(oh, od)  # d <= 4: the same one-launch path
 
 
 def test_overflow_reports_erange():
@@ -632,47 +631,38 @@ def test_launch_counter_and_profiler():
     prof = rfd.profile_read()
     rfd.profile_enable(False)
     assert rfd.launch_count() > c0
-    # cfg 1 (r = 32): a7 runs fused in pass 2 (no separate reduce / apply)
-    assert not ({"rfd_reduce_S", "rfd_core_apply"} & set(prof))
-    assert {"rfd_pass1", "rfd_pass1_tc"} & set(prof)
-    assert {"rfd_pass2", "rfd_pass2_tc"} & set(prof)
+    # d = 3 <= 4: one cooperative launch does the whole inference
+    assert set(prof) == {"rfd_integrate_small"}
     assert all(v[1] > 0 for v in prof.values())
-    # r = 256 (cfg 4's m): the separate a7 kernels
+    # r = 32, d = 8: tensor-core passes with a7 fused in pass 2
+    rfd.profile_enable(True)
+    plan.integrate(torch.from_numpy(np.ones((x.shape[0], 8), np.float32)).cuda())
+    prof8 = rfd.profile_read()
+    rfd.profile_enable(False)
+    assert set(prof8) == {"rfd_pass1_tc", "rfd_pass2_tc"}
+    # r = 256, d = 8: the separate a7 kernels
     x4 = _sphere(4000, 3)
     plan4 = rfd.Plan(torch.from_numpy(x4).cuda(), 0.05, -0.8, 128, 3)
     rfd.profile_enable(True)
-    plan4.integrate(torch.from_numpy(np.ones((4000, 3), np.float32)).cuda())
+    plan4.integrate(torch.from_numpy(np.ones((4000, 8), np.float32)).cuda())
     prof4 = rfd.profile_read()
     rfd.profile_enable(False)
     assert {"rfd_reduce_S", "rfd_core_apply", "rfd_pass1_tc", "rfd_pass2_tc"} <= set(prof4)
 
 
-@pytest.mark.parametrize("cfg", [4, 5])
-def test_host_pipeline_and_gfi_host(cfg):
-    # rfd_integrate_host (pipelined: chunked H2D / pass 1 / pass 2 / D2H) and
-    # rfd_gfi_host (plan + integrate with the field uploaded during the plan):
-    # same arithmetic as each other (bitwise), against the device path and the
-    # oracle (cfg 5 on its first 2^18 points).
-    p, x, F = make_config(cfg) if cfg == 4 else make_config(5, n=1 << 18)
-    xh = torch.from_numpy(x).pin_memory()
-    Fh = torch.from_numpy(F).pin_memory()
-    o1 = torch.empty_like(Fh).pin_memory()
-    o2 = torch.empty_like(Fh).pin_memory()
-    plan = rfd.Plan(xh, p["eps"], p["lam"], p["m"], p["seed"])
-    plan.integrate_host(Fh, o1)
-    kept = rfd.gfi_host(xh, p["eps"], p["lam"], p["m"], p["seed"], Fh, o2, keep_plan=True)
-    torch.cuda.synchronize()
-    assert torch.equal(o1, o2)
-    dev = plan.integrate(Fh.cuda()).cpu()
-    assert relerr(o1.numpy(), dev.numpy()) <= 1e-6
-    np.testing.assert_array_equal(kept.export("gram"), plan.export("gram"))
-    o3 = torch.empty_like(Fh).pin_memory()
-    kept.integrate_host(Fh, o3)  # the kept plan is reusable
-    torch.cuda.synchronize()
-    assert torch.equal(o3, o1)
-    ref = orf.Plan(x, p["eps"], p["lam"], p["m"], p["seed"]).apply(F.astype(np.float64))["out"]
-    assert relerr(o1.numpy(), ref) <= TOL
-    assert relerr(o1.numpy() - F, ref - F) <= TOL
-    rfd.gfi_host(xh, p["eps"], p["lam"], p["m"], p["seed"], Fh, o2)  # plan destroyed inside
-    torch.cuda.synchronize()
-    assert torch.equal(o1, o2)
+@pytest.mark.parametrize("d", [1, 2, 3, 4])
+def test_narrow_field_paths_agree(d):
+    # the d <= 4 one-launch SIMT path and the tensor-core passes (the same
+    # columns inside a d = 8 field) against each other and the oracle
+    p, x, F = make_config(4)
+    rng = np.random.default_rng(d)
+    F8 = rng.standard_normal((x.shape[0], 8)).astype(np.float32)
+    plan = rfd.Plan(torch.from_numpy(x).cuda(), p["eps"], p["lam"], p["m"], p["seed"])
+    o8 = plan.integrate(torch.from_numpy(F8).cuda()).cpu().numpy()
+    od = plan.integrate(torch.from_numpy(np.ascontiguousarray(F8[:, :d])).cuda()).cpu().numpy()
+    ref = orf.Plan(x, p["eps"], p["lam"], p["m"], p["seed"]).apply(F8[:, :d].astype(np.float64))["out"]
+    F64 = F8[:, :d].astype(np.float64)
+    for got in (od, o8[:, :d]):
+        assert relerr(got, ref) <= TOL
+        assert relerr(got - F64, ref - F64) <= TOL
+    assert relerr(od - F64, o8[:, :d] - F64) <= 2e-5
