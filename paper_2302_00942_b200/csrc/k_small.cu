@@ -28,6 +28,8 @@
 // Deterministic: fixed partition and reduction order, no floating-point
 // atomics.  Interleaved feature order (2k cos, 2k + 1 sin) as everywhere.
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "rfd_internal.h"
 
@@ -74,7 +76,17 @@ struct SmallArgs {
   double* S;             // batch x r x d
   float* Y;              // batch x r x d
   unsigned int* bar;     // 2 words, zero before the first launch
+  unsigned long long* trace;  // diagnostics (RFD_SMALL_TRACE=1): phase timestamps of CTA 0
 };
+
+__device__ __forceinline__ void stamp(unsigned long long* tr, int i) {
+  if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[i] = t;
+  }
+}
+__device__ unsigned long long g_small_trace[8];
 
 template <int D>
 __global__ void __launch_bounds__(kThreads)
@@ -83,6 +95,7 @@ integrate_small_kernel(const SmallArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = 2 * a.m;
   const int d = a.d;
+  stamp(a.trace, 0);
 
   // ------------------------------------------------ phase 1: S partials
   {
@@ -165,7 +178,9 @@ integrate_small_kernel(const SmallArgs a) {
       }
     }
   }
+  stamp(a.trace, 1);
   grid_sync(a.bar);
+  stamp(a.trace, 2);
 
   // ------------------------------------------------ phase 2: S (fp64, fixed order)
   {
@@ -181,7 +196,16 @@ integrate_small_kernel(const SmallArgs a) {
       if (ok) {
         const int64_t b = e0 / (int64_t(r) * d), rem = e0 - b * r * d;
         const float* src = a.part + b * a.segs * r * d + rem;
-        for (int sg = sl; sg < a.segs; sg += 8) acc += double(__ldg(src + int64_t(sg) * r * d));
+        const int64_t st = int64_t(r) * d;
+        int sg = sl;
+        for (; sg + 56 < a.segs; sg += 64) {  // 8 loads in flight, added in order
+          float v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (sg + 8 * u) * st);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc += double(v[u]);
+        }
+        for (; sg < a.segs; sg += 8) acc += double(__ldg(src + sg * st));
       }
       // fixed-order combine of the 8 slices (lanes 8i .. 8i + 7)
       const int base = lane & ~7;
@@ -192,6 +216,7 @@ integrate_small_kernel(const SmallArgs a) {
     }
   }
   grid_sync(a.bar);
+  stamp(a.trace, 3);
 
   // ------------------------------------------------ phase 3: Y = C^ S
   {
@@ -220,6 +245,7 @@ integrate_small_kernel(const SmallArgs a) {
     }
   }
   grid_sync(a.bar);
+  stamp(a.trace, 4);
 
   // ------------------------------------------------ phase 4: out = F + Phi Y
   {
@@ -299,10 +325,11 @@ integrate_small_kernel(const SmallArgs a) {
       }
     }
   }
+  stamp(a.trace, 5);
 }
 
 template <int D>
-cudaError_t launch_d(const SmallArgs& a, size_t smem, int sms, cudaStream_t s) {
+int max_ctas(size_t smem, int sms) {
   static int occ = -1;
   static size_t occ_smem = 0;
   if (occ < 0 || occ_smem != smem) {
@@ -314,10 +341,15 @@ cudaError_t launch_d(const SmallArgs& a, size_t smem, int sms, cudaStream_t s) {
     if (occ > 4) occ = 4;
     occ_smem = smem;
   }
+  return sms * occ;
+}
+
+template <int D>
+cudaError_t launch_d(const SmallArgs& a, int grid, size_t smem, cudaStream_t s) {
   // cooperative (all CTAs co-resident: the grid barriers), via cudaLaunchKernelEx
   // so that the launch can be captured in a CUDA graph
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(sms * occ);
+  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -329,13 +361,27 @@ cudaError_t launch_d(const SmallArgs& a, size_t smem, int sms, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, integrate_small_kernel<D>, a);
 }
 
+int frequency_block(int m) { return m <= 32 ? 32 : (m <= 64 ? 64 : (m <= 128 ? 128 : 256)); }
+
+// Grid (CTAs) sized to the work, at most what is co-resident: small clouds
+// get few CTAs (cheaper grid barriers), large ones the whole GPU.
+int small_grid(int m, int64_t n, int batch, int cap) {
+  const int nfb = (m + frequency_block(m) - 1) / frequency_block(m);
+  const int64_t items = int64_t(batch) * nfb * ((n + 1023) / 1024);  // >= 1024-point segments
+  const int64_t tiles = int64_t(batch) * ((n + kTilePts - 1) / kTilePts);
+  int64_t g = items > tiles ? items : tiles;
+  if (g > cap) g = cap;
+  return g < 1 ? 1 : int(g);
+}
+
 }  // namespace
 
 int small_segments(int m, int64_t n, int batch, int sms) {
-  // about 2 items per CTA slot (4 CTAs per SM), whole 4-point quads
-  const int fb = m <= 32 ? 32 : (m <= 64 ? 64 : (m <= 128 ? 128 : 256));
-  const int nfb = (m + fb - 1) / fb;
-  int64_t segs = (int64_t(sms) * 8 + int64_t(batch) * nfb - 1) / (int64_t(batch) * nfb);
+  // one phase-1 item (cloud, segment, frequency block) per CTA of the largest
+  // grid (4 CTAs per SM), whole 4-point quads
+  const int nfb = (m + frequency_block(m) - 1) / frequency_block(m);
+  const int grid = small_grid(m, n, batch, 4 * sms);
+  int64_t segs = grid / (int64_t(batch) * nfb);
   const int64_t maxs = (n + 255) / 256;
   if (segs > maxs) segs = maxs;
   return segs < 1 ? 1 : int(segs);
@@ -350,14 +396,11 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
   a.pts = pts;
   a.omega4 = omega4;
   a.m = m;
-  a.fb = m <= 32 ? 32 : (m <= 64 ? 64 : (m <= 128 ? 128 : 256));
+  a.fb = frequency_block(m);
   a.nfb = (m + a.fb - 1) / a.fb;
   a.n = n;
   a.batch = batch;
   a.d = d;
-  a.segs = small_segments(m, n, batch, sms);
-  a.seg_len = ((n + a.segs - 1) / a.segs + 3) & ~int64_t(3);
-  a.segs = int((n + a.seg_len - 1) / a.seg_len);
   a.F = F;
   a.out = out;
   a.C = C;
@@ -365,17 +408,46 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
   a.S = S;
   a.Y = Y;
   a.bar = bar;
+  static const bool trace = [] {
+    const char* e = getenv("RFD_SMALL_TRACE");
+    return e && e[0] == '1';
+  }();
+  if (trace) cudaGetSymbolAddress(reinterpret_cast<void**>(&a.trace), g_small_trace);
   const int D = d <= 1 ? 1 : (d <= 2 ? 2 : (d <= 3 ? 3 : 4));
   const int mp = (m + 3) & ~3;
   const size_t s1 = (size_t(3 + D) * kBatchPts + size_t(kThreads) * 2 * D) * sizeof(float);
   const size_t s4 = (size_t(3) * mp + size_t(mp) * 2 * D) * sizeof(float);
   const size_t smem = s1 > s4 ? s1 : s4;
+  int cap = 0;
   switch (D) {
-    case 1: return launch_d<1>(a, smem, sms, s);
-    case 2: return launch_d<2>(a, smem, sms, s);
-    case 3: return launch_d<3>(a, smem, sms, s);
-    default: return launch_d<4>(a, smem, sms, s);
+    case 1: cap = max_ctas<1>(smem, sms); break;
+    case 2: cap = max_ctas<2>(smem, sms); break;
+    case 3: cap = max_ctas<3>(smem, sms); break;
+    default: cap = max_ctas<4>(smem, sms); break;
   }
+  const int grid = small_grid(m, n, batch, cap);
+  a.segs = int(grid / (int64_t(batch) * a.nfb));
+  if (a.segs > small_segments(m, n, batch, sms)) a.segs = small_segments(m, n, batch, sms);
+  if (a.segs < 1) a.segs = 1;
+  a.seg_len = ((n + a.segs - 1) / a.segs + 3) & ~int64_t(3);
+  a.segs = int((n + a.seg_len - 1) / a.seg_len);
+  cudaError_t e = cudaSuccess;
+  switch (D) {
+    case 1: e = launch_d<1>(a, grid, smem, s); break;
+    case 2: e = launch_d<2>(a, grid, smem, s); break;
+    case 3: e = launch_d<3>(a, grid, smem, s); break;
+    default: e = launch_d<4>(a, grid, smem, s); break;
+  }
+  if (trace && e == cudaSuccess) {
+    unsigned long long h[8];
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(h, g_small_trace, sizeof(h));
+    fprintf(stderr, "small n=%lld batch=%d m=%d d=%d grid=%d segs=%d: phase1 %.1f us, sync %.1f, "
+            "S %.1f, Y %.1f, phase4 %.1f (total %.1f)\n", (long long)n, batch, m, d, grid, a.segs,
+            (h[1] - h[0]) * 1e-3, (h[2] - h[1]) * 1e-3, (h[3] - h[2]) * 1e-3, (h[4] - h[3]) * 1e-3,
+            (h[5] - h[4]) * 1e-3, (h[5] - h[0]) * 1e-3);
+  }
+  return e;
 }
 
 }  // namespace rfd
