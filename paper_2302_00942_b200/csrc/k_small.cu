@@ -40,23 +40,46 @@ constexpr int kThreads = 256;
 constexpr int kBatchPts = 512;  // points staged per phase-1 batch
 constexpr int kTilePts = 512;   // points per phase-4 tile (2 per thread)
 
-// Generation barrier over the whole (co-resident) grid: a CTA reads the
-// generation before arriving; the last arrival resets the count and advances
-// the generation (self-resetting: the next launch starts from count 0).
+// Generation barrier over the whole (co-resident) grid, two levels: CTAs
+// arrive on one of 32 group counters (same-address atomics serialise at L2:
+// ~8 us for 592 CTAs on one counter), the last CTA of each group on the top
+// counter, whose last arrival resets the counters and advances the
+// generation; the others poll the generation with acquire loads.  Release /
+// acquire at gpu scope order each CTA's writes before the barrier with the
+// reads after it (thread 0 acts for the CTA after __syncthreads).
+// Self-resetting: every launch starts from zero counts.  bar: [0] generation,
+// [1] top counter, [2 .. 34) group counters.
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned int atom_add_acqrel(unsigned int* p, unsigned int v) {
+  unsigned int old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+constexpr int kBarGroups = 32;
+constexpr int kBarWords = 2 + kBarGroups;
+static_assert(kBarWords == kSmallBarWords, "barrier words");
+
 __device__ __forceinline__ void grid_sync(unsigned int* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned int* gen = bar + 1;
-    const unsigned int my = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
+    const unsigned int my = ld_acquire(bar);
+    const unsigned int grp = blockIdx.x % kBarGroups;
+    const unsigned int in_grp = (gridDim.x - grp + kBarGroups - 1) / kBarGroups;
+    const unsigned int ngrp = gridDim.x < kBarGroups ? gridDim.x : kBarGroups;
+    bool last = atom_add_acqrel(bar + 2 + grp, 1u) == in_grp - 1;
+    if (last) last = atom_add_acqrel(bar + 1, 1u) == ngrp - 1;
+    if (last) {
+      for (unsigned int g = 0; g < ngrp; ++g) bar[2 + g] = 0u;
+      bar[1] = 0u;
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     } else {
-      while (*gen == my) __nanosleep(32);
+      while (ld_acquire(bar) == my) {
+      }
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -75,7 +98,8 @@ struct SmallArgs {
   float* part;           // batch x segs x r x d
   double* S;             // batch x r x d
   float* Y;              // batch x r x d
-  unsigned int* bar;     // 2 words, zero before the first launch
+  unsigned int* bar;     // kBarWords words, zero before the first launch
+  int fuse_a7;           // 1: S and Y per cloud in phase 4's prologue (small r, few segments)
   unsigned long long* trace;  // diagnostics (RFD_SMALL_TRACE=1): phase timestamps of CTA 0
 };
 
@@ -183,43 +207,38 @@ integrate_small_kernel(const SmallArgs a) {
   stamp(a.trace, 2);
 
   // ------------------------------------------------ phase 2: S (fp64, fixed order)
-  {
+  if (!a.fuse_a7) {
     // element e of (batch x r x d): 8 lanes per element, lane l sums segments
     // l, l + 8, ... in order; then the 8 slice sums in order
+    // one warp per element of (batch x r x d): lane l sums segments l, l + 32,
+    // ... in order (8 loads in flight), then the 32 lane sums in lane order
     const int64_t E = int64_t(a.batch) * r * d;
     const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
-    for (int64_t w0 = (int64_t(blockIdx.x) * (kThreads / 32) + warp) * 4; w0 < E; w0 += warps * 4) {
-      const int64_t e0 = w0 + (lane >> 3);  // 4 elements per warp (uniform trip count)
-      const bool ok = e0 < E;
-      const int sl = lane & 7;
+    const int64_t st = int64_t(r) * d;
+    for (int64_t e0 = int64_t(blockIdx.x) * (kThreads / 32) + warp; e0 < E; e0 += warps) {
+      const int64_t b = e0 / st, rem = e0 - b * st;
+      const float* src = a.part + b * a.segs * st + rem;
       double acc = 0.0;
-      if (ok) {
-        const int64_t b = e0 / (int64_t(r) * d), rem = e0 - b * r * d;
-        const float* src = a.part + b * a.segs * r * d + rem;
-        const int64_t st = int64_t(r) * d;
-        int sg = sl;
-        for (; sg + 56 < a.segs; sg += 64) {  // 8 loads in flight, added in order
-          float v[8];
+      int sg = lane;
+      for (; sg + 7 * 32 < a.segs; sg += 8 * 32) {
+        float v[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (sg + 8 * u) * st);
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (sg + 32 * u) * st);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) acc += double(v[u]);
-        }
-        for (; sg < a.segs; sg += 8) acc += double(__ldg(src + sg * st));
+        for (int u = 0; u < 8; ++u) acc += double(v[u]);
       }
-      // fixed-order combine of the 8 slices (lanes 8i .. 8i + 7)
-      const int base = lane & ~7;
+      for (; sg < a.segs; sg += 32) acc += double(__ldg(src + sg * st));
       double tot = 0.0;
 #pragma unroll
-      for (int l = 0; l < 8; ++l) tot += __shfl_sync(0xffffffffu, acc, base + l);
-      if (ok && sl == 0) a.S[e0] = tot;
+      for (int l = 0; l < 32; ++l) tot += __shfl_sync(0xffffffffu, acc, l);
+      if (lane == 0) a.S[e0] = tot;
     }
   }
-  grid_sync(a.bar);
+  if (!a.fuse_a7) grid_sync(a.bar);
   stamp(a.trace, 3);
 
   // ------------------------------------------------ phase 3: Y = C^ S
-  {
+  if (!a.fuse_a7) {
     // one warp per (cloud, row a): lanes split the r columns, fixed-order butterfly
     const int64_t rows = int64_t(a.batch) * r;
     for (int64_t row = int64_t(blockIdx.x) * (kThreads / 32) + warp; row < rows;
@@ -244,7 +263,7 @@ integrate_small_kernel(const SmallArgs a) {
       }
     }
   }
-  grid_sync(a.bar);
+  if (!a.fuse_a7) grid_sync(a.bar);
   stamp(a.trace, 4);
 
   // ------------------------------------------------ phase 4: out = F + Phi Y
@@ -254,6 +273,7 @@ integrate_small_kernel(const SmallArgs a) {
     float* oy = ox + mp;
     float* oz = oy + mp;
     float* yc = oz + mp;        // [mp][2D]: Yc[k][0..D), Ys[k][0..D) (zero-padded)
+    double* sb = reinterpret_cast<double*>(yc + mp * 2 * D + 2 * D);  // fused a7: S_b [r][D]
     for (int k = tid; k < mp; k += kThreads) {
       const float4 w = (k < a.m) ? a.omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
       ox[k] = w.x;
@@ -268,10 +288,55 @@ integrate_small_kernel(const SmallArgs a) {
       const int64_t base = (t - int64_t(b) * tpc) * kTilePts;
       if (b != cur_b) {
         __syncthreads();
-        const float* Yb = a.Y + int64_t(b) * r * d;
-        for (int e = tid; e < mp * 2 * D; e += kThreads) {
-          const int k = e / (2 * D), rem = e - k * 2 * D, tt = rem / D, j = rem - tt * D;
-          yc[e] = (k < a.m && j < d) ? Yb[(2 * k + tt) * d + j] : 0.0f;
+        if (a.fuse_a7) {
+          // a7 for this cloud: S_b = sum of its segment partials (fixed order,
+          // fp64), then Y_b = C^_b S_b by one warp per row (lanes over the
+          // columns, fixed-order butterfly) straight into the Y staging;
+          // the CTA holding the cloud's first tile also writes S_b, Y_b (export)
+          const bool owner = base == 0;
+          const float* pb = a.part + int64_t(b) * a.segs * r * d;
+          for (int e = tid; e < r * D; e += kThreads) {
+            const int ar = e / D, j = e - ar * D;
+            double acc = 0.0;
+            if (j < d)
+              for (int sg = 0; sg < a.segs; ++sg) acc += double(__ldg(pb + (int64_t(sg) * r + ar) * d + j));
+            sb[e] = acc;
+            if (owner && j < d) a.S[(int64_t(b) * r + ar) * d + j] = acc;
+          }
+          for (int e = tid; e < mp * 2 * D; e += kThreads) yc[e] = 0.0f;
+          __syncthreads();
+          const double* Cb = a.C + int64_t(b) * r * r;
+          for (int ar = warp; ar < r; ar += kThreads / 32) {
+            double acc[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) acc[j] = 0.0;
+            for (int c = lane; c < r; c += 32) {
+              const double cv = __ldg(Cb + int64_t(ar) * r + c);
+#pragma unroll
+              for (int j = 0; j < D; ++j) acc[j] = fma(cv, sb[c * D + j], acc[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+            }
+            if (lane == 0) {
+              const int k = ar >> 1, tt = ar & 1;
+#pragma unroll
+              for (int j = 0; j < D; ++j) {
+                if (j < d) {
+                  yc[k * 2 * D + tt * D + j] = float(acc[j]);
+                  if (owner) a.Y[(int64_t(b) * r + ar) * d + j] = float(acc[j]);
+                }
+              }
+            }
+          }
+        } else {
+          const float* Yb = a.Y + int64_t(b) * r * d;
+          for (int e = tid; e < mp * 2 * D; e += kThreads) {
+            const int k = e / (2 * D), rem = e - k * 2 * D, tt = rem / D, j = rem - tt * D;
+            yc[e] = (k < a.m && j < d) ? Yb[(2 * k + tt) * d + j] : 0.0f;
+          }
         }
         cur_b = b;
         __syncthreads();
@@ -416,7 +481,8 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
   const int D = d <= 1 ? 1 : (d <= 2 ? 2 : (d <= 3 ? 3 : 4));
   const int mp = (m + 3) & ~3;
   const size_t s1 = (size_t(3 + D) * kBatchPts + size_t(kThreads) * 2 * D) * sizeof(float);
-  const size_t s4 = (size_t(3) * mp + size_t(mp) * 2 * D) * sizeof(float);
+  const size_t s4 = (size_t(3) * mp + size_t(mp) * 2 * D + 2 * D) * sizeof(float) +
+                    size_t(2 * m) * D * sizeof(double);
   const size_t smem = s1 > s4 ? s1 : s4;
   int cap = 0;
   switch (D) {
@@ -431,6 +497,9 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
   if (a.segs < 1) a.segs = 1;
   a.seg_len = ((n + a.segs - 1) / a.segs + 3) & ~int64_t(3);
   a.segs = int((n + a.seg_len - 1) / a.seg_len);
+  // a7 in phase 4's prologue when every CTA's share of it is small (each CTA
+  // redoes it for the clouds it touches): two grid barriers fewer
+  a.fuse_a7 = (2 * m <= 128 && a.segs <= 64) ? 1 : 0;
   cudaError_t e = cudaSuccess;
   switch (D) {
     case 1: e = launch_d<1>(a, grid, smem, s); break;

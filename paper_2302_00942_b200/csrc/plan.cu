@@ -387,8 +387,8 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   RFD_CUDA(dalloc(&p->C, rr * batch, st));
   RFD_CUDA(dalloc(&p->flags, size_t(8), st));
   RFD_CUDA(cudaMemsetAsync(p->flags, 0, 8 * sizeof(int), st));
-  RFD_CUDA(dalloc(&p->bar, size_t(2), st));
-  RFD_CUDA(cudaMemsetAsync(p->bar, 0, 2 * sizeof(unsigned int), st));
+  RFD_CUDA(dalloc(&p->bar, size_t(rfd::kSmallBarWords), st));
+  RFD_CUDA(cudaMemsetAsync(p->bar, 0, rfd::kSmallBarWords * sizeof(unsigned int), st));
 
   TempBuffers tmp(st);
   const float* dev_xyz = points;
