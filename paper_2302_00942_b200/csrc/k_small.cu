@@ -85,21 +85,23 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar) {
 }
 
 struct SmallArgs {
-  const float4* pts;     // batch x n, centred (x, y, z, 0)
+  const float4* pts;     // batch x n, centred (x, y, z, 0): one array, clouds back to back
   const float4* omega4;  // m: fp32(2 pi omega)
   int m, fb, nfb;        // frequencies; frequency block (32..256, power of two); blocks
   int64_t n;
   int batch, d;
-  int segs;              // point segments per cloud (phase 1)
-  int64_t seg_len;       // points per segment (multiple of 4)
+  int R;                 // phase-1 point ranges (gridDim = R x nfb)
+  int64_t L;             // points per phase-1 range (multiple of 4)
+  int K;                 // partial slots per range (clouds a range can touch)
+  int64_t L4;            // points per phase-4 range (one per CTA)
   const float* F;        // (batch x) n x d
   float* out;            // same shape (may alias F)
   const double* C;       // batch x r x r
-  float* part;           // batch x segs x r x d
+  float* part;           // R x K x r x d: slot (range c, its k-th cloud)
   double* S;             // batch x r x d
   float* Y;              // batch x r x d
   unsigned int* bar;     // kBarWords words, zero before the first launch
-  int fuse_a7;           // 1: S and Y per cloud in phase 4's prologue (small r, few segments)
+  int fuse_a7;           // 1: S and Y per cloud in phase 4's prologue (small r)
   unsigned long long* trace;  // diagnostics (RFD_SMALL_TRACE=1): phase timestamps of CTA 0
 };
 
@@ -112,6 +114,20 @@ __device__ __forceinline__ void stamp(unsigned long long* tr, int i) {
 }
 __device__ unsigned long long g_small_trace[8];
 
+// S[b][row][j] = sum over the ranges overlapping cloud b, in range order, of
+// their slot for b (fp64).  Range c overlaps b iff [cL, cL+L) meets [bn, bn+n).
+__device__ __forceinline__ double sum_slots(const SmallArgs& a, int b, int row, int j) {
+  const int r = 2 * a.m;
+  const int64_t lo = int64_t(b) * a.n, hi = lo + a.n;
+  const int c0 = int(lo / a.L), c1 = int((hi - 1) / a.L);
+  double acc = 0.0;
+  for (int c = c0; c <= c1; ++c) {
+    const int k = b - int((int64_t(c) * a.L) / a.n);
+    acc += double(__ldg(a.part + ((int64_t(c) * a.K + k) * r + row) * a.d + j));
+  }
+  return acc;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads)
 integrate_small_kernel(const SmallArgs a) {
@@ -119,44 +135,46 @@ integrate_small_kernel(const SmallArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = 2 * a.m;
   const int d = a.d;
+  const int64_t ntot = int64_t(a.batch) * a.n;
   stamp(a.trace, 0);
 
   // ------------------------------------------------ phase 1: S partials
+  // CTA = (range c, frequency block f): the range's points, cloud by cloud,
+  // one partial slot per (range, cloud) -- equal ranges: every CTA (and SM)
+  // gets the same number of points whatever the cloud sizes
   {
     const int G = kThreads / a.fb;  // point groups
     const int g = tid / a.fb;
+    const int c = blockIdx.x / a.nfb, fbk = blockIdx.x % a.nfb;
     float* xs = sm;                         // [kBatchPts] x, y, z, then F[D][kBatchPts]
     float* ys = xs + kBatchPts;
     float* zs = ys + kBatchPts;
     float* fs = zs + kBatchPts;
     float* red = fs + D * kBatchPts;        // [G][fb][2D]
-    const int64_t items = int64_t(a.batch) * a.segs * a.nfb;
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-      const int fbk = int(it % a.nfb);
-      const int64_t bs = it / a.nfb;
-      const int b = int(bs / a.segs), seg = int(bs % a.segs);
-      const int k = fbk * a.fb + (tid % a.fb);
-      const float4 w = (k < a.m) ? a.omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float2 wx = make_float2(w.x, w.x), wy = make_float2(w.y, w.y), wz = make_float2(w.z, w.z);
+    const int k = fbk * a.fb + (tid % a.fb);
+    const float4 w = (k < a.m) ? a.omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float2 wx = make_float2(w.x, w.x), wy = make_float2(w.y, w.y), wz = make_float2(w.z, w.z);
+    const int64_t r0 = int64_t(c) * a.L, r1 = min(r0 + a.L, ntot);
+    const int bfirst = int(r0 / a.n);
+    for (int64_t p0 = r0; p0 < r1;) {  // one cloud part per iteration
+      const int b = int(p0 / a.n);
+      const int64_t p1 = min(r1, int64_t(b + 1) * a.n);
       float2 acc[D];
 #pragma unroll
       for (int j = 0; j < D; ++j) acc[j] = make_float2(0.f, 0.f);
-      const int64_t p0 = int64_t(seg) * a.seg_len, p1 = min(p0 + a.seg_len, a.n);
-      const float4* cloud = a.pts + int64_t(b) * a.n;
-      const float* Fb = a.F + int64_t(b) * a.n * d;
       for (int64_t base = p0; base < p1; base += kBatchPts) {
         const int np = int(p1 - base < kBatchPts ? p1 - base : kBatchPts);
         const int np4 = (np + 3) & ~3;
-        __syncthreads();  // the previous batch has been read
+        __syncthreads();  // the previous batch (and reduction) has been read
         for (int i = tid; i < np4; i += kThreads) {
-          const float4 x = (i < np) ? __ldg(cloud + base + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 x = (i < np) ? __ldg(a.pts + base + i) : make_float4(0.f, 0.f, 0.f, 0.f);
           xs[i] = x.x;
           ys[i] = x.y;
           zs[i] = x.z;
         }
         for (int i = tid; i < np4 * D; i += kThreads) {
           const int p = i / D, j = i - p * D;
-          fs[j * kBatchPts + p] = (p < np && j < d) ? __ldg(Fb + (base + p) * d + j) : 0.0f;
+          fs[j * kBatchPts + p] = (p < np && j < d) ? __ldg(a.F + (base + p) * d + j) : 0.0f;
         }
         __syncthreads();
         // group g takes 4-point quads g, g + G, ... of the batch
@@ -185,60 +203,40 @@ integrate_small_kernel(const SmallArgs a) {
           }
         }
       }
-      // the G point groups, added in group order
+      // the G point groups, added in group order, into slot (c, b - bfirst)
 #pragma unroll
       for (int j = 0; j < D; ++j) {
         red[(g * a.fb + tid % a.fb) * 2 * D + 2 * j] = acc[j].x;
         red[(g * a.fb + tid % a.fb) * 2 * D + 2 * j + 1] = acc[j].y;
       }
       __syncthreads();
+      float* slot = a.part + (int64_t(c) * a.K + (b - bfirst)) * r * d;
       for (int e = tid; e < a.fb * 2 * d; e += kThreads) {
         const int kk = e / (2 * d), rem = e - kk * 2 * d, t = rem / d, j = rem - t * d;
         const int kg = fbk * a.fb + kk;
         if (kg >= a.m) continue;
-        float s = 0.0f;
-        for (int gg = 0; gg < G; ++gg) s += red[(gg * a.fb + kk) * 2 * D + 2 * j + t];
-        a.part[((int64_t(b) * a.segs + seg) * r + 2 * kg + t) * d + j] = s;
+        float sum = 0.0f;
+        for (int gg = 0; gg < G; ++gg) sum += red[(gg * a.fb + kk) * 2 * D + 2 * j + t];
+        slot[(2 * kg + t) * d + j] = sum;
       }
+      p0 = p1;
     }
   }
   stamp(a.trace, 1);
   grid_sync(a.bar);
   stamp(a.trace, 2);
 
-  // ------------------------------------------------ phase 2: S (fp64, fixed order)
   if (!a.fuse_a7) {
-    // element e of (batch x r x d): 8 lanes per element, lane l sums segments
-    // l, l + 8, ... in order; then the 8 slice sums in order
-    // one warp per element of (batch x r x d): lane l sums segments l, l + 32,
-    // ... in order (8 loads in flight), then the 32 lane sums in lane order
+    // ---------------------------------------------- phase 2: S (fp64, fixed order)
     const int64_t E = int64_t(a.batch) * r * d;
-    const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
-    const int64_t st = int64_t(r) * d;
-    for (int64_t e0 = int64_t(blockIdx.x) * (kThreads / 32) + warp; e0 < E; e0 += warps) {
-      const int64_t b = e0 / st, rem = e0 - b * st;
-      const float* src = a.part + b * a.segs * st + rem;
-      double acc = 0.0;
-      int sg = lane;
-      for (; sg + 7 * 32 < a.segs; sg += 8 * 32) {
-        float v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (sg + 32 * u) * st);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc += double(v[u]);
-      }
-      for (; sg < a.segs; sg += 32) acc += double(__ldg(src + sg * st));
-      double tot = 0.0;
-#pragma unroll
-      for (int l = 0; l < 32; ++l) tot += __shfl_sync(0xffffffffu, acc, l);
-      if (lane == 0) a.S[e0] = tot;
+    for (int64_t e = int64_t(blockIdx.x) * kThreads + tid; e < E; e += int64_t(gridDim.x) * kThreads) {
+      const int b = int(e / (int64_t(r) * d));
+      const int rem = int(e - int64_t(b) * r * d);
+      a.S[e] = sum_slots(a, b, rem / d, rem % d);
     }
-  }
-  if (!a.fuse_a7) grid_sync(a.bar);
-  stamp(a.trace, 3);
-
-  // ------------------------------------------------ phase 3: Y = C^ S
-  if (!a.fuse_a7) {
+    grid_sync(a.bar);
+    stamp(a.trace, 3);
+    // ---------------------------------------------- phase 3: Y = C^ S
     // one warp per (cloud, row a): lanes split the r columns, fixed-order butterfly
     const int64_t rows = int64_t(a.batch) * r;
     for (int64_t row = int64_t(blockIdx.x) * (kThreads / 32) + warp; row < rows;
@@ -249,11 +247,12 @@ integrate_small_kernel(const SmallArgs a) {
       double acc[D];
 #pragma unroll
       for (int j = 0; j < D; ++j) acc[j] = 0.0;
-      for (int c = lane; c < r; c += 32) {
-        const double cv = __ldg(Crow + c);
+#pragma unroll 4
+      for (int cc = lane; cc < r; cc += 32) {
+        const double cv = __ldg(Crow + cc);
 #pragma unroll
         for (int j = 0; j < D; ++j)
-          if (j < d) acc[j] = fma(cv, __ldg(Sb + int64_t(c) * d + j), acc[j]);
+          if (j < d) acc[j] = fma(cv, __ldg(Sb + int64_t(cc) * d + j), acc[j]);
       }
 #pragma unroll
       for (int j = 0; j < D; ++j) {
@@ -262,11 +261,12 @@ integrate_small_kernel(const SmallArgs a) {
         if (lane == 0 && j < d) a.Y[row * d + j] = float(acc[j]);
       }
     }
+    grid_sync(a.bar);
   }
-  if (!a.fuse_a7) grid_sync(a.bar);
   stamp(a.trace, 4);
 
   // ------------------------------------------------ phase 4: out = F + Phi Y
+  // CTA c: points [c L4, (c+1) L4), sub-tiles of <= 512 points within one cloud
   {
     const int mp = (a.m + 3) & ~3;
     float* ox = sm;             // [mp] omega x, y, z (zero-padded)
@@ -274,62 +274,62 @@ integrate_small_kernel(const SmallArgs a) {
     float* oz = oy + mp;
     float* yc = oz + mp;        // [mp][2D]: Yc[k][0..D), Ys[k][0..D) (zero-padded)
     double* sb = reinterpret_cast<double*>(yc + mp * 2 * D + 2 * D);  // fused a7: S_b [r][D]
+    double* yq = sb + r * D;                                          // fused a7: [4][r][D]
     for (int k = tid; k < mp; k += kThreads) {
       const float4 w = (k < a.m) ? a.omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
       ox[k] = w.x;
       oy[k] = w.y;
       oz[k] = w.z;
     }
-    const int64_t tpc = (a.n + kTilePts - 1) / kTilePts;
-    const int64_t tiles = tpc * a.batch;
+    const int64_t q0 = int64_t(blockIdx.x) * a.L4, q1 = min(q0 + a.L4, ntot);
     int cur_b = -1;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int b = int(t / tpc);
-      const int64_t base = (t - int64_t(b) * tpc) * kTilePts;
+    for (int64_t base = q0; base < q1;) {
+      const int b = int(base / a.n);
+      const int64_t tend = min(min(base + kTilePts, q1), int64_t(b + 1) * a.n);
       if (b != cur_b) {
         __syncthreads();
         if (a.fuse_a7) {
-          // a7 for this cloud: S_b = sum of its segment partials (fixed order,
-          // fp64), then Y_b = C^_b S_b by one warp per row (lanes over the
-          // columns, fixed-order butterfly) straight into the Y staging;
-          // the CTA holding the cloud's first tile also writes S_b, Y_b (export)
-          const bool owner = base == 0;
-          const float* pb = a.part + int64_t(b) * a.segs * r * d;
+          // a7 for this cloud: S_b = its range slots in order (fp64), then
+          // Y_b = C^_b S_b: thread (row, quarter) sums a quarter of the columns
+          // with its loads in flight, the quarters added in order; the CTA
+          // holding the cloud's first point writes S_b, Y_b (export)
+          const bool owner = base == int64_t(b) * a.n;
           for (int e = tid; e < r * D; e += kThreads) {
             const int ar = e / D, j = e - ar * D;
-            double acc = 0.0;
-            if (j < d)
-              for (int sg = 0; sg < a.segs; ++sg) acc += double(__ldg(pb + (int64_t(sg) * r + ar) * d + j));
-            sb[e] = acc;
-            if (owner && j < d) a.S[(int64_t(b) * r + ar) * d + j] = acc;
+            const double v = (j < d) ? sum_slots(a, b, ar, j) : 0.0;
+            sb[e] = v;
+            if (owner && j < d) a.S[(int64_t(b) * r + ar) * d + j] = v;
           }
-          for (int e = tid; e < mp * 2 * D; e += kThreads) yc[e] = 0.0f;
           __syncthreads();
           const double* Cb = a.C + int64_t(b) * r * r;
-          for (int ar = warp; ar < r; ar += kThreads / 32) {
+          const int qw = (r + 3) / 4;
+          for (int e = tid; e < 4 * r; e += kThreads) {
+            const int ar = e % r, qq = e / r;
+            const int cb = qq * qw, ce = min(r, cb + qw);
             double acc[D];
 #pragma unroll
             for (int j = 0; j < D; ++j) acc[j] = 0.0;
-            for (int c = lane; c < r; c += 32) {
-              const double cv = __ldg(Cb + int64_t(ar) * r + c);
+#pragma unroll 8
+            for (int cc = cb; cc < ce; ++cc) {
+              const double cv = __ldg(Cb + int64_t(ar) * r + cc);
 #pragma unroll
-              for (int j = 0; j < D; ++j) acc[j] = fma(cv, sb[c * D + j], acc[j]);
+              for (int j = 0; j < D; ++j) acc[j] = fma(cv, sb[cc * D + j], acc[j]);
             }
 #pragma unroll
-            for (int j = 0; j < D; ++j) {
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+            for (int j = 0; j < D; ++j) yq[(qq * r + ar) * D + j] = acc[j];
+          }
+          __syncthreads();
+          for (int e = tid; e < mp * 2 * D; e += kThreads) {
+            const int k = e / (2 * D), rem = e - k * 2 * D, tt = rem / D, j = rem - tt * D;
+            float v = 0.0f;
+            if (k < a.m && j < d) {
+              const int ar = 2 * k + tt;
+              const double y = ((yq[ar * D + j] + yq[(r + ar) * D + j]) + yq[(2 * r + ar) * D + j]) +
+                               yq[(3 * r + ar) * D + j];
+              v = float(y);
+              if (owner) a.Y[(int64_t(b) * r + ar) * d + j] = v;
             }
-            if (lane == 0) {
-              const int k = ar >> 1, tt = ar & 1;
-#pragma unroll
-              for (int j = 0; j < D; ++j) {
-                if (j < d) {
-                  yc[k * 2 * D + tt * D + j] = float(acc[j]);
-                  if (owner) a.Y[(int64_t(b) * r + ar) * d + j] = float(acc[j]);
-                }
-              }
-            }
+            yc[e] = v;
           }
         } else {
           const float* Yb = a.Y + int64_t(b) * r * d;
@@ -342,9 +342,8 @@ integrate_small_kernel(const SmallArgs a) {
         __syncthreads();
       }
       const int64_t i0 = base + tid, i1 = base + tid + kThreads;
-      const float4* cloud = a.pts + int64_t(b) * a.n;
-      const float4 p0 = (i0 < a.n) ? __ldg(cloud + i0) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 p1 = (i1 < a.n) ? __ldg(cloud + i1) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 p0 = (i0 < tend) ? __ldg(a.pts + i0) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 p1 = (i1 < tend) ? __ldg(a.pts + i1) : make_float4(0.f, 0.f, 0.f, 0.f);
       const float2 X = make_float2(p0.x, p1.x), Yp = make_float2(p0.y, p1.y),
                    Z = make_float2(p0.z, p1.z);
       float2 acc[D];
@@ -368,26 +367,25 @@ integrate_small_kernel(const SmallArgs a) {
           float2 th = __fmul2_rn(X, make_float2(wxs[u], wxs[u]));
           th = __ffma2_rn(Yp, make_float2(wys[u], wys[u]), th);
           th = __ffma2_rn(Z, make_float2(wzs[u], wzs[u]), th);
-          float2 c, s;
-          __sincosf(th.x, &s.x, &c.x);
-          __sincosf(th.y, &s.y, &c.y);
+          float2 cv, sv;
+          __sincosf(th.x, &sv.x, &cv.x);
+          __sincosf(th.y, &sv.y, &cv.y);
 #pragma unroll
           for (int j = 0; j < D; ++j) {
-            acc[j] = __ffma2_rn(c, make_float2(yv[u * 2 * D + j], yv[u * 2 * D + j]), acc[j]);
-            acc[j] = __ffma2_rn(s, make_float2(yv[u * 2 * D + D + j], yv[u * 2 * D + D + j]), acc[j]);
+            acc[j] = __ffma2_rn(cv, make_float2(yv[u * 2 * D + j], yv[u * 2 * D + j]), acc[j]);
+            acc[j] = __ffma2_rn(sv, make_float2(yv[u * 2 * D + D + j], yv[u * 2 * D + D + j]), acc[j]);
           }
         }
       }
-      const float* Fb = a.F + int64_t(b) * a.n * d;
-      float* Ob = a.out + int64_t(b) * a.n * d;
       // (F and out may alias: each row is read before it is written, by this thread)
 #pragma unroll
       for (int j = 0; j < D; ++j) {
         if (j < d) {
-          if (i0 < a.n) Ob[i0 * d + j] = Fb[i0 * d + j] + acc[j].x;
-          if (i1 < a.n) Ob[i1 * d + j] = Fb[i1 * d + j] + acc[j].y;
+          if (i0 < tend) a.out[i0 * d + j] = a.F[i0 * d + j] + acc[j].x;
+          if (i1 < tend) a.out[i1 * d + j] = a.F[i1 * d + j] + acc[j].y;
         }
       }
+      base = tend;
     }
   }
   stamp(a.trace, 5);
@@ -428,35 +426,56 @@ cudaError_t launch_d(const SmallArgs& a, int grid, size_t smem, cudaStream_t s) 
 
 int frequency_block(int m) { return m <= 32 ? 32 : (m <= 64 ? 64 : (m <= 128 ? 128 : 256)); }
 
-// Grid (CTAs) sized to the work, at most what is co-resident: small clouds
-// get few CTAs (cheaper grid barriers), large ones the whole GPU.
-int small_grid(int m, int64_t n, int batch, int cap) {
+// Phase-1 ranges: about 1024 points each, at most what is co-resident (small
+// clouds get few CTAs: cheaper grid barriers; large ones the whole GPU);
+// K = partial slots per range (the clouds one range can touch).
+void small_geometry(int m, int64_t n, int batch, int cap, int* R, int64_t* L, int* K) {
   const int nfb = (m + frequency_block(m) - 1) / frequency_block(m);
-  const int64_t items = int64_t(batch) * nfb * ((n + 1023) / 1024);  // >= 1024-point segments
-  const int64_t tiles = int64_t(batch) * ((n + kTilePts - 1) / kTilePts);
-  int64_t g = items > tiles ? items : tiles;
-  if (g > cap) g = cap;
-  return g < 1 ? 1 : int(g);
+  const int64_t ntot = n * batch;
+  int64_t r = (ntot + 1023) / 1024;
+  if (r * nfb > cap) r = cap / nfb;
+  if (r < 1) r = 1;
+  *L = ((ntot + r - 1) / r + 3) & ~int64_t(3);
+  *R = int((ntot + *L - 1) / *L);
+  int64_t k = (*L + n - 1) / n + 1;
+  if (k > batch) k = batch;
+  *K = int(k);
+}
+
+size_t smem_bytes(int m, int D) {
+  const int mp = (m + 3) & ~3;
+  const size_t s1 = (size_t(3 + D) * kBatchPts + size_t(kThreads) * 2 * D) * sizeof(float);
+  const size_t s4 = (size_t(3) * mp + size_t(mp) * 2 * D + 2 * D) * sizeof(float) +
+                    size_t(2 * m) * D * 5 * sizeof(double);
+  return s1 > s4 ? s1 : s4;
+}
+
+int dclass(int d) { return d <= 1 ? 1 : (d <= 2 ? 2 : (d <= 3 ? 3 : 4)); }
+
+int cap_for(int m, int d, int sms) {
+  const size_t smem = smem_bytes(m, dclass(d));
+  switch (dclass(d)) {
+    case 1: return max_ctas<1>(smem, sms);
+    case 2: return max_ctas<2>(smem, sms);
+    case 3: return max_ctas<3>(smem, sms);
+    default: return max_ctas<4>(smem, sms);
+  }
 }
 
 }  // namespace
 
-int small_segments(int m, int64_t n, int batch, int sms) {
-  // one phase-1 item (cloud, segment, frequency block) per CTA of the largest
-  // grid (4 CTAs per SM), whole 4-point quads
-  const int nfb = (m + frequency_block(m) - 1) / frequency_block(m);
-  const int grid = small_grid(m, n, batch, 4 * sms);
-  int64_t segs = grid / (int64_t(batch) * nfb);
-  const int64_t maxs = (n + 255) / 256;
-  if (segs > maxs) segs = maxs;
-  return segs < 1 ? 1 : int(segs);
+size_t small_partial_elems(int m, int64_t n, int batch, int d, int sms) {
+  int R, K;
+  int64_t L;
+  small_geometry(m, n, batch, cap_for(m, d, sms), &R, &L, &K);
+  return size_t(R) * size_t(K) * size_t(2 * m) * size_t(d);
 }
 
 cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int m, int64_t n,
                                    int batch, int sms, const float* F, int d, float* out,
                                    const double* C, float* part, double* S, float* Y,
                                    unsigned int* bar, cudaStream_t s) {
-  LaunchScope L("rfd_integrate_small", s);
+  LaunchScope Ls("rfd_integrate_small", s);
   SmallArgs a{};
   a.pts = pts;
   a.omega4 = omega4;
@@ -478,28 +497,15 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
     return e && e[0] == '1';
   }();
   if (trace) cudaGetSymbolAddress(reinterpret_cast<void**>(&a.trace), g_small_trace);
-  const int D = d <= 1 ? 1 : (d <= 2 ? 2 : (d <= 3 ? 3 : 4));
-  const int mp = (m + 3) & ~3;
-  const size_t s1 = (size_t(3 + D) * kBatchPts + size_t(kThreads) * 2 * D) * sizeof(float);
-  const size_t s4 = (size_t(3) * mp + size_t(mp) * 2 * D + 2 * D) * sizeof(float) +
-                    size_t(2 * m) * D * sizeof(double);
-  const size_t smem = s1 > s4 ? s1 : s4;
-  int cap = 0;
-  switch (D) {
-    case 1: cap = max_ctas<1>(smem, sms); break;
-    case 2: cap = max_ctas<2>(smem, sms); break;
-    case 3: cap = max_ctas<3>(smem, sms); break;
-    default: cap = max_ctas<4>(smem, sms); break;
-  }
-  const int grid = small_grid(m, n, batch, cap);
-  a.segs = int(grid / (int64_t(batch) * a.nfb));
-  if (a.segs > small_segments(m, n, batch, sms)) a.segs = small_segments(m, n, batch, sms);
-  if (a.segs < 1) a.segs = 1;
-  a.seg_len = ((n + a.segs - 1) / a.segs + 3) & ~int64_t(3);
-  a.segs = int((n + a.seg_len - 1) / a.seg_len);
-  // a7 in phase 4's prologue when every CTA's share of it is small (each CTA
-  // redoes it for the clouds it touches): two grid barriers fewer
-  a.fuse_a7 = (2 * m <= 128 && a.segs <= 64) ? 1 : 0;
+  const int D = dclass(d);
+  const size_t smem = smem_bytes(m, D);
+  small_geometry(m, n, batch, cap_for(m, d, sms), &a.R, &a.L, &a.K);
+  const int grid = a.R * a.nfb;
+  const int64_t ntot = n * batch;
+  a.L4 = (ntot + grid - 1) / grid;
+  // a7 in phase 4's prologue for small r (each CTA redoes it for the clouds it
+  // touches): two grid barriers fewer
+  a.fuse_a7 = (2 * m <= 128) ? 1 : 0;
   cudaError_t e = cudaSuccess;
   switch (D) {
     case 1: e = launch_d<1>(a, grid, smem, s); break;
@@ -511,10 +517,10 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
     unsigned long long h[8];
     cudaStreamSynchronize(s);
     cudaMemcpyFromSymbol(h, g_small_trace, sizeof(h));
-    fprintf(stderr, "small n=%lld batch=%d m=%d d=%d grid=%d segs=%d: phase1 %.1f us, sync %.1f, "
-            "S %.1f, Y %.1f, phase4 %.1f (total %.1f)\n", (long long)n, batch, m, d, grid, a.segs,
-            (h[1] - h[0]) * 1e-3, (h[2] - h[1]) * 1e-3, (h[3] - h[2]) * 1e-3, (h[4] - h[3]) * 1e-3,
-            (h[5] - h[4]) * 1e-3, (h[5] - h[0]) * 1e-3);
+    fprintf(stderr, "small n=%lld batch=%d m=%d d=%d grid=%d slots=%d fuse=%d: phase1 %.1f us, "
+            "sync %.1f, S %.1f, Y %.1f, phase4 %.1f (total %.1f)\n", (long long)n, batch, m, d, grid,
+            a.K, a.fuse_a7, (h[1] - h[0]) * 1e-3, (h[2] - h[1]) * 1e-3, (h[3] - h[2]) * 1e-3,
+            (h[4] - h[3]) * 1e-3, (h[5] - h[4]) * 1e-3, (h[5] - h[0]) * 1e-3);
   }
   return e;
 }

@@ -126,7 +126,8 @@ struct rfd_plan {
   float* s_partial = nullptr; // batch*chunks*r*16
   double* S = nullptr;        // batch*r*d
   double* S_parts = nullptr;  // world*r*d (sharded plans: the gathered partials)
-  float* small_part = nullptr;  // d <= 4 path: batch*segments*r*4 segment partials
+  float* small_part = nullptr;  // d <= 4 path: range x cloud-slot partials
+  size_t small_part_elems = 0;
   unsigned int* bar = nullptr;  // d <= 4 path: grid barrier (2 words, self-resetting)
   float* Y = nullptr;         // batch*r*d
   int last_d = 0;
@@ -551,9 +552,12 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
   if (rs != RFD_OK) return rs;
   if (d <= 4 && p->world == 1) {
     // narrow fields: the whole inference in one cooperative SIMT launch (k_small.cu)
-    if (!p->small_part) {
-      const size_t segs = size_t(rfd::small_segments(p->m, p->n, p->batch, p->sms));
-      RFD_CUDA(dalloc(&p->small_part, size_t(p->batch) * segs * p->r * 4, st));
+    const size_t need = rfd::small_partial_elems(p->m, p->n, p->batch, d, p->sms);
+    if (p->small_part_elems < need) {
+      dfree(p->small_part, st);
+      p->small_part_elems = 0;
+      RFD_CUDA(dalloc(&p->small_part, need, st));
+      p->small_part_elems = need;
     }
     RFD_CUDA(rfd::launch_integrate_small(p->pts, p->omega_rad4, p->m, p->n, p->batch, p->sms, F, d,
                                          out, p->C, p->small_part, p->S, p->Y, p->bar, st));

@@ -173,10 +173,10 @@ void launch_pass2_tc(const float4* pts, const float4* omega4, int m, int64_t n, 
 
 // Narrow fields, d <= 4 (k_small.cu): the whole inference (S partials,
 // fixed-order S, Y = C^ S, out = F + Phi Y) in one cooperative launch.
-// part: batch x small_segments(...) x r x d fp32; S, Y: batch x r x d (plan
-// export); bar: kSmallBarWords words zeroed once (self-resetting grid barrier).
+// part: small_partial_elems(...) fp32; S, Y: batch x r x d (plan export);
+// bar: kSmallBarWords words zeroed once (self-resetting grid barrier).
 constexpr int kSmallBarWords = 34;
-int small_segments(int m, int64_t n, int batch, int sms);
+size_t small_partial_elems(int m, int64_t n, int batch, int d, int sms);
 cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int m, int64_t n,
                                    int batch, int sms, const float* F, int d, float* out,
                                    const double* C, float* part, double* S, float* Y,
