@@ -129,7 +129,7 @@ __device__ __forceinline__ double sum_slots(const SmallArgs& a, int b, int row, 
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
 integrate_small_kernel(const SmallArgs a) {
   extern __shared__ __align__(16) float sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -139,87 +139,116 @@ integrate_small_kernel(const SmallArgs a) {
   stamp(a.trace, 0);
 
   // ------------------------------------------------ phase 1: S partials
-  // CTA = (range c, frequency block f): the range's points, cloud by cloud,
-  // one partial slot per (range, cloud) -- equal ranges: every CTA (and SM)
-  // gets the same number of points whatever the cloud sizes
+  // CTA = (range c, frequency block f): the range's points in batches of <= 512
+  // (never across a cloud boundary), one partial slot per (range, cloud) --
+  // equal ranges: every CTA gets the same number of points whatever the
+  // cloud sizes.  Batches are double-buffered: the next one is copied
+  // (cp.async, global latency hidden) while this one is consumed.
   {
     const int G = kThreads / a.fb;  // point groups
     const int g = tid / a.fb;
     const int c = blockIdx.x / a.nfb, fbk = blockIdx.x % a.nfb;
-    float* xs = sm;                         // [kBatchPts] x, y, z, then F[D][kBatchPts]
-    float* ys = xs + kBatchPts;
-    float* zs = ys + kBatchPts;
-    float* fs = zs + kBatchPts;
-    float* red = fs + D * kBatchPts;        // [G][fb][2D]
+    // buffer b: points at sm + b * kBufF (float4 x 512), field rows after them
+    constexpr int kBufF = (4 + D) * kBatchPts;  // floats per buffer
+    auto pbuf = [&](int b) { return reinterpret_cast<float4*>(sm + b * kBufF); };
+    auto fbuf = [&](int b) { return sm + b * kBufF + 4 * kBatchPts; };
+    float* red = sm + 2 * kBufF;  // [G][fb][2D]
     const int k = fbk * a.fb + (tid % a.fb);
     const float4 w = (k < a.m) ? a.omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float2 wx = make_float2(w.x, w.x), wy = make_float2(w.y, w.y), wz = make_float2(w.z, w.z);
     const int64_t r0 = int64_t(c) * a.L, r1 = min(r0 + a.L, ntot);
     const int bfirst = int(r0 / a.n);
-    for (int64_t p0 = r0; p0 < r1;) {  // one cloud part per iteration
-      const int b = int(p0 / a.n);
-      const int64_t p1 = min(r1, int64_t(b + 1) * a.n);
-      float2 acc[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) acc[j] = make_float2(0.f, 0.f);
-      for (int64_t base = p0; base < p1; base += kBatchPts) {
-        const int np = int(p1 - base < kBatchPts ? p1 - base : kBatchPts);
-        const int np4 = (np + 3) & ~3;
-        __syncthreads();  // the previous batch (and reduction) has been read
-        for (int i = tid; i < np4; i += kThreads) {
-          const float4 x = (i < np) ? __ldg(a.pts + base + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-          xs[i] = x.x;
-          ys[i] = x.y;
-          zs[i] = x.z;
-        }
-        for (int i = tid; i < np4 * D; i += kThreads) {
-          const int p = i / D, j = i - p * D;
-          fs[j * kBatchPts + p] = (p < np && j < d) ? __ldg(a.F + (base + p) * d + j) : 0.0f;
-        }
-        __syncthreads();
-        // group g takes 4-point quads g, g + G, ... of the batch
-        for (int q = 4 * g; q < np4; q += 4 * G) {
-          const float4 X = *reinterpret_cast<const float4*>(xs + q);
-          const float4 Yv = *reinterpret_cast<const float4*>(ys + q);
-          const float4 Z = *reinterpret_cast<const float4*>(zs + q);
-          float2 t0 = __fmul2_rn(make_float2(X.x, X.y), wx);
-          float2 t1 = __fmul2_rn(make_float2(X.z, X.w), wx);
-          t0 = __ffma2_rn(make_float2(Yv.x, Yv.y), wy, t0);
-          t1 = __ffma2_rn(make_float2(Yv.z, Yv.w), wy, t1);
-          t0 = __ffma2_rn(make_float2(Z.x, Z.y), wz, t0);
-          t1 = __ffma2_rn(make_float2(Z.z, Z.w), wz, t1);
-          float2 cs[4];
-          __sincosf(t0.x, &cs[0].y, &cs[0].x);
-          __sincosf(t0.y, &cs[1].y, &cs[1].x);
-          __sincosf(t1.x, &cs[2].y, &cs[2].x);
-          __sincosf(t1.y, &cs[3].y, &cs[3].x);
-#pragma unroll
-          for (int j = 0; j < D; ++j) {
-            const float4 f = *reinterpret_cast<const float4*>(fs + j * kBatchPts + q);
-            acc[j] = __ffma2_rn(cs[0], make_float2(f.x, f.x), acc[j]);
-            acc[j] = __ffma2_rn(cs[1], make_float2(f.y, f.y), acc[j]);
-            acc[j] = __ffma2_rn(cs[2], make_float2(f.z, f.z), acc[j]);
-            acc[j] = __ffma2_rn(cs[3], make_float2(f.w, f.w), acc[j]);
-          }
-        }
+    // batch i: [start, end) -- at most 512 points, within one cloud
+    auto batch_end = [&](int64_t start) {
+      const int64_t cend = (start / a.n + 1) * a.n;
+      return min(min(start + kBatchPts, r1), cend);
+    };
+    auto issue = [&](int64_t start, int64_t end, int buf) {
+      const int np = int(end - start), np4 = (np + 3) & ~3;
+      for (int i = tid; i < np4; i += kThreads) {
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(pbuf(buf) + i));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+                     "l"(a.pts + (i < np ? start + i : start)), "r"(i < np ? 16 : 0) : "memory");
       }
-      // the G point groups, added in group order, into slot (c, b - bfirst)
+      // F rows of the batch: np * D floats, contiguous, 16-byte chunks (zero-filled tail)
+      const float* src = a.F + start * D;
+      const int nf = np * D, nc = (np4 * D) / 4;
+      for (int i = tid; i < nc; i += kThreads) {
+        const int bytes = max(0, min(16, (nf - 4 * i) * 4));
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(fbuf(buf) + 4 * i));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+                     "l"(bytes > 0 ? src + 4 * i : src), "r"(bytes) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    float2 acc[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) {
-        red[(g * a.fb + tid % a.fb) * 2 * D + 2 * j] = acc[j].x;
-        red[(g * a.fb + tid % a.fb) * 2 * D + 2 * j + 1] = acc[j].y;
+    for (int j = 0; j < D; ++j) acc[j] = make_float2(0.f, 0.f);
+    int64_t bs = r0, be = batch_end(r0);
+    if (bs < r1) issue(bs, be, 0);
+    for (int it = 0; bs < r1; ++it) {
+      const int buf = it & 1;
+      const int64_t ns = be, ne = ns < r1 ? batch_end(ns) : ns;
+      if (ns < r1) {
+        issue(ns, ne, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       __syncthreads();
-      float* slot = a.part + (int64_t(c) * a.K + (b - bfirst)) * r * d;
-      for (int e = tid; e < a.fb * 2 * d; e += kThreads) {
-        const int kk = e / (2 * d), rem = e - kk * 2 * d, t = rem / d, j = rem - t * d;
-        const int kg = fbk * a.fb + kk;
-        if (kg >= a.m) continue;
-        float sum = 0.0f;
-        for (int gg = 0; gg < G; ++gg) sum += red[(gg * a.fb + kk) * 2 * D + 2 * j + t];
-        slot[(2 * kg + t) * d + j] = sum;
+      const int np4 = (int(be - bs) + 3) & ~3;
+      const float4* xs = pbuf(buf);
+      const float* fs = fbuf(buf);
+      // group g takes 4-point quads g, g + G, ... of the batch
+      for (int q = 4 * g; q < np4; q += 4 * G) {
+        const float4 p0 = xs[q], p1 = xs[q + 1], p2 = xs[q + 2], p3 = xs[q + 3];
+        float2 t0 = __fmul2_rn(make_float2(p0.x, p1.x), wx);
+        float2 t1 = __fmul2_rn(make_float2(p2.x, p3.x), wx);
+        t0 = __ffma2_rn(make_float2(p0.y, p1.y), wy, t0);
+        t1 = __ffma2_rn(make_float2(p2.y, p3.y), wy, t1);
+        t0 = __ffma2_rn(make_float2(p0.z, p1.z), wz, t0);
+        t1 = __ffma2_rn(make_float2(p2.z, p3.z), wz, t1);
+        float2 cs[4];
+        __sincosf(t0.x, &cs[0].y, &cs[0].x);
+        __sincosf(t0.y, &cs[1].y, &cs[1].x);
+        __sincosf(t1.x, &cs[2].y, &cs[2].x);
+        __sincosf(t1.y, &cs[3].y, &cs[3].x);
+        // the quad's field rows: 4 D floats = D 16-byte loads
+        float f[4 * D];
+#pragma unroll
+        for (int v = 0; v < D; ++v)
+          *reinterpret_cast<float4*>(f + 4 * v) = *reinterpret_cast<const float4*>(fs + q * D + 4 * v);
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            acc[j] = __ffma2_rn(cs[u], make_float2(f[u * D + j], f[u * D + j]), acc[j]);
+        }
       }
-      p0 = p1;
+      // end of a cloud part: the G point groups, added in group order, into
+      // slot (c, b - bfirst)
+      const int b = int(bs / a.n);
+      if (ns >= r1 || ns / a.n != b) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          red[(g * a.fb + tid % a.fb) * 2 * D + 2 * j] = acc[j].x;
+          red[(g * a.fb + tid % a.fb) * 2 * D + 2 * j + 1] = acc[j].y;
+          acc[j] = make_float2(0.f, 0.f);
+        }
+        __syncthreads();
+        float* slot = a.part + (int64_t(c) * a.K + (b - bfirst)) * r * d;
+        for (int e = tid; e < a.fb * 2 * d; e += kThreads) {
+          const int kk = e / (2 * d), rem = e - kk * 2 * d, t = rem / d, j = rem - t * d;
+          const int kg = fbk * a.fb + kk;
+          if (kg >= a.m) continue;
+          float sum = 0.0f;
+          for (int gg = 0; gg < G; ++gg) sum += red[(gg * a.fb + kk) * 2 * D + 2 * j + t];
+          slot[(2 * kg + t) * d + j] = sum;
+        }
+      }
+      __syncthreads();  // this buffer (and red) is rewritten next
+      bs = ns;
+      be = ne;
     }
   }
   stamp(a.trace, 1);
@@ -228,11 +257,34 @@ integrate_small_kernel(const SmallArgs a) {
 
   if (!a.fuse_a7) {
     // ---------------------------------------------- phase 2: S (fp64, fixed order)
+    // one warp per element (cloud b, row, j): lane l sums the slots of ranges
+    // c0 + l, c0 + l + 32, ... in order (8 loads in flight), then the lane sums
+    // in lane order
     const int64_t E = int64_t(a.batch) * r * d;
-    for (int64_t e = int64_t(blockIdx.x) * kThreads + tid; e < E; e += int64_t(gridDim.x) * kThreads) {
+    const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
+    for (int64_t e = int64_t(blockIdx.x) * (kThreads / 32) + warp; e < E; e += warps) {
       const int b = int(e / (int64_t(r) * d));
       const int rem = int(e - int64_t(b) * r * d);
-      a.S[e] = sum_slots(a, b, rem / d, rem % d);
+      const int64_t lo = int64_t(b) * a.n, hi = lo + a.n;
+      const int c0 = int(lo / a.L), c1 = int((hi - 1) / a.L);
+      double acc = 0.0;
+      auto slot = [&](int c) {
+        const int kk = b - int((int64_t(c) * a.L) / a.n);
+        return __ldg(a.part + (int64_t(c) * a.K + kk) * r * d + rem);
+      };
+      int cc = c0 + lane;
+      for (; cc + 7 * 32 <= c1; cc += 8 * 32) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = slot(cc + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += double(v[u]);
+      }
+      for (; cc <= c1; cc += 32) acc += double(slot(cc));
+      double tot = 0.0;
+#pragma unroll
+      for (int l = 0; l < 32; ++l) tot += __shfl_sync(0xffffffffu, acc, l);
+      if (lane == 0) a.S[e] = tot;
     }
     grid_sync(a.bar);
     stamp(a.trace, 3);
@@ -426,13 +478,13 @@ cudaError_t launch_d(const SmallArgs& a, int grid, size_t smem, cudaStream_t s) 
 
 int frequency_block(int m) { return m <= 32 ? 32 : (m <= 64 ? 64 : (m <= 128 ? 128 : 256)); }
 
-// Phase-1 ranges: about 1024 points each, at most what is co-resident (small
+// Phase-1 ranges: >= 256 points each, at most what is co-resident (small
 // clouds get few CTAs: cheaper grid barriers; large ones the whole GPU);
 // K = partial slots per range (the clouds one range can touch).
 void small_geometry(int m, int64_t n, int batch, int cap, int* R, int64_t* L, int* K) {
   const int nfb = (m + frequency_block(m) - 1) / frequency_block(m);
   const int64_t ntot = n * batch;
-  int64_t r = (ntot + 1023) / 1024;
+  int64_t r = (ntot + 255) / 256;
   if (r * nfb > cap) r = cap / nfb;
   if (r < 1) r = 1;
   *L = ((ntot + r - 1) / r + 3) & ~int64_t(3);
@@ -444,7 +496,7 @@ void small_geometry(int m, int64_t n, int batch, int cap, int* R, int64_t* L, in
 
 size_t smem_bytes(int m, int D) {
   const int mp = (m + 3) & ~3;
-  const size_t s1 = (size_t(3 + D) * kBatchPts + size_t(kThreads) * 2 * D) * sizeof(float);
+  const size_t s1 = (size_t(2) * (4 + D) * kBatchPts + size_t(kThreads) * 2 * D) * sizeof(float);
   const size_t s4 = (size_t(3) * mp + size_t(mp) * 2 * D + 2 * D) * sizeof(float) +
                     size_t(2 * m) * D * 5 * sizeof(double);
   return s1 > s4 ? s1 : s4;
@@ -505,7 +557,7 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
   a.L4 = (ntot + grid - 1) / grid;
   // a7 in phase 4's prologue for small r (each CTA redoes it for the clouds it
   // touches): two grid barriers fewer
-  a.fuse_a7 = (2 * m <= 128) ? 1 : 0;
+  a.fuse_a7 = (2 * m <= 128 && (n + a.L - 1) / a.L + 1 <= 16) ? 1 : 0;
   cudaError_t e = cudaSuccess;
   switch (D) {
     case 1: e = launch_d<1>(a, grid, smem, s); break;
