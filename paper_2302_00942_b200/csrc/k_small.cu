@@ -77,8 +77,14 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar) {
       bar[1] = 0u;
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     } else {
-      while (ld_acquire(bar) == my) {
-      }
+      // relaxed polling with a short back-off (hundreds of CTAs polling one
+      // word with acquire loads slow the release down), then one acquire fence
+      unsigned int v;
+      do {
+        __nanosleep(40);
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      } while (v == my);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
   }
   __syncthreads();
@@ -113,6 +119,7 @@ __device__ __forceinline__ void stamp(unsigned long long* tr, int i) {
   }
 }
 __device__ unsigned long long g_small_trace[8];
+__device__ unsigned long long g_small_p1end[1024];  // trace: each CTA's end of phase 1
 
 // S[b][row][j] = sum over the ranges overlapping cloud b, in range order, of
 // their slot for b (fp64).  Range c overlaps b iff [cL, cL+L) meets [bn, bn+n).
@@ -252,6 +259,11 @@ integrate_small_kernel(const SmallArgs a) {
     }
   }
   stamp(a.trace, 1);
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_small_p1end[blockIdx.x] = t;
+  }
   grid_sync(a.bar);
   stamp(a.trace, 2);
 
@@ -566,9 +578,17 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
     default: e = launch_d<4>(a, grid, smem, s); break;
   }
   if (trace && e == cudaSuccess) {
-    unsigned long long h[8];
+    unsigned long long h[8], pe[1024];
     cudaStreamSynchronize(s);
     cudaMemcpyFromSymbol(h, g_small_trace, sizeof(h));
+    cudaMemcpyFromSymbol(pe, g_small_p1end, sizeof(pe));
+    unsigned long long mx = 0, mn = ~0ull;
+    for (int i = 0; i < grid && i < 1024; ++i) {
+      mx = pe[i] > mx ? pe[i] : mx;
+      mn = pe[i] < mn ? pe[i] : mn;
+    }
+    fprintf(stderr, "  phase-1 end over CTAs: first %.1f us, last %.1f us after start\n",
+            (mn - h[0]) * 1e-3, (mx - h[0]) * 1e-3);
     fprintf(stderr, "small n=%lld batch=%d m=%d d=%d grid=%d slots=%d fuse=%d: phase1 %.1f us, "
             "sync %.1f, S %.1f, Y %.1f, phase4 %.1f (total %.1f)\n", (long long)n, batch, m, d, grid,
             a.K, a.fuse_a7, (h[1] - h[0]) * 1e-3, (h[2] - h[1]) * 1e-3, (h[3] - h[2]) * 1e-3,
