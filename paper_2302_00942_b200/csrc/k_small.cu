@@ -103,7 +103,7 @@ struct SmallArgs {
   const float* F;        // (batch x) n x d
   float* out;            // same shape (may alias F)
   const double* C;       // batch x r x r
-  float* part;           // R x K x r x d: slot (range c, its k-th cloud)
+  float* part;           // K x r x d x R: slot (range c, its k-th cloud) at [(k r d + e) R + c]
   double* S;             // batch x r x d
   float* Y;              // batch x r x d
   unsigned int* bar;     // kBarWords words, zero before the first launch
@@ -120,6 +120,8 @@ __device__ __forceinline__ void stamp(unsigned long long* tr, int i) {
 }
 __device__ unsigned long long g_small_trace[8];
 __device__ unsigned long long g_small_p1end[1024];  // trace: each CTA's end of phase 1
+__device__ unsigned long long g_small_p1beg[1024];  // trace: each CTA's start
+__device__ unsigned int g_small_smid[1024];
 
 // S[b][row][j] = sum over the ranges overlapping cloud b, in range order, of
 // their slot for b (fp64).  Range c overlaps b iff [cL, cL+L) meets [bn, bn+n).
@@ -130,7 +132,7 @@ __device__ __forceinline__ double sum_slots(const SmallArgs& a, int b, int row, 
   double acc = 0.0;
   for (int c = c0; c <= c1; ++c) {
     const int k = b - int((int64_t(c) * a.L) / a.n);
-    acc += double(__ldg(a.part + ((int64_t(c) * a.K + k) * r + row) * a.d + j));
+    acc += double(__ldg(a.part + ((int64_t(k) * r + row) * a.d + j) * a.R + c));
   }
   return acc;
 }
@@ -144,6 +146,14 @@ integrate_small_kernel(const SmallArgs a) {
   const int d = a.d;
   const int64_t ntot = int64_t(a.batch) * a.n;
   stamp(a.trace, 0);
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
+    unsigned long long t;
+    unsigned int sid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sid));
+    g_small_p1beg[blockIdx.x] = t;
+    g_small_smid[blockIdx.x] = sid;
+  }
 
   // ------------------------------------------------ phase 1: S partials
   // CTA = (range c, frequency block f): the range's points in batches of <= 512
@@ -243,14 +253,14 @@ integrate_small_kernel(const SmallArgs a) {
           acc[j] = make_float2(0.f, 0.f);
         }
         __syncthreads();
-        float* slot = a.part + (int64_t(c) * a.K + (b - bfirst)) * r * d;
+        float* slot = a.part + int64_t(b - bfirst) * r * d * a.R + c;  // element e at slot[e R]
         for (int e = tid; e < a.fb * 2 * d; e += kThreads) {
           const int kk = e / (2 * d), rem = e - kk * 2 * d, t = rem / d, j = rem - t * d;
           const int kg = fbk * a.fb + kk;
           if (kg >= a.m) continue;
           float sum = 0.0f;
           for (int gg = 0; gg < G; ++gg) sum += red[(gg * a.fb + kk) * 2 * D + 2 * j + t];
-          slot[(2 * kg + t) * d + j] = sum;
+          slot[int64_t((2 * kg + t) * d + j) * a.R] = sum;
         }
       }
       __syncthreads();  // this buffer (and red) is rewritten next
@@ -280,9 +290,9 @@ integrate_small_kernel(const SmallArgs a) {
       const int64_t lo = int64_t(b) * a.n, hi = lo + a.n;
       const int c0 = int(lo / a.L), c1 = int((hi - 1) / a.L);
       double acc = 0.0;
-      auto slot = [&](int c) {
+      auto slot = [&](int c) {  // consecutive lanes: consecutive ranges (coalesced)
         const int kk = b - int((int64_t(c) * a.L) / a.n);
-        return __ldg(a.part + (int64_t(c) * a.K + kk) * r * d + rem);
+        return __ldg(a.part + (int64_t(kk) * r * d + rem) * a.R + c);
       };
       int cc = c0 + lane;
       for (; cc + 7 * 32 <= c1; cc += 8 * 32) {
@@ -561,6 +571,7 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
     return e && e[0] == '1';
   }();
   if (trace) cudaGetSymbolAddress(reinterpret_cast<void**>(&a.trace), g_small_trace);
+
   const int D = dclass(d);
   const size_t smem = smem_bytes(m, D);
   small_geometry(m, n, batch, cap_for(m, d, sms), &a.R, &a.L, &a.K);
@@ -582,13 +593,41 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
     cudaStreamSynchronize(s);
     cudaMemcpyFromSymbol(h, g_small_trace, sizeof(h));
     cudaMemcpyFromSymbol(pe, g_small_p1end, sizeof(pe));
-    unsigned long long mx = 0, mn = ~0ull;
+    unsigned long long pb[1024];
+    unsigned int sm[1024];
+    cudaMemcpyFromSymbol(pb, g_small_p1beg, sizeof(pb));
+    cudaMemcpyFromSymbol(sm, g_small_smid, sizeof(sm));
+    unsigned long long mx = 0, mn = ~0ull, bmx = 0, bmn = ~0ull, dmx = 0, dmn = ~0ull;
+    int per_sm[256] = {0};
     for (int i = 0; i < grid && i < 1024; ++i) {
       mx = pe[i] > mx ? pe[i] : mx;
       mn = pe[i] < mn ? pe[i] : mn;
+      bmx = pb[i] > bmx ? pb[i] : bmx;
+      bmn = pb[i] < bmn ? pb[i] : bmn;
+      const unsigned long long du = pe[i] - pb[i];
+      dmx = du > dmx ? du : dmx;
+      dmn = du < dmn ? du : dmn;
+      if (sm[i] < 256) per_sm[sm[i]]++;
     }
-    fprintf(stderr, "  phase-1 end over CTAs: first %.1f us, last %.1f us after start\n",
-            (mn - h[0]) * 1e-3, (mx - h[0]) * 1e-3);
+    int cmin = 1 << 30, cmax = 0;
+    for (int i = 0; i < sms; ++i) {
+      cmin = per_sm[i] < cmin ? per_sm[i] : cmin;
+      cmax = per_sm[i] > cmax ? per_sm[i] : cmax;
+    }
+    double lo_sum = 0, hi_sum = 0, lo_max = 0, hi_max = 0;
+    int lo_n = 0, hi_n = 0;
+    for (int i = 0; i < grid && i < 1024; ++i) {
+      const double du = (pe[i] - pb[i]) * 1e-3;
+      if (sm[i] < unsigned(sms / 2)) { lo_sum += du; ++lo_n; lo_max = du > lo_max ? du : lo_max; }
+      else { hi_sum += du; ++hi_n; hi_max = du > hi_max ? du : hi_max; }
+    }
+    fprintf(stderr, "  SMs < %d: mean %.1f max %.1f us (%d CTAs); SMs >= %d: mean %.1f max %.1f us (%d)\n",
+            sms / 2, lo_sum / (lo_n ? lo_n : 1), lo_max, lo_n, sms / 2, hi_sum / (hi_n ? hi_n : 1),
+            hi_max, hi_n);
+    fprintf(stderr, "  phase-1 end over CTAs: first %.1f us, last %.1f us after start; CTA starts "
+            "%.1f..%.1f us; own durations %.1f..%.1f us; CTAs per SM %d..%d\n",
+            (mn - h[0]) * 1e-3, (mx - h[0]) * 1e-3, (bmn - h[0]) * 1e-3, (bmx - h[0]) * 1e-3,
+            dmn * 1e-3, dmx * 1e-3, cmin, cmax);
     fprintf(stderr, "small n=%lld batch=%d m=%d d=%d grid=%d slots=%d fuse=%d: phase1 %.1f us, "
             "sync %.1f, S %.1f, Y %.1f, phase4 %.1f (total %.1f)\n", (long long)n, batch, m, d, grid,
             a.K, a.fuse_a7, (h[1] - h[0]) * 1e-3, (h[2] - h[1]) * 1e-3, (h[3] - h[2]) * 1e-3,
