@@ -239,10 +239,13 @@ void dfree(T*& ptr, cudaStream_t s) {
   ptr = nullptr;
 }
 
-void free_plan(rfd_plan* p) {
+// sync = false: every free is stream-ordered on the plan's stream (pool
+// memory: cudaFreeAsync), streams and events are destroyed deferred by the
+// driver -- nothing waits on the host (rfd_gfi_host's internal plans).
+void free_plan(rfd_plan* p, bool sync = true) {
   if (!p) return;
   cudaStream_t s = p->stream;
-  cudaStreamSynchronize(s);
+  if (sync) cudaStreamSynchronize(s);
   dfree(p->pts, s);
   dfree(p->pts16, s);
   dfree(p->centre, s);
@@ -876,7 +879,7 @@ rfd_status rfd_gfi_host(const float* points, int64_t n, double eps, double lambd
   struct StubGuard {
     rfd_plan* s;
     ~StubGuard() {
-      if (s) free_plan(s);
+      if (s) free_plan(s, false);
     }
   } sg{stub};
   stub->stream = st;
@@ -914,8 +917,7 @@ rfd_status rfd_gfi_host(const float* points, int64_t n, double eps, double lambd
   for (int i = 0; i < 2 * kPipeChunks + 2; ++i) std::swap(p->ev[i], stub->ev[i]);
   rs = integrate_host_pipelined(p, F_host, d, out_host, true, st);
   if (rs != RFD_OK || !plan_out) {
-    cudaStreamSynchronize(st);
-    rfd_destroy(p);
+    free_plan(p, false);  // stream-ordered: the host does not wait for the step
   } else {
     *plan_out = p;
   }
