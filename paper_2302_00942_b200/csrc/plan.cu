@@ -738,6 +738,29 @@ rfd_status barycenter_impl(rfd_plan* p, const float* mu_in, const float* area,
     return fail(RFD_EINVAL, "mu, area and out must be device pointers");
   p->stream = st;
   const int64_t n = p->n;
+  const char* fe = getenv("RFD_BARY_FUSED");  // "0": the unfused path (tests compare the two)
+  const bool no_fused = fe && fe[0] == '0';
+  if (!no_fused && p->m <= 32 && k <= 4 && n <= rfd::bary_fused_max_points(p->sms)) {
+    // the whole loop in one launch, feature rows cached on chip (k_bary_fused.cu)
+    TempBuffers tmp(st);
+    const int ctas = int((n + 511) / 512);
+    double *part = nullptr, *S = nullptr, *red = nullptr;
+    int* status = nullptr;
+    RFD_CUDA(tmp.alloc(&part, size_t(ctas) * p->r * k));
+    RFD_CUDA(tmp.alloc(&S, size_t(p->r) * k));
+    RFD_CUDA(tmp.alloc(&red, size_t(2) * ctas));
+    RFD_CUDA(tmp.alloc(&status, size_t(2)));
+    RFD_CUDA(cudaMemsetAsync(status, 0, 2 * sizeof(int), st));
+    RFD_CUDA(rfd::launch_bary_fused(p->pts, p->omega_rad4, p->C, mu_in, area, alpha, p->m, k, n,
+                                    max_iter, tol, part, S, red, p->bar, status, out, st));
+    int hs[2] = {0, 0};
+    RFD_CUDA(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    RFD_CUDA(cudaStreamSynchronize(st));
+    if (hs[0])
+      return fail(RFD_ERANGE, "barycenter: non-finite iterate at iteration " + std::to_string(hs[1]));
+    if (iters_out) *iters_out = hs[1];
+    return RFD_OK;
+  }
   const size_t nk = size_t(n) * k;
   const int nb = rfd::bary_blocks(n);
   TempBuffers tmp(st);

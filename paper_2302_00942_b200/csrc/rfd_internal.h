@@ -153,6 +153,22 @@ void launch_bary_step2(const float* area, const float* Y, const double* alpha, c
 void launch_bary_finish(const float* area, const double* mu, int64_t n, double* part, double* mass,
                         float* out, cudaStream_t s);
 
+// NEXT-1 fused (k_bary_fused.cu): the whole Alg. 1 loop in one cooperative
+// launch for m <= 32, k <= 4, n <= bary_fused_max_points(sms) (each CTA's
+// feature rows cached in shared memory).  part: ceil(n/512) x r x k fp64,
+// S: r x k, red: 2 ceil(n/512), bar: 2 words (zero), status: [0] non-finite
+// flag (zero before), [1] iterations run.
+struct Alpha16 {
+  double v[16];
+};
+size_t bary_fused_smem(int m, int k);
+int64_t bary_fused_max_points(int sms);
+cudaError_t launch_bary_fused(const float4* pts, const float4* omega4, const double* C,
+                              const float* mu_in, const float* area, const double* alpha, int m,
+                              int k, int64_t n, int max_iter, double tol, double* part, double* S,
+                              double* red, unsigned int* bar, int* status, float* out,
+                              cudaStream_t s);
+
 // ---------------------------------------------------------------- passes
 // S[b][2m][d] fp64 = fixed-order sum of the `chunks` range partials of
 // columns [c0, c0+dc) (partial[b][chunk][2m][dc] fp32, interleaved features).
