@@ -79,6 +79,7 @@ struct BaryArgs {
   double* part;          // gridDim x (r x k) CTA partials (fp64)
   double* S;             // r x k
   double* red;           // gridDim x 2: per-CTA delta / mass partials
+  double* smax;          // gridDim x 4: per-CTA column maxima of the next input
   unsigned int* bar;     // 2 words (generation, count)
   int* status;           // [0] non-finite flag, [1] iterations run
   float* out;            // n
@@ -95,6 +96,8 @@ __global__ void __launch_bounds__(kThreads, 1) bary_fused_kernel(const BaryArgs 
   double* yq = wpart + 8 * r * K;                     // [4][r][K] Y quarters
   __shared__ double redw[8][2];
   __shared__ double bcast[2];
+  __shared__ double redm[8][K];
+  __shared__ double scs[K];
 
   const int64_t pbase = int64_t(blockIdx.x) * kPts;
   const int64_t ip[2] = {pbase + tid, pbase + tid + kThreads};
@@ -131,10 +134,65 @@ __global__ void __launch_bounds__(kThreads, 1) bary_fused_kernel(const BaryArgs 
     for (int i = 0; i < K; ++i) {
       v[q][i] = 1.0;
       mui[q][i] = (ok[q] && i < a.k) ? __ldg(a.mu_in + int64_t(i) * a.n + ip[q]) : 0.0f;
-      X[q][i] = (i < a.k) ? float(double(ar[q]) * v[q][i]) : 0.0f;  // a v (v = 1)
     }
   }
   __syncthreads();
+
+  // The next FM_K input X = fp32(az sc), az = a v or a w (fp64), sc a power of
+  // two per column putting the column maximum in [1/2, 1) -- exact by
+  // linearity (FM_K(az) = FM_K(X) / sc), it keeps fp32 in range (v and w can
+  // grow by 1e30 per iteration where the clamp binds).  One grid barrier.
+  double sc[K];
+  auto set_inputs = [&](const double (&az)[2][K]) {
+    double mx[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      mx[i] = fmax(ok[0] ? fabs(az[0][i]) : 0.0, ok[1] ? fabs(az[1][i]) : 0.0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx[i] = fmax(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], o));
+      if (lane == 0) redm[warp][i] = mx[i];
+    }
+    __syncthreads();
+    if (tid < K) {
+      double m8 = 0.0;
+      for (int w8 = 0; w8 < 8; ++w8) m8 = fmax(m8, redm[w8][tid]);
+      a.smax[4 * blockIdx.x + tid] = m8;
+    }
+    grid_sync(a.bar);
+    if (warp == 0) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        double m = 0.0;
+        for (int c = lane; c < int(gridDim.x); c += 32) m = fmax(m, a.smax[4 * c + i]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) {
+          double sv = 1.0;
+          if (isfinite(m) && m > 0.0) {
+            int e = 0;
+            frexp(m, &e);
+            sv = ldexp(1.0, -e);
+          }
+          scs[i] = sv;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      sc[i] = scs[i];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) X[q][i] = (ok[q] && i < a.k) ? float(az[q][i] * sc[i]) : 0.0f;
+    }
+  };
+  {
+    double az[2][K];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int i = 0; i < K; ++i) az[q][i] = double(ar[q]);  // a v, v = 1
+    set_inputs(az);
+  }
 
   // S partial of the CTA for the current X (pass 1 on the cached rows), then
   // grid-wide S, then Y = C^ S in every CTA's shared memory
@@ -242,15 +300,16 @@ __global__ void __launch_bounds__(kThreads, 1) bary_fused_kernel(const BaryArgs 
     float o[2][K];
     // 1. w^i = mu^i / FM_K(a v^i); the next input a w^i
     apply_out(o);
-    double w[2][K];
+    double aw[2][K];
 #pragma unroll
     for (int q = 0; q < 2; ++q)
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        w[q][i] = double(mui[q][i]) / fmax(double(o[q][i]), kClamp);
-        X[q][i] = (ok[q] && i < a.k) ? float(double(ar[q]) * w[q][i]) : 0.0f;
-        bad |= !isfinite(X[q][i]);
+        const double w = double(mui[q][i]) / fmax(double(o[q][i]) / sc[i], kClamp);
+        aw[q][i] = double(ar[q]) * w;
+        bad |= !isfinite(w);
       }
+    set_inputs(aw);
     apply_S();
     // 2. d^i = v^i FM_K(a w^i); 3. mu = prod_i (d^i)^alpha_i; 4. v^i = v^i mu / d^i;
     // the next input a v^i
@@ -263,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) bary_fused_kernel(const BaryArgs 
 #pragma unroll
       for (int i = 0; i < K; ++i)
         if (i < a.k) {
-          dd[i] = fmax(v[q][i] * double(o[q][i]), kClamp);
+          dd[i] = fmax(v[q][i] * (double(o[q][i]) / sc[i]), kClamp);
           lg += a.alpha.v[i] * log(dd[i]);
         }
       const double mn = exp(lg);
@@ -271,8 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) bary_fused_kernel(const BaryArgs 
       for (int i = 0; i < K; ++i)
         if (i < a.k) {
           v[q][i] = v[q][i] * mn / dd[i];
-          X[q][i] = float(double(ar[q]) * v[q][i]);
-          bad |= !isfinite(v[q][i]) || !isfinite(X[q][i]);
+          bad |= !isfinite(v[q][i]);
         }
       bad |= !isfinite(mn);
       dl += fabs(mn - mu[q]);
@@ -288,6 +346,14 @@ __global__ void __launch_bounds__(kThreads, 1) bary_fused_kernel(const BaryArgs 
       double s = 0.0;
       for (int w8 = 0; w8 < 8; ++w8) s += redw[w8][0];
       a.red[2 * blockIdx.x] = s;
+    }
+    {
+      double av[2][K];
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int i = 0; i < K; ++i) av[q][i] = double(ar[q]) * v[q][i];
+      set_inputs(av);
     }
     apply_S();  // (its grid barriers publish the delta partials and the flag)
     if (tid == 0) {
@@ -368,6 +434,8 @@ cudaError_t launch_bary_fused(const float4* pts, const float4* omega4, const dou
                               double* red, unsigned int* bar, int* status, float* out,
                               cudaStream_t s) {
   LaunchScope L("rfd_bary_fused", s);
+  // (red holds 2 per CTA for the delta / mass partials, then 4 per CTA for the
+  // input column maxima)
   BaryArgs a{};
   a.pts = pts;
   a.omega4 = omega4;
@@ -383,6 +451,7 @@ cudaError_t launch_bary_fused(const float4* pts, const float4* omega4, const dou
   a.part = part;
   a.S = S;
   a.red = red;
+  a.smax = red + 2 * ((n + kPts - 1) / kPts);
   a.bar = bar;
   a.status = status;
   a.out = out;
