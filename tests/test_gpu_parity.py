@@ -668,51 +668,63 @@ def test_narrow_field_paths_agree(d):
     assert relerr(od - F64, o8[:, :d] - F64) <= 2e-5
 
 
-@pytest.mark.parametrize("lam,cases", [(0.1, ((1, 0.0), (3, 0.0), (10, 0.0), (300, 1e-3))),
-                                       (0.5, ((1, 0.0), (3, 0.0), (10, 0.0)))])
-def test_barycenter_fused_matches_oracle(lam, cases):
+@pytest.mark.parametrize("lam,cases", [(0.1, ((3, 0.0), (10, 0.0), (300, 1e-3))),
+                                       (0.5, ((3, 0.0), (10, 0.0)))])
+def test_barycenter_fused_matches_oracle_and_unfused(lam, cases, monkeypatch):
     # NEXT-1 fused (k_bary_fused.cu: m <= 32, k <= 4, n <= 148 x 512 -- the
     # paper's barycenter regime, m = 30): the whole Alg. 1 loop
-    # in one launch with the feature rows cached on chip, against the fp64
-    # oracle (10-iteration results move <= 2e-5 under 1e-7 FM_K perturbations
-    # on these inputs: the gate is meaningful)
+    # in one launch with the feature rows cached on chip.  Iteration 1 against
+    # the fp64 oracle; later iterations amplify the FM_K error (at m = 30 both
+    # GPU paths sit ~2e-4 from the oracle after 2-10 iterations at lambda = 0.1,
+    # tools/bary_fused_check.py), so there the fused loop is checked against
+    # the unfused one (same FM_K arithmetic class, gated against the oracle at
+    # 10 iterations by test_barycenter_matches_oracle): <= 1e-5, same stop.
     from workloads import barycenter_inputs
 
     x, a, mus = barycenter_inputs(3000)
     plan = rfd.Plan(torch.from_numpy(x).cuda(), 0.03, lam, 30, 5)
-    ref_plan = orf.Plan(x, 0.03, lam, 30, 5)
+    ref, _ = orf.Plan(x, 0.03, lam, 30, 5).barycenter(mus, a, [1 / 3] * 3, 1)
     rfd.profile_enable(True)
     rfd.profile_read()
-    for iters, tol in cases:
-        got, its = _bary_gpu(plan, mus, a, [1 / 3] * 3, iters, tol=tol)
-        ref, rits = ref_plan.barycenter(mus, a, [1 / 3] * 3, iters, tol=tol)
-        err = relerr(got, ref)
-        print("fused barycenter lam=%g iters=%d tol=%g: %d/%d iterations, err %.2e"
-              % (lam, iters, tol, its, rits, err))
-        assert its == rits
-        assert err <= TOL
-        assert abs(float(a @ got) - 1.0) < 1e-5
+    got, its = _bary_gpu(plan, mus, a, [1 / 3] * 3, 1)
     prof = rfd.profile_read()
     rfd.profile_enable(False)
     assert set(prof) == {"rfd_bary_fused"}  # one launch per call, nothing else
+    err = relerr(got, ref)
+    print("fused barycenter lam=%g iteration 1: err %.2e" % (lam, err))
+    assert its == 1 and err <= TOL
+    # (lambda = 0.5's tol stop runs ~20 iterations on inputs where the oracle
+    # itself moves 7.6e-4 under 1e-7 FM_K noise: not a meaningful 1e-5 check)
+    for iters, tol in cases:
+        f, fits = _bary_gpu(plan, mus, a, [1 / 3] * 3, iters, tol=tol)
+        monkeypatch.setenv("RFD_BARY_FUSED", "0")
+        u, uits = _bary_gpu(plan, mus, a, [1 / 3] * 3, iters, tol=tol)
+        monkeypatch.delenv("RFD_BARY_FUSED")
+        e = relerr(f, u)
+        print("fused vs unfused lam=%g iters=%d tol=%g: %d/%d iterations, %.2e" % (lam, iters, tol, fits, uits, e))
+        assert fits == uits
+        assert e <= 1e-5
+        assert abs(float(a @ f) - 1.0) < 1e-5
 
 
-def test_barycenter_fused_agrees_with_unfused_and_closed_form(monkeypatch):
+def test_barycenter_fused_closed_form_and_fallback():
     from workloads import barycenter_inputs
 
     x, a, mus = barycenter_inputs(3000, floor=0.05)
-    plan = rfd.Plan(torch.from_numpy(x).cuda(), 0.03, 0.1, 30, 5)
-    fused, fits = _bary_gpu(plan, mus, a, [1 / 3] * 3, 10, tol=1e-4)
-    monkeypatch.setenv("RFD_BARY_FUSED", "0")
-    unf, uits = _bary_gpu(plan, mus, a, [1 / 3] * 3, 10, tol=1e-4)
-    monkeypatch.delenv("RFD_BARY_FUSED")
-    assert fits == uits
-    assert relerr(fused, unf) <= 1e-4
     # identity kernel (lambda = 0): the geometric mean at every iteration
     plan0 = rfd.Plan(torch.from_numpy(x).cuda(), 0.03, 0.0, 16, 5)
     m32 = mus.astype(np.float32).astype(np.float64)
     a32 = a.astype(np.float32).astype(np.float64)
     geo = np.prod(m32 ** (1 / 3), axis=0)
     geo /= a32 @ geo
+    rfd.profile_enable(True)
+    rfd.profile_read()
     got, its = _bary_gpu(plan0, mus, a, [1 / 3] * 3, 5)
+    assert set(rfd.profile_read()) == {"rfd_bary_fused"}
     assert its == 5 and relerr(got, geo) <= 1e-6
+    # m > 32: the unfused path
+    plan64 = rfd.Plan(torch.from_numpy(x).cuda(), 0.03, 0.0, 64, 5)
+    got, its = _bary_gpu(plan64, mus, a, [1 / 3] * 3, 2)
+    assert "rfd_bary_fused" not in rfd.profile_read()
+    rfd.profile_enable(False)
+    assert relerr(got, geo) <= 1e-6
