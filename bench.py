@@ -495,13 +495,29 @@ def config_legs(args, pk):
         pmed = timed(mk, 5)[0]
         plan = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"])
         med, p10, p90 = timed(lambda: plan.integrate(Fd, out=od), 200)
+        # the same calls captured in a CUDA graph (20 per replay): device time
+        # without the per-call host cost (ctypes + launch) that bounds the
+        # plain loop for these sizes
+        s2 = torch.cuda.Stream()
+        s2.wait_stream(stream)
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s2):
+            plan.integrate(Fd, out=od, stream=s2)
+            with torch.cuda.graph(gr, stream=s2):
+                for _ in range(20):
+                    plan.integrate(Fd, out=od, stream=s2)
+        torch.cuda.synchronize()
+        gmed = timed(gr.replay, 20)[0] / 20
         N, m, d = p["n"], p["m"], p["d"]
         rl = roof(N, m, d)
         out["cfg%d" % cfg] = {"integrate_us": med * 1e3, "p10_us": p10 * 1e3, "p90_us": p90 * 1e3,
-                              "value": N * d / (med * 1e-3), "unit": UNIT,
-                              "strict_roofline_us": rl * 1e3, "strict_roofline_frac": rl / med,
-                              "plan_create_ms": pmed}
+                              "graph_us": gmed * 1e3,
+                              "value": N * d / (gmed * 1e-3), "unit": UNIT,
+                              "strict_roofline_us": rl * 1e3, "strict_roofline_frac": rl / gmed,
+                              "plan_create_ms": pmed,
+                              "path": "rfd_integrate_small (d <= 4: one cooperative launch)"}
         plan.close()
+        del gr
     # cfg 3: 50 applications back to back on device-resident vectors
     p, x, V = make_config(3)
     xd = torch.from_numpy(x).cuda()
@@ -574,6 +590,36 @@ def config_legs(args, pk):
     except rfd.RFDError as e:  # the iteration can leave fp32 range on this cloud
         out["cfg5_barycenter"] = {"error": str(e)}
     plan.reparam(p["eps"], p["lam"])
+    # NEXT-1 in the paper's regime (Table 2: meshes of 5k-19k nodes, m = 30,
+    # k = 3, lambda = 0.5): the fused loop (one
+    # launch, features cached on chip) vs the unfused one, per iteration
+    from workloads import barycenter_inputs
+    xb, ab, musb = barycenter_inputs(18944)
+    pb = rfd.Plan(torch.from_numpy(xb).cuda(), 0.03, 0.5, 30, 5)
+    mb = torch.from_numpy(musb.astype(np.float32)).cuda()
+    abd = torch.from_numpy(ab.astype(np.float32)).cuda()
+
+    def per_iter():
+        ts = []
+        for iters in (2, 22):
+            pb.barycenter(mb, abd, [1 / 3] * 3, iters)
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            pb.barycenter(mb, abd, [1 / 3] * 3, iters)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(ev0.elapsed_time(ev1))
+        return (ts[1] - ts[0]) / 20
+    fused_ms = per_iter()
+    os.environ["RFD_BARY_FUSED"] = "0"
+    unfused_ms = per_iter()
+    del os.environ["RFD_BARY_FUSED"]
+    out["paper_barycenter"] = {"n": 18944, "m": 30, "k": 3, "lambda": 0.5,
+                               "fused_ms_per_iteration": fused_ms,
+                               "unfused_ms_per_iteration": unfused_ms,
+                               "note": "rfd_barycenter on 18,944 sphere points (Octocat-sized; "
+                                       "synthetic bumps), (t(22 it) - t(2 it)) / 20"}
+    pb.close()
     out["cfg5_d64"] = {"integrate_ms": t64, "value": N * 64 / (t64 * 1e-3), "unit": UNIT,
                        "ms_per_16_columns": t64 / 4, "d16_ms": t_a,
                        "strict_roofline_ms": roof(N, p["m"], 64),
