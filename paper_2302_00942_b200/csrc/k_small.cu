@@ -90,6 +90,9 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar) {
   __syncthreads();
 }
 
+struct SmallArgs;
+__device__ __forceinline__ void sync_all(const SmallArgs& a);
+
 struct SmallArgs {
   const float4* pts;     // batch x n, centred (x, y, z, 0): one array, clouds back to back
   const float4* omega4;  // m: fp32(2 pi omega)
@@ -108,8 +111,16 @@ struct SmallArgs {
   float* Y;              // batch x r x d
   unsigned int* bar;     // kBarWords words, zero before the first launch
   int fuse_a7;           // 1: S and Y per cloud in phase 4's prologue (small r)
+  int local;             // 1: one CTA per cloud (ranges = clouds): no grid barrier at all
   unsigned long long* trace;  // diagnostics (RFD_SMALL_TRACE=1): phase timestamps of CTA 0
 };
+
+// local mode: every CTA reads only what it wrote itself (its cloud's slot),
+// so a CTA barrier orders phase 1's global writes before the reads
+__device__ __forceinline__ void sync_all(const SmallArgs& a) {
+  if (a.local) __syncthreads();
+  else grid_sync(a.bar);
+}
 
 __device__ __forceinline__ void stamp(unsigned long long* tr, int i) {
   if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -122,6 +133,7 @@ __device__ unsigned long long g_small_trace[8];
 __device__ unsigned long long g_small_p1end[1024];  // trace: each CTA's end of phase 1
 __device__ unsigned long long g_small_p1beg[1024];  // trace: each CTA's start
 __device__ unsigned int g_small_smid[1024];
+__device__ unsigned long long g_small_p4end[1024];  // trace: each CTA's end
 
 // S[b][row][j] = sum over the ranges overlapping cloud b, in range order, of
 // their slot for b (fp64).  Range c overlaps b iff [cL, cL+L) meets [bn, bn+n).
@@ -274,7 +286,7 @@ integrate_small_kernel(const SmallArgs a) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_small_p1end[blockIdx.x] = t;
   }
-  grid_sync(a.bar);
+  sync_all(a);
   stamp(a.trace, 2);
 
   if (!a.fuse_a7) {
@@ -308,7 +320,7 @@ integrate_small_kernel(const SmallArgs a) {
       for (int l = 0; l < 32; ++l) tot += __shfl_sync(0xffffffffu, acc, l);
       if (lane == 0) a.S[e] = tot;
     }
-    grid_sync(a.bar);
+    sync_all(a);
     stamp(a.trace, 3);
     // ---------------------------------------------- phase 3: Y = C^ S
     // one warp per (cloud, row a): lanes split the r columns, fixed-order butterfly
@@ -335,7 +347,7 @@ integrate_small_kernel(const SmallArgs a) {
         if (lane == 0 && j < d) a.Y[row * d + j] = float(acc[j]);
       }
     }
-    grid_sync(a.bar);
+    sync_all(a);
   }
   stamp(a.trace, 4);
 
@@ -463,6 +475,11 @@ integrate_small_kernel(const SmallArgs a) {
     }
   }
   stamp(a.trace, 5);
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_small_p4end[blockIdx.x] = t;
+  }
 }
 
 template <int D>
@@ -483,6 +500,16 @@ int max_ctas(size_t smem, int sms) {
 
 template <int D>
 cudaError_t launch_d(const SmallArgs& a, int grid, size_t smem, cudaStream_t s) {
+  if (a.local) {  // independent CTAs: a plain launch, any grid size
+    static bool configured = false;
+    if (!configured && smem > 48 * 1024) {
+      cudaFuncSetAttribute(integrate_small_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(smem));
+      configured = true;
+    }
+    integrate_small_kernel<D><<<grid, kThreads, smem, s>>>(a);
+    return cudaGetLastError();
+  }
   // cooperative (all CTAs co-resident: the grid barriers), via cudaLaunchKernelEx
   // so that the launch can be captured in a CUDA graph
   cudaLaunchConfig_t cfg = {};
@@ -494,7 +521,11 @@ cudaError_t launch_d(const SmallArgs& a, int grid, size_t smem, cudaStream_t s) 
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const bool plain = [] {  // (A/B measurement only: RFD_SMALL_COOP=0)
+    const char* e = getenv("RFD_SMALL_COOP");
+    return e && e[0] == '0';
+  }();
+  cfg.numAttrs = plain ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, integrate_small_kernel<D>, a);
 }
 
@@ -524,6 +555,11 @@ size_t smem_bytes(int m, int D) {
   return s1 > s4 ? s1 : s4;
 }
 
+bool local_mode(int m, int64_t n, int batch, int sms) {
+  if (m > 256) return false;  // one frequency block per CTA
+  return (n <= 1024 && batch == 1) || (n <= 8192 && batch >= 2 * sms / 3);
+}
+
 int dclass(int d) { return d <= 1 ? 1 : (d <= 2 ? 2 : (d <= 3 ? 3 : 4)); }
 
 int cap_for(int m, int d, int sms) {
@@ -542,6 +578,10 @@ size_t small_partial_elems(int m, int64_t n, int batch, int d, int sms) {
   int R, K;
   int64_t L;
   small_geometry(m, n, batch, cap_for(m, d, sms), &R, &L, &K);
+  if (local_mode(m, n, batch, sms)) {
+    R = batch;
+    K = 1;
+  }
   return size_t(R) * size_t(K) * size_t(2 * m) * size_t(d);
 }
 
@@ -574,13 +614,23 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
 
   const int D = dclass(d);
   const size_t smem = smem_bytes(m, D);
-  small_geometry(m, n, batch, cap_for(m, d, sms), &a.R, &a.L, &a.K);
+  // one CTA per cloud when the clouds are small and there are enough of them
+  // to fill the GPU (cfg 3), or for one tiny cloud (cfg 1): no grid barriers
+  a.local = local_mode(m, n, batch, sms) ? 1 : 0;
+  if (a.local) {
+    a.R = batch;
+    a.L = n;
+    a.K = 1;
+  } else {
+    small_geometry(m, n, batch, cap_for(m, d, sms), &a.R, &a.L, &a.K);
+  }
   const int grid = a.R * a.nfb;
   const int64_t ntot = n * batch;
-  a.L4 = (ntot + grid - 1) / grid;
+  a.L4 = a.local ? n : (ntot + grid - 1) / grid;
   // a7 in phase 4's prologue for small r (each CTA redoes it for the clouds it
   // touches): two grid barriers fewer
-  a.fuse_a7 = (2 * m <= 128 && (n + a.L - 1) / a.L + 1 <= 16) ? 1 : 0;
+  a.fuse_a7 = (a.local || (2 * m <= 128 && (n + a.L - 1) / a.L + 1 <= 16)) ? 1 : 0;
+  if (const char* fe = getenv("RFD_SMALL_FUSE")) a.fuse_a7 = fe[0] == '1' ? 1 : 0;  // (A/B only)
   cudaError_t e = cudaSuccess;
   switch (D) {
     case 1: e = launch_d<1>(a, grid, smem, s); break;
@@ -593,8 +643,12 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
     cudaStreamSynchronize(s);
     cudaMemcpyFromSymbol(h, g_small_trace, sizeof(h));
     cudaMemcpyFromSymbol(pe, g_small_p1end, sizeof(pe));
-    unsigned long long pb[1024];
+    unsigned long long pb[1024], p4[1024];
     unsigned int sm[1024];
+    cudaMemcpyFromSymbol(p4, g_small_p4end, sizeof(p4));
+    unsigned long long e4 = 0;
+    for (int i = 0; i < grid && i < 1024; ++i) e4 = p4[i] > e4 ? p4[i] : e4;
+    fprintf(stderr, "  last CTA end: %.1f us after start\n", (e4 - h[0]) * 1e-3);
     cudaMemcpyFromSymbol(pb, g_small_p1beg, sizeof(pb));
     cudaMemcpyFromSymbol(sm, g_small_smid, sizeof(sm));
     unsigned long long mx = 0, mn = ~0ull, bmx = 0, bmn = ~0ull, dmx = 0, dmn = ~0ull;
