@@ -521,11 +521,7 @@ cudaError_t launch_d(const SmallArgs& a, int grid, size_t smem, cudaStream_t s) 
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  static const bool plain = [] {  // (A/B measurement only: RFD_SMALL_COOP=0)
-    const char* e = getenv("RFD_SMALL_COOP");
-    return e && e[0] == '0';
-  }();
-  cfg.numAttrs = plain ? 0 : 1;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, integrate_small_kernel<D>, a);
 }
 
@@ -630,7 +626,6 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
   // a7 in phase 4's prologue for small r (each CTA redoes it for the clouds it
   // touches): two grid barriers fewer
   a.fuse_a7 = (a.local || (2 * m <= 128 && (n + a.L - 1) / a.L + 1 <= 16)) ? 1 : 0;
-  if (const char* fe = getenv("RFD_SMALL_FUSE")) a.fuse_a7 = fe[0] == '1' ? 1 : 0;  // (A/B only)
   cudaError_t e = cudaSuccess;
   switch (D) {
     case 1: e = launch_d<1>(a, grid, smem, s); break;
