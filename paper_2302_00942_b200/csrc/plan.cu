@@ -746,9 +746,9 @@ rfd_status barycenter_impl(rfd_plan* p, const float* mu_in, const float* area,
     const int ctas = int((n + 511) / 512);
     double *part = nullptr, *S = nullptr, *red = nullptr;
     int* status = nullptr;
-    RFD_CUDA(tmp.alloc(&part, size_t(ctas) * p->r * k));
+    RFD_CUDA(tmp.alloc(&part, size_t(2) * ctas * p->r * k));
     RFD_CUDA(tmp.alloc(&S, size_t(p->r) * k));
-    RFD_CUDA(tmp.alloc(&red, size_t(6) * ctas));
+    RFD_CUDA(tmp.alloc(&red, size_t(3) * ctas));
     RFD_CUDA(tmp.alloc(&status, size_t(2)));
     RFD_CUDA(cudaMemsetAsync(status, 0, 2 * sizeof(int), st));
     RFD_CUDA(rfd::launch_bary_fused(p->pts, p->omega_rad4, p->C, mu_in, area, alpha, p->m, k, n,

@@ -155,8 +155,8 @@ void launch_bary_finish(const float* area, const double* mu, int64_t n, double* 
 
 // NEXT-1 fused (k_bary_fused.cu): the whole Alg. 1 loop in one cooperative
 // launch for m <= 32, k <= 4, n <= bary_fused_max_points(sms) (each CTA's
-// feature rows cached in shared memory).  part: ceil(n/512) x r x k fp64,
-// S: r x k, red: 6 ceil(n/512), bar: 2 words (zero), status: [0] non-finite
+// feature rows cached in shared memory).  part: 2 ceil(n/512) x r x k fp64,
+// S: r x k (unused), red: 3 ceil(n/512), bar: 2 words (zero), status: [0] non-finite
 // flag (zero before), [1] iterations run.
 struct Alpha16 {
   double v[16];
