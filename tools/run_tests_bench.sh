@@ -1,5 +1,4 @@
-# GPU suite + full default bench (parity, eps-graph, cpu baseline, e2e) + a
-# 2-rank launch of bench.py on one GPU is NOT done (one GPU only).
+# GPU suite + full default bench (parity, eps-graph, cpu baseline, e2e).
 mkdir -p gpurun_out
 python -c "from paper_2302_00942_b200 import build; build.build()" > gpurun_out/build.log 2>&1
 timeout 180 python -m pytest tests/test_gpu_parity.py -x -q -s -k "config_parity" > gpurun_out/quick_parity.log 2>&1; rc=$?; echo quick rc $rc
