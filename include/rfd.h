@@ -275,6 +275,8 @@ typedef struct {
   int64_t n_total;  /* points of the whole cloud (= n unless sharded) */
   int32_t rank;     /* shard of this plan (0 unless sharded)          */
   int32_t world;    /* shards (1 unless sharded)                      */
+  int64_t gram_nodes; /* a4 went through a spread grid of this many nodes
+                         (0: the direct sum over the points) */
 } rfd_plan_info_t;
 rfd_status rfd_plan_info(const rfd_plan* plan, rfd_plan_info_t* info);
 

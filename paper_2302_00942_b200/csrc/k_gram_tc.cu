@@ -684,7 +684,9 @@ constexpr int kPRingOff = kPStages * int(kPStageBytes);          // 192 KB
 constexpr int kPOmegaOff = kPRingOff + kChunks * int(kChunkBytes);
 constexpr int kPSmemBytes = kPOmegaOff + kMaxFreqs * 16;         // 216 KB
 
-template <bool kTrace>
+// kWeighted: G = sum_p w_p^2 phi(x_p) phi(x_p)^T with w_p in the pad slot of
+// the point layout (the grid Gram of the spread path, k_nufft.cu).
+template <bool kTrace, bool kWeighted = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restrict__ omega4, int m,
                  int64_t n, const __grid_constant__ Sched sc, float* __restrict__ partial) {
@@ -903,12 +905,14 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
       const int cnt = (it == tail_it) ? tail : kStep;
       const float* grp = reinterpret_cast<const float*>(
           ring + (ch % kChunks) * kChunkBytes + (it % kChunkSteps) * kStepBytes + q * kGroupBytes);
-      float X[8], Y[8], Z[8];
+      float X[8], Y[8], Z[8], Wt[8];
 #pragma unroll
       for (int j = 0; j < 8; j += 4) {
         *reinterpret_cast<float4*>(X + j) = *reinterpret_cast<const float4*>(grp + j);
         *reinterpret_cast<float4*>(Y + j) = *reinterpret_cast<const float4*>(grp + 8 + j);
         *reinterpret_cast<float4*>(Z + j) = *reinterpret_cast<const float4*>(grp + 16 + j);
+        if (kWeighted)
+          *reinterpret_cast<float4*>(Wt + j) = *reinterpret_cast<const float4*>(grp + 24 + j);
       }
       const uint32_t stage = sbase + uint32_t(s) * kPStageBytes;
 #pragma unroll
@@ -926,6 +930,13 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
                                                   __fmul2_rn(wx, make_float2(X[j], X[j + 1]))));
           __sincosf(th.x, &sn[j], &c[j]);
           __sincosf(th.y, &sn[j + 1], &c[j + 1]);
+        }
+        if (kWeighted) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            c[j] *= Wt[j];
+            sn[j] *= Wt[j];
+          }
         }
         if (cnt < kStep) {
 #pragma unroll
@@ -1129,8 +1140,10 @@ float* gram_points(const GramGeom& g, int batch, float* partial, int64_t* per_cl
   return partial + gram_tc_partial_only(g, batch);
 }
 
+bool gram_tc_pairs(int m) { return use_pairs(m); }
+
 void launch_gram_tc(const float4* omega4, int m, int64_t n, int batch,
-                    const GramGeom& g, float* partial, double* G, cudaStream_t s) {
+                    const GramGeom& g, float* partial, double* G, cudaStream_t s, bool weighted) {
   const bool pairs = g.tile == 2 * kBlk;
   // same partition as gram_tc_geometry (G = g.chunks CTAs or CTA pairs)
   const Sched sc = pairs ? make_pair_sched(m, n, batch, 2 * g.chunks)
@@ -1143,6 +1156,8 @@ void launch_gram_tc(const float4* omega4, int m, int64_t n, int batch,
                          kPSmemBytes);
     cudaFuncSetAttribute(gram_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kPSmemBytes);
+    cudaFuncSetAttribute(gram_pair_kernel<false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmemBytes);
     const char* e = getenv("RFD_GRAM_TRACE");  // instrumentation only
     trace = e && e[0] == '1';
     configured = true;
@@ -1153,7 +1168,10 @@ void launch_gram_tc(const float4* omega4, int m, int64_t n, int batch,
   if (pairs) {
     {
       LaunchScope L("rfd_gram_tc", s);
-      if (trace) {
+      if (weighted) {
+        gram_pair_kernel<false, true><<<2 * sc.G, kThreads, kPSmemBytes, s>>>(gp, omega4, m, n,
+                                                                              sc, partial);
+      } else if (trace) {
         const char* tc_env = getenv("RFD_GRAM_TRACE_CTA");
         const int tcta = tc_env ? atoi(tc_env) : 0;
         cudaMemcpyToSymbol(g_trace_cta, &tcta, sizeof(int));

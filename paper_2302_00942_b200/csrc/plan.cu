@@ -117,6 +117,7 @@ struct rfd_plan {
   float4* centre = nullptr;   // batch: bounding-box midpoint subtracted from the points
   float4* omega4 = nullptr;   // m
   float4* omega_rad4 = nullptr;  // m: fp32(2 pi omega) for the tensor-core kernels
+  int64_t gram_nodes = 0;        // a4 through a spread grid of this many nodes (0: direct)
   double* nu = nullptr;       // m
   double* G = nullptr;        // batch*r*r (interleaved)
   double* C = nullptr;        // batch*r*r (interleaved)
@@ -332,6 +333,15 @@ rfd_status exchange(const rfd_plan* p, const double* send, double* recv, size_t 
   return RFD_OK;
 }
 
+// a4 path: RFD_GRAM_SPREAD=0 always direct, =2 spread whenever the grid is
+// feasible (tests), unset/1: spread when the grid has <= n / kSpreadRatio nodes.
+constexpr int64_t kSpreadRatio = 8;
+int gram_spread_mode() {
+  const char* e = getenv("RFD_GRAM_SPREAD");
+  if (!e || !e[0]) return 1;
+  return atoi(e);
+}
+
 rfd_status create_impl(const float* points, int batch, int64_t n, double eps, double lambda,
                        int m, uint64_t seed, const rfd_shard* shard, cudaStream_t st,
                        rfd_plan** plan_out) {
@@ -431,17 +441,39 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   rfd::launch_pack_points(dev_xyz, bbox, p->pts, p->pts16, gpts, gper, p->centre, n, batch, st);
   rfd::launch_freq(p->omega4, p->omega_rad4, p->nu, p->flags, m, seed, eps, RFD_TRUNCATION_R, cached_c_r(), st);
 
-  // a4: Gram on the tensor cores (tcgen05, fp16 hi/lo split)
+  // a4: Gram on the tensor cores (tcgen05, fp16 hi/lo split): directly over
+  // the points, or -- large single clouds -- over a spread grid (k_nufft.cu)
+  rfd::NufftGrid ng{};
+  bool spread = false;
+  const int spread_mode = gram_spread_mode();
+  if (spread_mode != 0 && batch == 1 && rfd::gram_tc_pairs(m)) {
+    unsigned int hb[6];
+    std::vector<float4> hom(static_cast<size_t>(m));
+    RFD_CUDA(cudaMemcpyAsync(hb, bbox, sizeof(hb), cudaMemcpyDeviceToHost, st));
+    RFD_CUDA(cudaMemcpyAsync(hom.data(), p->omega4, size_t(m) * sizeof(float4),
+                             cudaMemcpyDeviceToHost, st));
+    RFD_CUDA(cudaStreamSynchronize(st));
+    spread = rfd::nufft_grid(hb, hom.data(), m, n, &ng) &&
+             (spread_mode == 2 || ng.nodes * kSpreadRatio <= n);
+  }
+  double* Gdst = p->G;
+  double* parts = nullptr;
   if (world > 1) {  // this shard's partial, all-gathered, summed in rank order
-    double *Gl = nullptr, *parts = nullptr;
-    RFD_CUDA(tmp.alloc(&Gl, rr));
+    RFD_CUDA(tmp.alloc(&Gdst, rr));
     RFD_CUDA(tmp.alloc(&parts, rr * world));
-    rfd::launch_gram_tc(p->omega_rad4, m, n, batch, gg, gpart, Gl, st);
-    rfd_status xs = exchange(p, Gl, parts, rr, st);
+  }
+  if (spread) {
+    unsigned char* ws = nullptr;
+    RFD_CUDA(tmp.alloc(&ws, rfd::nufft_workspace_bytes(ng, n, m, p->sms)));
+    RFD_CUDA(rfd::launch_gram_nufft(p->pts, n, p->omega_rad4, m, ng, p->sms, ws, Gdst, st));
+  } else {
+    rfd::launch_gram_tc(p->omega_rad4, m, n, batch, gg, gpart, Gdst, st);
+  }
+  p->gram_nodes = spread ? ng.nodes : 0;
+  if (world > 1) {
+    rfd_status xs = exchange(p, Gdst, parts, rr, st);
     if (xs != RFD_OK) return xs;
     rfd::launch_sum_parts(parts, world, int64_t(rr), p->G, st);
-  } else {
-    rfd::launch_gram_tc(p->omega_rad4, m, n, batch, gg, gpart, p->G, st);
   }
 
   // a5: core
@@ -965,6 +997,7 @@ rfd_status rfd_plan_info(const rfd_plan* p, rfd_plan_info_t* info) {
   info->n_total = p->n_total;
   info->rank = p->rank;
   info->world = p->world;
+  info->gram_nodes = p->gram_nodes;
   return RFD_OK;
 }
 

@@ -103,8 +103,28 @@ size_t gram_tc_partial_elems(const GramGeom& g, int batch);
 // where launch_pack_points writes the points in the Gram's layout inside the
 // `partial` workspace (per_cloud: padded points per cloud)
 float* gram_points(const GramGeom& g, int batch, float* partial, int64_t* per_cloud);
+// weighted: sum_p w_p^2 phi phi^T with w_p in the layout's pad slot (CTA-pair
+// path only, gram_tc_pairs(m)).
+bool gram_tc_pairs(int m);
 void launch_gram_tc(const float4* omega4, int m, int64_t n, int batch, const GramGeom& g,
-                    float* partial, double* G, cudaStream_t s);
+                    float* partial, double* G, cudaStream_t s, bool weighted = false);
+
+// a4 through a spread grid (k_nufft.cu) for large single clouds.
+constexpr int kNufftWidth = 6;
+struct NufftGrid {
+  int L[3], n[3];          // node l at (l - L) h per axis, n = 2 L + 1 nodes
+  int64_t nodes;
+  float h[3], inv_h[3], inv_alpha[3], beta_l2e;   // what the kernels use
+  double alpha_eff[3], beta_eff;                  // the kernel they implement
+  double wscale;           // grid Gram weights sqrt(b wscale) (power of two)
+};
+// Grid for the cloud's bbox (launch_bbox encoding, host copy) and omega (host
+// copy); false when the grid would be too large.
+bool nufft_grid(const unsigned int* bbox, const float4* omega4, int m, int64_t n, NufftGrid* g);
+size_t nufft_workspace_bytes(const NufftGrid& g, int64_t n, int m, int sms);
+// G (r x r fp64, interleaved) of the centred points pts; ws: workspace bytes.
+cudaError_t launch_gram_nufft(const float4* pts, int64_t n, const float4* omega_rad4, int m,
+                              const NufftGrid& g, int sms, void* ws, double* G, cudaStream_t s);
 
 // ---------------------------------------------------------------- core
 // Z_b = lambda D^1/2 G D^1/2 (symmetric route) or lambda G D; atomicMax of

@@ -47,7 +47,7 @@ class PlanInfo(ctypes.Structure):
                 ("symmetric", ctypes.c_int32), ("eps", ctypes.c_double),
                 ("lam", ctypes.c_double), ("seed", ctypes.c_uint64),
                 ("n_total", ctypes.c_int64), ("rank", ctypes.c_int32),
-                ("world", ctypes.c_int32)]
+                ("world", ctypes.c_int32), ("gram_nodes", ctypes.c_int64)]
 
 
 # int allgather(void* ctx, const double* send, double* recv, size_t count, stream)

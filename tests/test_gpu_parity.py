@@ -650,6 +650,48 @@ def test_launch_counter_and_profiler():
     assert {"rfd_reduce_S", "rfd_core_apply", "rfd_pass1_tc", "rfd_pass2_tc"} <= set(prof4)
 
 
+@pytest.mark.parametrize("cfg,n,shift", [(4, None, 0.0), (5, 262144, 0.0), (5, 262144, 1000.0),
+                                         (4, None, 100.0)])
+def test_gram_spread_grid_parity(cfg, n, shift, monkeypatch):
+    # a4 through the spread grid (k_nufft.cu) against the oracle's direct sum
+    # and against the direct tensor-core Gram; bitwise deterministic (integer
+    # spreading) and exactly symmetric.  RFD_GRAM_SPREAD=2 forces the grid,
+    # =0 the direct path (the default picks the grid when it has <= n/8 nodes).
+    p, x, F = make_config(cfg, **({"n": n} if n else {}))
+    x = (x.astype(np.float64) + shift * np.array([1.0, -0.7, 0.4])).astype(np.float32)
+    p = dict(p, name="cfg%d n %d shift %g" % (cfg, x.shape[0], shift))
+    ref = orf.Plan(x, p["eps"], p["lam"], p["m"], p["seed"])
+    res = ref.apply(F.astype(np.float64))
+    F2 = F.reshape(F.shape[0], -1).astype(np.float64)
+    Gs = {}
+    for mode in ("0", "2"):
+        monkeypatch.setenv("RFD_GRAM_SPREAD", mode)
+        plan, out = _run_single(x, F, p)
+        nodes = plan.info()["gram_nodes"]
+        assert (nodes > 0) == (mode == "2"), nodes
+        G = plan.export("gram")
+        Gs[mode] = G
+        o2 = out.reshape(out.shape[0], -1)
+        errs = dict(G=relerr(G, ref.G), C=relerr(plan.export("core"), ref.C),
+                    out=relerr(o2, res["out"]), delta=relerr(o2 - F2, res["out"] - F2))
+        print(p["name"], "mode", mode, "nodes", nodes, {k: "%.2e" % v for k, v in errs.items()})
+        assert errs["G"] <= 2e-5 and max(errs.values()) <= TOL, errs
+        if mode == "2":
+            G2 = _run_single(x, F, p)[0].export("gram")
+            np.testing.assert_array_equal(G, G2)
+            assert relerr(G, G.T) <= 1e-15  # the export's rotation back rounds
+    assert relerr(Gs["2"], Gs["0"]) <= 2e-5
+
+
+def test_gram_spread_grid_declines_large_extent(monkeypatch):
+    # cfg 4's sheet scaled x 200 would need > 2^11 nodes per axis: even
+    # forced, the plan takes the direct Gram
+    monkeypatch.setenv("RFD_GRAM_SPREAD", "2")
+    p, x, F = make_config(4)
+    plan, _ = _run_single((x * 200.0).astype(np.float32), F, p)
+    assert plan.info()["gram_nodes"] == 0
+
+
 @pytest.mark.parametrize("d", [1, 2, 3, 4])
 def test_narrow_field_paths_agree(d):
     # the d <= 4 one-launch SIMT path and the tensor-core passes (the same

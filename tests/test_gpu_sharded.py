@@ -87,13 +87,17 @@ def _relerr(got, ref):
     return float(np.abs(np.asarray(got, np.float64) - ref).max() / np.abs(ref).max())
 
 
-@pytest.mark.parametrize("cfg,world", [(2, 2), (4, 3), (1, 2)])
-def test_sharded_cloud_matches_oracle(cfg, world):
+@pytest.mark.parametrize("cfg,world,spread", [(2, 2, "1"), (4, 3, "1"), (1, 2, "1"), (4, 2, "2")])
+def test_sharded_cloud_matches_oracle(cfg, world, spread, monkeypatch):
+    # spread "2": every rank's partial G through the spread grid (k_nufft.cu)
+    # on the merged bounding box
+    monkeypatch.setenv("RFD_GRAM_SPREAD", spread)
     p, x, F = make_config(cfg)
     res = _run_ranks(x, F, p, world, d_calls=2)
     ref = orf.Plan(x, p["eps"], p["lam"], p["m"], p["seed"])
     for r in res:
         assert r["info"]["n_total"] == x.shape[0] and r["info"]["world"] == world
+        assert (r["info"]["gram_nodes"] > 0) == (spread == "2")
         np.testing.assert_array_equal(r["G"], res[0]["G"])  # same bits on every rank
         np.testing.assert_array_equal(r["C"], res[0]["C"])
     eG, eC = _relerr(res[0]["G"], ref.G), _relerr(res[0]["C"], ref.C)
