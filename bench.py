@@ -59,24 +59,33 @@ def peaks():
 # Peaks: FP32 FMA pipe and MUFU from the B200 unit counts at
 # sm_max_mhz; dense fp16 tensor = the measured bf16 burst (same rate for fp16),
 # tf32 = half of it (the guide's nominal 1.1 vs 2.25 PFLOP/s ratio).
-def kernel_work(name, N, m, d):
+def kernel_work(name, N, m, d, nodes=0):
     """Algorithmic work of one launch: dict of {fma, mufu, bytes, tensor_flop, tensor_kind}.
 
     Algorithmic = what the method needs, not what the kernel
     executes: the 3-product hi/lo splits, masked tile halves, range reduction
     and loop control count against achieved efficiency, not the roofline.
+    nodes > 0: a4 went through the spread grid (k_nufft.cu):
+    the tensor-core Gram runs over the grid's nodes, the spread kernel does
+    6^3 multiply-adds and 18 kernel values (rsqrt + ex2) per point.
     """
     r = 2 * m
     dc = min(d, 16)
     if name in ("rfd_gram_partial", "rfd_gram_tc"):   # G = Phi^T Phi (upper triangle)
-        w = dict(fma=N * r * (r + 1) / 2 + 3.0 * N * m, mufu=2.0 * N * m, bytes=16.0 * N)
+        Ng = nodes if nodes > 0 else N
+        w = dict(fma=Ng * r * (r + 1) / 2 + 3.0 * Ng * m, mufu=2.0 * Ng * m, bytes=16.0 * Ng,
+                 proj=3.0 * Ng * m)
         if name == "rfd_gram_tc":
-            w.update(tensor_flop=2.0 * N * r * (r + 1) / 2, tensor_kind="f16")
+            w.update(tensor_flop=2.0 * Ng * r * (r + 1) / 2, tensor_kind="f16")
         return w
+    if name == "rfd_nufft_spread" and nodes > 0:
+        return dict(fma=N * (216.0 + 18 * 6), mufu=36.0 * N, bytes=16.0 * N + 8.0 * nodes)
     if name in ("rfd_pass1", "rfd_pass1_tc"):           # S = Phi^T F
-        w = dict(fma=2.0 * N * m * dc + 3.0 * N * m, mufu=2.0 * N * m, bytes=N * (16 + 4 * dc))
+        w = dict(fma=2.0 * N * m * dc + 3.0 * N * m, mufu=2.0 * N * m, bytes=N * (16 + 4 * dc),
+                 proj=3.0 * N * m)
     elif name in ("rfd_pass2", "rfd_pass2_tc"):         # out = F + Phi Y
-        w = dict(fma=2.0 * N * m * dc + 3.0 * N * m, mufu=2.0 * N * m, bytes=N * (16 + 8 * dc))
+        w = dict(fma=2.0 * N * m * dc + 3.0 * N * m, mufu=2.0 * N * m, bytes=N * (16 + 8 * dc),
+                 proj=3.0 * N * m)
     else:
         return None
     if name.endswith("_tc"):
@@ -103,11 +112,12 @@ def ncu_traffic(name):
         return None
 
 
-def roofline_of(name, N, m, d, ms_per_launch, pk):
+def roofline_of(name, N, m, d, ms_per_launch, pk, nodes=0):
     """Roofline of one kernel: the slowest of its algorithmic HBM bytes, tensor
     flops (tensor-core kernels: the contraction runs there) or FP32 FMA (SIMT
-    kernels), and MUFU work, each at its peak."""
-    w = kernel_work(name, N, m, d)
+    kernels), and MUFU work, each at its peak.  MUFU-bound kernels report
+    bound "alu" (pipe "mufu") against the derived 148 x 16/clk peak."""
+    w = kernel_work(name, N, m, d, nodes)
     if w is None or ms_per_launch <= 0:
         return None
     P = peaks_of(pk)
@@ -115,7 +125,7 @@ def roofline_of(name, N, m, d, ms_per_launch, pk):
     terms = {"hbm": w["bytes"] / P["hbm"], "sfu": w["mufu"] / P["mufu"]}
     if "tensor_flop" in w:
         terms["tensor"] = w["tensor_flop"] / P[w["tensor_kind"]]
-        terms["alu"] = 3.0 * N * m / P["fma"]          # projections only
+        terms["alu"] = w["proj"] / P["fma"]            # projections only
     else:
         terms["alu"] = w["fma"] / P["fma"]
     bound = max(terms, key=terms.get)
@@ -134,8 +144,10 @@ def roofline_of(name, N, m, d, ms_per_launch, pk):
         out.update(achieved=2 * w["fma"] / t / 1e12, peak=2 * P["fma"] / 1e12, unit="TFLOP/s",
                    peak_note="fp32 FMA pipe: 148 SM x 128 FMA/clk x %.0f MHz (derived)" % pk["sm_max_mhz"])
     else:
-        out.update(achieved=w["mufu"] / t / 1e12, peak=P["mufu"] / 1e12, unit="Tops/s",
-                   peak_note="MUFU: 148 SM x 16/clk x %.0f MHz (derived)" % pk["sm_max_mhz"])
+        out.update(bound="alu", pipe="mufu", achieved=w["mufu"] / t / 1e12, peak=P["mufu"] / 1e12,
+                   unit="Tops/s",
+                   peak_note="MUFU sin/cos: 148 SM x 16/clk x %.0f MHz (derived, DESIGN.md Sec. 6)"
+                   % pk["sm_max_mhz"])
     return out
 
 
@@ -301,6 +313,7 @@ def run_rfd(args, rank, world, local, pg):
 
     # ---- inference only (plan reused), same protocol
     plan = make_plan(xd)
+    gram_nodes = int(plan.info()["gram_nodes"])  # a4 via the spread grid (0: direct)
     for _ in range(args.warmup):
         plan.integrate(Fd, out=outd)
     torch.cuda.synchronize()
@@ -410,14 +423,14 @@ def run_rfd(args, rank, world, local, pg):
     for name, (cnt, tms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
         per = tms / cnt
         kernels[name] = {"launches": cnt, "ms_per_launch": per, "share": tms / total}
-        rl = roofline_of(name, N, m, d, per, pk)
+        rl = roofline_of(name, N, m, d, per, pk, gram_nodes)
         if rl:
             kernels[name]["roofline_frac"] = rl["frac"]
-            kernels[name]["bound"] = rl["bound"]
+            kernels[name]["bound"] = rl.get("pipe", rl["bound"])
     dom = max(prof.items(), key=lambda kv: kv[1][1])[0]
-    roof = roofline_of(dom, N, m, d, prof[dom][1] / prof[dom][0], pk) or {}
+    roof = roofline_of(dom, N, m, d, prof[dom][1] / prof[dom][0], pk, gram_nodes) or {}
     roof = dict(roof, kernel=dom, peak_src=pk["src"])
-    if dom == "rfd_gram_tc" and 2 * m >= 256 and roof.get("unit") == "TFLOP/s":
+    if dom == "rfd_gram_tc" and gram_nodes == 0 and 2 * m >= 256 and roof.get("unit") == "TFLOP/s":
         # What the kernel executes: per 256 x 256 pair tile and point, 2 (diagonal)
         # or 3 (off-diagonal) fp16 products of the hi/lo split (Gram):
         # even at a fully busy tensor pipe frac cannot exceed algorithmic/executed.
@@ -454,7 +467,7 @@ def run_rfd(args, rank, world, local, pg):
              "hbm_gbs_achieved": byts_i / (ims * 1e-3) / 1e9, "kernels": ikern}
     return dict(N=N, m=m, d=d, ms_step=ms_step, launches=launches, roofline=roof,
                 kernels=kernels, integrate=integ, e2e=e2e, clocks=sampler.summary(), params=p,
-                reparam=reparam, spectrum=spectrum)
+                reparam=reparam, spectrum=spectrum, gram_nodes=gram_nodes)
 
 
 def config_legs(args, pk):
@@ -792,7 +805,11 @@ def main():
             "gpu_launches": res["launches"], "clocks": res["clocks"],
             "parity": parity, "eps_graph_diagnostic": eps_graph,
             "integrate": res["integrate"], "reparam": res["reparam"], "spectrum": res["spectrum"], "configs": legs,
-            "kernels": res["kernels"]}
+            "kernels": res["kernels"],
+            "gram": {"path": "spread grid (k_nufft.cu)" if res["gram_nodes"] else "direct",
+                     "nodes": res["gram_nodes"],
+                     "note": "a4 over a 6^3-kernel spread grid of `nodes` points, deconvolved "
+                             "(DESIGN.md Sec. 6 'a4 spread grid'); parity as reported"}}
     print(json.dumps(line))
 
 

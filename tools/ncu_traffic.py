@@ -12,7 +12,8 @@ import subprocess
 import sys
 
 SCOPES = [(r"gram_pair_kernel|gram_tc_kernel", "rfd_gram_tc"), (r"pass1_tc", "rfd_pass1_tc"),
-          (r"pass2_tc", "rfd_pass2_tc"), (r"dgemm_kernel", "rfd_core_dgemm")]
+          (r"pass2_tc", "rfd_pass2_tc"), (r"dgemm_kernel", "rfd_core_dgemm"),
+          (r"nufft_spread", "rfd_nufft_spread")]
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 acc = {}

@@ -1,6 +1,6 @@
 # Full round measurement: GPU tests, smoke, default bench (cpu_baseline + e2e +
 # parity), reference arm, ncu launch list of the bench command, ncu --set full
-# of the top kernels (cfg 5 step; the narrow-field kernel at cfg 4; the fused
+# of the top kernels (cfg 5 step: spread, grid Gram, passes; the narrow-field kernel at cfg 4; the fused
 # barycenter), source-level stall summaries.  Outputs under gpurun_out/.
 mkdir -p gpurun_out
 python -c "from paper_2302_00942_b200 import build; build.build()" > gpurun_out/build.log 2>&1
@@ -14,7 +14,7 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 C="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-configs --no-parity"
 timeout 600 $C > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $C > gpurun_out/ncu_launches.log 2>&1; echo launches rc $?
 C2="python tools/profile_step.py"
-timeout 300 $C2 > gpurun_out/plain2.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"gram_pair_kernel|pass1_tc|pass2_tc" -c 3 -o gpurun_out/full $C2 > gpurun_out/ncu_full.log 2>&1; echo full rc $?
+timeout 300 $C2 > gpurun_out/plain2.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"nufft_spread|gram_pair_kernel|pass1_tc|pass2_tc" -c 4 -o gpurun_out/full $C2 > gpurun_out/ncu_full.log 2>&1; echo full rc $?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"dgemm" -c 1 -o gpurun_out/full2 $C2 > gpurun_out/ncu_full2.log 2>&1; echo full2 rc $?
 C3="python tools/profile_step.py --cfg 4"
 timeout 300 $C3 > gpurun_out/plain3.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:"integrate_small" -c 1 -o gpurun_out/full3 $C3 > gpurun_out/ncu_full3.log 2>&1; echo full3 rc $?
