@@ -298,11 +298,20 @@ def run_rfd(args, rank, world, local, pg):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with sampler:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)] \
+            if args.step_times else None
         ev0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            if evs:
+                evs[i].record(stream)
             step()
+        if evs:
+            evs[-1].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
+        if evs:
+            print("step ms:", " ".join("%.3f" % evs[i].elapsed_time(evs[i + 1])
+                                       for i in range(args.steps)), file=sys.stderr)
     barrier(pg)
     launches = rfd.launch_count() - l0
     prof = rfd.profile_read()
@@ -736,6 +745,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 20)
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config legs")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity leg")
+    ap.add_argument("--step-times", action="store_true",
+                    help="also record an event pair per timed step and print them to stderr")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
