@@ -309,9 +309,13 @@ rfd_status rfd_plan_export(const rfd_plan* plan, rfd_field which,
  *     on its stream; rfd_profile_read synchronizes, then returns up to `cap`
  *     per-kernel aggregates (name, launches, total ms) since the last
  *     enable / read, and resets them.  Returns the number of entries.
+ *   rfd_profile_only(name) restricts the events to launches of that kernel
+ *     name (NULL or "": every launch), so a timed region can measure one
+ *     kernel live without bracketing the others.
  */
 uint64_t rfd_launch_count(void);
 rfd_status rfd_profile_enable(int on);
+rfd_status rfd_profile_only(const char* name);
 typedef struct {
   char name[48];
   int64_t launches;

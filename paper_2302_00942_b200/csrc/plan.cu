@@ -51,6 +51,7 @@ std::vector<Pending> g_pending;
 std::vector<cudaEvent_t> g_free_events;
 std::map<std::string, std::pair<int64_t, double>> g_prof;
 thread_local cudaEvent_t t_open_event = nullptr;
+std::string g_prof_only;  // non-empty: profile only the launches of this name
 
 cudaEvent_t take_event() {
   if (!g_free_events.empty()) {
@@ -65,9 +66,10 @@ cudaEvent_t take_event() {
 }  // namespace
 
 namespace rfd {
-void launch_begin(const char*, cudaStream_t s) {
+void launch_begin(const char* name, cudaStream_t s) {
   if (g_profiling.load(std::memory_order_relaxed)) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof_only.empty() && g_prof_only != name) return;
     t_open_event = take_event();
     cudaEventRecord(t_open_event, s);
   }
@@ -1062,6 +1064,12 @@ uint64_t rfd_launch_count(void) { return g_launches.load(); }
 
 rfd_status rfd_profile_enable(int on) {
   g_profiling.store(on ? 1 : 0);
+  return RFD_OK;
+}
+
+rfd_status rfd_profile_only(const char* name) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_only = name ? name : "";
   return RFD_OK;
 }
 

@@ -32,7 +32,7 @@ EXPORTED = ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_create_shard
             "rfd_integrate_host", "rfd_gfi_host", "rfd_destroy", "rfd_last_error",
             "rfd_plan_info",
             "rfd_plan_export", "rfd_launch_count", "rfd_profile_enable",
-            "rfd_profile_read")
+            "rfd_profile_only", "rfd_profile_read")
 
 
 class RFDError(RuntimeError):
@@ -146,13 +146,14 @@ def load_library(path=LIB_PATH):
     lib.rfd_plan_export.argtypes = [vp, ctypes.c_int, vp, ctypes.c_size_t]
     lib.rfd_launch_count.restype = ctypes.c_uint64
     lib.rfd_profile_enable.argtypes = [ctypes.c_int]
+    lib.rfd_profile_only.argtypes = [ctypes.c_char_p]
     lib.rfd_profile_read.argtypes = [ctypes.POINTER(ProfileEntry), i32]
     lib.rfd_profile_read.restype = i32
     for name in ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_create_sharded",
                  "rfd_plan_reparam",
                  "rfd_plan_spectrum", "rfd_barycenter", "rfd_integrate",
                  "rfd_integrate_host", "rfd_gfi_host", "rfd_plan_info", "rfd_plan_export",
-                 "rfd_profile_enable"):
+                 "rfd_profile_enable", "rfd_profile_only"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -398,6 +399,11 @@ def launch_count():
 
 def profile_enable(on=True):
     _check(load_library().rfd_profile_enable(1 if on else 0))
+
+
+def profile_only(name=None):
+    """Profile only launches named `name` (None: every launch)."""
+    _check(load_library().rfd_profile_only(name.encode() if name else None))
 
 
 def profile_read(cap=64):
