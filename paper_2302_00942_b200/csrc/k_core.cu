@@ -32,43 +32,44 @@ constexpr int kPS = 5;        // Paterson-Stockmeyer block
 
 __device__ __forceinline__ double dweight(const double* nu, int a) { return nu[a >> 1]; }
 
-__global__ void core_prep_kernel(const double* __restrict__ G, const double* __restrict__ nu,
-                                 const int* __restrict__ flags, double lambda, int r,
-                                 double* __restrict__ Z) {
+// Z_b = lambda D^1/2 G D^1/2 (symmetric route) or lambda G D, and ||Z_b||_1 =
+// max column abs sum in the same pass: block (8 columns x 32 row groups, one
+// cloud), the column sums reduced in shared memory in a fixed order, the max
+// over blocks and clouds via atomicMax on the (non-negative) fp64 bits.
+__global__ void __launch_bounds__(256)
+core_prep_norm_kernel(const double* __restrict__ G, const double* __restrict__ nu,
+                      const int* __restrict__ flags, double lambda, int r,
+                      double* __restrict__ Z, unsigned long long* __restrict__ norm_bits) {
   const int b = blockIdx.y;
-  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= int64_t(r) * r) return;
-  const int a = int(e / r), c = int(e % r);
+  const int cl = threadIdx.x & 7, rg = threadIdx.x >> 3;
+  const int c = blockIdx.x * 8 + cl;
   const bool sym = (flags[0] & 1) == 0;
-  const double g = G[int64_t(b) * r * r + e];
-  const double da = dweight(nu, a), dc = dweight(nu, c);
-  Z[int64_t(b) * r * r + e] = sym ? lambda * sqrt(da) * g * sqrt(dc) : lambda * g * dc;
-}
-
-__global__ void core_norm_kernel(const double* __restrict__ Z, int r,
-                                 unsigned long long* __restrict__ norm_bits) {
-  // ||Z_b||_1 = max column abs sum; block (32 columns x 8 row groups), the
-  // max over blocks and clouds via atomicMax on the (non-negative) fp64 bits.
-  const int b = blockIdx.y;
-  const int c = blockIdx.x * 32 + (threadIdx.x & 31), rg = threadIdx.x >> 5;
-  const double* Zb = Z + int64_t(b) * r * r;
+  const double* Gb = G + int64_t(b) * r * r;
+  double* Zb = Z + int64_t(b) * r * r;
   double col = 0.0;
-  if (c < r)
-    for (int a = rg; a < r; a += 8) col += fabs(Zb[int64_t(a) * r + c]);
-  __shared__ double red[8][33];
-  red[rg][threadIdx.x & 31] = col;
+  if (c < r) {
+    const double dc = dweight(nu, c), sdc = sqrt(dc);
+    for (int a = rg; a < r; a += 32) {
+      const int64_t e = int64_t(a) * r + c;
+      const double da = dweight(nu, a);
+      const double z = sym ? lambda * sqrt(da) * Gb[e] * sdc : lambda * Gb[e] * dc;
+      Zb[e] = z;
+      col += fabs(z);
+    }
+  }
+  __shared__ double red[32][9];
+  red[rg][cl] = col;
   __syncthreads();
-  if (threadIdx.x < 32) {
+  if (threadIdx.x < 8) {
     double sum = 0.0;
-#pragma unroll
-    for (int g = 0; g < 8; ++g) sum += red[g][threadIdx.x];
+#pragma unroll 8
+    for (int g = 0; g < 32; ++g) sum += red[g][threadIdx.x];
     if (!isfinite(sum)) sum = __longlong_as_double(0x7FF0000000000000LL);  // +inf
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum = fmax(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+    for (int o = 4; o > 0; o >>= 1) sum = fmax(sum, __shfl_xor_sync(0xffu, sum, o));
     if (threadIdx.x == 0) atomicMax(norm_bits, (unsigned long long)__double_as_longlong(sum));
   }
 }
-
 
 struct GemmJob {
   const double* A;  // r x r, per-batch stride r*r
@@ -254,16 +255,9 @@ void launch_core_prep(const double* G, const double* nu, const int* flags, doubl
                       int m, int batch, double* Z, unsigned long long* norm_bits,
                       cudaStream_t s) {
   const int r = 2 * m;
-  const int64_t rr = int64_t(r) * r;
-  {
-    LaunchScope L("rfd_core_prep", s);
-    core_prep_kernel<<<dim3(unsigned((rr + 255) / 256), batch), 256, 0, s>>>(G, nu, flags,
-                                                                             lambda, r, Z);
-  }
-  {
-    LaunchScope L("rfd_core_norm", s);
-    core_norm_kernel<<<dim3((r + 31) / 32, batch), 256, 0, s>>>(Z, r, norm_bits);
-  }
+  LaunchScope L("rfd_core_prep", s);
+  core_prep_norm_kernel<<<dim3((r + 7) / 8, batch), 256, 0, s>>>(G, nu, flags, lambda, r, Z,
+                                                                  norm_bits);
 }
 
 void launch_core_eval(const double* Z, const double* nu, const int* flags, double lambda,

@@ -215,14 +215,17 @@ __device__ __forceinline__ float4 bbox_centre(const unsigned int* bb) {
 //          points in packed FP32 math); the tail group is zero-padded (the
 //          buffer is cleared first when n % 16 != 0);
 //   gpts   the Gram's layout: per cloud, gper points (whole 64-point K-steps)
-//          in groups of 8 as x[8] y[8] z[8] 0[8] (cleared first when padded).
+//          in groups of 8 as x[8] y[8] z[8] 0[8] (cleared first when padded);
+//          not written when NULL (a4 through the spread grid);
+// and with kCount the point's cell of a4's spread grid and its atomic rank
+// inside the cell (CellCount, rfd_internal.h).
 // centre[b] = c of cloud b.
 // I: index type (32-bit when the batch's points fit: no 64-bit division per point)
-template <typename I>
+template <typename I, bool kCount>
 __global__ void pack_kernel(const float* __restrict__ xyz, const unsigned int* __restrict__ bbox,
                             float4* __restrict__ pts, float* __restrict__ pts16,
                             float* __restrict__ gpts, I gper, float4* __restrict__ centre, I n,
-                            I total) {
+                            I total, const CellCount cc) {
   const I gpc = (n + 15) / 16;
   for (I i = blockIdx.x * I(blockDim.x) + threadIdx.x; i < total; i += I(gridDim.x) * blockDim.x) {
     const I b = i / n, k = i - b * n;
@@ -235,12 +238,19 @@ __global__ void pack_kernel(const float* __restrict__ xyz, const unsigned int* _
     g[0] = x;
     g[16] = y;
     g[32] = z;
-    const int64_t gi = int64_t(b) * gper + k;
-    float* h = gpts + (gi >> 3) * 32 + (gi & 7);
-    h[0] = x;
-    h[8] = y;
-    h[16] = z;
-    h[24] = 0.0f;
+    if (gpts) {
+      const int64_t gi = int64_t(b) * gper + k;
+      float* h = gpts + (gi >> 3) * 32 + (gi & 7);
+      h[0] = x;
+      h[8] = y;
+      h[16] = z;
+      h[24] = 0.0f;
+    }
+    if (kCount) {
+      const int c = grid_cell(x, y, z, cc);
+      cc.cell[i] = c;
+      cc.rank[i] = atomicAdd(cc.count + c, 1);
+    }
   }
 }
 
@@ -321,20 +331,26 @@ void launch_bbox(const float* xyz, unsigned int* bbox, unsigned int* part, int64
 
 void launch_pack_points(const float* xyz, const unsigned int* bbox, float4* pts, float* pts16,
                         float* gpts, int64_t gper, float4* centre, int64_t n, int batch,
-                        cudaStream_t s) {
+                        const CellCount* cc, cudaStream_t s) {
   LaunchScope L("rfd_pack_points", s);
   const int64_t total = n * batch;
   if (n % 16 != 0) cudaMemsetAsync(pts16, 0, size_t(batch) * ((n + 15) / 16) * 48 * sizeof(float), s);
-  if (gper != n) cudaMemsetAsync(gpts, 0, size_t(batch) * gper * 4 * sizeof(float), s);
+  if (gpts && gper != n) cudaMemsetAsync(gpts, 0, size_t(batch) * gper * 4 * sizeof(float), s);
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  if (total < (int64_t(1) << 30) && gper * batch < (int64_t(1) << 30))  // (i + grid stride < 2^31)
-    pack_kernel<int><<<int(blocks), 256, 0, s>>>(xyz, bbox, pts, pts16, gpts, int(gper), centre,
-                                                  int(n), int(total));
-  else
-    pack_kernel<int64_t><<<int(blocks), 256, 0, s>>>(xyz, bbox, pts, pts16, gpts, gper, centre, n,
-                                                      total);
+  const CellCount none{};
+  if (total < (int64_t(1) << 30) && gper * batch < (int64_t(1) << 30)) {  // (i + grid stride < 2^31)
+    if (cc)
+      pack_kernel<int, true><<<int(blocks), 256, 0, s>>>(xyz, bbox, pts, pts16, gpts, int(gper),
+                                                          centre, int(n), int(total), *cc);
+    else
+      pack_kernel<int, false><<<int(blocks), 256, 0, s>>>(xyz, bbox, pts, pts16, gpts, int(gper),
+                                                           centre, int(n), int(total), none);
+  } else {
+    pack_kernel<int64_t, false><<<int(blocks), 256, 0, s>>>(xyz, bbox, pts, pts16, gpts, gper,
+                                                            centre, n, total, none);
+  }
 }
 
 void launch_rotate(const double* X, const float* Xf, int r, int cols, int batch, bool right,

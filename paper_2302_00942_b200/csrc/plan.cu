@@ -415,12 +415,6 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
                              cudaMemcpyHostToDevice, st));
     dev_xyz = staged;
   }
-  // a4's workspace first: the pack kernel writes the Gram's point layout into it
-  const rfd::GramGeom gg = rfd::gram_tc_geometry(m, n, batch, p->sms);
-  float* gpart = nullptr;
-  RFD_CUDA(tmp.alloc(&gpart, rfd::gram_tc_partial_elems(gg, batch)));
-  int64_t gper = 0;
-  float* gpts = rfd::gram_points(gg, batch, gpart, &gper);
   unsigned int* bbox = nullptr;
   RFD_CUDA(tmp.alloc(&bbox, size_t(batch) * 6));
   unsigned int* bpart = nullptr;
@@ -440,11 +434,11 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
     p->n_total = 0;
     for (int q = 0; q < world; ++q) p->n_total += int64_t(h[size_t(q) * 7 + 6]);
   }
-  rfd::launch_pack_points(dev_xyz, bbox, p->pts, p->pts16, gpts, gper, p->centre, n, batch, st);
   rfd::launch_freq(p->omega4, p->omega_rad4, p->nu, p->flags, m, seed, eps, RFD_TRUNCATION_R, cached_c_r(), st);
 
   // a4: Gram on the tensor cores (tcgen05, fp16 hi/lo split): directly over
-  // the points, or -- large single clouds -- over a spread grid (k_nufft.cu)
+  // the points, or -- large single clouds -- over a spread grid (k_nufft.cu),
+  // sized from the bounding box and omega read back here
   rfd::NufftGrid ng{};
   bool spread = false;
   const int spread_mode = gram_spread_mode();
@@ -464,11 +458,22 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
     RFD_CUDA(tmp.alloc(&Gdst, rr));
     RFD_CUDA(tmp.alloc(&parts, rr * world));
   }
-  if (spread) {
+  if (spread) {  // the packing also counts the points into the grid's cells
     unsigned char* ws = nullptr;
     RFD_CUDA(tmp.alloc(&ws, rfd::nufft_workspace_bytes(ng, n, m, p->sms)));
+    rfd::CellCount cc{};
+    RFD_CUDA(rfd::nufft_cell_count(ng, n, m, p->sms, ws, &cc, st));
+    rfd::launch_pack_points(dev_xyz, bbox, p->pts, p->pts16, nullptr, n, p->centre, n, batch, &cc,
+                            st);
     RFD_CUDA(rfd::launch_gram_nufft(p->pts, n, p->omega_rad4, m, ng, p->sms, ws, Gdst, st));
-  } else {
+  } else {  // the packing writes the Gram's point layout into its workspace
+    const rfd::GramGeom gg = rfd::gram_tc_geometry(m, n, batch, p->sms);
+    float* gpart = nullptr;
+    RFD_CUDA(tmp.alloc(&gpart, rfd::gram_tc_partial_elems(gg, batch)));
+    int64_t gper = 0;
+    float* gpts = rfd::gram_points(gg, batch, gpart, &gper);
+    rfd::launch_pack_points(dev_xyz, bbox, p->pts, p->pts16, gpts, gper, p->centre, n, batch,
+                            nullptr, st);
     rfd::launch_gram_tc(p->omega_rad4, m, n, batch, gg, gpart, Gdst, st);
   }
   p->gram_nodes = spread ? ng.nodes : 0;

@@ -71,9 +71,27 @@ void launch_bbox(const float* xyz, unsigned int* bbox, unsigned int* part, int64
                  int sms, cudaStream_t s);
 // centre c = the bbox midpoint (centre: batch float4); pts / pts16 / gpts (the
 // Gram layout, gper points per cloud) = points - c.
+// Cell counting for a4's spread grid, fused into the packing (k_nufft.cu):
+// the cell of a centred point y on the grid (node l at (l - L) h) is
+// [(l - L) h, (l - L + 1) h) per axis, clamped so its 6-node window fits.
+struct CellCount {
+  int L[3], n[3];
+  float inv_h[3];
+  int* count;   // ncells + 1, zeroed by the caller
+  int* cell;    // n
+  int* rank;    // n: position inside the cell (atomic, arbitrary order)
+};
+__device__ __forceinline__ int grid_cell(float x, float y, float z, const CellCount& g) {
+  const int i0 = min(max(__float2int_rd(x * g.inv_h[0]) + g.L[0], 2), g.n[0] - 4);
+  const int i1 = min(max(__float2int_rd(y * g.inv_h[1]) + g.L[1], 2), g.n[1] - 4);
+  const int i2 = min(max(__float2int_rd(z * g.inv_h[2]) + g.L[2], 2), g.n[2] - 4);
+  return (i0 * g.n[1] + i1) * g.n[2] + i2;
+}
+// gpts NULL: no Gram layout (a4 through the spread grid); cc != NULL: also
+// count the points into the grid's cells (batch = 1).
 void launch_pack_points(const float* xyz, const unsigned int* bbox, float4* pts, float* pts16,
                         float* gpts, int64_t gper, float4* centre, int64_t n, int batch,
-                        cudaStream_t s);
+                        const CellCount* cc, cudaStream_t s);
 // out (fp64, batch x r x cols) = R X (right: R X R^T, cols = r) with R the
 // per-frequency rotation by 2 pi omega.c_b (centred -> paper basis).  X fp64,
 // or Xf fp32 when X is NULL.
@@ -122,7 +140,12 @@ struct NufftGrid {
 // copy); false when the grid would be too large.
 bool nufft_grid(const unsigned int* bbox, const float4* omega4, int m, int64_t n, NufftGrid* g);
 size_t nufft_workspace_bytes(const NufftGrid& g, int64_t n, int m, int sms);
-// G (r x r fp64, interleaved) of the centred points pts; ws: workspace bytes.
+// The cell-count arrays inside the workspace (count zeroed here, on s): for
+// launch_pack_points, which must run before launch_gram_nufft.
+cudaError_t nufft_cell_count(const NufftGrid& g, int64_t n, int m, int sms, void* ws,
+                             CellCount* cc, cudaStream_t s);
+// G (r x r fp64, interleaved) of the centred points pts, counted into the
+// workspace's cells by launch_pack_points.
 cudaError_t launch_gram_nufft(const float4* pts, int64_t n, const float4* omega_rad4, int m,
                               const NufftGrid& g, int sms, void* ws, double* G, cudaStream_t s);
 
