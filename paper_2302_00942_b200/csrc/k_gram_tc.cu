@@ -1017,28 +1017,16 @@ gram_pair_kernel(const unsigned char* __restrict__ gpts, const float4* __restric
   if (warp == 0) tc::tmem_dealloc_pair<512>(tmem);
 }
 
-// K2 (pairs): G[b] from the pair-tile partials (256 x 256 per segment).
+// K2 (pairs), two steps: (1) Dsum[b][unit] = the fixed-order fp64 sum of the
+// unit's segment partials, every element read coalesced once per segment;
+// (2) G from Dsum, on diagonal pair tiles G = (D + D^T) / 2 (the transposed
+// read touches the 256 x 256 sum once, not once per segment).
 __global__ void __launch_bounds__(256)
-gram_pair_reduce_kernel(const float* __restrict__ partial, int m, const __grid_constant__ Sched sc,
-                        double* __restrict__ G) {
+gram_pair_sum_kernel(const float* __restrict__ partial, const __grid_constant__ Sched sc,
+                     double* __restrict__ Dsum) {
   __shared__ int segs[kMaxCtas];
   __shared__ int nseg_sh;
-  const int b = blockIdx.y;
-  const int T = 2 * sc.T, r = 2 * m;  // 128-feature blocks
-  int tile = blockIdx.x >> 4;
-  const int chunk = blockIdx.x & 15;
-  int bi = 0, row = T;
-  while (tile >= row) {
-    tile -= row;
-    ++bi;
-    --row;
-  }
-  const int bj = bi + tile;
-  const int I = bi >> 1, J = bj >> 1;
-  // pair-tile index of (I, J), I <= J
-  int unit = 0;
-  for (int i = 0; i < I; ++i) unit += sc.T - i;
-  unit += J - I;
+  const int b = blockIdx.z, unit = blockIdx.y;
   const int64_t bu = int64_t(b) * sc.U + unit;
   if (threadIdx.x == 0) {
     int ns = 0;
@@ -1050,28 +1038,38 @@ gram_pair_reduce_kernel(const float* __restrict__ partial, int m, const __grid_c
   }
   __syncthreads();
   const int nseg = nseg_sh;
-  const bool diag = (I == J);
-  const int ro = 128 * (bi & 1), co = 128 * (bj & 1);
-#pragma unroll 1
-  for (int i = 0; i < 4; ++i) {
-    const int e = chunk * 1024 + i * 256 + threadIdx.x;
-    const int rr = e >> 7, cc = e & 127;
-    const int fr = bi * kFreqs + (rr & 63), fc = bj * kFreqs + (cc & 63);
-    if (fr >= m || fc >= m) continue;
-    const int64_t o1 = int64_t(ro + rr) * 256 + co + cc;
-    const int64_t o2 = int64_t(co + cc) * 256 + ro + rr;
-    double s1 = 0.0, s2 = 0.0;
-    for (int k = 0; k < nseg; ++k) {
-      const float* P = partial + int64_t(segs[k]) * (256 * 256);
-      s1 += double(P[o1]);
-      if (diag) s2 += double(P[o2]);
-    }
-    const double v = diag ? 0.5 * (s1 + s2) : s1;
-    const int a = 2 * fr + (rr >> 6), c = 2 * fc + (cc >> 6);
-    double* Gb = G + int64_t(b) * r * r;
-    Gb[int64_t(a) * r + c] = v;
-    Gb[int64_t(c) * r + a] = v;
+  const int e = blockIdx.x * 256 + threadIdx.x;  // 0 .. 65535
+  double acc = 0.0;
+  for (int k = 0; k < nseg; ++k) acc += double(partial[int64_t(segs[k]) * (256 * 256) + e]);
+  Dsum[bu * (256 * 256) + e] = acc;
+}
+
+__global__ void __launch_bounds__(256)
+gram_pair_write_kernel(const double* __restrict__ Dsum, int m, const __grid_constant__ Sched sc,
+                       double* __restrict__ G) {
+  const int b = blockIdx.z;
+  const int r = 2 * m;
+  const int e = blockIdx.x * 256 + threadIdx.x;  // (a, c) over the r x r upper triangle
+  const int a = e / r, c = e - (e / r) * r;
+  if (a >= r || c < a) return;
+  // a = 2 f + (sin), block of the feature = f / 64, super-block = block / 2
+  const int fa = a >> 1, fc = c >> 1;
+  int bi = fa / kFreqs, bj = fc / kFreqs;
+  int rr = (fa % kFreqs) + 64 * (a & 1), cc = (fc % kFreqs) + 64 * (c & 1);
+  int x = 128 * (bi & 1) + rr, y = 128 * (bj & 1) + cc;
+  int I = bi >> 1, J = bj >> 1;
+  if (I > J) {  // (only when a's super-block exceeds c's: not in the upper triangle of blocks)
+    const int t = I; I = J; J = t;
+    const int u = x; x = y; y = u;
   }
+  int unit = 0;
+  for (int i = 0; i < I; ++i) unit += sc.T - i;
+  unit += J - I;
+  const double* D = Dsum + (int64_t(b) * sc.U + unit) * (256 * 256);
+  const double v = (I == J) ? 0.5 * (D[x * 256 + y] + D[y * 256 + x]) : D[x * 256 + y];
+  double* Gb = G + int64_t(b) * r * r;
+  Gb[int64_t(a) * r + c] = v;
+  Gb[int64_t(c) * r + a] = v;
 }
 
 Sched make_pair_sched(int m, int64_t n, int batch, int sms) {
@@ -1132,8 +1130,15 @@ GramGeom gram_tc_geometry(int m, int64_t n, int batch, int sms) {
 static size_t gram_tc_partial_only(const GramGeom& g, int batch) {
   return size_t(g.chunks + int64_t(batch) * g.ntiles) * 256 * g.tile;
 }
+// pair path: then the fp64 unit sums of the two-step reduce (16-byte aligned)
+static size_t gram_tc_dsum_offset(const GramGeom& g, int batch) {
+  return (gram_tc_partial_only(g, batch) + size_t(batch) * size_t(g.chunk) * (kStepBytes / 4) + 3) &
+         ~size_t(3);
+}
 size_t gram_tc_partial_elems(const GramGeom& g, int batch) {
-  return gram_tc_partial_only(g, batch) + size_t(batch) * size_t(g.chunk) * (kStepBytes / 4);
+  const bool pairs = g.tile == 2 * kBlk;
+  return gram_tc_dsum_offset(g, batch) +
+         (pairs ? size_t(batch) * size_t(g.ntiles) * (256 * 256) * 2 : 0);
 }
 float* gram_points(const GramGeom& g, int batch, float* partial, int64_t* per_cloud) {
   *per_cloud = int64_t(g.chunk) * kStep;
@@ -1200,8 +1205,12 @@ void launch_gram_tc(const float4* omega4, int m, int64_t n, int batch,
     }
     {
       LaunchScope L("rfd_gram_reduce", s);
-      const int T = 2 * sc.T, tiles = T * (T + 1) / 2;
-      gram_pair_reduce_kernel<<<dim3(16 * tiles, batch), 256, 0, s>>>(partial, m, sc, G);
+      // Dsum: U x batch 256 x 256 fp64 behind the segment partials and points
+      double* Dsum = reinterpret_cast<double*>(partial + gram_tc_dsum_offset(g, batch));
+      gram_pair_sum_kernel<<<dim3(256, sc.U, batch), 256, 0, s>>>(partial, sc, Dsum);
+      const int r = 2 * m;
+      gram_pair_write_kernel<<<dim3(unsigned((int64_t(r) * r + 255) / 256), 1, batch), 256, 0, s>>>(
+          Dsum, m, sc, G);
     }
     return;
   }
