@@ -71,9 +71,12 @@ void launch_bbox(const float* xyz, unsigned int* bbox, unsigned int* part, int64
                  int sms, cudaStream_t s);
 // centre c = the bbox midpoint (centre: batch float4); pts / pts16 / gpts (the
 // Gram layout, gper points per cloud) = points - c.
+// a4's spread-grid kernel width in nodes per axis (k_nufft.cu)
+constexpr int kNufftWidth = 8;
 // Cell counting for a4's spread grid, fused into the packing (k_nufft.cu):
 // the cell of a centred point y on the grid (node l at (l - L) h) is
-// [(l - L) h, (l - L + 1) h) per axis, clamped so its 6-node window fits.
+// [(l - L) h, (l - L + 1) h) per axis, clamped so its kNufftWidth-node
+// window (l - w/2 + 1 .. l + w/2) fits.
 struct CellCount {
   int L[3], n[3];
   float inv_h[3];
@@ -82,9 +85,10 @@ struct CellCount {
   int* rank;    // n: position inside the cell (atomic, arbitrary order)
 };
 __device__ __forceinline__ int grid_cell(float x, float y, float z, const CellCount& g) {
-  const int i0 = min(max(__float2int_rd(x * g.inv_h[0]) + g.L[0], 2), g.n[0] - 4);
-  const int i1 = min(max(__float2int_rd(y * g.inv_h[1]) + g.L[1], 2), g.n[1] - 4);
-  const int i2 = min(max(__float2int_rd(z * g.inv_h[2]) + g.L[2], 2), g.n[2] - 4);
+  constexpr int lo = kNufftWidth / 2 - 1, hi = kNufftWidth / 2 + 1;
+  const int i0 = min(max(__float2int_rd(x * g.inv_h[0]) + g.L[0], lo), g.n[0] - hi);
+  const int i1 = min(max(__float2int_rd(y * g.inv_h[1]) + g.L[1], lo), g.n[1] - hi);
+  const int i2 = min(max(__float2int_rd(z * g.inv_h[2]) + g.L[2], lo), g.n[2] - hi);
   return (i0 * g.n[1] + i1) * g.n[2] + i2;
 }
 // gpts NULL: no Gram layout (a4 through the spread grid); cc != NULL: also
@@ -128,7 +132,6 @@ void launch_gram_tc(const float4* omega4, int m, int64_t n, int batch, const Gra
                     float* partial, double* G, cudaStream_t s, bool weighted = false);
 
 // a4 through a spread grid (k_nufft.cu) for large single clouds.
-constexpr int kNufftWidth = 6;
 struct NufftGrid {
   int L[3], n[3];          // node l at (l - L) h per axis, n = 2 L + 1 nodes
   int64_t nodes;

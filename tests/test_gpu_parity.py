@@ -683,6 +683,27 @@ def test_gram_spread_grid_parity(cfg, n, shift, monkeypatch):
     assert relerr(Gs["2"], Gs["0"]) <= 2e-5
 
 
+@pytest.mark.parametrize("mode", ["0", "2"])
+@pytest.mark.parametrize("shape", ["point", "line", "plane"])
+def test_gram_spread_grid_degenerate_extents(shape, mode, monkeypatch):
+    # zero extent on 3, 2 or 1 axes: the grid shrinks to the kernel's width on
+    # those axes (L = ceil(alpha / h) + 1); forced through the spread path
+    monkeypatch.setenv("RFD_GRAM_SPREAD", mode)
+    rng = np.random.default_rng(11)
+    n = 4096
+    x = np.zeros((n, 3))
+    if shape != "point":
+        x[:, 0] = rng.uniform(-0.5, 0.5, n)
+    if shape == "plane":
+        x[:, 1] = rng.uniform(-0.3, 0.3, n)
+    x = (x + np.array([0.25, -1.0, 3.0])).astype(np.float32)
+    F = rng.standard_normal((n, 8)).astype(np.float32)
+    p = dict(name="spread " + shape, eps=0.05, lam=-0.4, m=128, seed=6)
+    plan, out = _run_single(x, F, p)
+    assert (plan.info()["gram_nodes"] > 0) == (mode == "2")
+    _check_against_oracle(plan, out, x, F, p)
+
+
 def test_gram_spread_grid_declines_large_extent(monkeypatch):
     # cfg 4's sheet scaled x 200 would need > 2^11 nodes per axis: even
     # forced, the plan takes the direct Gram

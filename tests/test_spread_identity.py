@@ -30,7 +30,7 @@ def _phihat(s, alpha, beta, nq=200):
     return alpha * (np.cos(np.outer(s, alpha * z)) @ (wq * _es(z, beta)))
 
 
-def spread_grid_gram(X, omega, w=6, hfac=1.5):
+def spread_grid_gram(X, omega, w=8, hfac=1.5):
     """G through the spread grid, following the kernels' parameter rules."""
     beta = 2.30 * w
     lo, hi = X.min(0), X.max(0)
@@ -99,7 +99,7 @@ def test_spread_grid_width_matters():
     X = np.asarray(x, np.float64)
     omega = np.asarray(orf.frequencies(p["seed"], 32)[0])
     errs = []
-    for w in (4, 6):
+    for w in (4, 8):
         G, c, _ = spread_grid_gram(X, omega, w=w)
         Gd = orf.gram(X - c, omega)
         errs.append(np.abs(G - Gd).max() / np.abs(Gd).max())
