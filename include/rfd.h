@@ -86,7 +86,7 @@ typedef enum {
  * Steps: frequencies + nu (a1-a2), Gram G = Phi^T Phi (a4), core C^ (a5).
  * a4 is the sum over points or -- one cloud, m > 64,
  * N >= 2^19, when the spread grid has <= N/8 nodes -- the same G through a spread grid
- * (a type-3 NUFFT identity; G within 2e-7 normwise of the exact sum, DESIGN.md
+ * (a type-3 NUFFT identity; G within 3e-7 normwise of the exact sum, DESIGN.md
  * Sec. 6; rfd_plan_info_t.gram_nodes says which).  Blocks the host until the
  * plan is ready (it reads back the bounding box and omega to size that grid,
  * the core's scaling exponent and an overflow flag).  Errors: EINVAL, ENOMEM,
