@@ -40,6 +40,7 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # B200 unit counts (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz; CUDA
 # throughput table for cc 10.0: 128 FP32 FMA and 16 MUFU results / clk / SM).
 SMS, FMA_PER_CLK, MUFU_PER_CLK = 148, 128, 16
+SPREAD_WIDTH = 8   # a4 spread-grid kernel width (csrc/rfd_internal.h kNufftWidth)
 METRIC = "GFI points x dims / s (RFD plan + integrate, cfg5 N=4M m=256 d=16)"
 UNIT = "points*dims/s"
 
@@ -67,7 +68,8 @@ def kernel_work(name, N, m, d, nodes=0):
     and loop control count against achieved efficiency, not the roofline.
     nodes > 0: a4 went through the spread grid (k_nufft.cu):
     the tensor-core Gram runs over the grid's nodes, the spread kernel does
-    6^3 multiply-adds and 18 kernel values (rsqrt + ex2) per point.
+    W^3 multiply-adds and 3W kernel values (rsqrt + ex2, ~6 FMA) per point,
+    W = SPREAD_WIDTH.
     """
     r = 2 * m
     dc = min(d, 16)
@@ -79,7 +81,9 @@ def kernel_work(name, N, m, d, nodes=0):
             w.update(tensor_flop=2.0 * Ng * r * (r + 1) / 2, tensor_kind="f16")
         return w
     if name == "rfd_nufft_spread" and nodes > 0:
-        return dict(fma=N * (216.0 + 18 * 6), mufu=36.0 * N, bytes=16.0 * N + 8.0 * nodes)
+        W = SPREAD_WIDTH
+        return dict(fma=N * (W ** 3 + 3.0 * W * 6), mufu=2.0 * 3 * W * N,
+                    bytes=20.0 * N + 8.0 * nodes)
     if name in ("rfd_pass1", "rfd_pass1_tc"):           # S = Phi^T F
         w = dict(fma=2.0 * N * m * dc + 3.0 * N * m, mufu=2.0 * N * m, bytes=N * (16 + 4 * dc),
                  proj=3.0 * N * m)
