@@ -559,7 +559,9 @@ def config_legs(args, pk):
                               "value": N * d / (gmed * 1e-3), "unit": UNIT,
                               "strict_roofline_us": rl * 1e3, "strict_roofline_frac": rl / gmed,
                               "plan_create_ms": pmed,
-                              "path": "rfd_integrate_small (d <= 4: one cooperative launch)"}
+                              "path": ("rfd_integrate_small (one cooperative launch)"
+                                       if (d == 1 or N <= 4096) else
+                                       "tensor-core passes (pass 1, a7 fused into pass 2)")}
         plan.close()
         del gr
     # cfg 3: 50 applications back to back on device-resident vectors

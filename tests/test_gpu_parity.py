@@ -714,9 +714,11 @@ def test_gram_spread_grid_declines_large_extent(monkeypatch):
 
 
 @pytest.mark.parametrize("d", [1, 2, 3, 4])
-def test_narrow_field_paths_agree(d):
-    # the d <= 4 one-launch SIMT path and the tensor-core passes (the same
-    # columns inside a d = 8 field) against each other and the oracle
+def test_narrow_field_paths_agree(d, monkeypatch):
+    # the d <= 4 one-launch SIMT path (forced: RFD_NARROW=2) and the
+    # tensor-core passes (the same columns inside a d = 8 field) against each
+    # other and the oracle
+    monkeypatch.setenv("RFD_NARROW", "2")
     p, x, F = make_config(4)
     rng = np.random.default_rng(d)
     F8 = rng.standard_normal((x.shape[0], 8)).astype(np.float32)
