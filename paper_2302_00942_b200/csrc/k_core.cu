@@ -86,15 +86,22 @@ struct GemmJobs {
 };
 
 // fp64 tensor-core GEMM (DMMA, mma.sync m8n8k4 f64): CTA tile 32 x 32, 4
-// warps as 2 x 2 (each 16 x 16 = 2 x 2 fragments), K in steps of 32 through a
+// warps as 2 x 2 (each 16 x 16 = 2 x 2 fragments), K in steps of 64 through a
 // 3-stage cp.async pipeline (padded strides: conflict-free fragment loads);
-// 55 KB of shared memory, so several CTAs share an SM (r = 512: 256 tiles;
-// measured 23 us per launch at r = 512 vs 32 us with 32 x 64 tiles; splitting
-// K over 8 warps measured slower).
+// 105 KB of shared memory (r = 512: 256 tiles; measured per launch at r =
+// 512: 21.0 us, vs 23.2 us with K steps of 32, 23.7 / 24.4 us with 128 / 64
+// and 2 stages, 32 us with 32 x 64 tiles; splitting K over 8 warps, two
+// accumulator sets per warp and a 4-CTA split-K cluster were slower).
 // Every product of the core is a polynomial in Z, so on the symmetric route
 // (Z = lambda D^1/2 G D^1/2) every result is symmetric: only the tiles on and
 // above the diagonal are computed, and each writes C_ij and C_ji (i <= j).
-constexpr int kBM = 32, kBN = 32, kBK = 32, kGStages = 3;
+#ifndef RFD_DGEMM_BK
+#define RFD_DGEMM_BK 64
+#endif
+#ifndef RFD_DGEMM_STAGES
+#define RFD_DGEMM_STAGES 3
+#endif
+constexpr int kBM = 32, kBN = 32, kBK = RFD_DGEMM_BK, kGStages = RFD_DGEMM_STAGES;
 constexpr int kSA = kBK + 4;   // A tile row stride (doubles): 8g + 2t banks, distinct
 constexpr int kSB = kBN + 4;   // B tile row stride (doubles)
 constexpr int kGemmSmem = kGStages * (kBM * kSA + kBK * kSB) * 8;
@@ -134,16 +141,17 @@ dgemm_kernel(GemmJobs jobs, int njobs, int r, int sym) {
   double* Bs = gsm + kGStages * kBM * kSA;           // [stage][kBK][kSB]
 
   auto load_tile = [&](int st, int k0) {
-    // A: 32 rows x 32 doubles = 512 chunks of 16 B; B: 32 x 32 likewise
+    // A: 32 rows x kBK doubles, B: kBK rows x 32 doubles, in 16-byte chunks
+    constexpr int kAc = kBK / 2;  // chunks per A row
 #pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      const int e = tid + 128 * l, row = e >> 4, kc = (e & 15) * 2;
+    for (int l = 0; l < kBM * kAc / 128; ++l) {
+      const int e = tid + 128 * l, row = e / kAc, kc = (e % kAc) * 2;
       const int gi = i0 + row, gk = k0 + kc;
       const bool ok = gi < r && gk < r;
       cp_async16(As + (st * kBM + row) * kSA + kc, ok ? A + int64_t(gi) * r + gk : A, ok);
     }
 #pragma unroll
-    for (int l = 0; l < 4; ++l) {
+    for (int l = 0; l < kBK * 16 / 128; ++l) {
       const int e = tid + 128 * l, kk = e >> 4, col = (e & 15) * 2;
       const int gk = k0 + kk, gj = j0 + col;
       const bool ok = gk < r && gj < r;
