@@ -480,9 +480,15 @@ pass1_tc_kernel(const float* __restrict__ pts16, const float4* __restrict__ omeg
 // The one-chunk kernel (N = 16): two D buffers (no MMA stall at a drain) and
 // the long-term sums in the drain warps' registers.  Kept separate from the
 // wide template: measured 9 % faster than its NC = 1 instance at cfg 5.
+#ifndef RFD_P1_STAGES
+#define RFD_P1_STAGES 3
+#endif
+#ifndef RFD_P1_EPOCH
+#define RFD_P1_EPOCH 8
+#endif
 namespace k16 {
-constexpr int kStages = 3;
-constexpr int kEpoch = 8;           // chunks per TMEM accumulation epoch
+constexpr int kStages = RFD_P1_STAGES;
+constexpr int kEpoch = RFD_P1_EPOCH;  // chunks per TMEM accumulation epoch
 constexpr uint32_t kColA = 64;      // D buffers (cos 16 + sin 16) at 0 and 32
 constexpr int kBBytes = 16 * kChunk * 2;        // one fp16 B operand (hi or lo): 2 KB
 constexpr int kChunkB = 2 * kBBytes;            // hi + lo of one chunk

@@ -39,7 +39,10 @@ struct Roles {
   static constexpr int kThreads = (PW + 5) * 32;
 };
 constexpr int kTile = 128;      // points per tile (= TMEM lanes)
-constexpr int kStages = 3;
+#ifndef RFD_P2_STAGES
+#define RFD_P2_STAGES 2
+#endif
+constexpr int kStages = RFD_P2_STAGES;
 // TMEM columns: accumulators [0, nw) and [nw, 2 nw) (nw = the launch's column
 // width, a multiple of 16, <= 64); stage s: hi at 2 nw + 128 s (64 cols = 128
 // fp16), lo at +64.
