@@ -560,7 +560,7 @@ def config_legs(args, pk):
                               "strict_roofline_us": rl * 1e3, "strict_roofline_frac": rl / gmed,
                               "plan_create_ms": pmed,
                               "path": ("rfd_integrate_small (one cooperative launch)"
-                                       if (d == 1 or N <= 4096) else
+                                       if (d == 1 or N <= 4096 or N > 65536) else
                                        "tensor-core passes (pass 1, a7 fused into pass 2)")}
         plan.close()
         del gr

@@ -597,14 +597,17 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
   rfd_status rs = ensure_workspace(p, d, st);
   if (rs != RFD_OK) return rs;
   // narrow fields: the whole inference in one cooperative SIMT launch
-  // (k_small.cu) for d = 1, batched clouds and tiny clouds; single clouds with
-  // 2 <= d <= 4 are faster on the tensor-core passes (measured, graph replay:
-  // cfg 2 d = 3 16.1 vs 24.2 us, cfg 4 d = 4 58.3 vs 63.1 us; cfg 1 and d = 1
-  // favour the narrow kernel).  RFD_NARROW=0 / 2 force either side (tests).
+  // (k_small.cu) for d = 1, batched, tiny and large clouds; single clouds of
+  // 4097 .. 65536 points with 2 <= d <= 4 are faster on the tensor-core passes
+  // (measured, graph replay: cfg 2 d = 3 16.1 vs 24.2 us; 18,944 points d = 3
+  // (barycenter) faster too; cfg 4 (200k) even; at 4M points d = 3 the narrow
+  // kernel wins: its contraction costs 2d FMA, the passes' split and MMA a
+  // fixed 16 columns).  RFD_NARROW=0 / 2 force either side (tests).
   const char* ne = getenv("RFD_NARROW");
   const int narrow_env = (ne && ne[0]) ? atoi(ne) : 1;
   const bool narrow = d <= 4 && p->world == 1 && narrow_env != 0 &&
-                      (narrow_env == 2 || d == 1 || p->batch > 1 || p->n <= 4096);
+                      (narrow_env == 2 || d == 1 || p->batch > 1 || p->n <= 4096 ||
+                       p->n > 65536);
   if (narrow) {
     const size_t need = rfd::small_partial_elems(p->m, p->n, p->batch, d, p->sms);
     if (p->small_part_elems < need) {
