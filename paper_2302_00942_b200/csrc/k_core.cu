@@ -248,13 +248,15 @@ GemmJob job(const double* A, const double* B, double* C, double alpha, double si
 
 // T = sum_i mc[i] M[i] + gamma I (elementwise; the first Horner operand)
 __global__ void combo_kernel(double* __restrict__ T, const double* M0, const double* M1,
-                             const double* M2, const double* M3, double c0, double c1, double c2,
-                             double c3, double gamma, int r) {
+                             const double* M2, const double* M3, const double* M4, double c0,
+                             double c1, double c2, double c3, double c4, double gamma, int r) {
   const int b = blockIdx.y;
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= int64_t(r) * r) return;
   const int64_t o = int64_t(b) * r * r + e;
-  T[o] = c0 * M0[o] + c1 * M1[o] + c2 * M2[o] + c3 * M3[o] + ((e / r == e % r) ? gamma : 0.0);
+  const double t =
+      c0 * M0[o] + c1 * M1[o] + c2 * M2[o] + c3 * M3[o] + ((e / r == e % r) ? gamma : 0.0);
+  T[o] = t + c4 * M4[o];
 }
 
 }  // namespace
@@ -305,15 +307,10 @@ void launch_core_eval(const double* Z, const double* nu, const int* flags, doubl
   }
   // B_q = sum_{i<5} c_{5q+i} Z0^i  (Z0^1 = alpha Z); Horner in Z0^5 from the top:
   // T = B_3 + c_20 Z0^5, then T <- Z0^5 T + B_q for q = 2, 1, 0.
-  {
+  {  // T = B_3 + c_20 Z0^5
     LaunchScope L("rfd_core_combo", s);
-    combo_kernel<<<egrid, 256, 0, s>>>(Ta, Z, Z2, Z3, Z4, c[16] * alpha, c[17], c[18], c[19],
-                                       c[15], r);
-  }
-  {
-    // + c_20 Z0^5: fold into T via one more combo term (M = Z5)
-    LaunchScope L("rfd_core_combo", s);
-    combo_kernel<<<egrid, 256, 0, s>>>(Ta, Ta, Z5, Z5, Z5, 1.0, c[20], 0.0, 0.0, 0.0, r);
+    combo_kernel<<<egrid, 256, 0, s>>>(Ta, Z, Z2, Z3, Z4, Z5, c[16] * alpha, c[17], c[18], c[19],
+                                       c[20], c[15], r);
   }
   double* T = Ta;
   double* Tn = Tb;
@@ -334,11 +331,11 @@ void launch_core_eval(const double* Z, const double* nu, const int* flags, doubl
     j.job[0] = job(Z, P, E, alpha, 0.0, 1.0);
     gemm(j, 1, r, batch, sym, s);
   }
-  for (int i = 0; i < s_scale; ++i) {  // P <- (E + I) P / 2 ; E <- E E
+  for (int i = 0; i < s_scale; ++i) {  // P <- (E + I) P / 2 ; E <- E E (not after the last)
     GemmJobs j{};
     j.job[0] = job(E, P, Pn, 0.5, 1.0, 0.0);
     j.job[1] = job(E, E, En, 1.0, 0.0, 0.0);
-    gemm(j, 2, r, batch, sym, s);
+    gemm(j, i + 1 < s_scale ? 2 : 1, r, batch, sym, s);
     double* t = P; P = Pn; Pn = t;
     t = E; E = En; En = t;
   }
