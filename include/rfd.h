@@ -242,6 +242,26 @@ rfd_status rfd_integrate_host(rfd_plan* plan, const float* F_host, int32_t d,
                               float* out_host, rfd_stream stream);
 
 /*
+ * rfd_gfi -- the whole graph-field integration i = exp(lambda W~) F (PAPER.md
+ * Eq. 1 with Sec. 2.4's kernel: pre-processing + inference) for a DEVICE
+ * field in one call.  The field's pass 1 (S = Phi^T F, which needs only the
+ * points, omega and F) runs on an internal second stream beside the plan's
+ * core, whose small fp64 GEMMs fit on the SMs next to pass 1's CTAs; then
+ * a7 and pass 2 on `stream`.  Same kernels and results (bitwise) as
+ * rfd_plan_create + rfd_integrate.
+ *   points  n x 3 fp32, HOST or DEVICE (as rfd_plan_create).
+ *   F, out  n x d DEVICE fp32, 16-byte aligned (out may alias F).
+ *   plan_out  NULL (the plan is destroyed, stream-ordered) or receives the
+ *           plan for reuse (rfd_integrate on further fields).
+ * Blocks the host while the plan's core is formed (as rfd_plan_create); out
+ * is ready when `stream` is.  Errors: as rfd_plan_create and rfd_integrate;
+ * EINVAL if F or out is host memory.
+ */
+rfd_status rfd_gfi(const float* points, int64_t n, double eps, double lambda, int32_t m,
+                   uint64_t seed, const float* F, int32_t d, float* out, rfd_stream stream,
+                   rfd_plan** plan_out);
+
+/*
  * rfd_gfi_host -- the whole graph-field integration i = exp(lambda W~) F
  * (Eq. 1 with Sec. 2.4's kernel: pre-processing + inference) from
  * HOST buffers in one call, overlapping the transfers with the computation:

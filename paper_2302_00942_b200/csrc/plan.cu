@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <functional>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -140,6 +141,7 @@ struct rfd_plan {
   float* pipe_partial = nullptr;  // pass-1 partials of the chunked (pipelined) host path
   size_t pipe_partial_elems = 0;
   cudaStream_t cs_h2d = nullptr, cs_d2h = nullptr;  // copy streams of the host path
+  cudaStream_t aux = nullptr;  // rfd_gfi: pass 1 beside the plan's core
   cudaEvent_t ev[2 * 16 + 2] = {};
   cudaStream_t stream = nullptr;  // stream of the last call (frees are ordered on it)
 };
@@ -248,6 +250,18 @@ void dfree(T*& ptr, cudaStream_t s) {
 void free_plan(rfd_plan* p, bool sync = true) {
   if (!p) return;
   cudaStream_t s = p->stream;
+  if (p->aux) {  // the frees below (stream-ordered on s) come after its work
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(e, p->aux);
+      cudaStreamWaitEvent(s, e, 0);
+      cudaEventDestroy(e);
+    } else {
+      cudaStreamSynchronize(p->aux);
+    }
+    cudaStreamDestroy(p->aux);
+    p->aux = nullptr;
+  }
   if (sync) cudaStreamSynchronize(s);
   dfree(p->pts, s);
   dfree(p->pts16, s);
@@ -347,9 +361,12 @@ int gram_spread_mode() {
   return atoi(e);
 }
 
+// before_core (rfd_gfi): called once G, the points and omega are on the
+// stream, before the core -- the one-shot GFI starts the field's pass 1 there.
 rfd_status create_impl(const float* points, int batch, int64_t n, double eps, double lambda,
                        int m, uint64_t seed, const rfd_shard* shard, cudaStream_t st,
-                       rfd_plan** plan_out) {
+                       rfd_plan** plan_out,
+                       const std::function<rfd_status(rfd_plan*)>& before_core = nullptr) {
   if (!plan_out) return fail(RFD_EINVAL, "plan_out is NULL");
   *plan_out = nullptr;
   if (!points) return fail(RFD_EINVAL, "points is NULL");
@@ -487,6 +504,11 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
     rfd::launch_sum_parts(parts, world, int64_t(rr), p->G, st);
   }
 
+  if (before_core) {
+    const rfd_status hs = before_core(p);
+    if (hs != RFD_OK) return hs;
+  }
+
   // a5: core
   {
     int sc = 0, sym = 1;
@@ -587,48 +609,34 @@ rfd_status ensure_workspace(rfd_plan* p, int d, cudaStream_t st) {
   return RFD_OK;
 }
 
-rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaStream_t st) {
-  if (!p) return fail(RFD_EINVAL, "plan is NULL");
-  if (!F || !out) return fail(RFD_EINVAL, "F/out is NULL");
-  if (d < 1) return fail(RFD_EINVAL, "d must be >= 1");
-  if (reinterpret_cast<uintptr_t>(F) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0)
-    return fail(RFD_EINVAL, "F/out must be 16-byte aligned");
-  p->stream = st;
-  rfd_status rs = ensure_workspace(p, d, st);
-  if (rs != RFD_OK) return rs;
-  // narrow fields: the whole inference in one cooperative SIMT launch
-  // (k_small.cu) for d = 1, batched, tiny and large clouds; single clouds of
-  // 4097 .. 65536 points with 2 <= d <= 4 are faster on the tensor-core passes
-  // (measured, graph replay: cfg 2 d = 3 16.1 vs 24.2 us; 18,944 points d = 3
-  // (barycenter) faster too; cfg 4 (200k) even; at 4M points d = 3 the narrow
-  // kernel wins: its contraction costs 2d FMA, the passes' split and MMA a
-  // fixed 16 columns).  RFD_NARROW=0 / 2 force either side (tests).
+// narrow fields: the whole inference in one cooperative SIMT launch
+// (k_small.cu) for d = 1, batched, tiny and large clouds; single clouds of
+// 4097 .. 65536 points with 2 <= d <= 4 are faster on the tensor-core passes
+// (measured, graph replay: cfg 2 d = 3 16.1 vs 24.2 us; 18,944 points d = 3
+// (barycenter) faster too; cfg 4 (200k) even; at 4M points d = 3 the narrow
+// kernel wins: its contraction costs 2d FMA, the passes' split and MMA a
+// fixed 16 columns).  RFD_NARROW=0 / 2 force either side (tests).
+bool use_narrow(const rfd_plan* p, int d) {
   const char* ne = getenv("RFD_NARROW");
   const int narrow_env = (ne && ne[0]) ? atoi(ne) : 1;
-  const bool narrow = d <= 4 && p->world == 1 && narrow_env != 0 &&
-                      (narrow_env == 2 || d == 1 || p->batch > 1 || p->n <= 4096 ||
-                       p->n > 65536);
-  if (narrow) {
-    const size_t need = rfd::small_partial_elems(p->m, p->n, p->batch, d, p->sms);
-    if (p->small_part_elems < need) {
-      dfree(p->small_part, st);
-      p->small_part_elems = 0;
-      RFD_CUDA(dalloc(&p->small_part, need, st));
-      p->small_part_elems = need;
-    }
-    RFD_CUDA(rfd::launch_integrate_small(p->pts, p->omega_rad4, p->m, p->n, p->batch, p->sms, F, d,
-                                         out, p->C, p->small_part, p->S, p->Y, p->bar, st));
-    p->last_d = d;
-    return RFD_OK;
-  }
+  return d <= 4 && p->world == 1 && narrow_env != 0 &&
+         (narrow_env == 2 || d == 1 || p->batch > 1 || p->n <= 4096 || p->n > 65536);
+}
+
+// Small r (<= 128) with d in one chunk and few partials: a7 (S reduction and
+// Y = C^ S) runs fused in pass 2's prologue -- two launches fewer per call
+// (every pass-2 CTA re-reduces its cloud's partials, hence the bound).
+bool fuse_a7(const rfd_plan* p, int d, int ranges) {
+  return p->world == 1 && p->r <= 128 && d <= 64 && int64_t(ranges) * p->r * d <= 16384;
+}
+
+// a6 (+ the S reduction unless fused): pass 1 on the tensor cores takes up to
+// 64 columns per launch (MMA N = the chunk's columns): the features are
+// regenerated once per chunk (NEXT-2).  Needs the plan's points, omega and
+// workspace (ensure_workspace) but not its core.
+void pass1_part(rfd_plan* p, const float* F, int d, cudaStream_t st) {
   const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
-  // Small r (<= 128) with d in one chunk and few partials: a7 (S reduction and
-  // Y = C^ S) runs fused in pass 2's prologue -- two launches fewer per call
-  // (every pass-2 CTA re-reduces its cloud's partials, hence the bound).
-  const bool fuse = p->world == 1 && p->r <= 128 && d <= 64 &&
-                    int64_t(ranges) * p->r * d <= 16384;
-  // pass 1 on the tensor cores takes up to 64 columns per launch (MMA N = the
-  // chunk's columns): the features are regenerated once per chunk (NEXT-2)
+  const bool fuse = fuse_a7(p, d, ranges);
   const int w1 = 64;
   for (int c0 = 0; c0 < d; c0 += w1) {
     const int dc = (d - c0 < w1) ? d - c0 : w1;
@@ -636,6 +644,13 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
                          dc, p->s_partial, st);
     if (!fuse) rfd::launch_reduce_S(p->s_partial, p->m, p->batch, ranges, d, c0, dc, p->S, st);
   }
+}
+
+// the rest of the inference after pass1_part: the shards' S exchange, a7
+// (unless fused into pass 2) and a8
+rfd_status tail_part(rfd_plan* p, const float* F, int d, float* out, cudaStream_t st) {
+  const int ranges = rfd::pass1_tc_ranges(p->m, p->n, p->batch, p->sms);
+  const bool fuse = fuse_a7(p, d, ranges);
   if (p->world > 1) {  // S = sum over the shards' partials, rank order
     rfd_status xs = exchange(p, p->S, p->S_parts, size_t(p->r) * d, st);
     if (xs != RFD_OK) return xs;
@@ -652,6 +667,87 @@ rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaSt
   }
   RFD_CUDA(cudaGetLastError());
   p->last_d = d;
+  return RFD_OK;
+}
+
+rfd_status check_field(const float* F, int d, const float* out) {
+  if (!F || !out) return fail(RFD_EINVAL, "F/out is NULL");
+  if (d < 1) return fail(RFD_EINVAL, "d must be >= 1");
+  if (reinterpret_cast<uintptr_t>(F) % 16 != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0)
+    return fail(RFD_EINVAL, "F/out must be 16-byte aligned");
+  return RFD_OK;
+}
+
+rfd_status integrate_impl(rfd_plan* p, const float* F, int d, float* out, cudaStream_t st) {
+  if (!p) return fail(RFD_EINVAL, "plan is NULL");
+  const rfd_status cf = check_field(F, d, out);
+  if (cf != RFD_OK) return cf;
+  p->stream = st;
+  rfd_status rs = ensure_workspace(p, d, st);
+  if (rs != RFD_OK) return rs;
+  if (use_narrow(p, d)) {
+    const size_t need = rfd::small_partial_elems(p->m, p->n, p->batch, d, p->sms);
+    if (p->small_part_elems < need) {
+      dfree(p->small_part, st);
+      p->small_part_elems = 0;
+      RFD_CUDA(dalloc(&p->small_part, need, st));
+      p->small_part_elems = need;
+    }
+    RFD_CUDA(rfd::launch_integrate_small(p->pts, p->omega_rad4, p->m, p->n, p->batch, p->sms, F, d,
+                                         out, p->C, p->small_part, p->S, p->Y, p->bar, st));
+    p->last_d = d;
+    return RFD_OK;
+  }
+  pass1_part(p, F, d, st);
+  return tail_part(p, F, d, out, st);
+}
+
+// One-shot GFI on device fields (rfd_gfi): plan and inference with pass 1
+// (which needs only the points, omega and the field) on a second stream
+// beside the plan's core -- the core's small DMMA GEMMs (128 threads, no
+// TMEM) fit on the SMs next to pass 1's persistent CTAs.  Same kernels and
+// results as rfd_plan_create + rfd_integrate.
+rfd_status gfi_impl(const float* points, int64_t n, double eps, double lambda, int m,
+                    uint64_t seed, const float* F, int d, float* out, cudaStream_t st,
+                    rfd_plan** plan_out) {
+  const rfd_status cf = check_field(F, d, out);
+  if (cf != RFD_OK) return cf;
+  if (!is_device_pointer(F) || !is_device_pointer(out))
+    return fail(RFD_EINVAL, "rfd_gfi: F and out must be device memory (rfd_gfi_host for host)");
+  rfd_plan* p = nullptr;
+  bool early = false;
+  auto hook = [&](rfd_plan* q) -> rfd_status {
+    q->stream = st;
+    if (use_narrow(q, d)) return RFD_OK;  // one launch after the plan
+    rfd_status rs = ensure_workspace(q, d, st);
+    if (rs != RFD_OK) return rs;
+    if (!q->aux) RFD_CUDA(cudaStreamCreateWithFlags(&q->aux, cudaStreamNonBlocking));
+    if (!q->ev[0]) RFD_CUDA(cudaEventCreateWithFlags(&q->ev[0], cudaEventDisableTiming));
+    if (!q->ev[1]) RFD_CUDA(cudaEventCreateWithFlags(&q->ev[1], cudaEventDisableTiming));
+    RFD_CUDA(cudaEventRecord(q->ev[0], st));
+    RFD_CUDA(cudaStreamWaitEvent(q->aux, q->ev[0], 0));
+    pass1_part(q, F, d, q->aux);
+    RFD_CUDA(cudaGetLastError());
+    RFD_CUDA(cudaEventRecord(q->ev[1], q->aux));
+    early = true;
+    return RFD_OK;
+  };
+  const rfd_status cs = create_impl(points, 1, n, eps, lambda, m, seed, nullptr, st, &p, hook);
+  if (cs != RFD_OK) return cs;
+  rfd_status rs = RFD_OK;
+  if (early) {
+    rs = cudaStreamWaitEvent(st, p->ev[1], 0) == cudaSuccess ? RFD_OK
+                                                            : fail(RFD_ECUDA, "rfd_gfi: event wait");
+    if (rs == RFD_OK) rs = tail_part(p, F, d, out, st);
+  } else {
+    rs = integrate_impl(p, F, d, out, st);
+  }
+  if (rs != RFD_OK || !plan_out) {
+    free_plan(p, false);  // stream-ordered (after the aux stream's work)
+    if (plan_out) *plan_out = nullptr;
+    return rs;
+  }
+  *plan_out = p;
   return RFD_OK;
 }
 
@@ -911,6 +1007,13 @@ rfd_status rfd_plan_spectrum(rfd_plan* plan, int32_t k, double* out, rfd_stream 
 rfd_status rfd_integrate(rfd_plan* plan, const float* F, int32_t d, float* out,
                          rfd_stream stream) {
   return integrate_impl(plan, F, d, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+rfd_status rfd_gfi(const float* points, int64_t n, double eps, double lambda, int32_t m,
+                   uint64_t seed, const float* F, int32_t d, float* out, rfd_stream stream,
+                   rfd_plan** plan_out) {
+  return gfi_impl(points, n, eps, lambda, m, seed, F, d, out,
+                  reinterpret_cast<cudaStream_t>(stream), plan_out);
 }
 
 rfd_status rfd_integrate_host(rfd_plan* plan, const float* F_host, int32_t d, float* out_host,

@@ -29,7 +29,7 @@ FIELDS = {"omega": 0, "nu": 1, "gram": 2, "core": 3, "S": 4, "Y": 5}
 EXPORTED = ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_create_sharded",
             "rfd_plan_reparam",
             "rfd_plan_spectrum", "rfd_barycenter", "rfd_integrate",
-            "rfd_integrate_host", "rfd_gfi_host", "rfd_destroy", "rfd_last_error",
+            "rfd_integrate_host", "rfd_gfi", "rfd_gfi_host", "rfd_destroy", "rfd_last_error",
             "rfd_plan_info",
             "rfd_plan_export", "rfd_launch_count", "rfd_profile_enable",
             "rfd_profile_only", "rfd_profile_read")
@@ -139,6 +139,7 @@ def load_library(path=LIB_PATH):
     lib.rfd_integrate.argtypes = [vp, vp, i32, vp, vp]
     lib.rfd_integrate_host.argtypes = [vp, vp, i32, vp, vp]
     lib.rfd_gfi_host.argtypes = [vp, i64, dbl, dbl, i32, u64, vp, i32, vp, vp, pp]
+    lib.rfd_gfi.argtypes = [vp, i64, dbl, dbl, i32, u64, vp, i32, vp, vp, pp]
     lib.rfd_destroy.argtypes = [vp]
     lib.rfd_destroy.restype = None
     lib.rfd_last_error.restype = ctypes.c_char_p
@@ -152,7 +153,7 @@ def load_library(path=LIB_PATH):
     for name in ("rfd_plan_create", "rfd_plan_create_batched", "rfd_plan_create_sharded",
                  "rfd_plan_reparam",
                  "rfd_plan_spectrum", "rfd_barycenter", "rfd_integrate",
-                 "rfd_integrate_host", "rfd_gfi_host", "rfd_plan_info", "rfd_plan_export",
+                 "rfd_integrate_host", "rfd_gfi", "rfd_gfi_host", "rfd_plan_info", "rfd_plan_export",
                  "rfd_profile_enable", "rfd_profile_only"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -367,6 +368,41 @@ class Plan:
         return arr
 
 
+def _plan_from_handle(handle, n, eps, lam, m, seed):
+    plan = Plan.__new__(Plan)
+    plan._h, plan._keep, plan._shard = handle, None, None
+    plan.batch, plan.n, plan.m, plan.r = 1, n, int(m), 2 * int(m)
+    plan.eps, plan.lam, plan.seed = float(eps), float(lam), int(seed)
+    return plan
+
+
+def gfi(points, eps, lam, m, seed, F, out=None, keep_plan=False, stream=None):
+    """rfd_gfi: plan + integrate of a DEVICE field in one call (pass 1 beside
+    the plan's core).  points (N, 3) float32 (host or device); F (N[, d])
+    float32 on the GPU; out like F (allocated when None).  Returns out, or
+    (out, Plan) when keep_plan."""
+    import torch
+    lib = load_library()
+    _check_f32(points, "points")
+    _check_f32(F, "F")
+    n = int(points.shape[0])
+    if tuple(points.shape) != (n, 3) or int(F.shape[0]) != n:
+        raise ValueError("points (N, 3) and F (N[, d]) expected")
+    if out is None:
+        out = torch.empty_like(F)
+    _check_f32(out, "out")
+    if tuple(out.shape) != tuple(F.shape):
+        raise ValueError("out must have F's shape")
+    d = 1 if len(F.shape) == 1 else int(F.shape[1])
+    handle = ctypes.c_void_p()
+    _check(lib.rfd_gfi(_ptr(points), n, float(eps), float(lam), int(m), int(seed), _ptr(F), d,
+                       _ptr(out), _stream_handle(stream),
+                       ctypes.byref(handle) if keep_plan else None))
+    if not keep_plan:
+        return out
+    return out, _plan_from_handle(handle, n, eps, lam, m, seed)
+
+
 def gfi_host(points, eps, lam, m, seed, F_host, out_host, keep_plan=False, stream=None):
     """rfd_gfi_host: plan + integrate from HOST buffers in one call, the
     transfers overlapped with the computation.  points (N, 3), F_host and
@@ -386,11 +422,7 @@ def gfi_host(points, eps, lam, m, seed, F_host, out_host, keep_plan=False, strea
                             ctypes.byref(handle) if keep_plan else None))
     if not keep_plan:
         return None
-    plan = Plan.__new__(Plan)
-    plan._h, plan._keep, plan._shard = handle, None, None
-    plan.batch, plan.n, plan.m, plan.r = 1, n, int(m), 2 * int(m)
-    plan.eps, plan.lam, plan.seed = float(eps), float(lam), int(seed)
-    return plan
+    return _plan_from_handle(handle, n, eps, lam, m, seed)
 
 
 def launch_count():

@@ -683,6 +683,26 @@ def test_gram_spread_grid_parity(cfg, n, shift, monkeypatch):
     assert relerr(Gs["2"], Gs["0"]) <= 2e-5
 
 
+@pytest.mark.parametrize("cfg,n,spread", [(1, None, "1"), (2, None, "1"), (5, 262144, "2"),
+                                          (5, 262144, "0")])
+def test_gfi_one_shot_equals_plan_and_integrate(cfg, n, spread, monkeypatch):
+    # rfd_gfi runs pass 1 on a second stream beside the plan's core: same
+    # kernels, so bitwise the two-call result; the returned plan is reusable
+    monkeypatch.setenv("RFD_GRAM_SPREAD", spread)
+    p, x, F = make_config(cfg, **({"n": n} if n else {}))
+    xd, Fd = torch.from_numpy(x).cuda(), torch.from_numpy(np.ascontiguousarray(F)).cuda()
+    ref = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"]).integrate(Fd)
+    out = rfd.gfi(xd, p["eps"], p["lam"], p["m"], p["seed"], Fd)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    out2, plan = rfd.gfi(x, p["eps"], p["lam"], p["m"], p["seed"], Fd, keep_plan=True)  # host points
+    assert torch.equal(out2, ref)
+    assert torch.equal(plan.integrate(Fd), ref)
+    with pytest.raises(rfd.RFDError):
+        rfd.gfi(xd, p["eps"], p["lam"], p["m"], p["seed"], torch.from_numpy(np.ascontiguousarray(F)),
+                torch.empty_like(Fd))
+
+
 @pytest.mark.parametrize("mode", ["0", "2"])
 @pytest.mark.parametrize("shape", ["point", "line", "plane"])
 def test_gram_spread_grid_degenerate_extents(shape, mode, monkeypatch):
