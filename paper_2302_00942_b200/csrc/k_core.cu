@@ -101,7 +101,11 @@ struct GemmJobs {
 #ifndef RFD_DGEMM_STAGES
 #define RFD_DGEMM_STAGES 3
 #endif
-constexpr int kBM = 32, kBN = 32, kBK = RFD_DGEMM_BK, kGStages = RFD_DGEMM_STAGES;
+#ifndef RFD_DGEMM_BM
+#define RFD_DGEMM_BM 32
+#endif
+constexpr int kBM = RFD_DGEMM_BM, kBN = 32, kBK = RFD_DGEMM_BK, kGStages = RFD_DGEMM_STAGES;
+constexpr int kGThreads = 64 * (kBM / 16);  // warps of 16 x 16: (kBM / 16) x 2
 constexpr int kSA = kBK + 4;   // A tile row stride (doubles): 8g + 2t banks, distinct
 constexpr int kSB = kBN + 4;   // B tile row stride (doubles)
 constexpr int kGemmSmem = kGStages * (kBM * kSA + kBK * kSB) * 8;
@@ -123,12 +127,12 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kGThreads)
 dgemm_kernel(GemmJobs jobs, int njobs, int r, int sym) {
   extern __shared__ __align__(16) double gsm[];
   const int jb = blockIdx.z % njobs, b = blockIdx.z / njobs;
   const int i0 = blockIdx.y * kBM, j0 = blockIdx.x * kBN;
-  if (sym && i0 > j0) return;  // strictly below the diagonal: the mirror of (j, i)
+  if (sym && i0 >= j0 + kBN) return;  // strictly below the diagonal: the mirror of (j, i)
   const GemmJob& J = (jb == 0) ? jobs.job[0] : jobs.job[1];
   const int64_t off = int64_t(b) * r * r;
   const double* __restrict__ A = J.A + off;
@@ -144,15 +148,15 @@ dgemm_kernel(GemmJobs jobs, int njobs, int r, int sym) {
     // A: 32 rows x kBK doubles, B: kBK rows x 32 doubles, in 16-byte chunks
     constexpr int kAc = kBK / 2;  // chunks per A row
 #pragma unroll
-    for (int l = 0; l < kBM * kAc / 128; ++l) {
-      const int e = tid + 128 * l, row = e / kAc, kc = (e % kAc) * 2;
+    for (int l = 0; l < kBM * kAc / kGThreads; ++l) {
+      const int e = tid + kGThreads * l, row = e / kAc, kc = (e % kAc) * 2;
       const int gi = i0 + row, gk = k0 + kc;
       const bool ok = gi < r && gk < r;
       cp_async16(As + (st * kBM + row) * kSA + kc, ok ? A + int64_t(gi) * r + gk : A, ok);
     }
 #pragma unroll
-    for (int l = 0; l < kBK * 16 / 128; ++l) {
-      const int e = tid + 128 * l, kk = e >> 4, col = (e & 15) * 2;
+    for (int l = 0; l < kBK * 16 / kGThreads; ++l) {
+      const int e = tid + kGThreads * l, kk = e >> 4, col = (e & 15) * 2;
       const int gk = k0 + kk, gj = j0 + col;
       const bool ok = gk < r && gj < r;
       cp_async16(Bs + (st * kBK + kk) * kSB + col, ok ? B + int64_t(gk) * r + gj : B, ok);
@@ -234,7 +238,7 @@ void gemm(const GemmJobs& jobs, int njobs, int r, int batch, bool sym, cudaStrea
     configured = true;
   }
   const dim3 grid((r + kBN - 1) / kBN, (r + kBM - 1) / kBM, njobs * batch);
-  dgemm_kernel<<<grid, 128, kGemmSmem, s>>>(jobs, njobs, r, sym ? 1 : 0);
+  dgemm_kernel<<<grid, kGThreads, kGemmSmem, s>>>(jobs, njobs, r, sym ? 1 : 0);
 }
 
 GemmJob job(const double* A, const double* B, double* C, double alpha, double sigma = 0.0,
