@@ -9,6 +9,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2302_00942_b200 import rfd  # noqa: E402
 from workloads import make_config  # noqa: E402
 
+if len(sys.argv) > 1:  # another build of the library (A/B)
+    rfd.load_library(sys.argv[1])
 p, x, F = make_config(5)
 xd, Fd = torch.from_numpy(x).cuda(), torch.from_numpy(F).cuda()
 out = torch.empty_like(Fd)
