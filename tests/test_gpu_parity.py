@@ -724,6 +724,22 @@ def test_gram_spread_grid_degenerate_extents(shape, mode, monkeypatch):
     _check_against_oracle(plan, out, x, F, p)
 
 
+def test_gram_spread_grid_cell_beyond_fold(monkeypatch):
+    # 20,000 points in one grid cell: more than the tensor-core spread's 8192
+    # points per exact class-sum fold, so the fold carries its remainder
+    # (k_nufft.cu); parity and bitwise determinism as everywhere else
+    monkeypatch.setenv("RFD_GRAM_SPREAD", "2")
+    rng = np.random.default_rng(5)
+    n = 20000
+    x = (np.array([0.1, 0.2, -0.3]) + 1e-4 * rng.standard_normal((n, 3))).astype(np.float32)
+    F = rng.standard_normal((n, 4)).astype(np.float32)
+    p = dict(name="spread one cell", eps=0.05, lam=-0.4, m=128, seed=2)
+    plan, out = _run_single(x, F, p)
+    assert plan.info()["gram_nodes"] > 0
+    np.testing.assert_array_equal(plan.export("gram"), _run_single(x, F, p)[0].export("gram"))
+    _check_against_oracle(plan, out, x, F, p)
+
+
 def test_gram_spread_grid_declines_large_extent(monkeypatch):
     # cfg 4's sheet scaled x 200 would need > 2^11 nodes per axis: even
     # forced, the plan takes the direct Gram
