@@ -107,6 +107,9 @@ struct GemmJobs {
 #endif
 constexpr int kBM = RFD_DGEMM_BM, kBN = 32, kBK = RFD_DGEMM_BK, kGStages = RFD_DGEMM_STAGES;
 static_assert(kBM == kBN, "the symmetric route enumerates square tiles");
+#ifndef RFD_DGEMM_PDL
+#define RFD_DGEMM_PDL 1  // (gfi step at cfg 5: 2.287 -> 2.279 ms)
+#endif
 #ifndef RFD_DGEMM_KSPLIT
 #define RFD_DGEMM_KSPLIT 2  // (measured at r = 512: 18.4 / 17.6 / 19.1 us with 1 / 2 / 4)
 #endif
@@ -158,6 +161,12 @@ dgemm_kernel(GemmJobs jobs, int njobs, int r, int sym) {
   const int wm = (wq >> 1) * 16, wn = (wq & 1) * 16;  // the warp's 16 x 16
   double* As = gsm;                                  // [stage][kBM][kSA]
   double* Bs = gsm + kGStages * kBM * kSA;           // [stage][kBK][kSB]
+#if RFD_DGEMM_PDL
+  // programmatic dependent launch: the next product's CTAs may be scheduled
+  // now; this one's operands are read only once the previous grid is done
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
 
   auto load_tile = [&](int st, int k0) {
     // A: 32 rows x kBK doubles, B: kBK rows x 32 doubles, in 16-byte chunks
@@ -273,7 +282,11 @@ void gemm(const GemmJobs& jobs, int njobs, int r, int batch, bool sym, cudaStrea
   const int T = (r + kBN - 1) / kBN;
   const dim3 grid = sym ? dim3(T * (T + 1) / 2, 1, njobs * batch)
                         : dim3((r + kBN - 1) / kBN, (r + kBM - 1) / kBM, njobs * batch);
+#if RFD_DGEMM_PDL
+  launch_pdl(dgemm_kernel, grid, dim3(kGThreads), kGemmSmem, s, jobs, njobs, r, sym ? 1 : 0);
+#else
   dgemm_kernel<<<grid, kGThreads, kGemmSmem, s>>>(jobs, njobs, r, sym ? 1 : 0);
+#endif
 }
 
 GemmJob job(const double* A, const double* B, double* C, double alpha, double sigma = 0.0,
