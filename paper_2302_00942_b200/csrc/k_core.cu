@@ -111,7 +111,8 @@ static_assert(kBM == kBN, "the symmetric route enumerates square tiles");
 #define RFD_DGEMM_PDL 1  // (gfi step at cfg 5: 2.287 -> 2.279 ms)
 #endif
 #ifndef RFD_DGEMM_KSPLIT
-#define RFD_DGEMM_KSPLIT 2  // (measured at r = 512: 18.4 / 17.6 / 19.1 us with 1 / 2 / 4)
+#define RFD_DGEMM_KSPLIT 1  // (alone at r = 512: 18.4 / 17.6 / 19.1 us with 1 / 2 / 4; 2 groups
+                            // do not fit beside pass 1: rfd_gfi 2.10 vs 2.24 ms)
 #endif
 constexpr int kKS = RFD_DGEMM_KSPLIT;  // warp groups splitting each K tile
 constexpr int kGThreads = 64 * (kBM / 16) * kKS;  // warps of 16 x 16: (kBM / 16) x 2 per group
@@ -136,7 +137,13 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-__global__ void __launch_bounds__(kGThreads)
+// 128 threads at <= 80 registers: one warp per sub-partition fits beside a
+// pass-1 CTA (k_pass1_tc.cu, RFD_P1_MAXNREG), so rfd_gfi's core runs on the
+// SMs beside pass 1 (uncapped, the 1-group kernel takes 96 registers)
+#ifndef RFD_DGEMM_MINB
+#define RFD_DGEMM_MINB (RFD_DGEMM_KSPLIT == 1 ? 6 : 1)
+#endif
+__global__ void __launch_bounds__(kGThreads, RFD_DGEMM_MINB)
 dgemm_kernel(GemmJobs jobs, int njobs, int r, int sym) {
   extern __shared__ __align__(16) double gsm[];
   const int jb = blockIdx.z % njobs, b = blockIdx.z / njobs;
@@ -274,6 +281,8 @@ void gemm(const GemmJobs& jobs, int njobs, int r, int batch, bool sym, cudaStrea
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(dgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+    // (the whole carveout: the CTA fits beside a pass-1 CTA, rfd_gfi)
+    cudaFuncSetAttribute(dgemm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     configured = true;
   }
   // symmetric route: only the T (T + 1) / 2 tiles on and above the diagonal

@@ -501,8 +501,22 @@ constexpr int kSmem = 2 * kEpochB + kStageF;
 // Diagnostics (RFD_P1_TRACE=1): per-chunk timestamps of CTA (0, 0, 0).
 __device__ long long g_p1trace[1024][12];
 
+// At most 72 registers (maxnreg): with 21 warps per CTA, sub-partition 0
+// holds 6 of them; at 72 registers (2304 per warp) 2560 of its 16384 remain,
+// enough for one warp of the core's DMMA GEMM (80 registers) -- so in rfd_gfi
+// the core's GEMMs run on the SMs beside pass 1 instead of waiting for it
+// (gfi step 2.27 -> 2.10 ms at cfg 5; at 80 registers no GEMM CTA fits).
+// Pass 1 alone is also faster at 72 (0.756 -> 0.739 ms; spills the same).
+#ifndef RFD_P1_MAXNREG
+#define RFD_P1_MAXNREG 72
+#endif
+#if RFD_P1_MAXNREG
+#define P1_BOUNDS(t) __maxnreg__(RFD_P1_MAXNREG)
+#else
+#define P1_BOUNDS(t) __launch_bounds__(t, 1)
+#endif
 template <int PW, bool kTr = false>
-__global__ void __launch_bounds__((PW + 5) * 32, 1)
+__global__ void P1_BOUNDS((PW + 5) * 32)
 pass1_tc_kernel16(const float* __restrict__ pts16, const float4* __restrict__ omega4, int m,
                 int64_t n, int ranges, const float* __restrict__ F, int d, int c0, int dc,
                 float* __restrict__ partial) {
@@ -1321,6 +1335,9 @@ void launch_pass1_tc(const float* pts16, const float4* omega4, int m, int64_t n,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, k16::kSmem);
         cudaFuncSetAttribute(pass1_tc_kernel16<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              k16::kSmem);
+        // the whole shared-memory carveout: room for a core GEMM CTA beside
+        cudaFuncSetAttribute(pass1_tc_kernel16<16>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             100);
         configured = true;
       }
       if (trace) {

@@ -1198,6 +1198,22 @@ rfd_status rfd_profile_only(const char* name) {
 
 int32_t rfd_profile_read(rfd_profile_entry* entries, int32_t cap) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
+  // RFD_TIMELINE=path (instrumentation): also append every launch's start and
+  // end (ms from the first recorded launch) -- the overlap of the streams
+  if (const char* tl = getenv("RFD_TIMELINE")) {
+    if (FILE* f = (tl[0] && !g_pending.empty()) ? fopen(tl, "a") : nullptr) {
+      const cudaEvent_t t0 = g_pending.front().a;
+      for (const Pending& pe : g_pending) {
+        float s0 = 0.0f, s1 = 0.0f;
+        cudaEventSynchronize(pe.b);
+        cudaEventElapsedTime(&s0, t0, pe.a);
+        cudaEventElapsedTime(&s1, t0, pe.b);
+        fprintf(f, "%s %.4f %.4f\n", pe.name, s0, s1);
+      }
+      fprintf(f, "--\n");
+      fclose(f);
+    }
+  }
   for (const Pending& pe : g_pending) {
     float ms = 0.0f;
     cudaEventSynchronize(pe.b);
