@@ -9,6 +9,9 @@ import torch  # noqa: E402
 from paper_2302_00942_b200 import rfd  # noqa: E402
 from workloads import make_config  # noqa: E402
 
+if len(sys.argv) > 1:  # another build of the library (A/B)
+    rfd.load_library(sys.argv[1])
+
 for cfg in (1, 2, 4, 3):
     p, x, F = make_config(cfg)
     if cfg == 3:
