@@ -331,13 +331,40 @@ void launch_core_prep(const double* G, const double* nu, const int* flags, doubl
                                                                   norm_bits);
 }
 
+void launch_core_powers(const double* Z, int m, int batch, bool sym, double alpha, double* work,
+                        cudaStream_t s) {
+  const int r = 2 * m;
+  const int64_t S = int64_t(r) * r * batch;
+  double* Z2 = work;
+  double* Z3 = work + S;
+  double* Z4 = work + 2 * S;
+  double* Z5 = work + 3 * S;
+  // (alpha Z)^2 = a^2 Z Z; (alpha Z)^3 = a Z2 Z and (alpha Z)^4 = Z2 Z2
+  // together; (alpha Z)^5 = a Z4 Z
+  GemmJobs j{};
+  j.job[0] = job(Z, Z, Z2, alpha * alpha);
+  gemm(j, 1, r, batch, sym, s);
+  j.job[0] = job(Z2, Z, Z3, alpha);
+  j.job[1] = job(Z2, Z2, Z4, 1.0);
+  gemm(j, 2, r, batch, sym, s);
+  j.job[0] = job(Z4, Z, Z5, alpha);
+  gemm(j, 1, r, batch, sym, s);
+}
+
 void launch_core_eval(const double* Z, const double* nu, const int* flags, double lambda,
-                      int m, int batch, int s_scale, bool sym, double* work, double* C,
-                      int* oflag, cudaStream_t s) {
+                      int m, int batch, int s_scale, bool sym, double pw_alpha, double* work,
+                      double* C, int* oflag, cudaStream_t s) {
   const int r = 2 * m;
   const int64_t rr = int64_t(r) * r;
   const dim3 egrid(unsigned((rr + 255) / 256), batch);
   const double alpha = ldexp(1.0, -s_scale);  // Z0 = alpha Z
+  // work[0..4) holds (pw_alpha Z)^k, k = 2..5 (launch_core_powers); Z0^k =
+  // q[k] (pw_alpha Z)^k with q[k] = (alpha / pw_alpha)^k, a power of two:
+  // folded into the coefficients below (exact, so the result does not depend
+  // on when the powers were formed)
+  double q[6];
+  q[0] = 1.0;
+  for (int k = 1; k <= 5; ++k) q[k] = q[k - 1] * (alpha / pw_alpha);
   // Taylor coefficients of phi1: c_k = 1 / (k+1)!
   double c[kTaylor + 1];
   double f = 1.0;
@@ -346,7 +373,7 @@ void launch_core_eval(const double* Z, const double* nu, const int* flags, doubl
     c[k] = 1.0 / f;
   }
   const int64_t S = rr * batch;  // one matrix (all clouds)
-  double* Z2 = work;             // Z0^2 .. Z0^5
+  double* Z2 = work;             // (pw_alpha Z)^2 .. (pw_alpha Z)^5
   double* Z3 = work + S;
   double* Z4 = work + 2 * S;
   double* Z5 = work + 3 * S;
@@ -356,33 +383,23 @@ void launch_core_eval(const double* Z, const double* nu, const int* flags, doubl
   double* E = work + 7 * S;
   double* Pn = work + 8 * S;
   double* En = work + 9 * S;
-  {  // powers: Z0^2 = a^2 Z Z; Z0^3 = a Z0^2 Z and Z0^4 = Z0^2 Z0^2 together; Z0^5 = a Z0^4 Z
-    GemmJobs j{};
-    j.job[0] = job(Z, Z, Z2, alpha * alpha);
-    gemm(j, 1, r, batch, sym, s);
-    j.job[0] = job(Z2, Z, Z3, alpha);
-    j.job[1] = job(Z2, Z2, Z4, 1.0);
-    gemm(j, 2, r, batch, sym, s);
-    j.job[0] = job(Z4, Z, Z5, alpha);
-    gemm(j, 1, r, batch, sym, s);
-  }
   // B_q = sum_{i<5} c_{5q+i} Z0^i  (Z0^1 = alpha Z); Horner in Z0^5 from the top:
   // T = B_3 + c_20 Z0^5, then T <- Z0^5 T + B_q for q = 2, 1, 0.
   {  // T = B_3 + c_20 Z0^5
     LaunchScope L("rfd_core_combo", s);
-    combo_kernel<<<egrid, 256, 0, s>>>(Ta, Z, Z2, Z3, Z4, Z5, c[16] * alpha, c[17], c[18], c[19],
-                                       c[20], c[15], r);
+    combo_kernel<<<egrid, 256, 0, s>>>(Ta, Z, Z2, Z3, Z4, Z5, c[16] * alpha, c[17] * q[2],
+                                       c[18] * q[3], c[19] * q[4], c[20] * q[5], c[15], r);
   }
   double* T = Ta;
   double* Tn = Tb;
-  for (int q = 2; q >= 0; --q) {
+  for (int h = 2; h >= 0; --h) {
     GemmJobs j{};
-    GemmJob g = job(Z5, T, q == 0 ? P : Tn, 1.0, 0.0, c[kPS * q]);
+    GemmJob g = job(Z5, T, h == 0 ? P : Tn, q[5], 0.0, c[kPS * h]);
     g.nm = 4;
-    g.M[0] = Z; g.mc[0] = c[kPS * q + 1] * alpha;
-    g.M[1] = Z2; g.mc[1] = c[kPS * q + 2];
-    g.M[2] = Z3; g.mc[2] = c[kPS * q + 3];
-    g.M[3] = Z4; g.mc[3] = c[kPS * q + 4];
+    g.M[0] = Z; g.mc[0] = c[kPS * h + 1] * alpha;
+    g.M[1] = Z2; g.mc[1] = c[kPS * h + 2] * q[2];
+    g.M[2] = Z3; g.mc[2] = c[kPS * h + 3] * q[3];
+    g.M[3] = Z4; g.mc[3] = c[kPS * h + 4] * q[4];
     j.job[0] = g;
     gemm(j, 1, r, batch, sym, s);
     double* t = T; T = Tn; Tn = t;

@@ -144,6 +144,7 @@ struct rfd_plan {
   cudaStream_t aux = nullptr;  // rfd_gfi: pass 1 beside the plan's core
   cudaEvent_t ev[2 * 16 + 2] = {};
   cudaStream_t stream = nullptr;  // stream of the last call (frees are ordered on it)
+  bool core_pending = false;      // the core's overflow flag is read back but not yet checked
 };
 
 namespace {
@@ -302,13 +303,99 @@ struct TempBuffers {
   }
 };
 
+// Host read-backs (the bounding box, omega and the frequency flags for a4's
+// grid; ||Z||_1 and the overflow flag of the core) go through a per-thread
+// pinned buffer and an event: a pageable cudaMemcpyAsync blocks the host for
+// its own round trip (two in a row plus a stream synchronisation took ~44 us
+// of idle GPU in the cfg-5 step), and an event wait does not wait for work
+// enqueued behind the copy.  Slots: the core's flags, the box, the frequency
+// flags, omega (RFD_MAX_M float4).
+struct HostSlot {
+  char* buf = nullptr;
+  cudaEvent_t ev = nullptr, ev_src = nullptr;
+  cudaStream_t side = nullptr;  // copies the work stream must not wait for
+  int dev = -1;
+};
+constexpr size_t kSlotCore = 0, kSlotBox = 64, kSlotFlags = 128, kSlotOmega = 256;
+constexpr size_t kSlotBytes = kSlotOmega + size_t(RFD_MAX_M) * sizeof(float4);
+rfd_status host_slot(HostSlot** out) {
+  thread_local HostSlot h;  // lives as long as the thread (not freed at exit)
+  int dev = 0;
+  RFD_CUDA(cudaGetDevice(&dev));
+  if (h.dev != dev) {  // (a thread that moves to another device: fresh events, stream)
+    RFD_CUDA(cudaEventCreateWithFlags(&h.ev, cudaEventDisableTiming));
+    RFD_CUDA(cudaEventCreateWithFlags(&h.ev_src, cudaEventDisableTiming));
+    RFD_CUDA(cudaStreamCreateWithFlags(&h.side, cudaStreamNonBlocking));
+    h.dev = dev;
+  }
+  if (!h.buf) RFD_CUDA(cudaMallocHost(&h.buf, kSlotBytes));
+  *out = &h;
+  return RFD_OK;
+}
+// wait for everything enqueued on st up to now (not for later work)
+rfd_status slot_wait(HostSlot* h, cudaStream_t st) {
+  RFD_CUDA(cudaEventRecord(h->ev, st));
+  RFD_CUDA(cudaEventSynchronize(h->ev));
+  return RFD_OK;
+}
+
+// One kernel gathers what a4's grid sizing needs (the box, the frequency
+// flags, omega) straight into the pinned slot buffer (mapped: cudaMallocHost
+// memory is device-accessible under unified addressing) -- one small launch
+// instead of three in-stream copies, each with the copy engine's latency.
+__global__ void gather_readback_kernel(const unsigned int* __restrict__ bbox,
+                                       const int* __restrict__ flags,
+                                       const float4* __restrict__ omega4, int m,
+                                       char* __restrict__ host) {
+  unsigned int* hb = reinterpret_cast<unsigned int*>(host + kSlotBox);
+  int* hf = reinterpret_cast<int*>(host + kSlotFlags);
+  float4* ho = reinterpret_cast<float4*>(host + kSlotOmega);
+  if (threadIdx.x < 6) hb[threadIdx.x] = bbox[threadIdx.x];
+  if (threadIdx.x == 0) hf[0] = flags[0];
+  for (int k = threadIdx.x; k < m; k += blockDim.x) ho[k] = omega4[k];
+}
+
+// D2H copy of what st has computed so far into the slot buffer, on the side
+// stream: an in-stream copy delays st's next kernel by the copy's latency
+// (~8-17 us measured between the core's kernels); h->ev marks its completion
+rfd_status slot_copy_side(HostSlot* h, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  RFD_CUDA(cudaEventRecord(h->ev_src, st));
+  RFD_CUDA(cudaStreamWaitEvent(h->side, h->ev_src, 0));
+  RFD_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->side));
+  RFD_CUDA(cudaEventRecord(h->ev, h->side));
+  return RFD_OK;
+}
+
+// the core's overflow flag, copied back by core_impl (deferred check)
+rfd_status core_finish(rfd_plan* p) {
+  if (!p->core_pending) return RFD_OK;
+  p->core_pending = false;
+  HostSlot* h = nullptr;
+  const rfd_status hs = host_slot(&h);
+  if (hs != RFD_OK) return hs;
+  RFD_CUDA(cudaEventSynchronize(h->ev));
+  int of = 0;
+  memcpy(&of, h->buf + kSlotCore + 4 * sizeof(int), sizeof(int));
+  if (of) return fail(RFD_ERANGE, "core: exp(lambda W~) overflows (lambda > 0 or negative nu)");
+  return RFD_OK;
+}
+
 // a5 on the plan's G: C = lambda D phi1(lambda G D) for the given nu (its
-// sign flags in flags[0]); the scaling exponent is read back first.  Blocks
-// the host.  flags[2..4] are scratch.
+// sign flags in flags[0]); ||Z||_1 is read back for the scaling exponent s.
+// flags[2..4] are scratch.  known_sym: the route, when the host has already
+// read the frequency flags (-1: not yet) -- the powers Z^2..Z^5 (independent
+// of s, launch_core_powers with pw_alpha = 1) are then enqueued before the
+// host waits, so the GEMM chain has no gap.  defer: the overflow flag is
+// copied back but not waited for (p->core_pending; core_finish checks it once
+// the caller has enqueued its next work); otherwise this blocks the host.
 rfd_status core_impl(rfd_plan* p, const double* nu, int* flags, double lambda, double* C,
-                     int* scaling_out, int* symmetric_out, cudaStream_t st) {
+                     int* scaling_out, int* symmetric_out, cudaStream_t st, int known_sym = -1,
+                     bool defer = false) {
   const int m = p->m, batch = p->batch;
   const size_t rr = size_t(p->r) * p->r;
+  HostSlot* h = nullptr;
+  const rfd_status hs = host_slot(&h);
+  if (hs != RFD_OK) return hs;
   TempBuffers tmp(st);
   double *Z = nullptr, *work = nullptr;
   RFD_CUDA(tmp.alloc(&Z, rr * batch));
@@ -316,11 +403,16 @@ rfd_status core_impl(rfd_plan* p, const double* nu, int* flags, double lambda, d
   rfd::launch_core_prep(p->G, nu, flags, lambda, m, batch, Z,
                         reinterpret_cast<unsigned long long*>(flags + 2), st);
   RFD_CUDA(cudaGetLastError());
-  int hflags[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  RFD_CUDA(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
-  RFD_CUDA(cudaStreamSynchronize(st));
+  int* hflags = reinterpret_cast<int*>(h->buf + kSlotCore);
+  rfd_status xs = slot_copy_side(h, hflags, flags, 8 * sizeof(int), st);
+  if (xs != RFD_OK) return xs;
+  // unscaled powers are safe (no overflow) while ||Z||_1 <= 1e40
+  constexpr double kUnscaledMax = 1e40;
+  if (known_sym >= 0) rfd::launch_core_powers(Z, m, batch, known_sym == 1, 1.0, work, st);
+  RFD_CUDA(cudaEventSynchronize(h->ev));
   if (hflags[0] & 2)
     return fail(RFD_ERANGE, "frequency sampler exhausted its attempts (R too small?)");
+  const bool sym = (hflags[0] & 1) == 0;
   double znorm;
   memcpy(&znorm, hflags + 2, sizeof(double));
   // Scaling exponent: smallest s >= 0 with ||Z||_1 / 2^s <= kCoreTheta.
@@ -328,16 +420,21 @@ rfd_status core_impl(rfd_plan* p, const double* nu, int* flags, double lambda, d
     return fail(RFD_ERANGE, "core: ||lambda G D|| is not finite or too large");
   int s_scale = 0;
   while (ldexp(znorm, -s_scale) > rfd::kCoreTheta) ++s_scale;
-  rfd::launch_core_eval(Z, nu, flags, lambda, m, batch, s_scale, (hflags[0] & 1) == 0, work, C,
-                        flags + 4, st);
+  double pw = 1.0;
+  if (znorm > kUnscaledMax) {
+    pw = ldexp(1.0, -s_scale);
+    rfd::launch_core_powers(Z, m, batch, sym, pw, work, st);
+  } else if (known_sym < 0) {
+    rfd::launch_core_powers(Z, m, batch, sym, 1.0, work, st);
+  }
+  rfd::launch_core_eval(Z, nu, flags, lambda, m, batch, s_scale, sym, pw, work, C, flags + 4, st);
   RFD_CUDA(cudaGetLastError());
-  RFD_CUDA(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
-  RFD_CUDA(cudaStreamSynchronize(st));
-  if (hflags[4])
-    return fail(RFD_ERANGE, "core: exp(lambda W~) overflows (lambda > 0 or negative nu)");
   *scaling_out = s_scale;
-  *symmetric_out = (hflags[0] & 1) ? 0 : 1;
-  return RFD_OK;
+  *symmetric_out = sym ? 1 : 0;
+  xs = slot_copy_side(h, hflags, flags, 8 * sizeof(int), st);
+  if (xs != RFD_OK) return xs;
+  p->core_pending = true;
+  return defer ? RFD_OK : core_finish(p);
 }
 
 // all-gather of `count` fp64 through the caller's collective (sharded plans)
@@ -366,7 +463,8 @@ int gram_spread_mode() {
 rfd_status create_impl(const float* points, int batch, int64_t n, double eps, double lambda,
                        int m, uint64_t seed, const rfd_shard* shard, cudaStream_t st,
                        rfd_plan** plan_out,
-                       const std::function<rfd_status(rfd_plan*)>& before_core = nullptr) {
+                       const std::function<rfd_status(rfd_plan*)>& before_core = nullptr,
+                       bool defer_core = false) {
   if (!plan_out) return fail(RFD_EINVAL, "plan_out is NULL");
   *plan_out = nullptr;
   if (!points) return fail(RFD_EINVAL, "points is NULL");
@@ -461,16 +559,22 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   // sized from the bounding box and omega read back here
   rfd::NufftGrid ng{};
   bool spread = false;
+  int known_sym = -1;  // the core's route, once the frequency flags are read back
   const int spread_mode = gram_spread_mode();
   if (spread_mode != 0 && batch == 1 && rfd::gram_tc_pairs(m) &&
       (spread_mode == 2 || n >= kSpreadMinPoints)) {
-    unsigned int hb[6];
-    std::vector<float4> hom(static_cast<size_t>(m));
-    RFD_CUDA(cudaMemcpyAsync(hb, bbox, sizeof(hb), cudaMemcpyDeviceToHost, st));
-    RFD_CUDA(cudaMemcpyAsync(hom.data(), p->omega4, size_t(m) * sizeof(float4),
-                             cudaMemcpyDeviceToHost, st));
-    RFD_CUDA(cudaStreamSynchronize(st));
-    spread = rfd::nufft_grid(hb, hom.data(), m, n, &ng) &&
+    HostSlot* h = nullptr;
+    const rfd_status hs = host_slot(&h);
+    if (hs != RFD_OK) return hs;
+    unsigned int* hb = reinterpret_cast<unsigned int*>(h->buf + kSlotBox);
+    int* hf = reinterpret_cast<int*>(h->buf + kSlotFlags);
+    float4* hom = reinterpret_cast<float4*>(h->buf + kSlotOmega);
+    gather_readback_kernel<<<1, 256, 0, st>>>(bbox, p->flags, p->omega4, m, h->buf);
+    RFD_CUDA(cudaGetLastError());
+    const rfd_status ws = slot_wait(h, st);
+    if (ws != RFD_OK) return ws;
+    known_sym = (hf[0] & 1) ? 0 : 1;
+    spread = rfd::nufft_grid(hb, hom, m, n, &ng) &&
              (spread_mode == 2 || (ng.nodes * kSpreadRatio <= n && n >= kSpreadMinPoints));
   }
   double* Gdst = p->G;
@@ -512,7 +616,8 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   // a5: core
   {
     int sc = 0, sym = 1;
-    const rfd_status cs = core_impl(p, p->nu, p->flags, lambda, p->C, &sc, &sym, st);
+    const rfd_status cs =
+        core_impl(p, p->nu, p->flags, lambda, p->C, &sc, &sym, st, known_sym, defer_core);
     if (cs != RFD_OK) return cs;
     p->scaling = sc;
     p->symmetric = sym;
@@ -732,7 +837,10 @@ rfd_status gfi_impl(const float* points, int64_t n, double eps, double lambda, i
     early = true;
     return RFD_OK;
   };
-  const rfd_status cs = create_impl(points, 1, n, eps, lambda, m, seed, nullptr, st, &p, hook);
+  // the core's overflow check waits until the inference is enqueued behind it
+  // (no idle GPU while the host reads the flag back)
+  const rfd_status cs =
+      create_impl(points, 1, n, eps, lambda, m, seed, nullptr, st, &p, hook, true);
   if (cs != RFD_OK) return cs;
   rfd_status rs = RFD_OK;
   if (early) {
@@ -742,6 +850,8 @@ rfd_status gfi_impl(const float* points, int64_t n, double eps, double lambda, i
   } else {
     rs = integrate_impl(p, F, d, out, st);
   }
+  const rfd_status fs = core_finish(p);  // (out is unspecified on RFD_ERANGE)
+  if (rs == RFD_OK) rs = fs;
   if (rs != RFD_OK || !plan_out) {
     free_plan(p, false);  // stream-ordered (after the aux stream's work)
     if (plan_out) *plan_out = nullptr;

@@ -163,11 +163,16 @@ void launch_core_prep(const double* G, const double* nu, const int* flags,
 // D^1/2 (or lambda D P); oflag = 1 on overflow.  work: kCoreWork matrices.
 // sym: the symmetric route was taken (flags[0] bit 0 clear, read back by the
 // host): every product is symmetric and only its upper tiles are computed.
+// work[0..4) must hold (pw_alpha Z)^k, k = 2..5, from launch_core_powers
+// (pw_alpha a power of two: 1 lets the powers be formed before the host knows
+// s; 2^-s is the classic order -- bitwise the same result either way).
 constexpr double kCoreTheta = 2.0;
 constexpr int kCoreWork = 10;
+void launch_core_powers(const double* Z, int m, int batch, bool sym, double pw_alpha,
+                        double* work, cudaStream_t s);
 void launch_core_eval(const double* Z, const double* nu, const int* flags,
-                      double lambda, int m, int batch, int s_scale, bool sym, double* work,
-                      double* C, int* oflag, cudaStream_t s);
+                      double lambda, int m, int batch, int s_scale, bool sym, double pw_alpha,
+                      double* work, double* C, int* oflag, cudaStream_t s);
 
 // ---------------------------------------------------------------- spectrum
 // NEXT-3 (k_spectrum.cu): k smallest eigenvalues of exp(lambda W~) per cloud.
