@@ -312,7 +312,7 @@ struct TempBuffers {
 // flags, omega (RFD_MAX_M float4).
 struct HostSlot {
   char* buf = nullptr;
-  cudaEvent_t ev = nullptr, ev_src = nullptr;
+  cudaEvent_t ev = nullptr, ev_src = nullptr, ev_join = nullptr;
   cudaStream_t side = nullptr;  // copies the work stream must not wait for
   int dev = -1;
 };
@@ -325,6 +325,7 @@ rfd_status host_slot(HostSlot** out) {
   if (h.dev != dev) {  // (a thread that moves to another device: fresh events, stream)
     RFD_CUDA(cudaEventCreateWithFlags(&h.ev, cudaEventDisableTiming));
     RFD_CUDA(cudaEventCreateWithFlags(&h.ev_src, cudaEventDisableTiming));
+    RFD_CUDA(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
     RFD_CUDA(cudaStreamCreateWithFlags(&h.side, cudaStreamNonBlocking));
     h.dev = dev;
   }
@@ -332,10 +333,16 @@ rfd_status host_slot(HostSlot** out) {
   *out = &h;
   return RFD_OK;
 }
-// wait for everything enqueued on st up to now (not for later work)
+// wait for everything enqueued on st up to now (not for later work).  Used
+// where the GPU idles until the host has read the result (a4's grid sizing),
+// so the host polls the event instead of sleeping in cudaEventSynchronize
+// (the wake-up is on the critical path; the wait is tens of microseconds).
 rfd_status slot_wait(HostSlot* h, cudaStream_t st) {
   RFD_CUDA(cudaEventRecord(h->ev, st));
-  RFD_CUDA(cudaEventSynchronize(h->ev));
+  cudaError_t e;
+  while ((e = cudaEventQuery(h->ev)) == cudaErrorNotReady) {
+  }
+  RFD_CUDA(e);
   return RFD_OK;
 }
 
@@ -588,9 +595,20 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
     RFD_CUDA(tmp.alloc(&ws, rfd::nufft_workspace_bytes(ng, n, m, p->sms)));
     rfd::CellCount cc{};
     RFD_CUDA(rfd::nufft_cell_count(ng, n, m, p->sms, ws, &cc, st));
+    // (the host's first launch after its wait: the packing -- then the grid's
+    // zeroing and the phi^ tables on the side stream beside it, off the
+    // critical path: 10-13 us at cfg 5)
+    HostSlot* h = nullptr;
+    const rfd_status hs = host_slot(&h);
+    if (hs != RFD_OK) return hs;
+    RFD_CUDA(cudaEventRecord(h->ev_src, st));  // (after the workspace's allocation)
     rfd::launch_pack_points(dev_xyz, bbox, p->pts, p->pts16, nullptr, n, p->centre, n, batch, &cc,
                             st);
-    RFD_CUDA(rfd::launch_gram_nufft(p->pts, n, p->omega_rad4, m, ng, p->sms, ws, Gdst, st));
+    RFD_CUDA(cudaStreamWaitEvent(h->side, h->ev_src, 0));
+    RFD_CUDA(rfd::launch_nufft_side(p->omega_rad4, m, n, ng, p->sms, ws, h->side));
+    RFD_CUDA(cudaEventRecord(h->ev_join, h->side));
+    RFD_CUDA(rfd::launch_gram_nufft(p->pts, n, p->omega_rad4, m, ng, p->sms, ws, Gdst, st,
+                                    h->ev_join));
   } else {  // the packing writes the Gram's point layout into its workspace
     const rfd::GramGeom gg = rfd::gram_tc_geometry(m, n, batch, p->sms);
     float* gpart = nullptr;

@@ -149,8 +149,15 @@ cudaError_t nufft_cell_count(const NufftGrid& g, int64_t n, int m, int sms, void
                              CellCount* cc, cudaStream_t s);
 // G (r x r fp64, interleaved) of the centred points pts, counted into the
 // workspace's cells by launch_pack_points.
+// The grid's zeroing and the phi^ tables (they need only omega and the grid
+// geometry): launch_gram_nufft does them itself when side_done is NULL;
+// otherwise the caller ran launch_nufft_side on another stream and side_done
+// marks its end.
+cudaError_t launch_nufft_side(const float4* omega_rad4, int m, int64_t n, const NufftGrid& g,
+                              int sms, void* ws, cudaStream_t s);
 cudaError_t launch_gram_nufft(const float4* pts, int64_t n, const float4* omega_rad4, int m,
-                              const NufftGrid& g, int sms, void* ws, double* G, cudaStream_t s);
+                              const NufftGrid& g, int sms, void* ws, double* G, cudaStream_t s,
+                              cudaEvent_t side_done = nullptr);
 
 // ---------------------------------------------------------------- core
 // Z_b = lambda D^1/2 G D^1/2 (symmetric route) or lambda G D; atomicMax of
