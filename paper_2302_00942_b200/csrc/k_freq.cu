@@ -112,54 +112,52 @@ __device__ __forceinline__ float dec_f32(unsigned int e) {
   return __uint_as_float((e & 0x80000000u) ? (e & 0x7fffffffu) : ~e);
 }
 
-// Two levels, no atomics: bbox_part_kernel writes each block's 6 encoded
-// extrema (grid (chunks, batch), 16-byte loads of the interleaved xyz), then
-// bbox_final_kernel folds a cloud's chunks: bbox[b][0..2] = max ~enc (the
-// minima), bbox[b][3..5] = max enc (the maxima).  (Per-warp atomics on the
-// same 6 words serialised at L2: 54 us at cfg 5.)
+// One launch, two levels: every block writes its 6 encoded extrema (grid
+// (chunks, batch)), and the last block of a cloud to finish (an atomic
+// ticket) folds the cloud's chunks in chunk order: bbox[b][0..2] = max ~enc
+// (the minima), bbox[b][3..5] = max enc (the maxima).  Loads: three float4s
+// = four whole points per thread and step (no per-element component index);
+// the unaligned head / ragged tail by scalar loads.  (Per-warp atomics on the
+// same 6 words serialised at L2: 54 us at cfg 5; two launches with a 64-bit
+// modulo per float4: 30 us.)  tickets: batch words, zero before the launch;
+// the last block resets its cloud's word.
 __global__ void __launch_bounds__(256)
-bbox_part_kernel(const float* __restrict__ xyz, int64_t n, unsigned int* __restrict__ part) {
+bbox_kernel(const float* __restrict__ xyz, int64_t n, unsigned int* __restrict__ part,
+            unsigned int* __restrict__ tickets, unsigned int* __restrict__ bbox) {
   __shared__ unsigned int red[8][6];
+  __shared__ bool last;
   const int b = blockIdx.y;
-  // the cloud's 3n floats as float4s where aligned: a float4 at flat index q
-  // holds coordinates q*4 .. q*4+3, i.e. components (4q + j) % 3
   const float* src = xyz + int64_t(b) * n * 3;
-  const int64_t nf = 3 * n;
   unsigned int v[6] = {0u, 0u, 0u, 0u, 0u, 0u};
-  // (components are selected with compile-time indices only: a runtime index
-  // into v[] would put it in local memory)
   auto take = [&](int k, float x) {
     const unsigned int e = enc_f32(x);
     v[k] = max(v[k], ~e);
     v[3 + k] = max(v[3 + k], e);
   };
-  const bool al = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-  const int64_t n4 = al ? nf / 4 : 0;
-  const int64_t per = (n4 + gridDim.x - 1) / gridDim.x;
-  const int64_t q0 = int64_t(blockIdx.x) * per, q1 = min(q0 + per, n4);
-  const float4* s4 = reinterpret_cast<const float4*>(src);
+  // points [p0, p0 + 4 nq) as float4 triples when 16-byte aligned there
+  const int64_t mis = (reinterpret_cast<uintptr_t>(src) >> 2) & 3;  // floats past 16 B
+  const int64_t p0 = mis;  // 3 p0 + mis = 0 (mod 4): point p0 starts on 16 bytes
+  const int64_t nq = n > p0 ? (n - p0) / 4 : 0;
+  const float4* q4 = reinterpret_cast<const float4*>(src + 3 * p0);
+  const int64_t per = (nq + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = int64_t(blockIdx.x) * per, t1 = min(t0 + per, nq);
 #pragma unroll 4
-  for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
-    const float4 w = __ldg(s4 + q);
-    // flat float 4q + j is component (4q + j) mod 3 = (c + j) mod 3, c = q mod 3:
-    // component k holds element (k - c) mod 3, and element 3 too when k == c
-    const int c = int(q % 3);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int j0 = (k - c + 3) % 3;
-      take(k, j0 == 0 ? w.x : (j0 == 1 ? w.y : w.z));
-      if (k == c) take(k, w.w);
-    }
+  for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+    const float4 a = __ldg(q4 + 3 * t), c = __ldg(q4 + 3 * t + 1), d = __ldg(q4 + 3 * t + 2);
+    take(0, a.x); take(1, a.y); take(2, a.z);
+    take(0, a.w); take(1, c.x); take(2, c.y);
+    take(0, c.z); take(1, c.w); take(2, d.x);
+    take(0, d.y); take(1, d.z); take(2, d.w);
   }
-  // the unaligned remainder (tail floats, or everything when not 16-byte aligned)
-  if (blockIdx.x == 0)
-    for (int64_t i = 4 * n4 + threadIdx.x; i < nf; i += blockDim.x) {
-      const int k = int(i % 3);
-      const float x = __ldg(src + i);
-      if (k == 0) take(0, x);
-      else if (k == 1) take(1, x);
-      else take(2, x);
-    }
+  if (blockIdx.x == 0) {  // the head points [0, p0) and the tail [p0 + 4 nq, n)
+    auto take3 = [&](int64_t i) {
+      take(0, __ldg(src + 3 * i));
+      take(1, __ldg(src + 3 * i + 1));
+      take(2, __ldg(src + 3 * i + 2));
+    };
+    for (int64_t i = threadIdx.x; i < min(p0, n); i += blockDim.x) take3(i);
+    for (int64_t i = p0 + 4 * nq + threadIdx.x; i < n; i += blockDim.x) take3(i);
+  }
 #pragma unroll
   for (int c = 0; c < 6; ++c)
 #pragma unroll
@@ -172,30 +170,21 @@ bbox_part_kernel(const float* __restrict__ xyz, int64_t n, unsigned int* __restr
     unsigned int mx = 0u;
     for (int w = 0; w < 8; ++w) mx = max(mx, red[w][threadIdx.x]);
     part[(int64_t(b) * gridDim.x + blockIdx.x) * 6 + threadIdx.x] = mx;
+    __threadfence();  // (the threadFenceReduction pattern)
   }
-}
-
-__global__ void __launch_bounds__(256)
-bbox_final_kernel(const unsigned int* __restrict__ part, int chunks, unsigned int* __restrict__ bbox) {
-  __shared__ unsigned int red[8][6];
-  const int b = blockIdx.x;
-  unsigned int v[6] = {0u, 0u, 0u, 0u, 0u, 0u};
-  for (int k = threadIdx.x; k < chunks; k += blockDim.x)
-#pragma unroll
-    for (int c = 0; c < 6; ++c) v[c] = max(v[c], part[(int64_t(b) * chunks + k) * 6 + c]);
-#pragma unroll
-  for (int c = 0; c < 6; ++c)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v[c] = max(v[c], __shfl_xor_sync(0xffffffffu, v[c], o));
-  if ((threadIdx.x & 31) == 0)
-#pragma unroll
-    for (int c = 0; c < 6; ++c) red[threadIdx.x >> 5][c] = v[c];
+  // the cloud's last block folds the chunks
   __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(tickets + b, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
   if (threadIdx.x < 6) {
     unsigned int mx = 0u;
-    for (int w = 0; w < 8; ++w) mx = max(mx, red[w][threadIdx.x]);
+    for (int k = 0; k < int(gridDim.x); ++k)
+      mx = max(mx, __ldcg(part + (int64_t(b) * gridDim.x + k) * 6 + threadIdx.x));
     bbox[6 * b + threadIdx.x] = mx;
   }
+  if (threadIdx.x == 0) tickets[b] = 0u;
 }
 
 __device__ __forceinline__ float4 bbox_centre(const unsigned int* bb) {
@@ -315,7 +304,9 @@ void launch_nu(const float4* omega4, double* nu, int* flags, int m, double eps, 
 }
 
 int bbox_chunks(int64_t n, int batch, int sms) {
-  int64_t chunks = (int64_t(sms) * 8 + batch - 1) / batch;
+  // 2 blocks per SM (the blocks' tickets are same-address atomics: 8 per SM
+  // serialised to ~12 us at cfg 5)
+  int64_t chunks = (int64_t(sms) * 2 + batch - 1) / batch;
   const int64_t maxc = (n + 2047) / 2048;
   if (chunks > maxc) chunks = maxc;
   return chunks < 1 ? 1 : int(chunks);
@@ -325,8 +316,10 @@ void launch_bbox(const float* xyz, unsigned int* bbox, unsigned int* part, int64
                  int sms, cudaStream_t s) {
   LaunchScope L("rfd_bbox", s);
   const int chunks = bbox_chunks(n, batch, sms);
-  bbox_part_kernel<<<dim3(unsigned(chunks), unsigned(batch)), 256, 0, s>>>(xyz, n, part);
-  bbox_final_kernel<<<batch, 256, 0, s>>>(part, chunks, bbox);
+  // part: chunks * batch * 6 words, then batch ticket words (zeroed here)
+  unsigned int* tickets = part + size_t(chunks) * batch * 6;
+  cudaMemsetAsync(tickets, 0, size_t(batch) * sizeof(unsigned int), s);
+  bbox_kernel<<<dim3(unsigned(chunks), unsigned(batch)), 256, 0, s>>>(xyz, n, part, tickets, bbox);
 }
 
 void launch_pack_points(const float* xyz, const unsigned int* bbox, float4* pts, float* pts16,

@@ -543,7 +543,7 @@ rfd_status create_impl(const float* points, int batch, int64_t n, double eps, do
   unsigned int* bbox = nullptr;
   RFD_CUDA(tmp.alloc(&bbox, size_t(batch) * 6));
   unsigned int* bpart = nullptr;
-  RFD_CUDA(tmp.alloc(&bpart, size_t(rfd::bbox_chunks(n, batch, p->sms)) * batch * 6));
+  RFD_CUDA(tmp.alloc(&bpart, size_t(rfd::bbox_chunks(n, batch, p->sms)) * batch * 6 + batch));
   rfd::launch_bbox(dev_xyz, bbox, bpart, n, batch, p->sms, st);
   if (world > 1) {  // one centre for the whole cloud: merge the shards' boxes
     double *send = nullptr, *recv = nullptr;

@@ -65,7 +65,7 @@ void launch_nu(const float4* omega4, double* nu, int* flags, int m, double eps, 
 // ---------------------------------------------------------------- pack
 // Per-cloud bounding box of the points (bbox: batch x 6 uint, ordered
 // encoding: [0..2] = max ~enc(x) (the minima), [3..5] = max enc(x)).
-// part: scratch of bbox_chunks(n, batch, sms) x batch x 6 uint.
+// part: scratch of bbox_chunks(n, batch, sms) x batch x 6 + batch uint.
 int bbox_chunks(int64_t n, int batch, int sms);
 void launch_bbox(const float* xyz, unsigned int* bbox, unsigned int* part, int64_t n, int batch,
                  int sms, cudaStream_t s);

@@ -746,6 +746,40 @@ def test_gram_spread_grid_cell_beyond_fold(monkeypatch):
     _check_against_oracle(plan, out, x, F, p)
 
 
+@pytest.mark.parametrize("offset", [0, 1, 2, 3])
+def test_bounding_box_misaligned_points_and_extremes(offset, monkeypatch):
+    # The bounding box (k_freq.cu bbox_kernel) reads whole points as float4
+    # triples from the first 16-byte boundary on, the head and the ragged
+    # tail by scalar loads: the extreme points sit exactly there (indices 0-2
+    # and the last two), the cloud starts `offset` floats past a 16-byte
+    # boundary, and n is odd.  The box sizes a4's spread grid, so a missed
+    # point would change the node count (and put the point off the grid);
+    # a view and a copy of the same points give bitwise the same plan.
+    monkeypatch.setenv("RFD_GRAM_SPREAD", "2")
+    rng = np.random.default_rng(17)
+    n = 6001
+    x = rng.uniform(-0.2, 0.2, (n, 3))
+    x[0] = [0.9, 0.0, 0.0]
+    x[1] = [0.0, -0.8, 0.0]
+    x[2] = [0.0, 0.0, 0.7]
+    x[n - 2] = [-0.6, 0.0, 0.0]
+    x[n - 1] = [0.0, 0.5, -0.9]
+    x = x.astype(np.float32)
+    buf = torch.zeros(3 * n + 8, dtype=torch.float32, device="cuda")
+    buf[offset:offset + 3 * n] = torch.from_numpy(x.reshape(-1)).cuda()
+    view = buf[offset:offset + 3 * n].view(n, 3)
+    assert (view.data_ptr() % 16) == 4 * offset
+    p = dict(name="bbox offset %d" % offset, eps=0.05, lam=-0.4, m=128, seed=4)
+    F = rng.standard_normal((n, 5)).astype(np.float32)
+    plan_v = rfd.Plan(view, p["eps"], p["lam"], p["m"], p["seed"])
+    plan_c, out_c = _run_single(x, F, p)
+    assert plan_v.info()["gram_nodes"] == plan_c.info()["gram_nodes"] > 0
+    np.testing.assert_array_equal(plan_v.export("gram"), plan_c.export("gram"))
+    out_v = plan_v.integrate(torch.from_numpy(F).cuda()).cpu().numpy()
+    np.testing.assert_array_equal(out_v, out_c)
+    _check_against_oracle(plan_c, out_c, x, F, p)
+
+
 def test_gram_spread_grid_declines_large_extent(monkeypatch):
     # cfg 4's sheet scaled x 200 would need > 2^11 nodes per axis: even
     # forced, the plan takes the direct Gram
