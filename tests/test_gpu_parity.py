@@ -780,6 +780,20 @@ def test_bounding_box_misaligned_points_and_extremes(offset, monkeypatch):
     _check_against_oracle(plan_c, out_c, x, F, p)
 
 
+def test_gram_spread_grid_scan_variants_agree(monkeypatch):
+    # the cell-start scan: one CTA for grids of <= 2^18 cells, two tiled
+    # kernels above (forced here: RFD_NUFFT_SCAN_TILES=1); the exact integer
+    # spreading makes G bitwise independent of the point order in a cell
+    monkeypatch.setenv("RFD_GRAM_SPREAD", "2")
+    p, x, F = make_config(4)
+    plan1, out1 = _run_single(x, F, p)
+    monkeypatch.setenv("RFD_NUFFT_SCAN_TILES", "1")
+    plan2, out2 = _run_single(x, F, p)
+    assert plan1.info()["gram_nodes"] == plan2.info()["gram_nodes"] > 4096
+    np.testing.assert_array_equal(plan1.export("gram"), plan2.export("gram"))
+    np.testing.assert_array_equal(out1, out2)
+
+
 def test_gram_spread_grid_declines_large_extent(monkeypatch):
     # cfg 4's sheet scaled x 200 would need > 2^11 nodes per axis: even
     # forced, the plan takes the direct Gram
