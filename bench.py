@@ -854,7 +854,7 @@ def main():
             "kernels": res["kernels"],
             "gram": {"path": "spread grid (k_nufft.cu)" if res["gram_nodes"] else "direct",
                      "nodes": res["gram_nodes"],
-                     "note": "a4 over a 6^3-kernel spread grid of `nodes` points, deconvolved "
+                     "note": "a4 over a spread grid of `nodes` points (width-8 ES kernel, 8^3 taps), deconvolved "
                              "(DESIGN.md Sec. 6 'a4 spread grid'); parity as reported"}}
     print(json.dumps(line))
 
