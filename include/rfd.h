@@ -253,9 +253,11 @@ rfd_status rfd_integrate_host(rfd_plan* plan, const float* F_host, int32_t d,
  *   F, out  n x d DEVICE fp32, 16-byte aligned (out may alias F).
  *   plan_out  NULL (the plan is destroyed, stream-ordered) or receives the
  *           plan for reuse (rfd_integrate on further fields).
- * Blocks the host while the plan's core is formed (as rfd_plan_create); out
- * is ready when `stream` is.  Errors: as rfd_plan_create and rfd_integrate;
- * EINVAL if F or out is host memory.
+ * Blocks the host while the plan's core is formed (as rfd_plan_create); the
+ * core's overflow check waits until the inference is enqueued behind it, so
+ * on RFD_ERANGE the contents of out are unspecified.  out is ready when
+ * `stream` is.  Errors: as rfd_plan_create and rfd_integrate; EINVAL if F or
+ * out is host memory.
  */
 rfd_status rfd_gfi(const float* points, int64_t n, double eps, double lambda, int32_t m,
                    uint64_t seed, const float* F, int32_t d, float* out, rfd_stream stream,

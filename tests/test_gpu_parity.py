@@ -600,6 +600,22 @@ def test_overflow_reports_erange():
     with pytest.raises(rfd.RFDError) as ei:
         rfd.Plan(torch.from_numpy(x).cuda(), p["eps"], 200.0, p["m"], p["seed"])
     assert ei.value.status == rfd.RFD_ERANGE
+    # rfd_gfi checks the core's overflow flag only after the inference is
+    # enqueued (plan.cu core_finish): the error still surfaces, on the narrow
+    # path, the tensor-core path and the spread-grid path (its early powers),
+    # and the next call on the same thread is unaffected
+    for cfg, kw, d in ((2, {}, 1), (2, {}, 8), (5, {"n": 262144}, 16)):
+        p, x, F = make_config(cfg, **kw)
+        xd = torch.from_numpy(x).cuda()
+        Fd = torch.from_numpy(np.ascontiguousarray(F.reshape(x.shape[0], -1)[:, :1])).cuda()
+        Fd = Fd.repeat(1, d).contiguous()
+        with pytest.raises(rfd.RFDError) as ei:
+            rfd.gfi(xd, p["eps"], 200.0, p["m"], p["seed"], Fd)
+        assert ei.value.status == rfd.RFD_ERANGE
+        out = rfd.gfi(xd, p["eps"], p["lam"], p["m"], p["seed"], Fd)
+        ref = rfd.Plan(xd, p["eps"], p["lam"], p["m"], p["seed"]).integrate(Fd)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
 
 
 def test_cuda_graph_capture_of_reuse_loop():
