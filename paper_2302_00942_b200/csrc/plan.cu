@@ -844,7 +844,16 @@ rfd_status gfi_impl(const float* points, int64_t n, double eps, double lambda, i
     if (use_narrow(q, d)) return RFD_OK;  // one launch after the plan
     rfd_status rs = ensure_workspace(q, d, st);
     if (rs != RFD_OK) return rs;
-    if (!q->aux) RFD_CUDA(cudaStreamCreateWithFlags(&q->aux, cudaStreamNonBlocking));
+    if (!q->aux) {
+      // pass 1 (persistent, one CTA per SM) must be placed before the core's
+      // GEMM CTAs, which are launched right behind it on `st` now that the
+      // powers of Z no longer wait for the host: two GEMM CTAs on one SM
+      // leave no room for pass 1's CTA there.  The higher-priority stream's
+      // pending CTAs are dispatched first.
+      int lo = 0, hi = 0;
+      RFD_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      RFD_CUDA(cudaStreamCreateWithPriority(&q->aux, cudaStreamNonBlocking, hi));
+    }
     if (!q->ev[0]) RFD_CUDA(cudaEventCreateWithFlags(&q->ev[0], cudaEventDisableTiming));
     if (!q->ev[1]) RFD_CUDA(cudaEventCreateWithFlags(&q->ev[1], cudaEventDisableTiming));
     RFD_CUDA(cudaEventRecord(q->ev[0], st));
