@@ -165,9 +165,14 @@ def _check(status):
         raise RFDError(status, load_library().rfd_last_error().decode())
 
 
-def _stream_handle(stream):
+def _stream_handle(stream, device=None):
     import torch
     if stream is None:
+        # the current stream's raw handle without building a Stream object
+        # (the per-call host cost bounds the small configurations' plain loop)
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        if raw is not None:
+            return ctypes.c_void_p(raw(torch.cuda.current_device() if device is None else device))
         stream = torch.cuda.current_stream()
     return ctypes.c_void_p(stream.cuda_stream)
 
@@ -184,8 +189,11 @@ def _ptr(a):
 
 
 def _check_f32(a, name):
-    dt = a.dtype
-    ok = (dt == np.float32) if isinstance(a, np.ndarray) else (str(dt) == "torch.float32")
+    if isinstance(a, np.ndarray):
+        ok = a.dtype == np.float32
+    else:
+        import torch
+        ok = a.dtype is torch.float32
     if not ok:
         raise TypeError("%s must be float32" % name)
 
@@ -327,7 +335,7 @@ class Plan:
         else:
             _check_f32(out, "out")
         _check(load_library().rfd_integrate(self._h, _ptr(F), d, _ptr(out),
-                                            _stream_handle(stream)))
+                                            _stream_handle(stream, F.device.index)))
         return out
 
     def integrate_host(self, F_host, out_host, stream=None):
