@@ -36,9 +36,9 @@
 namespace rfd {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kLocalThreads = 256, kWideThreads = 768;  // CTA sizes (see the kernel)
 constexpr int kBatchPts = 512;  // points staged per phase-1 batch
-constexpr int kTilePts = 512;   // points per phase-4 tile (2 per thread)
+// points per phase-4 tile: 2 per thread
 
 // Generation barrier over the whole (co-resident) grid, two levels: CTAs
 // arrive on one of 32 group counters (same-address atomics serialise at L2:
@@ -149,9 +149,15 @@ __device__ __forceinline__ double sum_slots(const SmallArgs& a, int b, int row, 
   return acc;
 }
 
-template <int D>
-__global__ void __launch_bounds__(kThreads, 3)
+// NT threads per CTA: 256 (3 CTAs per SM) in local mode; 768 (one CTA per
+// SM) otherwise -- the same warps per SM for the MUFU work, a third of the
+// phase-1 ranges for phase 2 to sum and of the CTAs in every grid barrier,
+// and no uneven sharing of an SM by three CTAs (cfg 4: the SM's last CTA
+// finished phase 1 at ~60 % of the MUFU rate; 58 -> see DESIGN.md).
+template <int D, int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1)
 integrate_small_kernel(const SmallArgs a) {
+  constexpr int kThreads = NT, kTilePts = 2 * NT;
   extern __shared__ __align__(16) float sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = 2 * a.m;
@@ -482,15 +488,15 @@ integrate_small_kernel(const SmallArgs a) {
   }
 }
 
-template <int D>
+template <int D, int NT>
 int max_ctas(size_t smem, int sms) {
   static int occ = -1;
   static size_t occ_smem = 0;
   if (occ < 0 || occ_smem != smem) {
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(integrate_small_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, integrate_small_kernel<D>, kThreads, smem);
+      cudaFuncSetAttribute(integrate_small_kernel<D, NT>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, integrate_small_kernel<D, NT>, NT, smem);
     if (occ < 1) occ = 1;
     if (occ > 4) occ = 4;
     occ_smem = smem;
@@ -498,23 +504,23 @@ int max_ctas(size_t smem, int sms) {
   return sms * occ;
 }
 
-template <int D>
+template <int D, int NT>
 cudaError_t launch_d(const SmallArgs& a, int grid, size_t smem, cudaStream_t s) {
   if (a.local) {  // independent CTAs: a plain launch, any grid size
     static bool configured = false;
     if (!configured && smem > 48 * 1024) {
-      cudaFuncSetAttribute(integrate_small_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(smem));
+      cudaFuncSetAttribute(integrate_small_kernel<D, NT>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       configured = true;
     }
-    integrate_small_kernel<D><<<grid, kThreads, smem, s>>>(a);
+    integrate_small_kernel<D, NT><<<grid, NT, smem, s>>>(a);
     return cudaGetLastError();
   }
   // cooperative (all CTAs co-resident: the grid barriers), via cudaLaunchKernelEx
   // so that the launch can be captured in a CUDA graph
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -522,7 +528,7 @@ cudaError_t launch_d(const SmallArgs& a, int grid, size_t smem, cudaStream_t s) 
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, integrate_small_kernel<D>, a);
+  return cudaLaunchKernelEx(&cfg, integrate_small_kernel<D, NT>, a);
 }
 
 int frequency_block(int m) { return m <= 32 ? 32 : (m <= 64 ? 64 : (m <= 128 ? 128 : 256)); }
@@ -543,9 +549,9 @@ void small_geometry(int m, int64_t n, int batch, int cap, int* R, int64_t* L, in
   *K = int(k);
 }
 
-size_t smem_bytes(int m, int D) {
+size_t smem_bytes(int m, int D, int nt) {
   const int mp = (m + 3) & ~3;
-  const size_t s1 = (size_t(2) * (4 + D) * kBatchPts + size_t(kThreads) * 2 * D) * sizeof(float);
+  const size_t s1 = (size_t(2) * (4 + D) * kBatchPts + size_t(nt) * 2 * D) * sizeof(float);
   const size_t s4 = (size_t(3) * mp + size_t(mp) * 2 * D + 2 * D) * sizeof(float) +
                     size_t(2 * m) * D * 5 * sizeof(double);
   return s1 > s4 ? s1 : s4;
@@ -558,13 +564,14 @@ bool local_mode(int m, int64_t n, int batch, int sms) {
 
 int dclass(int d) { return d <= 1 ? 1 : (d <= 2 ? 2 : (d <= 3 ? 3 : 4)); }
 
+// (grid-barrier mode: the wide CTAs)
 int cap_for(int m, int d, int sms) {
-  const size_t smem = smem_bytes(m, dclass(d));
+  const size_t smem = smem_bytes(m, dclass(d), kWideThreads);
   switch (dclass(d)) {
-    case 1: return max_ctas<1>(smem, sms);
-    case 2: return max_ctas<2>(smem, sms);
-    case 3: return max_ctas<3>(smem, sms);
-    default: return max_ctas<4>(smem, sms);
+    case 1: return max_ctas<1, kWideThreads>(smem, sms);
+    case 2: return max_ctas<2, kWideThreads>(smem, sms);
+    case 3: return max_ctas<3, kWideThreads>(smem, sms);
+    default: return max_ctas<4, kWideThreads>(smem, sms);
   }
 }
 
@@ -609,7 +616,6 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
   if (trace) cudaGetSymbolAddress(reinterpret_cast<void**>(&a.trace), g_small_trace);
 
   const int D = dclass(d);
-  const size_t smem = smem_bytes(m, D);
   // one CTA per cloud when the clouds are small and there are enough of them
   // to fill the GPU (cfg 3), or for one tiny cloud (cfg 1): no grid barriers
   a.local = local_mode(m, n, batch, sms) ? 1 : 0;
@@ -627,11 +633,22 @@ cudaError_t launch_integrate_small(const float4* pts, const float4* omega4, int 
   // touches): two grid barriers fewer
   a.fuse_a7 = (a.local || (2 * m <= 128 && (n + a.L - 1) / a.L + 1 <= 16)) ? 1 : 0;
   cudaError_t e = cudaSuccess;
-  switch (D) {
-    case 1: e = launch_d<1>(a, grid, smem, s); break;
-    case 2: e = launch_d<2>(a, grid, smem, s); break;
-    case 3: e = launch_d<3>(a, grid, smem, s); break;
-    default: e = launch_d<4>(a, grid, smem, s); break;
+  if (a.local) {
+    const size_t smem = smem_bytes(m, D, kLocalThreads);
+    switch (D) {
+      case 1: e = launch_d<1, kLocalThreads>(a, grid, smem, s); break;
+      case 2: e = launch_d<2, kLocalThreads>(a, grid, smem, s); break;
+      case 3: e = launch_d<3, kLocalThreads>(a, grid, smem, s); break;
+      default: e = launch_d<4, kLocalThreads>(a, grid, smem, s); break;
+    }
+  } else {
+    const size_t smem = smem_bytes(m, D, kWideThreads);
+    switch (D) {
+      case 1: e = launch_d<1, kWideThreads>(a, grid, smem, s); break;
+      case 2: e = launch_d<2, kWideThreads>(a, grid, smem, s); break;
+      case 3: e = launch_d<3, kWideThreads>(a, grid, smem, s); break;
+      default: e = launch_d<4, kWideThreads>(a, grid, smem, s); break;
+    }
   }
   if (trace && e == cudaSuccess) {
     unsigned long long h[8], pe[1024];

@@ -11,6 +11,8 @@ from paper_2302_00942_b200 import rfd  # noqa: E402
 from workloads import make_config  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+if len(sys.argv) > 2:  # another build of the library (A/B)
+    rfd.load_library(sys.argv[2])
 p, x, F = make_config(cfg)
 if cfg == 3:
     plan = rfd.Plan(torch.from_numpy(x).cuda(), p["eps"], p["lam"], p["m"], p["seed"])
