@@ -180,17 +180,28 @@ integrate_small_kernel(const SmallArgs a) {
   // cloud sizes.  Batches are double-buffered: the next one is copied
   // (cp.async, global latency hidden) while this one is consumed.
   {
-    const int G = kThreads / a.fb;  // point groups
-    const int g = tid / a.fb;
+    // KF frequencies per thread (kk0, kk0 + fb / KF, ...): each broadcast
+    // point / field load serves KF frequencies (2 in the wide CTAs: the
+    // shared-memory loads share the MIO queue with MUFU)
+    constexpr int KF = (NT == 768) ? 2 : 1;
+    const int fbh = a.fb / KF;
+    const int G = kThreads / fbh;  // point groups
+    const int g = tid / fbh, kk0 = tid % fbh;
     const int c = blockIdx.x / a.nfb, fbk = blockIdx.x % a.nfb;
     // buffer b: points at sm + b * kBufF (float4 x 512), field rows after them
     constexpr int kBufF = (4 + D) * kBatchPts;  // floats per buffer
     auto pbuf = [&](int b) { return reinterpret_cast<float4*>(sm + b * kBufF); };
     auto fbuf = [&](int b) { return sm + b * kBufF + 4 * kBatchPts; };
     float* red = sm + 2 * kBufF;  // [G][fb][2D]
-    const int k = fbk * a.fb + (tid % a.fb);
-    const float4 w = (k < a.m) ? a.omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float2 wx = make_float2(w.x, w.x), wy = make_float2(w.y, w.y), wz = make_float2(w.z, w.z);
+    float2 wx[KF], wy[KF], wz[KF];
+#pragma unroll
+    for (int u = 0; u < KF; ++u) {
+      const int k = fbk * a.fb + kk0 + u * fbh;
+      const float4 w = (k < a.m) ? a.omega4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+      wx[u] = make_float2(w.x, w.x);
+      wy[u] = make_float2(w.y, w.y);
+      wz[u] = make_float2(w.z, w.z);
+    }
     const int64_t r0 = int64_t(c) * a.L, r1 = min(r0 + a.L, ntot);
     const int bfirst = int(r0 / a.n);
     // batch i: [start, end) -- at most 512 points, within one cloud
@@ -216,9 +227,11 @@ integrate_small_kernel(const SmallArgs a) {
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    float2 acc[D];
+    float2 acc[KF][D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) acc[j] = make_float2(0.f, 0.f);
+    for (int u = 0; u < KF; ++u)
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc[u][j] = make_float2(0.f, 0.f);
     int64_t bs = r0, be = batch_end(r0);
     if (bs < r1) issue(bs, be, 0);
     for (int it = 0; bs < r1; ++it) {
@@ -237,27 +250,30 @@ integrate_small_kernel(const SmallArgs a) {
       // group g takes 4-point quads g, g + G, ... of the batch
       for (int q = 4 * g; q < np4; q += 4 * G) {
         const float4 p0 = xs[q], p1 = xs[q + 1], p2 = xs[q + 2], p3 = xs[q + 3];
-        float2 t0 = __fmul2_rn(make_float2(p0.x, p1.x), wx);
-        float2 t1 = __fmul2_rn(make_float2(p2.x, p3.x), wx);
-        t0 = __ffma2_rn(make_float2(p0.y, p1.y), wy, t0);
-        t1 = __ffma2_rn(make_float2(p2.y, p3.y), wy, t1);
-        t0 = __ffma2_rn(make_float2(p0.z, p1.z), wz, t0);
-        t1 = __ffma2_rn(make_float2(p2.z, p3.z), wz, t1);
-        float2 cs[4];
-        __sincosf(t0.x, &cs[0].y, &cs[0].x);
-        __sincosf(t0.y, &cs[1].y, &cs[1].x);
-        __sincosf(t1.x, &cs[2].y, &cs[2].x);
-        __sincosf(t1.y, &cs[3].y, &cs[3].x);
         // the quad's field rows: 4 D floats = D 16-byte loads
         float f[4 * D];
 #pragma unroll
         for (int v = 0; v < D; ++v)
           *reinterpret_cast<float4*>(f + 4 * v) = *reinterpret_cast<const float4*>(fs + q * D + 4 * v);
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
+        for (int uf = 0; uf < KF; ++uf) {
+          float2 t0 = __fmul2_rn(make_float2(p0.x, p1.x), wx[uf]);
+          float2 t1 = __fmul2_rn(make_float2(p2.x, p3.x), wx[uf]);
+          t0 = __ffma2_rn(make_float2(p0.y, p1.y), wy[uf], t0);
+          t1 = __ffma2_rn(make_float2(p2.y, p3.y), wy[uf], t1);
+          t0 = __ffma2_rn(make_float2(p0.z, p1.z), wz[uf], t0);
+          t1 = __ffma2_rn(make_float2(p2.z, p3.z), wz[uf], t1);
+          float2 cs[4];
+          __sincosf(t0.x, &cs[0].y, &cs[0].x);
+          __sincosf(t0.y, &cs[1].y, &cs[1].x);
+          __sincosf(t1.x, &cs[2].y, &cs[2].x);
+          __sincosf(t1.y, &cs[3].y, &cs[3].x);
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            acc[j] = __ffma2_rn(cs[u], make_float2(f[u * D + j], f[u * D + j]), acc[j]);
+          for (int j = 0; j < D; ++j) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              acc[uf][j] = __ffma2_rn(cs[u], make_float2(f[u * D + j], f[u * D + j]), acc[uf][j]);
+          }
         }
       }
       // end of a cloud part: the G point groups, added in group order, into
@@ -265,11 +281,14 @@ integrate_small_kernel(const SmallArgs a) {
       const int b = int(bs / a.n);
       if (ns >= r1 || ns / a.n != b) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-          red[(g * a.fb + tid % a.fb) * 2 * D + 2 * j] = acc[j].x;
-          red[(g * a.fb + tid % a.fb) * 2 * D + 2 * j + 1] = acc[j].y;
-          acc[j] = make_float2(0.f, 0.f);
-        }
+        for (int uf = 0; uf < KF; ++uf)
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const int kk = kk0 + uf * fbh;
+            red[(g * a.fb + kk) * 2 * D + 2 * j] = acc[uf][j].x;
+            red[(g * a.fb + kk) * 2 * D + 2 * j + 1] = acc[uf][j].y;
+            acc[uf][j] = make_float2(0.f, 0.f);
+          }
         __syncthreads();
         float* slot = a.part + int64_t(b - bfirst) * r * d * a.R + c;  // element e at slot[e R]
         for (int e = tid; e < a.fb * 2 * d; e += kThreads) {
@@ -551,7 +570,8 @@ void small_geometry(int m, int64_t n, int batch, int cap, int* R, int64_t* L, in
 
 size_t smem_bytes(int m, int D, int nt) {
   const int mp = (m + 3) & ~3;
-  const size_t s1 = (size_t(2) * (4 + D) * kBatchPts + size_t(nt) * 2 * D) * sizeof(float);
+  const int kf = nt == 768 ? 2 : 1;  // frequencies per phase-1 thread (the kernel's KF)
+  const size_t s1 = (size_t(2) * (4 + D) * kBatchPts + size_t(kf) * nt * 2 * D) * sizeof(float);
   const size_t s4 = (size_t(3) * mp + size_t(mp) * 2 * D + 2 * D) * sizeof(float) +
                     size_t(2 * m) * D * 5 * sizeof(double);
   return s1 > s4 ? s1 : s4;
